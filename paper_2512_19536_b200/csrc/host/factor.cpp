@@ -1,0 +1,260 @@
+#include "factor.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <string>
+
+namespace pdg {
+
+std::int64_t SupernodalFactor::values() const {
+  std::int64_t n = 0;
+  for (const auto& s : sn) n += static_cast<std::int64_t>(s.Linv.size() + s.B.size());
+  return n;
+}
+
+NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
+                         const std::vector<Pt>& pos, int leaf) {
+  NdTree t;
+  t.order.reserve(m);
+  t.sn_start.push_back(0);
+  std::vector<int> side(m, -1);
+  auto emit = [&](const std::vector<int>& nodes) {
+    for (int v : nodes) t.order.push_back(v);
+    t.sn_start.push_back(static_cast<int>(t.order.size()));
+    t.parent.push_back(-1);
+    return static_cast<int>(t.parent.size()) - 1;
+  };
+  std::function<void(std::vector<int>&, std::vector<int>&)> rec =
+      [&](std::vector<int>& nodes, std::vector<int>& roots) {
+        roots.clear();
+        if (nodes.empty()) return;
+        if (static_cast<int>(nodes.size()) <= leaf) {
+          roots.push_back(emit(nodes));
+          return;
+        }
+        double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+        for (int v : nodes) {
+          x0 = std::min(x0, pos[v].x);
+          x1 = std::max(x1, pos[v].x);
+          y0 = std::min(y0, pos[v].y);
+          y1 = std::max(y1, pos[v].y);
+        }
+        const bool by_x = (x1 - x0) >= (y1 - y0);
+        std::sort(nodes.begin(), nodes.end(), [&](int a, int b) {
+          const double ca = by_x ? pos[a].x : pos[a].y, cb = by_x ? pos[b].x : pos[b].y;
+          return ca < cb || (ca == cb && a < b);
+        });
+        const std::size_t half = nodes.size() / 2;
+        for (std::size_t i = 0; i < nodes.size(); ++i) side[nodes[i]] = i < half ? 0 : 1;
+        std::vector<int> sep_l, sep_r;
+        for (std::size_t i = 0; i < nodes.size(); ++i) {
+          const int v = nodes[i];
+          const int sv = side[v];
+          for (int k = adj_ptr[v]; k < adj_ptr[v + 1]; ++k) {
+            const int u = adj[k];
+            if (side[u] >= 0 && side[u] != sv) {
+              (sv == 0 ? sep_l : sep_r).push_back(v);
+              break;
+            }
+          }
+        }
+        for (int v : nodes) side[v] = -1;
+        std::vector<int>& sep = sep_r.size() < sep_l.size() ? sep_r : sep_l;
+        if (2 * sep.size() > nodes.size()) {
+          roots.push_back(emit(nodes));
+          return;
+        }
+        for (int v : sep) side[v] = 2;
+        std::vector<int> left, right;
+        for (std::size_t i = 0; i < nodes.size(); ++i) {
+          const int v = nodes[i];
+          if (side[v] == 2) continue;
+          (i < half ? left : right).push_back(v);
+        }
+        for (int v : sep) side[v] = -1;
+        std::vector<int> rl, rr;
+        rec(left, rl);
+        rec(right, rr);
+        if (sep.empty()) {
+          roots = rl;
+          roots.insert(roots.end(), rr.begin(), rr.end());
+          return;
+        }
+        std::vector<int> sep_nodes = sep;
+        const int id = emit(sep_nodes);
+        for (int c : rl) t.parent[c] = id;
+        for (int c : rr) t.parent[c] = id;
+        roots.push_back(id);
+      };
+  std::vector<int> all(m);
+  for (int i = 0; i < m; ++i) all[i] = i;
+  std::vector<int> roots;
+  rec(all, roots);
+  return t;
+}
+
+BlockMatrix permute(const BlockMatrix& A, const std::vector<int>& order) {
+  const int m = A.m, bs2 = A.bs * A.bs;
+  std::vector<int> inv(m);
+  for (int i = 0; i < m; ++i) inv[order[i]] = i;
+  BlockMatrix P;
+  P.m = m;
+  P.bs = A.bs;
+  P.ptr.assign(m + 1, 0);
+  for (int i = 0; i < m; ++i) P.ptr[i + 1] = P.ptr[i] + (A.ptr[order[i] + 1] - A.ptr[order[i]]);
+  P.col.resize(A.col.size());
+  P.val.resize(A.val.size());
+  std::vector<std::pair<int, int>> row;
+  for (int i = 0; i < m; ++i) {
+    const int o = order[i];
+    row.clear();
+    for (int k = A.ptr[o]; k < A.ptr[o + 1]; ++k) row.emplace_back(inv[A.col[k]], k);
+    std::sort(row.begin(), row.end());
+    int dst = P.ptr[i];
+    for (const auto& [c, k] : row) {
+      P.col[dst] = c;
+      std::copy(A.val.begin() + static_cast<std::size_t>(k) * bs2,
+                A.val.begin() + static_cast<std::size_t>(k + 1) * bs2,
+                P.val.begin() + static_cast<std::size_t>(dst) * bs2);
+      ++dst;
+    }
+  }
+  return P;
+}
+
+SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
+  const int m = A.m, bs = A.bs;
+  const int nsn = static_cast<int>(nd.sn_start.size()) - 1;
+  SupernodalFactor F;
+  F.m = m;
+  F.bs = bs;
+  F.sn.resize(nsn);
+  F.sn_of.resize(m);
+  std::vector<std::vector<int>> children(nsn);
+  for (int s = 0; s < nsn; ++s) {
+    F.sn[s].s0 = nd.sn_start[s];
+    F.sn[s].s1 = nd.sn_start[s + 1];
+    F.sn[s].parent = nd.parent[s];
+    for (int p = F.sn[s].s0; p < F.sn[s].s1; ++p) F.sn_of[p] = s;
+    if (nd.parent[s] >= 0) children[nd.parent[s]].push_back(s);
+  }
+  // symbolic: rows(S) = (adj(S) u rows(children)) restricted to positions >= s1
+  std::vector<int> mark(m, -1);
+  for (int s = 0; s < nsn; ++s) {
+    Supernode& S = F.sn[s];
+    auto add = [&](int q) {
+      if (q >= S.s1 && mark[q] != s) {
+        mark[q] = s;
+        S.rows.push_back(q);
+      }
+    };
+    for (int p = S.s0; p < S.s1; ++p)
+      for (int k = A.ptr[p]; k < A.ptr[p + 1]; ++k) add(A.col[k]);
+    for (int c : children[s])
+      for (int q : F.sn[c].rows) add(q);
+    std::sort(S.rows.begin(), S.rows.end());
+  }
+  // updaters of S: descendants D whose rows touch S (ascending D)
+  std::vector<std::vector<int>> upd(nsn);
+  std::vector<int> last(nsn, -1);
+  for (int d = 0; d < nsn; ++d)
+    for (int q : F.sn[d].rows) {
+      const int s = F.sn_of[q];
+      if (last[s] != d) {
+        last[s] = d;
+        upd[s].push_back(d);
+      }
+    }
+
+  std::vector<int> rowcell(m, -1);
+  std::vector<double> P, x;
+  for (int s = 0; s < nsn; ++s) {
+    Supernode& S = F.sn[s];
+    const int nc = S.s1 - S.s0, w = nc * bs, r = static_cast<int>(S.rows.size());
+    const int H = w + r * bs;
+    P.assign(static_cast<std::size_t>(H) * w, 0.0);
+    for (int p = S.s0; p < S.s1; ++p) rowcell[p] = p - S.s0;
+    for (int k = 0; k < r; ++k) rowcell[S.rows[k]] = nc + k;
+    auto at = [&](int row, int col) -> double& { return P[static_cast<std::size_t>(col) * H + row]; };
+    // original entries (lower part): A_ij for i >= j, j in S
+    for (int j = S.s0; j < S.s1; ++j) {
+      const int jc = j - S.s0;
+      for (int k = A.ptr[j]; k < A.ptr[j + 1]; ++k) {
+        const int i = A.col[k];
+        if (i < j) continue;
+        const int rc = rowcell[i];
+        const double* blk = A.block(k);  // A_{j,i}, column-major
+        for (int c = 0; c < bs; ++c)
+          for (int rr = 0; rr < bs; ++rr) at(rc * bs + rr, jc * bs + c) = blk[rr * bs + c];
+      }
+    }
+    // left-looking updates from descendants
+    for (int d : upd[s]) {
+      const Supernode& D = F.sn[d];
+      const int wD = D.w(bs), nrD = static_cast<int>(D.rows.size());
+      const int ld = nrD * bs;
+      const int a = static_cast<int>(std::lower_bound(D.rows.begin(), D.rows.end(), S.s0) - D.rows.begin());
+      const int ce = static_cast<int>(std::lower_bound(D.rows.begin(), D.rows.end(), S.s1) - D.rows.begin());
+      for (int l = a; l < ce; ++l) {
+        const int colcell = rowcell[D.rows[l]];
+        for (int cc = 0; cc < bs; ++cc) {
+          const int colP = colcell * bs + cc;
+          double* pcol = P.data() + static_cast<std::size_t>(colP) * H;
+          for (int t = 0; t < wD; ++t) {
+            const double* bcol = D.B.data() + static_cast<std::size_t>(t) * ld;
+            const double coef = bcol[l * bs + cc];
+            if (coef == 0.0) continue;
+            for (int k = l; k < nrD; ++k) {
+              const int rb = rowcell[D.rows[k]] * bs;
+              const double* src = bcol + k * bs;
+              for (int rr = 0; rr < bs; ++rr) pcol[rb + rr] -= src[rr] * coef;
+            }
+          }
+        }
+      }
+    }
+    // right-looking Cholesky of the diagonal block, with the below rows solved in the same sweep
+    for (int j = 0; j < w; ++j) {
+      double* cj = P.data() + static_cast<std::size_t>(j) * H;
+      double d = cj[j];
+      if (!(d > 0.0) || !std::isfinite(d))
+        throw SolverError("factorization failed (not positive definite)");
+      d = std::sqrt(d);
+      cj[j] = d;
+      const double inv = 1.0 / d;
+      for (int i = j + 1; i < H; ++i) cj[i] *= inv;
+      for (int k = j + 1; k < w; ++k) {
+        const double lkj = cj[k];
+        if (lkj == 0.0) continue;
+        double* ck = P.data() + static_cast<std::size_t>(k) * H;
+        for (int i = k; i < H; ++i) ck[i] -= cj[i] * lkj;
+      }
+    }
+    // inv(L_SS), packed column-major lower
+    S.Linv.assign(static_cast<std::size_t>(w) * (w + 1) / 2, 0.0);
+    x.resize(w);
+    std::size_t off = 0;
+    for (int j = 0; j < w; ++j) {
+      std::fill(x.begin(), x.end(), 0.0);
+      x[j] = 1.0;
+      for (int k = j; k < w; ++k) {
+        const double* ck = P.data() + static_cast<std::size_t>(k) * H;
+        x[k] /= ck[k];
+        const double xk = x[k];
+        if (xk == 0.0) continue;
+        for (int i = k + 1; i < w; ++i) x[i] -= ck[i] * xk;
+      }
+      for (int i = j; i < w; ++i) S.Linv[off++] = x[i];
+    }
+    S.B.resize(static_cast<std::size_t>(r) * bs * w);
+    for (int j = 0; j < w; ++j)
+      std::copy(P.begin() + static_cast<std::size_t>(j) * H + w, P.begin() + static_cast<std::size_t>(j + 1) * H,
+                S.B.begin() + static_cast<std::size_t>(j) * r * bs);
+    for (int p = S.s0; p < S.s1; ++p) rowcell[p] = -1;
+    for (int q : S.rows) rowcell[q] = -1;
+  }
+  return F;
+}
+
+}  // namespace pdg

@@ -1,0 +1,63 @@
+// Exact local solvers for the Schwarz preconditioner: geometric nested
+// dissection + block supernodal Cholesky, packed for the device sweep.
+//
+// Replaces the reference's per-subdomain Eigen::LLT / SimplicialLLT factors
+// (/root/reference/proj/src/schwarz.cpp:99-146) and the coarse SimplicialLLT
+// (:138-146). Any exact factorisation satisfies the preconditioner contract
+// z_i = K_i^{-1} r_i (P9); the ordering here is chosen for the GPU: every
+// nested-dissection separator and leaf is a dense supernode, and the device
+// stores inv(L_SS) so each supernode's triangular solve is one parallel
+// triangular mat-vec instead of a w-step dependency chain.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "core.hpp"
+
+namespace pdg {
+
+// Symmetric block matrix over m nodes with bs x bs blocks (column-major
+// blocks, both triangles stored, diagonal present).
+struct BlockMatrix {
+  int m = 0, bs = 0;
+  std::vector<int> ptr, col;
+  std::vector<double> val;
+  const double* block(int k) const { return val.data() + static_cast<std::size_t>(k) * bs * bs; }
+};
+
+struct NdTree {
+  std::vector<int> order;     // position -> node
+  std::vector<int> sn_start;  // supernode s covers positions [sn_start[s], sn_start[s+1])
+  std::vector<int> parent;    // supernode parent, -1 for roots (postorder: parent > child)
+};
+
+// Recursive coordinate bisection; separators are the smaller one-sided
+// boundary of the cut. Deterministic (ties broken by node id).
+NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
+                         const std::vector<Pt>& pos, int leaf_nodes);
+
+struct Supernode {
+  int s0 = 0, s1 = 0;         // positions
+  int parent = -1;
+  std::vector<int> rows;      // below-diagonal row nodes (positions, ascending)
+  std::vector<double> Linv;   // inv(L_SS), packed column-major lower (w(w+1)/2)
+  std::vector<double> B;      // L_{R,S}, column-major (rows.size()*bs x w)
+  int w(int bs) const { return (s1 - s0) * bs; }
+};
+
+struct SupernodalFactor {
+  int m = 0, bs = 0;
+  std::vector<Supernode> sn;
+  std::vector<int> sn_of;     // position -> supernode
+  std::int64_t values() const;
+};
+
+// A must already be in position order (node i of A == position i).
+// Throws SolverError("... not positive definite") on a non-positive pivot.
+SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd);
+
+// Permutes a block matrix: out node i = in node order[i].
+BlockMatrix permute(const BlockMatrix& A, const std::vector<int>& order);
+
+}  // namespace pdg

@@ -1,0 +1,898 @@
+// Problem setup (see problem.hpp). Reference anchors:
+//   config validation          timestepper.cpp:15-34
+//   conductivity tensors       assembly.cpp:13-32, penalty :38-47
+//   mass / SIPG stiffness      assembly.cpp:89-183 (volume first, then faces)
+//   K = C_m chi_m M + dt/2 A    assembly.cpp:185-202
+//   mass block solver          assembly.cpp:204-226
+//   L2 projection              assembly.cpp:228-242
+//   coarse embedding E         schwarz.cpp:13-77, K0 = E^T K E :138-146
+//   subdomain factors          schwarz.cpp:99-136
+#include "problem.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <random>
+#include <string>
+
+#include "parallel.hpp"
+#include "quadrature.hpp"
+
+namespace pdg {
+
+namespace {
+
+struct Tensor {
+  double t00, t01, t10, t11;
+};
+
+Tensor make_tensor(double sl, double sn, double fx, double fy) {
+  const double len = std::hypot(fx, fy);
+  if (!(len > 0.0)) throw ConfigError("conductivity: zero fiber direction");
+  const double nx = -fy / len, ny = fx / len;
+  Tensor t{sl, 0.0, 0.0, sl};
+  t.t00 += (sn - sl) * nx * nx;
+  t.t01 += (sn - sl) * nx * ny;
+  t.t10 += (sn - sl) * ny * nx;
+  t.t11 += (sn - sl) * ny * ny;
+  return t;
+}
+
+bool is_pow2(int r) { return r >= 2 && (r & (r - 1)) == 0; }
+
+std::uint32_t morton(double x, double y, const Box& d) {
+  auto q = [](double v) {
+    v = std::clamp(v, 0.0, 1.0);
+    return static_cast<std::uint32_t>(v * 65535.0);
+  };
+  auto spread = [](std::uint32_t v) {
+    v &= 0xffff;
+    v = (v | (v << 8)) & 0x00ff00ff;
+    v = (v | (v << 4)) & 0x0f0f0f0f;
+    v = (v | (v << 2)) & 0x33333333;
+    v = (v | (v << 1)) & 0x55555555;
+    return v;
+  };
+  return spread(q((x - d.xmin) / d.width())) | (spread(q((y - d.ymin) / d.height())) << 1);
+}
+
+// In-place inverse of a small SPD block (column-major) through Cholesky.
+void spd_inverse(int n, const double* a, double* inv) {
+  std::vector<double> L(static_cast<std::size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= L[k * n + j] * L[k * n + j];
+    if (!(d > 0.0)) throw SolverError("mass block is not positive definite");
+    d = std::sqrt(d);
+    L[j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[j * n + i];
+      for (int k = 0; k < j; ++k) s -= L[k * n + i] * L[k * n + j];
+      L[j * n + i] = s / d;
+    }
+  }
+  // inv = L^-T L^-1 column by column
+  std::vector<double> x(n);
+  for (int c = 0; c < n; ++c) {
+    std::fill(x.begin(), x.end(), 0.0);
+    x[c] = 1.0;
+    for (int i = 0; i < n; ++i) {
+      double s = x[i];
+      for (int k = 0; k < i; ++k) s -= L[k * n + i] * x[k];
+      x[i] = s / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int k = i + 1; k < n; ++k) s -= L[i * n + k] * x[k];
+      x[i] = s / L[i * n + i];
+    }
+    for (int i = 0; i < n; ++i) inv[c * n + i] = x[i];
+  }
+}
+
+// Solve SPD (n x n, column-major) X = R (n x m) via Cholesky.
+void spd_solve(int n, int m, const double* a, double* r) {
+  std::vector<double> inv(static_cast<std::size_t>(n) * n);
+  std::vector<double> L(static_cast<std::size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= L[k * n + j] * L[k * n + j];
+    if (!(d > 0.0)) throw SolverError("coarse embedding: cell mass not positive definite");
+    d = std::sqrt(d);
+    L[j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[j * n + i];
+      for (int k = 0; k < j; ++k) s -= L[k * n + i] * L[k * n + j];
+      L[j * n + i] = s / d;
+    }
+  }
+  for (int c = 0; c < m; ++c) {
+    double* x = r + static_cast<std::size_t>(c) * n;
+    for (int i = 0; i < n; ++i) {
+      double s = x[i];
+      for (int k = 0; k < i; ++k) s -= L[k * n + i] * x[k];
+      x[i] = s / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int k = i + 1; k < n; ++k) s -= L[i * n + k] * x[k];
+      x[i] = s / L[i * n + i];
+    }
+  }
+}
+
+double init_value(const pdg_config& c, Pt x) {
+  switch (c.init_kind) {
+    case PDG_INIT_DISC: {
+      const double dx = x.x - c.omega0[0], dy = x.y - c.omega0[1];
+      return dx * dx + dy * dy < c.omega0_r2 ? c.u_patch : c.u_rest;
+    }
+    case PDG_INIT_CONSTANT:
+      return c.init_params[0];
+    case PDG_INIT_COSINE:
+      return c.init_params[0] * std::cos(M_PI * x.x) * std::cos(M_PI * x.y) + c.init_params[1];
+    case PDG_INIT_BILINEAR:
+      return c.init_params[0] + c.init_params[1] * x.x + c.init_params[2] * x.y +
+             c.init_params[3] * x.x * x.y;
+  }
+  throw ConfigError("unknown initial condition kind");
+}
+
+}  // namespace
+
+void validate_config(const pdg_config& c) {
+  if (!(c.dt > 0.0)) throw ConfigError("time.dt must be positive");
+  if (!(c.T >= c.dt)) throw ConfigError("time.T must be at least one step");
+  if (!(c.tol > 0.0 && c.tol < 1.0)) throw ConfigError("solver.tol must lie in (0, 1)");
+  if (c.degree < 1) throw ConfigError("fem.degree must be >= 1");
+  if (c.degree > 6) throw ConfigError("fem.degree above 6 is not supported on the device path");
+  if (!(c.eta0 > 0.0)) throw ConfigError("fem.eta0 must be positive");
+  if (!(c.chi_m > 0.0)) throw ConfigError("membrane.chi must be positive");
+  if (!(c.C_m > 0.0)) throw ConfigError("membrane.Cm must be positive");
+  if (!(c.sigma_grey_l > 0.0 && c.sigma_grey_n > 0.0 && c.sigma_white_l > 0.0 && c.sigma_white_n > 0.0))
+    throw ConfigError("conductivity: all sigma values must be positive");
+  if (c.mesh_cells < 1) throw ConfigError("generate_polygonal_mesh: n_cells must be >= 1");
+  if (c.precond_kind < 0 || c.precond_kind > 2) throw ConfigError("precond.kind must be none, block-jacobi or two-level");
+  if (c.precond_kind == PDG_PRECOND_TWO_LEVEL) {
+    if (c.coarse_count == 0 && !is_pow2(c.h_ratio))
+      throw ConfigError("precond.H_ratio must be a power of two >= 2");
+    const int q = c.q > 0 ? c.q : c.degree;
+    if (q > c.degree) throw ConfigError("precond.q must not exceed fem.degree");
+    if (c.coarse_count == -1 && c.subdomains <= 0)
+      throw ConfigError("precond.coarse = subdomains needs precond.subdomains > 0");
+  }
+  if (c.subdomains < 0 || c.subdomains > c.mesh_cells)
+    throw ConfigError("precond.subdomains must lie in [0, mesh.cells]");
+  if (c.coarse_count > c.mesh_cells || c.coarse_count < -1)
+    throw ConfigError("precond.coarse must lie in [-1, mesh.cells]");
+  if (c.ionic_model == PDG_IONIC_FHN) {
+    if (!(c.fhn[6] > c.fhn[5])) throw ConfigError("fhn: u_max must exceed u_min");
+    if (!(c.fhn[1] >= 0.0 && c.fhn[2] > 0.0)) throw ConfigError("fhn: invalid rate constants");
+  } else if (c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN) {
+    throw ConfigError(
+        "ionic model 'barreto-cressman': the kinetics are not distributed with the reference; "
+        "parity is unpinned (SURVEY.md 8(c))");
+  } else if (c.ionic_model != PDG_IONIC_NONE) {
+    throw ConfigError("unknown ionic model");
+  }
+  if (c.world < 1 || c.rank < 0 || c.rank >= c.world) throw ConfigError("invalid rank/world");
+}
+
+std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
+  validate_config(cfg);
+  auto P = std::make_unique<Problem>();
+  Problem& pr = *P;
+  pr.cfg = cfg;
+  const Box dom{cfg.domain[0], cfg.domain[1], cfg.domain[2], cfg.domain[3]};
+  {
+    Mesh m = generate_mesh(cfg.mesh_cells, dom, cfg.mesh_seed, cfg.mesh_lloyd);
+    pr.mesh = (cfg.split_y > dom.ymin && cfg.split_y < dom.ymax) ? assign_regions(m, cfg.split_y) : std::move(m);
+  }
+  const Mesh& mesh = pr.mesh;
+  const int N = mesh.n_cells();
+  pr.p = cfg.degree;
+  pr.b = n_modes(pr.p);
+  pr.q = cfg.q > 0 ? cfg.q : cfg.degree;
+  pr.bq = n_modes(pr.q);
+  pr.has_precond = cfg.precond_kind != PDG_PRECOND_NONE;
+  pr.two_level = cfg.precond_kind == PDG_PRECOND_TWO_LEVEL;
+  pr.n_comp = cfg.ionic_model == PDG_IONIC_FHN ? 1 : 0;
+  const int b = pr.b, b2 = b * b;
+
+  // ---- partitions (timestepper.cpp:92-102 + ext) ----
+  pr.sub = cfg.subdomains > 0 ? agglomerate(mesh, cfg.subdomains) : identity_partition(mesh);
+  if (pr.two_level) {
+    if (cfg.coarse_count == -1 || (cfg.coarse_count > 0 && cfg.coarse_count == cfg.subdomains))
+      pr.coarse = pr.sub;
+    else if (cfg.coarse_count > 0)
+      pr.coarse = agglomerate(mesh, cfg.coarse_count);
+    else {
+      const int levels = static_cast<int>(std::lround(std::log2(static_cast<double>(cfg.h_ratio))));
+      pr.coarse = agglomerate_hierarchy(mesh, levels).back();
+    }
+  }
+
+  // ---- adjacency (reference cell ids) ----
+  std::vector<std::vector<int>> nbr(N);
+  for (const Face& f : mesh.interior_faces()) {
+    nbr[f.cell_in].push_back(f.cell_out);
+    nbr[f.cell_out].push_back(f.cell_in);
+  }
+  for (auto& v : nbr) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+
+  // ---- placement units and internal order ----
+  std::vector<std::vector<int>> units;
+  const bool multi_sub = cfg.subdomains > 0;
+  if (multi_sub) {
+    units = pr.sub.members();
+  } else if (pr.two_level) {
+    units = pr.coarse.members();
+  } else {
+    std::vector<int> cells(N);
+    std::iota(cells.begin(), cells.end(), 0);
+    std::vector<std::uint32_t> code(N);
+    for (int c = 0; c < N; ++c) code[c] = morton(mesh.centroid(c).x, mesh.centroid(c).y, dom);
+    std::stable_sort(cells.begin(), cells.end(), [&](int a, int b2_) { return code[a] < code[b2_]; });
+    for (int s = 0; s < N; s += 256)
+      units.emplace_back(cells.begin() + s, cells.begin() + std::min(N, s + 256));
+  }
+  const int n_units = static_cast<int>(units.size());
+  std::vector<int> unit_order(n_units);
+  std::iota(unit_order.begin(), unit_order.end(), 0);
+  {
+    std::vector<std::uint32_t> code(n_units);
+    for (int u = 0; u < n_units; ++u) {
+      double sx = 0, sy = 0;
+      for (int c : units[u]) {
+        sx += mesh.centroid(c).x;
+        sy += mesh.centroid(c).y;
+      }
+      code[u] = morton(sx / units[u].size(), sy / units[u].size(), dom);
+    }
+    std::stable_sort(unit_order.begin(), unit_order.end(), [&](int a, int c) { return code[a] < code[c]; });
+  }
+  // contiguous split of the ordered units over ranks, balanced by cells
+  std::vector<int> unit_rank(n_units, 0);
+  pr.rank_cell_start.assign(cfg.world + 1, 0);
+  {
+    std::int64_t acc = 0;
+    int r = 0;
+    for (int k = 0; k < n_units; ++k) {
+      const int u = unit_order[k];
+      while (r < cfg.world - 1 && acc >= static_cast<std::int64_t>(N) * (r + 1) / cfg.world) ++r;
+      unit_rank[u] = r;
+      acc += static_cast<std::int64_t>(units[u].size());
+    }
+  }
+  // ND inside each multi-cell subdomain
+  const int leaf = std::clamp(64 / b, 4, 16);
+  std::vector<NdTree> nd(n_units);
+  std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
+  parallel_for(n_units, [&](int u) {
+    const auto& cells = units[u];
+    const int m = static_cast<int>(cells.size());
+    if (!multi_sub) {
+      unit_cells[u] = cells;
+      return;
+    }
+    std::map<int, int> loc;
+    for (int i = 0; i < m; ++i) loc[cells[i]] = i;
+    std::vector<int> ap{0}, aj;
+    std::vector<Pt> pos(m);
+    for (int i = 0; i < m; ++i) {
+      for (int nb : nbr[cells[i]]) {
+        auto it = loc.find(nb);
+        if (it != loc.end()) aj.push_back(it->second);
+      }
+      ap.push_back(static_cast<int>(aj.size()));
+      pos[i] = mesh.centroid(cells[i]);
+    }
+    nd[u] = nested_dissection(m, ap, aj, pos, leaf);
+    unit_cells[u].resize(m);
+    for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
+  });
+  pr.perm.clear();
+  std::vector<int> unit_start(n_units, 0);
+  for (int r = 0; r < cfg.world; ++r) {
+    pr.rank_cell_start[r] = static_cast<int>(pr.perm.size());
+    for (int k = 0; k < n_units; ++k) {
+      const int u = unit_order[k];
+      if (unit_rank[u] != r) continue;
+      unit_start[u] = static_cast<int>(pr.perm.size());
+      pr.perm.insert(pr.perm.end(), unit_cells[u].begin(), unit_cells[u].end());
+    }
+  }
+  pr.rank_cell_start[cfg.world] = N;
+  pr.iperm.assign(N, -1);
+  for (int i = 0; i < N; ++i) pr.iperm[pr.perm[i]] = i;
+  pr.cell_begin = pr.rank_cell_start[cfg.rank];
+  pr.cell_end = pr.rank_cell_start[cfg.rank + 1];
+  const int nloc = pr.cell_end - pr.cell_begin;
+
+  // ---- assembly of local rows (assembly.cpp:89-183) ----
+  pr.keep_matrices = static_cast<std::int64_t>(N) * b <= 2000000;
+  Bsr& A = pr.A;
+  A.rows = nloc;
+  A.b = b;
+  A.ptr.assign(nloc + 1, 0);
+  for (int i = 0; i < nloc; ++i) A.ptr[i + 1] = A.ptr[i] + 1 + static_cast<int>(nbr[pr.perm[pr.cell_begin + i]].size());
+  A.col.resize(A.ptr[nloc]);
+  for (int i = 0; i < nloc; ++i) {
+    const int c = pr.perm[pr.cell_begin + i];
+    std::vector<int> cols{pr.cell_begin + i};
+    for (int nb : nbr[c]) cols.push_back(pr.iperm[nb]);
+    std::sort(cols.begin(), cols.end());
+    std::copy(cols.begin(), cols.end(), A.col.begin() + A.ptr[i]);
+  }
+  A.val.assign(static_cast<std::size_t>(A.ptr[nloc]) * b2, 0.0);
+  auto find_block = [&](int i_loc, int j_glob) {
+    const int* b0 = A.col.data() + A.ptr[i_loc];
+    const int* e0 = A.col.data() + A.ptr[i_loc + 1];
+    const int* it = std::lower_bound(b0, e0, j_glob);
+    return static_cast<int>(it - A.col.data());
+  };
+  // conductivity per cell
+  std::vector<Tensor> sig(N);
+  std::vector<double> sig_norm(N);
+  {
+    std::vector<double> theta;
+    if (cfg.fiber_random) {
+      std::mt19937_64 rng(cfg.fiber_seed);
+      theta.resize(N);
+      for (int c = 0; c < N; ++c) theta[c] = M_PI * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+    }
+    for (int c = 0; c < N; ++c) {
+      const bool grey = mesh.region(c) == kGrey;
+      const double sl = grey ? cfg.sigma_grey_l : cfg.sigma_white_l;
+      const double sn = grey ? cfg.sigma_grey_n : cfg.sigma_white_n;
+      double fx = grey ? cfg.fiber_grey[0] : cfg.fiber_white[0];
+      double fy = grey ? cfg.fiber_grey[1] : cfg.fiber_white[1];
+      if (cfg.fiber_random) {
+        fx = std::cos(theta[c]);
+        fy = std::sin(theta[c]);
+      }
+      sig[c] = make_tensor(sl, sn, fx, fy);
+      sig_norm[c] = std::max(sl, sn);
+    }
+  }
+  const int order = 2 * pr.p + 2;
+  pr.M.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
+  pr.Minv.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
+  pr.U0.assign(static_cast<std::size_t>(nloc) * b, 0.0);
+  pr.Y0.assign(static_cast<std::size_t>(nloc) * b * pr.n_comp, 0.0);
+  pr.bbox.resize(static_cast<std::size_t>(nloc) * 4);
+  pr.tri_ptr.assign(nloc + 1, 0);
+  std::vector<std::vector<double>> tri_loc(nloc);
+  parallel_for(nloc, [&](int i) {
+    const int c = pr.perm[pr.cell_begin + i];
+    const std::vector<Pt> poly = mesh.cell_points(c);
+    const Box bx = bbox_of(poly.data(), static_cast<int>(poly.size()));
+    pr.bbox[4 * i] = bx.xmin;
+    pr.bbox[4 * i + 1] = bx.ymin;
+    pr.bbox[4 * i + 2] = bx.xmax;
+    pr.bbox[4 * i + 3] = bx.ymax;
+    std::vector<std::array<Pt, 3>> tris;
+    cell_triangles(poly, tris);
+    for (const auto& t : tris)
+      for (const Pt& v : t) {
+        tri_loc[i].push_back(v.x);
+        tri_loc[i].push_back(v.y);
+      }
+    const Rule rule = polygon_rule(poly, order);
+    const int nq = static_cast<int>(rule.size());
+    std::vector<double> val(static_cast<std::size_t>(nq) * b), gx(val.size()), gy(val.size());
+    for (int k = 0; k < nq; ++k) basis_at(bx, pr.p, rule.pts[k], &val[k * b], &gx[k * b], &gy[k * b]);
+    std::vector<double> mloc(b2, 0.0), aloc(b2, 0.0);
+    const Tensor& s = sig[c];
+    for (int k = 0; k < nq; ++k) {
+      const double w = rule.w[k];
+      const double* v = &val[k * b];
+      for (int ii = 0; ii < b; ++ii)
+        for (int jj = ii; jj < b; ++jj) mloc[jj * b + ii] += w * v[ii] * v[jj];
+    }
+    for (int k = 0; k < nq; ++k) {
+      const double w = rule.w[k];
+      const double* X = &gx[k * b];
+      const double* Y = &gy[k * b];
+      for (int jj = 0; jj < b; ++jj) {
+        const double sx = s.t00 * X[jj] + s.t01 * Y[jj];
+        const double sy = s.t10 * X[jj] + s.t11 * Y[jj];
+        for (int ii = 0; ii <= jj; ++ii) aloc[jj * b + ii] += w * (X[ii] * sx + Y[ii] * sy);
+      }
+    }
+    double* Mb = &pr.M[static_cast<std::size_t>(i) * b2];
+    double* Ab = &A.val[static_cast<std::size_t>(find_block(i, pr.cell_begin + i)) * b2];
+    for (int jj = 0; jj < b; ++jj)
+      for (int ii = 0; ii <= jj; ++ii) {
+        Mb[jj * b + ii] = Mb[ii * b + jj] = mloc[jj * b + ii];
+        Ab[jj * b + ii] = Ab[ii * b + jj] = aloc[jj * b + ii];
+      }
+    spd_inverse(b, Mb, &pr.Minv[static_cast<std::size_t>(i) * b2]);
+    // initial data: l2 projection (assembly.cpp:228-242), Y at the model rest state (0 for FHN)
+    std::vector<double> rhs(b, 0.0);
+    for (int k = 0; k < nq; ++k) {
+      const double g = init_value(cfg, rule.pts[k]);
+      for (int ii = 0; ii < b; ++ii) rhs[ii] += rule.w[k] * g * val[k * b + ii];
+    }
+    const double* Mi = &pr.Minv[static_cast<std::size_t>(i) * b2];
+    for (int ii = 0; ii < b; ++ii) {
+      double acc = 0.0;
+      for (int jj = 0; jj < b; ++jj) acc += Mi[jj * b + ii] * rhs[jj];
+      pr.U0[static_cast<std::size_t>(i) * b + ii] = acc;
+    }
+  }, 16);
+  for (int i = 0; i < nloc; ++i) pr.tri_ptr[i + 1] = pr.tri_ptr[i] + static_cast<int>(tri_loc[i].size() / 6);
+  pr.tri.reserve(static_cast<std::size_t>(pr.tri_ptr[nloc]) * 6);
+  for (auto& t : tri_loc) pr.tri.insert(pr.tri.end(), t.begin(), t.end());
+  gauss_legendre((order + 3) / 2, pr.gl_x, pr.gl_w);
+
+  // interior faces (sequential in face order so the diagonal sums keep the reference order)
+  {
+    const auto& faces = mesh.interior_faces();
+    const int nf = static_cast<int>(faces.size());
+    std::vector<int> touched;
+    for (int f = 0; f < nf; ++f) {
+      const int iK = pr.iperm[faces[f].cell_in], iL = pr.iperm[faces[f].cell_out];
+      const bool lk = iK >= pr.cell_begin && iK < pr.cell_end;
+      const bool ll = iL >= pr.cell_begin && iL < pr.cell_end;
+      if (lk || ll) touched.push_back(f);
+    }
+    const int nt = static_cast<int>(touched.size());
+    std::vector<double> blocks(static_cast<std::size_t>(nt) * 3 * b2);
+    parallel_for(nt, [&](int t) {
+      const Face& f = faces[touched[t]];
+      const int K = f.cell_in, L = f.cell_out;
+      const double nk = sig_norm[K], nl = sig_norm[L];
+      const double hk = mesh.diameter(K), hl = mesh.diameter(L);
+      const double eta = cfg.eta0 * (0.5 * (nk + nl)) * pr.p * pr.p / (2.0 * hk * hl / (hk + hl));
+      const Tensor& sk = sig[K];
+      const Tensor& sl = sig[L];
+      const std::vector<Pt> pk = mesh.cell_points(K), pl = mesh.cell_points(L);
+      const Box bk = bbox_of(pk.data(), static_cast<int>(pk.size()));
+      const Box bl = bbox_of(pl.data(), static_cast<int>(pl.size()));
+      const Rule rule = segment_rule(f.a, f.b, order);
+      double* kk = &blocks[static_cast<std::size_t>(t) * 3 * b2];
+      double* lL = kk + b2;
+      double* kl = lL + b2;
+      std::vector<double> vk(b), vl(b), gxk(b), gyk(b), gxl(b), gyl(b), ak(b), al(b);
+      for (std::size_t k = 0; k < rule.size(); ++k) {
+        const double w = rule.w[k];
+        basis_at(bk, pr.p, rule.pts[k], vk.data(), gxk.data(), gyk.data());
+        basis_at(bl, pr.p, rule.pts[k], vl.data(), gxl.data(), gyl.data());
+        for (int m = 0; m < b; ++m) {
+          ak[m] = (sk.t00 * gxk[m] + sk.t01 * gyk[m]) * f.normal.x + (sk.t10 * gxk[m] + sk.t11 * gyk[m]) * f.normal.y;
+          al[m] = (sl.t00 * gxl[m] + sl.t01 * gyl[m]) * f.normal.x + (sl.t10 * gxl[m] + sl.t11 * gyl[m]) * f.normal.y;
+        }
+        for (int ii = 0; ii < b; ++ii) {
+          const double vki = vk[ii], vli = vl[ii];
+          for (int jj = ii; jj < b; ++jj) {
+            kk[jj * b + ii] += w * (-0.5 * (ak[jj] * vki + ak[ii] * vk[jj]) + eta * vk[jj] * vki);
+            lL[jj * b + ii] += w * (0.5 * (al[jj] * vli + al[ii] * vl[jj]) + eta * vl[jj] * vli);
+          }
+          for (int jj = 0; jj < b; ++jj)
+            kl[jj * b + ii] += w * (-0.5 * al[jj] * vki + 0.5 * ak[ii] * vl[jj] - eta * vl[jj] * vki);
+        }
+      }
+    }, 64);
+    for (int t = 0; t < nt; ++t) {
+      const Face& f = faces[touched[t]];
+      const int iK = pr.iperm[f.cell_in], iL = pr.iperm[f.cell_out];
+      const double* kk = &blocks[static_cast<std::size_t>(t) * 3 * b2];
+      const double* lL = kk + b2;
+      const double* kl = lL + b2;
+      if (iK >= pr.cell_begin && iK < pr.cell_end) {
+        const int li = iK - pr.cell_begin;
+        double* D = &A.val[static_cast<std::size_t>(find_block(li, iK)) * b2];
+        for (int jj = 0; jj < b; ++jj)
+          for (int ii = 0; ii <= jj; ++ii) {
+            D[jj * b + ii] += kk[jj * b + ii];
+            if (ii != jj) D[ii * b + jj] += kk[jj * b + ii];
+          }
+        double* O = &A.val[static_cast<std::size_t>(find_block(li, iL)) * b2];
+        for (int k = 0; k < b2; ++k) O[k] += kl[k];
+      }
+      if (iL >= pr.cell_begin && iL < pr.cell_end) {
+        const int li = iL - pr.cell_begin;
+        double* D = &A.val[static_cast<std::size_t>(find_block(li, iL)) * b2];
+        for (int jj = 0; jj < b; ++jj)
+          for (int ii = 0; ii <= jj; ++ii) {
+            D[jj * b + ii] += lL[jj * b + ii];
+            if (ii != jj) D[ii * b + jj] += lL[jj * b + ii];
+          }
+        double* O = &A.val[static_cast<std::size_t>(find_block(li, iK)) * b2];
+        for (int jj = 0; jj < b; ++jj)
+          for (int ii = 0; ii < b; ++ii) O[jj * b + ii] += kl[ii * b + jj];
+      }
+    }
+  }
+  // K = C_m chi_m M + dt/2 A (assembly.cpp:197-202)
+  {
+    const double a = cfg.C_m * cfg.chi_m, hb = 0.5 * cfg.dt;
+    pr.K.rows = nloc;
+    pr.K.b = b;
+    pr.K.ptr = A.ptr;
+    pr.K.col = A.col;
+    pr.K.val.resize(A.val.size());
+    for (int i = 0; i < nloc; ++i)
+      for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        const bool diag = A.col[k] == pr.cell_begin + i;
+        const double* a_ = &A.val[static_cast<std::size_t>(k) * b2];
+        double* kv = &pr.K.val[static_cast<std::size_t>(k) * b2];
+        const double* m_ = &pr.M[static_cast<std::size_t>(i) * b2];
+        for (int e = 0; e < b2; ++e) kv[e] = diag ? a * m_[e] + hb * a_[e] : hb * a_[e];
+      }
+    if (!pr.keep_matrices) {
+      A.val.clear();
+      A.val.shrink_to_fit();
+    }
+  }
+
+  // ---- Schwarz local factors (schwarz.cpp:99-136) ----
+  struct UnitFactor {
+    int unit;
+    SupernodalFactor F;
+  };
+  std::vector<int> my_units;
+  for (int k = 0; k < n_units; ++k)
+    if (unit_rank[unit_order[k]] == cfg.rank) my_units.push_back(unit_order[k]);
+  std::vector<UnitFactor> factors;
+  if (pr.has_precond) {
+    if (multi_sub) {
+      factors.resize(my_units.size());
+      parallel_for(static_cast<int>(my_units.size()), [&](int k) {
+        const int u = my_units[k];
+        const int m = static_cast<int>(unit_cells[u].size());
+        const int s0 = unit_start[u];
+        BlockMatrix Bm;
+        Bm.m = m;
+        Bm.bs = b;
+        Bm.ptr.assign(m + 1, 0);
+        for (int i = 0; i < m; ++i) {
+          const int li = s0 + i - pr.cell_begin;
+          for (int kk = pr.K.ptr[li]; kk < pr.K.ptr[li + 1]; ++kk) {
+            const int j = pr.K.col[kk];
+            if (j < s0 || j >= s0 + m) continue;
+            Bm.col.push_back(j - s0);
+            Bm.val.insert(Bm.val.end(), pr.K.val.begin() + static_cast<std::size_t>(kk) * b2,
+                          pr.K.val.begin() + static_cast<std::size_t>(kk + 1) * b2);
+          }
+          Bm.ptr[i + 1] = static_cast<int>(Bm.col.size());
+        }
+        NdTree t;
+        t.order.resize(m);
+        std::iota(t.order.begin(), t.order.end(), 0);
+        t.sn_start = nd[u].sn_start;
+        t.parent = nd[u].parent;
+        factors[k].unit = u;
+        try {
+          factors[k].F = supernodal_cholesky(Bm, t);
+        } catch (const SolverError&) {
+          throw SolverError("schwarz: subdomain " + std::to_string(u) +
+                            " factorization failed (not positive definite)");
+        }
+      });
+    } else {
+      // one element per subdomain: dense b x b Cholesky (schwarz.cpp:103-112)
+      factors.resize(nloc);
+      parallel_for(nloc, [&](int i) {
+        BlockMatrix Bm;
+        Bm.m = 1;
+        Bm.bs = b;
+        Bm.ptr = {0, 1};
+        Bm.col = {0};
+        const int k = A.ptr[i] + static_cast<int>(std::lower_bound(pr.K.col.begin() + pr.K.ptr[i],
+                                                                 pr.K.col.begin() + pr.K.ptr[i + 1],
+                                                                 pr.cell_begin + i) -
+                                                  (pr.K.col.begin() + pr.K.ptr[i]));
+        Bm.val.assign(pr.K.val.begin() + static_cast<std::size_t>(k) * b2,
+                      pr.K.val.begin() + static_cast<std::size_t>(k + 1) * b2);
+        NdTree t;
+        t.order = {0};
+        t.sn_start = {0, 1};
+        t.parent = {-1};
+        factors[i].unit = pr.sub.owner[pr.perm[pr.cell_begin + i]];
+        try {
+          factors[i].F = supernodal_cholesky(Bm, t);
+        } catch (const SolverError&) {
+          throw SolverError("schwarz: subdomain " + std::to_string(factors[i].unit) +
+                            " block is not positive definite");
+        }
+      }, 256);
+    }
+  }
+  // pack fine tasks
+  auto add_unit_tasks = [&](const SupernodalFactor& F, int coarse, std::int64_t dof_base,
+                            const std::function<std::int64_t(int)>& pos_dof) {
+    const int bs = F.bs;
+    const int base = static_cast<int>(pr.tasks.size());
+    const int nsn = static_cast<int>(F.sn.size());
+    std::vector<std::vector<int>> kids(nsn);
+    for (int s = 0; s < nsn; ++s)
+      if (F.sn[s].parent >= 0) kids[F.sn[s].parent].push_back(s);
+    std::vector<int> height(nsn, 0), depth(nsn, 0);
+    for (int s = 0; s < nsn; ++s)
+      for (int c : kids[s]) height[s] = std::max(height[s], height[c] + 1);
+    for (int s = nsn - 1; s >= 0; --s)
+      if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
+    // in-slot base of each supernode
+    std::vector<int> slot(nsn);
+    for (int s = 0; s < nsn; ++s) {
+      const Supernode& S = F.sn[s];
+      TaskDesc t;
+      t.coarse = coarse;
+      t.bs = bs;
+      t.w = S.w(bs);
+      t.nr = static_cast<int>(S.rows.size()) * bs;
+      t.dof0 = dof_base + pos_dof(S.s0);
+      t.val_off = static_cast<std::int64_t>(pr.fvals.size());
+      pr.fvals.insert(pr.fvals.end(), S.Linv.begin(), S.Linv.end());
+      pr.fvals.insert(pr.fvals.end(), S.B.begin(), S.B.end());
+      t.rows_off = static_cast<int>(pr.row_dof.size());
+      for (int qpos : S.rows) pr.row_dof.push_back(dof_base + pos_dof(qpos));
+      t.ubuf_off = pr.ubuf_size;
+      pr.ubuf_size += t.nr;
+      t.parent = S.parent >= 0 ? base + S.parent : -1;
+      t.child_off = static_cast<int>(pr.task_child.size());
+      for (int c : kids[s]) pr.task_child.push_back(base + c);
+      t.n_child = static_cast<int>(kids[s].size());
+      t.height = height[s];
+      t.depth = depth[s];
+      slot[s] = static_cast<int>(pr.in_ptr.size()) - 1;
+      t.in_off = slot[s];
+      for (int cc = S.s0; cc < S.s1; ++cc) pr.in_ptr.push_back(pr.in_ptr.back());  // filled below
+      pr.tasks.push_back(t);
+    }
+    // incoming lists: (S, cell) <- ubuf slices of descendants D, in D order
+    std::vector<std::vector<std::int64_t>> inc(F.m);
+    for (int d = 0; d < nsn; ++d) {
+      const Supernode& D = F.sn[d];
+      for (std::size_t k = 0; k < D.rows.size(); ++k)
+        inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
+    }
+    for (int s = 0; s < nsn; ++s) {
+      const Supernode& S = F.sn[s];
+      int at = slot[s];
+      for (int cc = S.s0; cc < S.s1; ++cc) {
+        pr.in_idx.insert(pr.in_idx.end(), inc[cc].begin(), inc[cc].end());
+        pr.in_ptr[at + 1] = static_cast<int>(pr.in_idx.size());
+        ++at;
+      }
+    }
+  };
+  pr.in_ptr = {0};
+  for (const UnitFactor& uf : factors) {
+    std::int64_t base;
+    if (multi_sub)
+      base = static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b;
+    else
+      base = static_cast<std::int64_t>(&uf - factors.data()) * b;
+    add_unit_tasks(uf.F, 0, base, [b](int pos) { return static_cast<std::int64_t>(pos) * b; });
+    pr.factor_values += uf.F.values();
+  }
+  pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
+  factors.clear();
+
+  // ---- coarse embedding E (schwarz.cpp:13-77) and local K0 contribution ----
+  if (pr.two_level) {
+    const int na = pr.coarse.count;
+    std::vector<Box> abox(na);
+    std::vector<bool> seen(na, false);
+    for (int c = 0; c < N; ++c) {
+      const int a = pr.coarse.owner[c];
+      const std::vector<Pt> pts = mesh.cell_points(c);
+      const Box cb = bbox_of(pts.data(), static_cast<int>(pts.size()));
+      if (!seen[a]) {
+        abox[a] = cb;
+        seen[a] = true;
+      } else {
+        abox[a].xmin = std::min(abox[a].xmin, cb.xmin);
+        abox[a].xmax = std::max(abox[a].xmax, cb.xmax);
+        abox[a].ymin = std::min(abox[a].ymin, cb.ymin);
+        abox[a].ymax = std::max(abox[a].ymax, cb.ymax);
+      }
+    }
+    // coarse internal order: ND over the agglomerate graph
+    std::vector<std::vector<int>> anbr(na);
+    for (const Face& f : mesh.interior_faces()) {
+      const int a = pr.coarse.owner[f.cell_in], c2 = pr.coarse.owner[f.cell_out];
+      if (a != c2) {
+        anbr[a].push_back(c2);
+        anbr[c2].push_back(a);
+      }
+    }
+    std::vector<int> ap{0}, aj;
+    std::vector<Pt> apos(na);
+    for (int a = 0; a < na; ++a) {
+      auto& v = anbr[a];
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      aj.insert(aj.end(), v.begin(), v.end());
+      ap.push_back(static_cast<int>(aj.size()));
+      apos[a] = {0.5 * (abox[a].xmin + abox[a].xmax), 0.5 * (abox[a].ymin + abox[a].ymax)};
+    }
+    const NdTree cnd = nested_dissection(na, ap, aj, apos, std::clamp(64 / pr.bq, 4, 16));
+    pr.n_agg = na;
+    pr.agg_order = cnd.order;  // position -> label
+    pr.coarse_nd = cnd;
+    std::vector<int> apos_of(na);
+    for (int i = 0; i < na; ++i) apos_of[cnd.order[i]] = i;
+    // E for local cells and for the halo cells their rows touch
+    const int bq = pr.bq;
+    std::vector<int> need;  // global internal cells needing E
+    {
+      std::vector<char> mark(N, 0);
+      for (int i = 0; i < nloc; ++i)
+        for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1]; ++k) mark[pr.K.col[k]] = 1;
+      for (int g = 0; g < N; ++g)
+        if (mark[g]) need.push_back(g);
+    }
+    std::vector<int> e_slot(N, -1);
+    for (std::size_t k = 0; k < need.size(); ++k) e_slot[need[k]] = static_cast<int>(k);
+    std::vector<double> Eall(need.size() * static_cast<std::size_t>(b) * bq);
+    parallel_for(static_cast<int>(need.size()), [&](int k) {
+      const int c = pr.perm[need[k]];
+      const int a = pr.coarse.owner[c];
+      const std::vector<Pt> poly = mesh.cell_points(c);
+      const Box cb = bbox_of(poly.data(), static_cast<int>(poly.size()));
+      const Rule rule = polygon_rule(poly, order);
+      std::vector<double> mass(static_cast<std::size_t>(b) * b, 0.0), rhs(static_cast<std::size_t>(b) * bq, 0.0);
+      std::vector<double> fv(b), cv(bq);
+      for (std::size_t qp = 0; qp < rule.size(); ++qp) {
+        const double w = rule.w[qp];
+        basis_at(cb, pr.p, rule.pts[qp], fv.data());
+        basis_at(abox[a], pr.q, rule.pts[qp], cv.data());
+        for (int jj = 0; jj < b; ++jj)
+          for (int ii = 0; ii < b; ++ii) mass[jj * b + ii] += w * fv[ii] * fv[jj];
+        for (int m = 0; m < bq; ++m)
+          for (int ii = 0; ii < b; ++ii) rhs[m * b + ii] += w * fv[ii] * cv[m];
+      }
+      spd_solve(b, bq, mass.data(), rhs.data());
+      std::copy(rhs.begin(), rhs.end(), Eall.begin() + static_cast<std::size_t>(k) * b * bq);
+    }, 64);
+    pr.E.resize(static_cast<std::size_t>(nloc) * b * bq);
+    pr.cell_agg.resize(nloc);
+    for (int i = 0; i < nloc; ++i) {
+      const int g = pr.cell_begin + i;
+      std::copy(Eall.begin() + static_cast<std::size_t>(e_slot[g]) * b * bq,
+                Eall.begin() + static_cast<std::size_t>(e_slot[g] + 1) * b * bq,
+                pr.E.begin() + static_cast<std::size_t>(i) * b * bq);
+      pr.cell_agg[i] = apos_of[pr.coarse.owner[pr.perm[g]]];
+    }
+    // agglomerate -> local cells
+    pr.agg_cell_ptr.assign(na + 1, 0);
+    for (int i = 0; i < nloc; ++i) ++pr.agg_cell_ptr[pr.cell_agg[i] + 1];
+    for (int a = 0; a < na; ++a) pr.agg_cell_ptr[a + 1] += pr.agg_cell_ptr[a];
+    pr.agg_cells.resize(nloc);
+    {
+      std::vector<int> fill(pr.agg_cell_ptr.begin(), pr.agg_cell_ptr.end() - 1);
+      for (int i = 0; i < nloc; ++i) pr.agg_cells[fill[pr.cell_agg[i]]++] = i;
+    }
+    // K0 partial over local rows: K0[a,a'] += E_i^T K_ij E_j, coarse internal order
+    Bsr& K0 = pr.K0;
+    K0.rows = na;
+    K0.b = bq;
+    K0.ptr.assign(na + 1, 0);
+    for (int i = 0; i < na; ++i) {
+      const int a = cnd.order[i];
+      std::vector<int> cols{i};
+      for (int nb : anbr[a]) cols.push_back(apos_of[nb]);
+      std::sort(cols.begin(), cols.end());
+      K0.col.insert(K0.col.end(), cols.begin(), cols.end());
+      K0.ptr[i + 1] = static_cast<int>(K0.col.size());
+    }
+    const int bq2 = bq * bq;
+    K0.val.assign(static_cast<std::size_t>(K0.col.size()) * bq2, 0.0);
+    std::vector<double> KE(static_cast<std::size_t>(b) * bq);
+    for (int i = 0; i < nloc; ++i) {
+      const int ai = pr.cell_agg[i];
+      const double* Ei = &pr.E[static_cast<std::size_t>(i) * b * bq];
+      for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1]; ++k) {
+        const int j = pr.K.col[k];
+        const int aj2 = apos_of[pr.coarse.owner[pr.perm[j]]];
+        const double* Ej = &Eall[static_cast<std::size_t>(e_slot[j]) * b * bq];
+        const double* Kb = &pr.K.val[static_cast<std::size_t>(k) * b2];
+        // KE = K_ij E_j  (b x bq)
+        for (int m = 0; m < bq; ++m)
+          for (int r = 0; r < b; ++r) {
+            double s = 0.0;
+            for (int c = 0; c < b; ++c) s += Kb[c * b + r] * Ej[m * b + c];
+            KE[m * b + r] = s;
+          }
+        const int* c0 = K0.col.data() + K0.ptr[ai];
+        const int* c1 = K0.col.data() + K0.ptr[ai + 1];
+        const int blk = static_cast<int>(std::lower_bound(c0, c1, aj2) - K0.col.data());
+        double* out = &K0.val[static_cast<std::size_t>(blk) * bq2];
+        for (int m2 = 0; m2 < bq; ++m2)
+          for (int m1 = 0; m1 < bq; ++m1) {
+            double s = 0.0;
+            for (int r = 0; r < b; ++r) s += Ei[m1 * b + r] * KE[m2 * b + r];
+            out[m2 * bq + m1] += s;
+          }
+      }
+    }
+    if (cfg.world == 1) finish_coarse(pr);
+  }
+  return P;
+}
+
+void finish_coarse(Problem& pr) {
+  if (!pr.two_level) return;
+  // the coarse unit is replicated on every rank; K0 is already in the coarse
+  // nested-dissection position order, so the tree applies directly
+  BlockMatrix Pm;
+  Pm.m = pr.K0.rows;
+  Pm.bs = pr.K0.b;
+  Pm.ptr = pr.K0.ptr;
+  Pm.col = pr.K0.col;
+  Pm.val = pr.K0.val;
+  NdTree tid = pr.coarse_nd;
+  std::iota(tid.order.begin(), tid.order.end(), 0);
+  SupernodalFactor F;
+  try {
+    F = supernodal_cholesky(Pm, tid);
+  } catch (const SolverError&) {
+    throw SolverError("schwarz: coarse operator factorization failed");
+  }
+  // pack coarse tasks (vector set 1: r0 -> y0)
+  const int bs = F.bs;
+  const int base = static_cast<int>(pr.tasks.size());
+  const int nsn = static_cast<int>(F.sn.size());
+  std::vector<std::vector<int>> kids(nsn);
+  for (int s = 0; s < nsn; ++s)
+    if (F.sn[s].parent >= 0) kids[F.sn[s].parent].push_back(s);
+  std::vector<int> height(nsn, 0), depth(nsn, 0);
+  for (int s = 0; s < nsn; ++s)
+    for (int c : kids[s]) height[s] = std::max(height[s], height[c] + 1);
+  for (int s = nsn - 1; s >= 0; --s)
+    if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
+  std::vector<int> slot(nsn);
+  for (int s = 0; s < nsn; ++s) {
+    const Supernode& S = F.sn[s];
+    TaskDesc td;
+    td.coarse = 1;
+    td.bs = bs;
+    td.w = S.w(bs);
+    td.nr = static_cast<int>(S.rows.size()) * bs;
+    td.dof0 = static_cast<std::int64_t>(S.s0) * bs;
+    td.val_off = static_cast<std::int64_t>(pr.fvals.size());
+    pr.fvals.insert(pr.fvals.end(), S.Linv.begin(), S.Linv.end());
+    pr.fvals.insert(pr.fvals.end(), S.B.begin(), S.B.end());
+    td.rows_off = static_cast<int>(pr.row_dof.size());
+    for (int qpos : S.rows) pr.row_dof.push_back(static_cast<std::int64_t>(qpos) * bs);
+    td.ubuf_off = pr.ubuf_size;
+    pr.ubuf_size += td.nr;
+    td.parent = S.parent >= 0 ? base + S.parent : -1;
+    td.child_off = static_cast<int>(pr.task_child.size());
+    for (int c : kids[s]) pr.task_child.push_back(base + c);
+    td.n_child = static_cast<int>(kids[s].size());
+    td.height = height[s];
+    td.depth = depth[s];
+    slot[s] = static_cast<int>(pr.in_ptr.size()) - 1;
+    td.in_off = slot[s];
+    for (int cc = S.s0; cc < S.s1; ++cc) pr.in_ptr.push_back(pr.in_ptr.back());
+    pr.tasks.push_back(td);
+  }
+  std::vector<std::vector<std::int64_t>> inc(F.m);
+  for (int d = 0; d < nsn; ++d) {
+    const Supernode& D = F.sn[d];
+    for (std::size_t k = 0; k < D.rows.size(); ++k)
+      inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
+  }
+  for (int s = 0; s < nsn; ++s) {
+    const Supernode& S = F.sn[s];
+    int at = slot[s];
+    for (int cc = S.s0; cc < S.s1; ++cc) {
+      pr.in_idx.insert(pr.in_idx.end(), inc[cc].begin(), inc[cc].end());
+      pr.in_ptr[at + 1] = static_cast<int>(pr.in_idx.size());
+      ++at;
+    }
+  }
+  pr.factor_values += F.values();
+}
+
+}  // namespace pdg

@@ -1,0 +1,105 @@
+// Host-side problem setup: config -> mesh -> partitions -> internal ordering
+// -> assembly (BSR) -> Schwarz factors -> coarse space, packed as flat
+// arrays ("device image") that the CUDA side uploads once.
+//
+// Mirrors the setup half of Simulation::Simulation
+// (/root/reference/proj/src/timestepper.cpp:67-126) with the BASELINE.json
+// extensions (multi-cell subdomains, explicit coarse count, per-element
+// fibres). K_h is time-independent (timestepper.hpp:113-115), so everything
+// here runs once.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "../../../include/polydg_b200.h"
+#include "factor.hpp"
+#include "mesh.hpp"
+
+namespace pdg {
+
+// Block-sparse rows over internal cells. Block (row i, col j) at
+// val[k*b*b + c*b + r] = entry (r, c) (column-major blocks).
+struct Bsr {
+  int rows = 0, b = 0;
+  std::vector<int> ptr, col;
+  std::vector<double> val;
+};
+
+// One supernode task of the device sweep (fine subdomain or coarse problem).
+struct TaskDesc {
+  int coarse = 0;      // 0 = fine vector set (r -> z), 1 = coarse (r0 -> y0)
+  int bs = 0;          // block size of this unit
+  int w = 0;           // supernode columns (cells * bs)
+  int nr = 0;          // below rows (|R| * bs)
+  std::int64_t dof0 = 0;    // first dof of the supernode in its vector
+  std::int64_t val_off = 0; // Linv (w(w+1)/2) then B (nr*w)
+  int rows_off = 0;    // R cell dof-starts in row_dof[rows_off .. + nr/bs)
+  std::int64_t ubuf_off = 0;  // update buffer slot (nr doubles)
+  int in_off = 0;      // incoming CSR: in_ptr[in_off .. in_off + w/bs]
+  int parent = -1;     // task id (ND parent), -1 = root
+  int child_off = 0, n_child = 0;  // children ids in task_child[]
+  int height = 0, depth = 0;
+};
+
+struct Problem {
+  pdg_config cfg{};
+  Mesh mesh;
+  int p = 1, b = 3, q = 1, bq = 3;
+  Partition sub, coarse;  // subdomain / coarse partitions (reference cell ids)
+  bool two_level = false, has_precond = false;
+
+  // internal order
+  std::vector<int> perm, iperm;  // internal -> reference cell, inverse
+  int cell_begin = 0, cell_end = 0;   // this rank's internal cell range
+  std::vector<int> rank_cell_start;   // world+1
+
+  // operators (local rows, global internal columns)
+  Bsr K, A;                  // A kept only when keep_matrices
+  std::vector<double> M;     // local diag mass blocks (b*b each, column-major)
+  std::vector<double> Minv;  // inverses
+  bool keep_matrices = true;
+
+  // Schwarz local solves
+  std::vector<TaskDesc> tasks;
+  std::vector<int> task_child, fwd_order, bwd_order;
+  std::vector<double> fvals;     // all Linv/B values
+  std::vector<std::int64_t> row_dof;  // below-row cell dof starts
+  std::vector<int> in_ptr;       // incoming CSR (per supernode cell slot)
+  std::vector<std::int64_t> in_idx;   // ubuf offsets
+  std::int64_t ubuf_size = 0;
+  int n_fine_tasks = 0;
+
+  // coarse space: per local cell E block (b x bq, column-major) and coarse dof start
+  std::vector<double> E;
+  std::vector<int> cell_agg;            // local cell -> coarse internal node
+  std::vector<int> agg_cell_ptr, agg_cells;  // coarse node -> local cells (for E^T r)
+  int n_agg = 0;                        // coarse nodes
+  std::vector<int> agg_order;           // coarse internal node -> coarse label
+  NdTree coarse_nd;                     // coarse supernode tree (positions)
+  Bsr K0;                               // coarse matrix in coarse internal order
+  std::int64_t factor_values = 0;
+
+  // ionic geometry per local cell: bbox (4) and fan triangles
+  std::vector<double> bbox;
+  std::vector<int> tri_ptr;
+  std::vector<double> tri;   // 6 doubles per triangle
+  std::vector<double> gl_x, gl_w;  // 1-D Gauss nodes for the volume rule
+
+  // initial state (local, internal order)
+  std::vector<double> U0;
+  std::vector<double> Y0;    // n_comp fields
+  int n_comp = 0;
+
+  std::int64_t n_local_dofs() const { return static_cast<std::int64_t>(cell_end - cell_begin) * b; }
+  std::int64_t n_global_dofs() const { return static_cast<std::int64_t>(mesh.n_cells()) * b; }
+};
+
+void validate_config(const pdg_config& cfg);
+std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
+// coarse factorisation + task packing; split out so a multi-rank run can sum
+// K0 partials before factorising.
+void finish_coarse(Problem& P);
+
+}  // namespace pdg
