@@ -1,0 +1,63 @@
+// Device-side shared definitions for the sm_100a solver kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../capi_internal.hpp"
+
+#define PDG_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::pdg::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+namespace pdg {
+
+// One supernode of the Schwarz sweep (see host/problem.hpp TaskDesc).
+struct DevTask {
+  int coarse, bs, w, nr;
+  long long dof0, val_off, ubuf_off;
+  int rows_off, in_off, parent, child_off, n_child, pad;
+};
+
+// Scalars of one PCG solve, resident in device memory. The iteration index,
+// convergence and breakdown are decided on the device so the host only polls.
+struct PcgScalars {
+  double rho;      // r.z of the current iterate
+  double denom;    // ||b - K x0||
+  double tol;
+  double pq;
+  double rr;
+  double alpha, beta;
+  int iter;        // completed iterations
+  int maxit;
+  int stop;        // 1 = no more work this solve
+  int converged;
+  int error;       // PcgError
+  int pad;
+};
+
+enum PcgError : int {
+  kPcgOk = 0,
+  kPcgRhoNonFinite0 = 1,  // "non-finite preconditioned product"
+  kPcgRhoNonPos0 = 2,     // "preconditioner is not positive definite"
+  kPcgPqNonFinite = 3,    // "non-finite operator product"
+  kPcgPqNonPos = 4,       // "operator is not positive definite"
+  kPcgRhoNonFinite = 5,   // "non-finite scalar"
+  kPcgRhoNonPos = 6,      // "preconditioner is not positive definite"
+};
+
+// Reduction scratch: per-CTA partials + arrival counter (last block finalises).
+struct Reducer {
+  double* partial;
+  unsigned int* counter;
+};
+
+constexpr int kSweepThreads = 256;
+constexpr int kVecThreads = 256;
+
+}  // namespace pdg

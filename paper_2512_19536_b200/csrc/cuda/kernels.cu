@@ -1,0 +1,752 @@
+// sm_100a kernels of the per-step solve. Reference hot loops replaced
+// (SURVEY.md §2.1):
+//   K1/K2 SpMV + fused dot / CN rhs      krylov.hpp:26, timestepper.cpp:148
+//   K3/K4 PCG vector updates             krylov.cpp:54-71
+//   K5    Schwarz local solves           schwarz.cpp:155-164
+//   K6/K8 coarse restriction/prolong.    schwarz.cpp:166-167
+//   K7    coarse solve (same sweep)      schwarz.cpp:167
+//   K9-11 ionic terms, stimulus, Y update ionics.cpp:61-113, timestepper.cpp:128-186
+// Reductions are deterministic: fixed per-CTA trees, partials summed in index
+// order by the last CTA to arrive, so reruns are bit-identical (the
+// reference's determinism contract, parallel.hpp:14-16).
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace pdg {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;  // lane 0
+}
+
+// blockDim.x must be a multiple of 32; result valid in thread 0.
+__device__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < static_cast<int>(blockDim.x >> 5) ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ void apply_finish(const ReduceCtx& rc, double s) {
+  PcgScalars* S = rc.S;
+  auto fail = [&](int e) {
+    S->error = e;
+    S->stop = 1;
+  };
+  switch (rc.finish) {
+    case kFinPq:
+      S->pq = s;
+      break;
+    case kFinDenom: {
+      const double d = sqrt(s);
+      S->denom = d;
+      if (d == 0.0) {
+        S->converged = 1;
+        S->stop = 1;
+        rc.H.resid[0] = 0.0;
+      }
+      break;
+    }
+    case kFinRr: {
+      const int it = S->iter;
+      const double rel = sqrt(s) / S->denom;
+      rc.H.resid[it] = rel;
+      S->rr = s;
+      S->iter = it + 1;
+      if (rel < S->tol) {
+        S->converged = 1;
+        S->stop = 1;
+      }
+      break;
+    }
+    case kFinRzInit:
+      if (!isfinite(s)) fail(kPcgRhoNonFinite0);
+      else if (s <= 0.0) fail(kPcgRhoNonPos0);
+      else S->rho = s;
+      if (S->maxit <= 0) S->stop = 1;
+      break;
+    case kFinRz:
+      if (!isfinite(s)) {
+        fail(kPcgRhoNonFinite);
+      } else if (s <= 0.0) {
+        fail(kPcgRhoNonPos);
+      } else {
+        const double beta = s / S->rho;
+        rc.H.beta[S->iter - 1] = beta;
+        S->beta = beta;
+        S->rho = s;
+        if (S->iter >= S->maxit) S->stop = 1;
+      }
+      break;
+    case kFinStore:
+      *rc.out = s;
+      break;
+    default:
+      break;
+  }
+}
+
+// Publishes this CTA's partial; the last CTA sums all partials in index order.
+__device__ void grid_finish(double block_total, const ReduceCtx& rc) {
+  __shared__ int is_last;
+  if (threadIdx.x == 0) {
+    rc.red.partial[blockIdx.x] = block_total;
+    __threadfence();
+    const unsigned t = atomicAdd(rc.red.counter, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) s += __ldcg(rc.red.partial + i);
+  s = block_sum(s);
+  if (threadIdx.x == 0) {
+    *rc.red.counter = 0u;
+    apply_finish(rc, s);
+  }
+}
+
+template <int B>
+struct RowGeom {
+  static constexpr int kRows = 256 / B;
+  static constexpr int kThreads = ((kRows * B + 31) / 32) * 32;
+};
+
+// One thread per scalar row r of block-row `row`; blocks column-major so the
+// B threads of a block-row read B consecutive doubles per column step.
+template <int B>
+__device__ __forceinline__ double bsr_row_dot(int row, int r, const int* __restrict__ ptr,
+                                              const int* __restrict__ col,
+                                              const double* __restrict__ val,
+                                              const double* __restrict__ x) {
+  double acc0 = 0.0, acc1 = 0.0;
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  for (int k = k0; k < k1; ++k) {
+    const int c = __ldg(col + k);
+    const double* blk = val + static_cast<long long>(k) * (B * B) + r;
+    const double* xb = x + static_cast<long long>(c) * B;
+#pragma unroll
+    for (int cc = 0; cc < B; cc += 2) {
+      acc0 = fma(__ldg(blk + cc * B), __ldg(xb + cc), acc0);
+      if (cc + 1 < B) acc1 = fma(__ldg(blk + (cc + 1) * B), __ldg(xb + cc + 1), acc1);
+    }
+  }
+  return acc0 + acc1;
+}
+
+template <int B>
+__global__ void __launch_bounds__(RowGeom<B>::kThreads)
+    spmv_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+  if (honor_stop && rc.S->stop) return;
+  const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
+  const int row = blockIdx.x * RowGeom<B>::kRows + lr;
+  double contrib = 0.0;
+  if (lr < RowGeom<B>::kRows && row < rows) {
+    const double acc = bsr_row_dot<B>(row, r, ptr, col, val, x);
+    const long long i = static_cast<long long>(row) * B + r;
+    y[i] = acc;
+    if (dotw) contrib = dotw[i] * acc;
+  }
+  if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
+}
+
+template <int B>
+__global__ void __launch_bounds__(RowGeom<B>::kThreads)
+    residual_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
+                    const double* __restrict__ val, const double* __restrict__ x,
+                    const double* __restrict__ bvec, double* __restrict__ rvec, ReduceCtx rc) {
+  const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
+  const int row = blockIdx.x * RowGeom<B>::kRows + lr;
+  double contrib = 0.0;
+  if (lr < RowGeom<B>::kRows && row < rows) {
+    const double acc = bsr_row_dot<B>(row, r, ptr, col, val, x);
+    const long long i = static_cast<long long>(row) * B + r;
+    const double v = bvec[i] - acc;
+    rvec[i] = v;
+    contrib = v * v;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
+template <int B>
+__global__ void __launch_bounds__(RowGeom<B>::kThreads)
+    rhs_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
+               const double* __restrict__ val, const double* __restrict__ M, double two_a,
+               const double* __restrict__ U, const double* __restrict__ ion, int warm,
+               double* __restrict__ rhs, double* __restrict__ x, double* __restrict__ rvec,
+               ReduceCtx rc) {
+  const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
+  const int row = blockIdx.x * RowGeom<B>::kRows + lr;
+  double contrib = 0.0;
+  if (lr < RowGeom<B>::kRows && row < rows) {
+    const double ku = bsr_row_dot<B>(row, r, ptr, col, val, U);
+    const double* mb = M + static_cast<long long>(row) * (B * B) + r;
+    const double* ub = U + static_cast<long long>(row) * B;
+    double mu = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < B; ++cc) mu = fma(__ldg(mb + cc * B), __ldg(ub + cc), mu);
+    const long long i = static_cast<long long>(row) * B + r;
+    double b = two_a * mu - ku;
+    if (ion) b += ion[i];
+    rhs[i] = b;
+    const double rv = warm ? b - ku : b;
+    x[i] = warm ? ub[r] : 0.0;
+    rvec[i] = rv;
+    contrib = rv * rv;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
+__global__ void update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
+                              const double* __restrict__ p, const double* __restrict__ q,
+                              ReduceCtx rc) {
+  PcgScalars* S = rc.S;
+  if (S->stop) return;
+  const double pq = S->pq;
+  const int it = S->iter;
+  if (!isfinite(pq) || pq <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S->error = !isfinite(pq) ? kPcgPqNonFinite : kPcgPqNonPos;
+      S->stop = 1;
+    }
+    return;
+  }
+  const double alpha = S->rho / pq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rc.H.alpha[it] = alpha;
+    S->alpha = alpha;
+  }
+  double contrib = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    x[i] += alpha * p[i];
+    const double rv = r[i] - alpha * q[i];
+    r[i] = rv;
+    contrib += rv * rv;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
+__global__ void pupdate_kernel(long long n, double* __restrict__ p, const double* __restrict__ z,
+                               const PcgScalars* S, int first) {
+  if (!first && S->stop) return;
+  const double beta = first ? 0.0 : S->beta;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+template <int B, int BQ>
+__global__ void prolong_dot_kernel(int ncells, const double* __restrict__ E,
+                                   const int* __restrict__ cell_agg, const double* __restrict__ y0,
+                                   const double* __restrict__ r, double* __restrict__ z,
+                                   ReduceCtx rc) {
+  if (rc.S->stop) return;
+  const long long n = static_cast<long long>(ncells) * B;
+  double contrib = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double zi = z[i];
+    if constexpr (BQ > 0) {
+      const long long c = i / B;
+      const int rr = static_cast<int>(i - c * B);
+      const double* e = E + c * (B * BQ) + rr;
+      const double* y = y0 + static_cast<long long>(__ldg(cell_agg + c)) * BQ;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < BQ; ++m) acc = fma(__ldg(e + m * B), __ldg(y + m), acc);
+      zi += acc;
+      z[i] = zi;
+    }
+    contrib += r[i] * zi;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
+template <int B, int BQ>
+__global__ void restrict_kernel(const int* __restrict__ agg_ptr, const int* __restrict__ agg_cells,
+                                const double* __restrict__ E, const double* __restrict__ r,
+                                double* __restrict__ r0, const PcgScalars* S) {
+  if (S && S->stop) return;
+  const int a = blockIdx.x;
+  const int c0 = agg_ptr[a], c1 = agg_ptr[a + 1];
+  double acc[BQ];
+#pragma unroll
+  for (int m = 0; m < BQ; ++m) acc[m] = 0.0;
+  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const long long c = agg_cells[k];
+    const double* e = E + c * (B * BQ);
+    const double* rc = r + c * B;
+    double rl[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) rl[i] = rc[i];
+#pragma unroll
+    for (int m = 0; m < BQ; ++m) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < B; ++i) s = fma(__ldg(e + m * B + i), rl[i], s);
+      acc[m] += s;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < BQ; ++m) {
+    const double s = block_sum(acc[m]);
+    if (threadIdx.x == 0) r0[static_cast<long long>(a) * BQ + m] = s;
+  }
+}
+
+// ---------------- Schwarz supernode sweeps (sync-free, ticketed) ----------------
+
+__device__ __forceinline__ long long col_start(int j, int w) {
+  return static_cast<long long>(j) * w - static_cast<long long>(j) * (j - 1) / 2;
+}
+
+__global__ void __launch_bounds__(kSweepThreads) sweep_fwd_kernel(SweepArgs a) {
+  if (a.S && a.S->stop) return;
+  extern __shared__ double sm[];
+  __shared__ int s_task;
+  if (threadIdx.x == 0) s_task = a.order[atomicAdd(a.ticket, 1u)];
+  __syncthreads();
+  const int tid = s_task;
+  const DevTask T = a.tasks[tid];
+  if (threadIdx.x == 0)
+    for (int k = 0; k < T.n_child; ++k) {
+      const int c = a.task_child[T.child_off + k];
+      while (ld_acquire(a.flags + c) == 0) __nanosleep(64);
+    }
+  __syncthreads();
+  const double* in = T.coarse ? a.r0 : a.r;
+  double* out = T.coarse ? a.y0 : a.z;
+  const int w = T.w, nr = T.nr, bs = T.bs;
+  double* t = sm;
+  double* y = sm + w;
+  for (int i = threadIdx.x; i < w; i += blockDim.x) {
+    const int cell = i / bs, rr = i - cell * bs;
+    double v = in[T.dof0 + i];
+    const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
+    for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
+    t[i] = v;
+  }
+  __syncthreads();
+  const double* Linv = a.vals + T.val_off;
+  for (int i = threadIdx.x; i < w; i += blockDim.x) {
+    double acc0 = 0.0, acc1 = 0.0;
+    long long p = i;  // col_start(0) + i - 0
+    int j = 0;
+    for (; j + 1 <= i; j += 2) {
+      acc0 = fma(__ldg(Linv + p), t[j], acc0);
+      p += w - j - 1;
+      acc1 = fma(__ldg(Linv + p), t[j + 1], acc1);
+      p += w - j - 2;
+    }
+    if (j <= i) acc0 = fma(__ldg(Linv + p), t[j], acc0);
+    const double v = acc0 + acc1;
+    y[i] = v;
+    out[T.dof0 + i] = v;
+  }
+  __syncthreads();
+  if (nr > 0) {
+    const double* Bm = Linv + static_cast<long long>(w) * (w + 1) / 2;
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+      double acc0 = 0.0, acc1 = 0.0;
+      int j = 0;
+      for (; j + 1 < w; j += 2) {
+        acc0 = fma(__ldg(Bm + static_cast<long long>(j) * nr + k), y[j], acc0);
+        acc1 = fma(__ldg(Bm + static_cast<long long>(j + 1) * nr + k), y[j + 1], acc1);
+      }
+      if (j < w) acc0 = fma(__ldg(Bm + static_cast<long long>(j) * nr + k), y[j], acc0);
+      a.ubuf[T.ubuf_off + k] = acc0 + acc1;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(a.flags + tid, 1);
+}
+
+__global__ void __launch_bounds__(kSweepThreads) sweep_bwd_kernel(SweepArgs a) {
+  if (a.S && a.S->stop) return;
+  extern __shared__ double sm[];
+  __shared__ int s_task;
+  if (threadIdx.x == 0) s_task = a.order[atomicAdd(a.ticket, 1u)];
+  __syncthreads();
+  const int tid = s_task;
+  const DevTask T = a.tasks[tid];
+  if (threadIdx.x == 0 && T.parent >= 0)
+    while (ld_acquire(a.flags + T.parent) == 0) __nanosleep(64);
+  __syncthreads();
+  double* out = T.coarse ? a.y0 : a.z;
+  const int w = T.w, nr = T.nr, bs = T.bs;
+  double* s = sm;
+  double* xr = sm + w;
+  for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+    const int cell = k / bs, rr = k - cell * bs;
+    xr[k] = __ldcg(out + a.row_dof[T.rows_off + cell] + rr);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const double* Linv = a.vals + T.val_off;
+  const double* Bm = Linv + static_cast<long long>(w) * (w + 1) / 2;
+  for (int j = warp; j < w; j += nwarp) {
+    double acc = 0.0;
+    const double* colj = Bm + static_cast<long long>(j) * nr;
+    for (int k = lane; k < nr; k += 32) acc = fma(__ldg(colj + k), xr[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) s[j] = __ldcg(out + T.dof0 + j) - acc;
+  }
+  __syncthreads();
+  for (int j = warp; j < w; j += nwarp) {
+    double acc = 0.0;
+    const double* colj = Linv + col_start(j, w);
+    for (int i = j + lane; i < w; i += 32) acc = fma(__ldg(colj + (i - j)), s[i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[T.dof0 + j] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(a.flags + tid, 1);
+}
+
+// ---------------- ionic terms at quadrature nodes ----------------
+
+__constant__ double c_glx[16];
+__constant__ double c_glw[16];
+
+template <int P>
+__device__ __forceinline__ void basis_eval(double xi, double eta, double inv, double* phi) {
+  double px[P + 1], py[P + 1];
+  px[0] = 1.0;
+  py[0] = 1.0;
+  px[1] = xi;
+  py[1] = eta;
+#pragma unroll
+  for (int k = 1; k < P; ++k) {
+    px[k + 1] = ((2 * k + 1) * xi * px[k] - k * px[k - 1]) / (k + 1);
+    py[k + 1] = ((2 * k + 1) * eta * py[k] - k * py[k - 1]) / (k + 1);
+  }
+  int m = 0;
+#pragma unroll
+  for (int d = 0; d <= P; ++d)
+#pragma unroll
+    for (int ax = d; ax >= 0; --ax, ++m) {
+      const int ay = d - ax;
+      phi[m] = inv * (sqrt(2.0 * ax + 1.0) * px[ax]) * (sqrt(2.0 * ay + 1.0) * py[ay]);
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) ionic_kernel(IonicArgs a) {
+  constexpr int B = (P + 1) * (P + 2) / 2;
+  __shared__ double sc[8][4 * B];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 8 + wl;
+  if (c >= a.ncells) return;
+  const long long o = static_cast<long long>(c) * B;
+  double* Us = sc[wl];          // extrapolated U*
+  double* Ys = sc[wl] + B;      // extrapolated Y*
+  double* Uc = sc[wl] + 2 * B;  // current U
+  double* Yc = sc[wl] + 3 * B;  // current Y
+  const bool model = a.model != 0 && a.n_comp > 0;
+  for (int k = lane; k < B; k += 32) {
+    const double u = a.U[o + k];
+    Uc[k] = u;
+    Us[k] = a.has_prev ? 2.0 * u - a.Up[o + k] : u;
+    if (model) {
+      const double y = a.Y[o + k];
+      Yc[k] = y;
+      Ys[k] = a.has_prev ? 2.0 * y - a.Yp[o + k] : y;
+    }
+  }
+  __syncwarp();
+  const double bx0 = a.bbox[4 * c], by0 = a.bbox[4 * c + 1], bx1 = a.bbox[4 * c + 2], by1 = a.bbox[4 * c + 3];
+  const double wx = bx1 - bx0, wy = by1 - by0;
+  const double inv = 1.0 / sqrt(wx * wy);
+  const int t0 = a.tri_ptr[c], t1 = a.tri_ptr[c + 1];
+  const int ng = a.ngl, npt = (t1 - t0) * ng * ng;
+  double accI[B], accF[B], accG[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) accI[k] = accF[k] = accG[k] = 0.0;
+  const double span = a.fhn[6] - a.fhn[5];
+  int flag = 0;
+  for (int pidx = lane; pidx < npt; pidx += 32) {
+    const int tri = pidx / (ng * ng), rem = pidx - tri * ng * ng;
+    const int i = rem / ng, j = rem - i * ng;
+    const double* T = a.tri + static_cast<long long>(t0 + tri) * 6;
+    const double ax = T[0], ay = T[1], bxx = T[2], byy = T[3], cx = T[4], cy = T[5];
+    const double s = 0.5 * (c_glx[i] + 1.0), tt = 0.5 * (c_glx[j] + 1.0);
+    const double eta = tt * (1.0 - s);
+    const double area2 = (bxx - ax) * (cy - ay) - (byy - ay) * (cx - ax);
+    const double px = ax + (bxx - ax) * s + (cx - ax) * eta;
+    const double py = ay + (byy - ay) * s + (cy - ay) * eta;
+    const double w = c_glw[i] * c_glw[j] * 0.25 * (1.0 - s) * area2;
+    double phi[B];
+    basis_eval<P>((2.0 * px - bx0 - bx1) / wx, (2.0 * py - by0 - by1) / wy, inv, phi);
+    if (model) {
+      double us = 0.0, ys = 0.0, uc = 0.0, yc = 0.0;
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        us = fma(Us[k], phi[k], us);
+        ys = fma(Ys[k], phi[k], ys);
+        uc = fma(Uc[k], phi[k], uc);
+        yc = fma(Yc[k], phi[k], yc);
+      }
+      if (!isfinite(us) || !isfinite(ys) || !isfinite(uc) || !isfinite(yc)) flag |= 2;
+      const double slack = 10.0 * span;
+      if (us < a.fhn[5] - slack || us > a.fhn[6] + slack || uc < a.fhn[5] - slack || uc > a.fhn[6] + slack)
+        flag |= 1;
+      // FitzHugh-Nagumo, Rogers-McCulloch form (ionics.cpp:20-33)
+      const double v = (us - a.fhn[5]) / span;
+      const double f = a.fhn[7] * (a.fhn[2] * v * (v - a.fhn[0]) * (v - 1.0) + a.fhn[3] * v * ys) * span;
+      const double vc = (uc - a.fhn[5]) / span;
+      const double m = -a.fhn[1] * (vc - a.fhn[4] * yc);
+      const double wf = w * f, wm = w * m;
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        accI[k] = fma(wf, phi[k], accI[k]);
+        accG[k] = fma(wm, phi[k], accG[k]);
+      }
+    }
+    if (a.stim != 0) {
+      double g = 0.0;
+      if (a.stim == 1)
+        g = (px < a.stim_p[1] && a.t_mid < a.stim_p[2]) ? a.stim_p[0] : 0.0;
+      else
+        g = a.stim_p[0] * cos(M_PI * px) * cos(M_PI * py) * exp(-a.stim_p[1] * a.t_mid);
+      const double wg = w * g;
+#pragma unroll
+      for (int k = 0; k < B; ++k) accF[k] = fma(wg, phi[k], accF[k]);
+    }
+  }
+  // warp reductions (lane 0 holds the sums), broadcast through shared memory
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    accI[k] = warp_sum(accI[k]);
+    accF[k] = warp_sum(accF[k]);
+    accG[k] = warp_sum(accG[k]);
+  }
+  flag = __reduce_or_sync(0xffffffffu, flag);
+  if (lane == 0) {
+    if (flag) atomicOr(a.flags, flag);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      a.ion[o + k] = -(a.chi * a.dt) * accI[k] + a.dt * accF[k];
+      Us[k] = accG[k];  // reuse as G
+    }
+  }
+  __syncwarp();
+  if (model) {
+    const double* Mi = a.Minv + static_cast<long long>(c) * B * B;
+    for (int k = lane; k < B; k += 32) {
+      double acc = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) acc = fma(Mi[jj * B + k], Us[jj], acc);
+      a.Ynext[o + k] = Yc[k] - a.dt * acc;
+    }
+  }
+}
+
+__global__ void gather_perm_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                   const int* __restrict__ perm, int ncells, int b, int nfields,
+                                   long long ss, long long sd) {
+  const long long n = static_cast<long long>(ncells) * b;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = i / b;
+    const int r = static_cast<int>(i - c * b);
+    const long long s = static_cast<long long>(perm[c]) * b + r;
+    for (int f = 0; f < nfields; ++f) dst[f * sd + i] = src[f * ss + s];
+  }
+}
+
+__global__ void scatter_perm_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                    const int* __restrict__ perm, int ncells, int b, int nfields,
+                                    long long ss, long long sd) {
+  const long long n = static_cast<long long>(ncells) * b;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = i / b;
+    const int r = static_cast<int>(i - c * b);
+    const long long d = static_cast<long long>(perm[c]) * b + r;
+    for (int f = 0; f < nfields; ++f) dst[f * sd + d] = src[f * ss + i];
+  }
+}
+
+int vec_grid(long long n) {
+  long long g = (n + kVecThreads - 1) / kVecThreads;
+  if (g > 148 * 16) g = 148 * 16;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+#define PDG_B_DISPATCH(b, MACRO) \
+  switch (b) {                   \
+    case 3: MACRO(3); break;     \
+    case 6: MACRO(6); break;     \
+    case 10: MACRO(10); break;   \
+    case 15: MACRO(15); break;   \
+    case 21: MACRO(21); break;   \
+    case 28: MACRO(28); break;   \
+    default: throw CudaError("unsupported block size"); \
+  }
+
+void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val, const double* x,
+                 double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
+#define L(B)                                                                                  \
+  {                                                                                           \
+    const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \
+    spmv_kernel<B><<<g, RowGeom<B>::kThreads, 0, st>>>(rows, ptr, col, val, x, y, dotw, rc,   \
+                                                       honor_stop ? 1 : 0);                   \
+  }
+  if (rows > 0) PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+void launch_residual(int b, int rows, const int* ptr, const int* col, const double* val,
+                     const double* x, const double* bvec, double* r, ReduceCtx rc, cudaStream_t st) {
+#define L(B)                                                                                  \
+  {                                                                                           \
+    const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \
+    residual_kernel<B><<<g, RowGeom<B>::kThreads, 0, st>>>(rows, ptr, col, val, x, bvec, r, rc); \
+  }
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+void launch_rhs(int b, int rows, const int* ptr, const int* col, const double* val, const double* M,
+                double two_a, const double* U, const double* ion, int warm, double* rhs, double* x,
+                double* r, ReduceCtx rc, cudaStream_t st) {
+#define L(B)                                                                                   \
+  {                                                                                            \
+    const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                          \
+    rhs_kernel<B><<<g, RowGeom<B>::kThreads, 0, st>>>(rows, ptr, col, val, M, two_a, U, ion,   \
+                                                      warm, rhs, x, r, rc);                    \
+  }
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+void launch_update(long long n, double* x, double* r, const double* p, const double* q, ReduceCtx rc,
+                   cudaStream_t st) {
+  update_kernel<<<vec_grid(n), kVecThreads, 0, st>>>(n, x, r, p, q, rc);
+}
+
+void launch_pupdate(long long n, double* p, const double* z, const PcgScalars* S, bool first,
+                    cudaStream_t st) {
+  pupdate_kernel<<<vec_grid(n), kVecThreads, 0, st>>>(n, p, z, S, first ? 1 : 0);
+}
+
+template <int B>
+static void prolong_dispatch(int bq, int ncells, const double* E, const int* cell_agg,
+                             const double* y0, const double* r, double* z, ReduceCtx rc,
+                             cudaStream_t st) {
+  const int g = vec_grid(static_cast<long long>(ncells) * B);
+  switch (bq) {
+    case 0: prolong_dot_kernel<B, 0><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break;
+    case 3: prolong_dot_kernel<B, 3><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break;
+    case 6: if constexpr (B >= 6) { prolong_dot_kernel<B, 6><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    [[fallthrough]];
+    case 10: if constexpr (B >= 10) { prolong_dot_kernel<B, 10><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    [[fallthrough]];
+    case 15: if constexpr (B >= 15) { prolong_dot_kernel<B, 15><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    [[fallthrough]];
+    default: throw CudaError("unsupported coarse block size");
+  }
+}
+
+void launch_prolong_dot(int b, int bq, int ncells, const double* E, const int* cell_agg,
+                        const double* y0, const double* r, double* z, ReduceCtx rc, cudaStream_t st) {
+#define L(B) prolong_dispatch<B>(bq, ncells, E, cell_agg, y0, r, z, rc, st)
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+template <int B>
+static void restrict_dispatch(int bq, int n_agg, const int* agg_ptr, const int* agg_cells,
+                              const double* E, const double* r, double* r0, const PcgScalars* S,
+                              cudaStream_t st) {
+  switch (bq) {
+    case 3: restrict_kernel<B, 3><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break;
+    case 6: if constexpr (B >= 6) { restrict_kernel<B, 6><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    [[fallthrough]];
+    case 10: if constexpr (B >= 10) { restrict_kernel<B, 10><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    [[fallthrough]];
+    case 15: if constexpr (B >= 15) { restrict_kernel<B, 15><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    [[fallthrough]];
+    default: throw CudaError("unsupported coarse block size");
+  }
+}
+
+void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* agg_cells,
+                     const double* E, const double* r, double* r0, const PcgScalars* S, cudaStream_t st) {
+#define L(B) restrict_dispatch<B>(bq, n_agg, agg_ptr, agg_cells, E, r, r0, S, st)
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+void launch_sweep_fwd(const SweepArgs& a, int smem, cudaStream_t st) {
+  if (a.n_tasks == 0) return;
+  sweep_fwd_kernel<<<a.n_tasks, kSweepThreads, smem, st>>>(a);
+}
+void launch_sweep_bwd(const SweepArgs& a, int smem, cudaStream_t st) {
+  if (a.n_tasks == 0) return;
+  sweep_bwd_kernel<<<a.n_tasks, kSweepThreads, smem, st>>>(a);
+}
+
+void set_sweep_smem(int bytes) {
+  PDG_CUDA(cudaFuncSetAttribute(sweep_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void set_gauss_nodes(const double* x, const double* w, int n) {
+  PDG_CUDA(cudaMemcpyToSymbol(c_glx, x, sizeof(double) * n));
+  PDG_CUDA(cudaMemcpyToSymbol(c_glw, w, sizeof(double) * n));
+}
+
+void launch_ionic(const IonicArgs& a, cudaStream_t st) {
+  const int g = (a.ncells + 7) / 8;
+  if (a.ncells == 0) return;
+  switch (a.p) {
+    case 1: ionic_kernel<1><<<g, 256, 0, st>>>(a); break;
+    case 2: ionic_kernel<2><<<g, 256, 0, st>>>(a); break;
+    case 3: ionic_kernel<3><<<g, 256, 0, st>>>(a); break;
+    case 4: ionic_kernel<4><<<g, 256, 0, st>>>(a); break;
+    case 5: ionic_kernel<5><<<g, 256, 0, st>>>(a); break;
+    case 6: ionic_kernel<6><<<g, 256, 0, st>>>(a); break;
+    default: throw CudaError("unsupported degree for the ionic kernel");
+  }
+}
+
+void launch_gather_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nf,
+                        long long ss, long long sd, cudaStream_t st) {
+  gather_perm_kernel<<<vec_grid(static_cast<long long>(ncells) * b), kVecThreads, 0, st>>>(src, dst, perm, ncells, b, nf, ss, sd);
+}
+void launch_scatter_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nf,
+                         long long ss, long long sd, cudaStream_t st) {
+  scatter_perm_kernel<<<vec_grid(static_cast<long long>(ncells) * b), kVecThreads, 0, st>>>(src, dst, perm, ncells, b, nf, ss, sd);
+}
+
+}  // namespace pdg

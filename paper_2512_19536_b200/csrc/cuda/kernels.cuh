@@ -1,0 +1,111 @@
+// Launch wrappers for the sm_100a kernels (kernels.cu). All FP64; the whole
+// per-step path is HBM-bound, so the kernels are organised around one
+// coalesced pass over each operand.
+#pragma once
+
+#include "common.cuh"
+
+namespace pdg {
+
+struct PcgHist {
+  double* resid;
+  double* alpha;
+  double* beta;
+};
+
+// What the last CTA does with a grid-wide deterministic sum.
+enum Finish : int {
+  kFinNone = 0,
+  kFinPq = 1,      // S->pq = sum
+  kFinDenom = 2,   // S->denom = sqrt(sum); zero -> converged with 0 iterations
+  kFinRr = 3,      // residual history, iteration count, convergence
+  kFinRzInit = 4,  // first rho with breakdown checks
+  kFinRz = 5,      // rho_next, beta, maxit
+  kFinStore = 6,   // *out = sum
+};
+
+struct ReduceCtx {
+  Reducer red;
+  PcgScalars* S;
+  PcgHist H;
+  double* out;  // kFinStore target
+  int finish;
+};
+
+// y = K x (+ grid dot with `dotw`), BSR rows [0, rows). Early-exits when S->stop.
+void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val,
+                 const double* x, double* y, const double* dotw, ReduceCtx rc, bool honor_stop,
+                 cudaStream_t st);
+// r = bvec - K x ; x untouched ; sum r.r -> kFinDenom
+void launch_residual(int b, int rows, const int* ptr, const int* col, const double* val,
+                     const double* x, const double* bvec, double* r, ReduceCtx rc, cudaStream_t st);
+// CN right-hand side and the warm-started residual in one pass over K:
+//   KU = K U ; rhs = 2 a M U - KU + ion ; x = warm ? U : 0 ; r = rhs - (warm ? KU : 0)
+void launch_rhs(int b, int rows, const int* ptr, const int* col, const double* val,
+                const double* M, double two_a, const double* U, const double* ion, int warm,
+                double* rhs, double* x, double* r, ReduceCtx rc, cudaStream_t st);
+// alpha = rho/pq ; x += alpha p ; r -= alpha q ; sum r.r -> kFinRr
+void launch_update(long long n, double* x, double* r, const double* p, const double* q,
+                   ReduceCtx rc, cudaStream_t st);
+// p = z + beta p  (beta from S) ; or p = z when first
+void launch_pupdate(long long n, double* p, const double* z, const PcgScalars* S, bool first,
+                    cudaStream_t st);
+// z += E y0 (coarse prolongation, optional) ; sum r.z -> kFinRzInit / kFinRz
+void launch_prolong_dot(int b, int bq, int ncells, const double* E, const int* cell_agg,
+                        const double* y0, const double* r, double* z, ReduceCtx rc,
+                        cudaStream_t st);
+// r0 = E^T r per coarse node
+void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* agg_cells,
+                     const double* E, const double* r, double* r0, const PcgScalars* S,
+                     cudaStream_t st);
+
+struct SweepArgs {
+  const DevTask* tasks;
+  const int* order;
+  int n_tasks;
+  unsigned int* ticket;
+  int* flags;
+  const int* task_child;
+  const double* vals;
+  const long long* row_dof;
+  const int* in_ptr;
+  const long long* in_idx;
+  double* ubuf;
+  const double* r;
+  double* z;
+  const double* r0;
+  double* y0;
+  const PcgScalars* S;
+};
+void launch_sweep_fwd(const SweepArgs& a, int smem_bytes, cudaStream_t st);
+void launch_sweep_bwd(const SweepArgs& a, int smem_bytes, cudaStream_t st);
+
+// Ionic model + stimulus at quadrature nodes (one warp per cell).
+struct IonicArgs {
+  int b, p, ncells, n_comp, ngl, has_prev, model, stim;
+  const double* bbox;
+  const int* tri_ptr;
+  const double* tri;
+  const double* U;
+  const double* Up;
+  const double* Y;    // n_comp fields of n (current)
+  const double* Yp;   // previous
+  double* Ynext;      // Y - dt M^-1 G
+  const double* Minv;
+  double* ion;        // -chi dt I* + dt F
+  long long n;
+  double chi, dt, t_mid;
+  double fhn[8];
+  double stim_p[4];
+  int* flags;         // bit0 out-of-range warning, bit1 non-finite state
+};
+void set_gauss_nodes(const double* x, const double* w, int n);
+void launch_ionic(const IonicArgs& a, cudaStream_t st);
+
+// dst_int[i*b + r] = src_ref[perm[i]*b + r] and the inverse
+void launch_gather_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nfields,
+                        long long stride_src, long long stride_dst, cudaStream_t st);
+void launch_scatter_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nfields,
+                         long long stride_src, long long stride_dst, cudaStream_t st);
+
+}  // namespace pdg

@@ -1,0 +1,504 @@
+// Device-resident solver: uploads the host setup once (K_h is constant in
+// time, timestepper.hpp:113-115) and runs Simulation::step / pcg_solve on the
+// GPU. The PCG loop is one CUDA graph whose body is a conditional WHILE node,
+// so an entire solve is a single launch and the iteration count, convergence
+// test (krylov.cpp:58-64) and breakdown checks (:46-53, :66-68) are decided on
+// the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../host/problem.hpp"
+#include "kernels.cuh"
+#include "sim.cuh"
+
+namespace pdg {
+
+template <class T>
+static T* dalloc(std::size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  PDG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+template <class T>
+static T* dupload(const std::vector<T>& v, cudaStream_t st) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty()) PDG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return p;
+}
+
+static const char* pcg_error_message(int e) {
+  switch (e) {
+    case kPcgRhoNonFinite0: return "pcg: non-finite preconditioned product";
+    case kPcgRhoNonPos0: return "pcg: preconditioner is not positive definite";
+    case kPcgPqNonFinite: return "pcg: non-finite operator product";
+    case kPcgPqNonPos: return "pcg: operator is not positive definite";
+    case kPcgRhoNonFinite: return "pcg: non-finite scalar";
+    case kPcgRhoNonPos: return "pcg: preconditioner is not positive definite";
+  }
+  return "pcg: unknown breakdown";
+}
+
+__global__ void set_condition_kernel(cudaGraphConditionalHandle h, const PcgScalars* S) {
+  cudaGraphSetConditional(h, S->stop ? 0u : 1u);
+}
+
+DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
+  const Problem& pr = *P;
+  PDG_CUDA(cudaSetDevice(pr.cfg.device));
+  PDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  PDG_CUDA(cudaEventCreate(&ev0));
+  PDG_CUDA(cudaEventCreate(&ev1));
+  PDG_CUDA(cudaEventCreate(&ev2));
+  b = pr.b;
+  bq = pr.two_level ? pr.bq : 0;
+  ncells = pr.cell_end - pr.cell_begin;
+  n = static_cast<long long>(ncells) * b;
+  n_comp = pr.n_comp;
+  maxit_default = pr.cfg.maxit > 0 ? pr.cfg.maxit : pdg_default_max_iterations(pr.n_global_dofs());
+
+  // ---- operator: columns remapped to local positions (halo appended, multi-rank) ----
+  std::vector<int> col(pr.K.col.size());
+  halo_cells.clear();
+  {
+    std::vector<int> halo_slot(pr.mesh.n_cells(), -1);
+    for (std::size_t k = 0; k < pr.K.col.size(); ++k) {
+      const int g = pr.K.col[k];
+      if (g >= pr.cell_begin && g < pr.cell_end) {
+        col[k] = g - pr.cell_begin;
+      } else {
+        if (halo_slot[g] < 0) {
+          halo_slot[g] = static_cast<int>(halo_cells.size());
+          halo_cells.push_back(g);
+        }
+        col[k] = ncells + halo_slot[g];
+      }
+    }
+  }
+  n_ext = n + static_cast<long long>(halo_cells.size()) * b;
+  d_ptr = dupload(pr.K.ptr, st);
+  d_col = dupload(col, st);
+  d_kval = dupload(pr.K.val, st);
+  d_M = dupload(pr.M, st);
+  d_Minv = dupload(pr.Minv, st);
+
+  for (auto& v : d_U) v = dalloc<double>(n_ext);
+  d_x = dalloc<double>(n_ext);
+  d_p = dalloc<double>(n_ext);
+  d_r = dalloc<double>(n);
+  d_z = dalloc<double>(n);
+  d_q = dalloc<double>(n);
+  d_rhs = dalloc<double>(n);
+  d_ion = dalloc<double>(n);
+  d_tmp = dalloc<double>(n_ext);
+  d_tmp2 = dalloc<double>(n_ext);
+  d_scratch = dalloc<double>(8);
+  for (auto& v : d_Y) v = dalloc<double>(std::max<long long>(n * n_comp, 1));
+  PDG_CUDA(cudaMemsetAsync(d_p, 0, n_ext * sizeof(double), st));
+  PDG_CUDA(cudaMemsetAsync(d_x, 0, n_ext * sizeof(double), st));
+  for (auto& v : d_U) PDG_CUDA(cudaMemsetAsync(v, 0, n_ext * sizeof(double), st));
+
+  // ---- coarse space ----
+  if (pr.two_level) {
+    d_E = dupload(pr.E, st);
+    d_cell_agg = dupload(pr.cell_agg, st);
+    d_agg_ptr = dupload(pr.agg_cell_ptr, st);
+    d_agg_cells = dupload(pr.agg_cells, st);
+    d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
+    d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
+  }
+  upload_tasks();
+
+  // ---- ionic geometry ----
+  d_bbox = dupload(pr.bbox, st);
+  d_tri_ptr = dupload(pr.tri_ptr, st);
+  d_tri = dupload(pr.tri, st);
+  set_gauss_nodes(pr.gl_x.data(), pr.gl_w.data(), static_cast<int>(pr.gl_x.size()));
+  d_ionflags = dalloc<int>(1);
+  PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
+
+  // ---- reductions / scalars / history ----
+  const long long max_grid = std::max<long long>(ncells + 1, 4096) + 4096;
+  red.partial = dalloc<double>(max_grid);
+  red.counter = dalloc<unsigned int>(4);
+  PDG_CUDA(cudaMemsetAsync(red.counter, 0, 4 * sizeof(unsigned int), st));
+  d_S = dalloc<PcgScalars>(1);
+  PDG_CUDA(cudaMallocHost(&h_S, sizeof(PcgScalars)));
+  hist_cap = std::max(maxit_default, 16) + 2;
+  alloc_history(hist_cap);
+  d_perm = dupload(std::vector<int>(pr.perm.begin() + pr.cell_begin, pr.perm.begin() + pr.cell_end), st);
+
+  // ---- state ----
+  PDG_CUDA(cudaMemcpyAsync(d_U[0], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  PDG_CUDA(cudaMemcpyAsync(d_U[1], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (n_comp > 0) {
+    PDG_CUDA(cudaMemcpyAsync(d_Y[0], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
+    PDG_CUDA(cudaMemcpyAsync(d_Y[1], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceSim::alloc_history(int cap) {
+  if (d_hist) cudaFree(d_hist);
+  d_hist = dalloc<double>(static_cast<std::size_t>(cap) * 3);
+  hist_cap = cap;
+  H.resid = d_hist;
+  H.alpha = d_hist + cap;
+  H.beta = d_hist + 2 * cap;
+  for (auto& g : graphs) g.reset();
+}
+
+void DeviceSim::upload_tasks() {
+  const Problem& pr = *P;
+  n_tasks = static_cast<int>(pr.tasks.size());
+  std::vector<DevTask> t(n_tasks);
+  int wmax = 0, nrmax = 0;
+  for (int i = 0; i < n_tasks; ++i) {
+    const TaskDesc& s = pr.tasks[i];
+    t[i] = DevTask{s.coarse, s.bs, s.w, s.nr, s.dof0, s.val_off, s.ubuf_off,
+                   s.rows_off, s.in_off, s.parent, s.child_off, s.n_child, 0};
+    wmax = std::max(wmax, s.w);
+    nrmax = std::max(nrmax, s.nr);
+  }
+  // topological ticket orders: forward by height (children first), backward
+  // by depth (parents first); larger supernodes first within a level
+  std::vector<int> fo(n_tasks), bo(n_tasks);
+  for (int i = 0; i < n_tasks; ++i) fo[i] = bo[i] = i;
+  std::stable_sort(fo.begin(), fo.end(), [&](int a, int c) {
+    const auto &A = pr.tasks[a], &C = pr.tasks[c];
+    if (A.height != C.height) return A.height < C.height;
+    return A.w * (A.w + A.nr) > C.w * (C.w + C.nr);
+  });
+  std::stable_sort(bo.begin(), bo.end(), [&](int a, int c) {
+    const auto &A = pr.tasks[a], &C = pr.tasks[c];
+    if (A.depth != C.depth) return A.depth < C.depth;
+    return A.w * (A.w + A.nr) > C.w * (C.w + C.nr);
+  });
+  smem_fwd = 2 * wmax * static_cast<int>(sizeof(double));
+  smem_bwd = (wmax + nrmax) * static_cast<int>(sizeof(double));
+  const int smem_max = std::max(smem_fwd, smem_bwd);
+  if (smem_max > 220 * 1024)
+    throw SolverError("schwarz: supernode too large for the device sweep (w=" + std::to_string(wmax) +
+                      ", rows=" + std::to_string(nrmax) + ")");
+  if (smem_max > 48 * 1024) set_sweep_smem(smem_max);
+  d_tasks = dupload(t, st);
+  d_fwd_order = dupload(fo, st);
+  d_bwd_order = dupload(bo, st);
+  d_task_child = dupload(pr.task_child, st);
+  d_vals = dupload(pr.fvals, st);
+  std::vector<long long> rd(pr.row_dof.begin(), pr.row_dof.end());
+  d_row_dof = dupload(rd, st);
+  d_in_ptr = dupload(pr.in_ptr, st);
+  std::vector<long long> ii(pr.in_idx.begin(), pr.in_idx.end());
+  d_in_idx = dupload(ii, st);
+  d_ubuf = dalloc<double>(std::max<std::int64_t>(pr.ubuf_size, 1));
+  d_flags = dalloc<int>(2 * std::max(n_tasks, 1));
+  d_ticket = dalloc<unsigned int>(2);
+}
+
+DeviceSim::~DeviceSim() {
+  for (auto& g : graphs) g.reset();
+  void* ptrs[] = {d_ptr, d_col, d_kval, d_M, d_Minv, d_U[0], d_U[1], d_x, d_p, d_r, d_z, d_q,
+                  d_rhs, d_ion, d_tmp, d_tmp2, d_Y[0], d_Y[1], d_E, d_cell_agg, d_agg_ptr,
+                  d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_order, d_bwd_order, d_task_child,
+                  d_vals, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
+                  d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
+                  d_Y[2], d_scratch};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h_S) cudaFreeHost(h_S);
+  if (st) cudaStreamDestroy(st);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaEventDestroy(ev2);
+}
+
+ReduceCtx DeviceSim::rctx(int finish, double* out) {
+  if (!out) out = d_scratch;
+  ReduceCtx rc;
+  rc.red = red;
+  rc.S = d_S;
+  rc.H = H;
+  rc.out = out;
+  rc.finish = finish;
+  return rc;
+}
+
+SweepArgs DeviceSim::sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S) {
+  SweepArgs a;
+  a.tasks = d_tasks;
+  a.order = fwd ? d_fwd_order : d_bwd_order;
+  a.n_tasks = n_tasks;
+  a.ticket = d_ticket + (fwd ? 0 : 1);
+  a.flags = d_flags + (fwd ? 0 : std::max(n_tasks, 1));
+  a.task_child = d_task_child;
+  a.vals = d_vals;
+  a.row_dof = d_row_dof;
+  a.in_ptr = d_in_ptr;
+  a.in_idx = d_in_idx;
+  a.ubuf = d_ubuf;
+  a.r = r;
+  a.z = z;
+  a.r0 = d_r0;
+  a.y0 = d_y0;
+  a.S = S;
+  return a;
+}
+
+// z = B r with the r.z reduction finished as `finish`. `S_honor` makes every
+// kernel a no-op once the solve has stopped.
+void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor) {
+  const Problem& pr = *P;
+  const PcgScalars* Sh = honor ? d_S : nullptr;
+  if (!use_pc()) {
+    // plain CG: z aliases r (krylov.cpp:39-42: out = in)
+    launch_prolong_dot(b, 0, ncells, nullptr, nullptr, nullptr, r, const_cast<double*>(r), rctx(finish), st);
+    return;
+  }
+  if (pr.two_level) {
+    launch_restrict(b, bq, pr.n_agg, d_agg_ptr, d_agg_cells, d_E, r, d_r0, Sh, st);
+    coarse_reduce_hook();
+  }
+  PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
+  PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
+  launch_sweep_fwd(sweep_args(true, r, z, Sh), smem_fwd, st);
+  launch_sweep_bwd(sweep_args(false, r, z, Sh), smem_bwd, st);
+  launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, rctx(finish), st);
+}
+
+double* DeviceSim::z_of(double* r) { return use_pc() ? d_z : r; }
+
+void DeviceSim::halo_exchange(double* v) { (void)v; }
+void DeviceSim::coarse_reduce_hook() {}
+void DeviceSim::dot_reduce_hook(int) {}
+
+// The body of one PCG iteration (krylov.cpp:49-73), every kernel gated on S->stop.
+void DeviceSim::record_iteration() {
+  halo_exchange(d_p);
+  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rctx(kFinPq), true, st);
+  launch_update(n, d_x, d_r, d_p, d_q, rctx(kFinRr), st);
+  precond_apply(d_r, z_of(d_r), kFinRz, true);
+  launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
+}
+
+// PCG after r = b - K x0 and denom are in place: z = B r, rho, p = z, then
+// the while loop.
+void DeviceSim::record_solve_tail() {
+  precond_apply(d_r, z_of(d_r), kFinRzInit, true);
+  launch_pupdate(n, d_p, z_of(d_r), d_S, true, st);
+}
+
+DeviceSim::Graph::~Graph() { reset(); }
+void DeviceSim::Graph::reset() {
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  exec = nullptr;
+  graph = nullptr;
+}
+
+void DeviceSim::build_solve_graph(Graph& g) {
+  g.reset();
+  PDG_CUDA(cudaGraphCreate(&g.graph, 0));
+  // tail (z, rho, p) captured into the outer graph
+  cudaGraph_t tail = nullptr;
+  PDG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  record_solve_tail();
+  PDG_CUDA(cudaStreamEndCapture(st, &tail));
+  cudaGraphNode_t tail_node;
+  PDG_CUDA(cudaGraphAddChildGraphNode(&tail_node, g.graph, nullptr, 0, tail));
+  cudaGraphDestroy(tail);
+
+  cudaGraphConditionalHandle handle;
+  PDG_CUDA(cudaGraphConditionalHandleCreate(&handle, g.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond_node;
+  PDG_CUDA(cudaGraphAddNode(&cond_node, g.graph, &tail_node, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  PDG_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  record_iteration();
+  set_condition_kernel<<<1, 1, 0, st>>>(handle, d_S);
+  PDG_CUDA(cudaStreamEndCapture(st, &body));
+  PDG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+}
+
+void DeviceSim::reset_scalars(double tol, int maxit) {
+  std::memset(h_S, 0, sizeof(PcgScalars));
+  h_S->tol = tol;
+  h_S->maxit = maxit;
+  PDG_CUDA(cudaMemcpyAsync(d_S, h_S, sizeof(PcgScalars), cudaMemcpyHostToDevice, st));
+}
+
+// Runs the device loop on (d_r, d_x) prepared by the caller; fills rep.
+void DeviceSim::run_solve(int maxit, PcgResult& res) {
+  if (maxit + 2 > hist_cap) alloc_history(maxit + 2);
+  Graph& g = graphs[use_pc() ? 1 : 0];
+  if (!g.exec) build_solve_graph(g);
+  PDG_CUDA(cudaGraphLaunch(g.exec, st));
+  PDG_CUDA(cudaMemcpyAsync(h_S, d_S, sizeof(PcgScalars), cudaMemcpyDeviceToHost, st));
+  PDG_CUDA(cudaStreamSynchronize(st));
+  res.iterations = h_S->iter;
+  res.converged = h_S->converged;
+  res.error = h_S->error;
+  res.denom = h_S->denom;
+  const int m = h_S->iter;
+  res.resid.resize(std::max(m, 1));
+  res.alpha.resize(m);
+  res.beta.resize(m);
+  if (h_S->denom == 0.0 && h_S->error == 0) {
+    res.resid.assign(1, 0.0);
+    res.alpha.clear();
+    res.beta.clear();
+    return;
+  }
+  if (m > 0) {
+    PDG_CUDA(cudaMemcpyAsync(res.resid.data(), H.resid, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(res.alpha.data(), H.alpha, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(res.beta.data(), H.beta, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+  } else {
+    res.resid.clear();
+  }
+  // betas recorded so far: one per completed precond apply after an iteration
+  int nb = m;
+  if (res.converged) nb = m - 1;
+  if (res.error != 0) nb = std::max(0, m - 1);
+  res.beta.resize(std::max(nb, 0));
+  if (res.error) throw SolverError(pcg_error_message(res.error));
+}
+
+// pcg_solve(K, b, precond, tol, maxit, x0) on internal-order device vectors.
+PcgResult DeviceSim::pcg(const double* d_b, const double* d_x0, double* d_xout, double tol, int maxit) {
+  if (!(tol > 0.0 && tol < 1.0)) throw SolverError("pcg: tol must lie in (0, 1)");
+  if (maxit <= 0) maxit = maxit_default;
+  PcgResult res;
+  reset_scalars(tol, maxit);
+  if (d_x0 != d_x) PDG_CUDA(cudaMemcpyAsync(d_x, d_x0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  halo_exchange(d_x);
+  launch_residual(b, ncells, d_ptr, d_col, d_kval, d_x, d_b, d_r, rctx(kFinDenom), st);
+  run_solve(maxit, res);
+  if (d_xout != d_x) PDG_CUDA(cudaMemcpyAsync(d_xout, d_x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  PDG_CUDA(cudaStreamSynchronize(st));
+  return res;
+}
+
+void DeviceSim::apply_K(const double* x, double* y) {
+  PDG_CUDA(cudaMemcpyAsync(d_tmp, x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  halo_exchange(d_tmp);
+  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_tmp, y, nullptr, rctx(kFinNone), false, st);
+  PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceSim::apply_precond(const double* r, double* z) {
+  reset_scalars(0.5, 1);
+  // r.z is computed into scratch; z may not alias r
+  PDG_CUDA(cudaMemsetAsync(z, 0, n * sizeof(double), st));
+  if (!use_pc()) {
+    PDG_CUDA(cudaMemcpyAsync(z, r, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    precond_apply(r, z, kFinStore, false);  // r.z -> scratch
+  }
+  PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+// Simulation::step (timestepper.cpp:144-200)
+StepResult DeviceSim::step() {
+  const Problem& pr = *P;
+  const pdg_config& c = pr.cfg;
+  const bool has_prev = k > 0;
+  StepResult out;
+  const int maxit = maxit_default;
+  PDG_CUDA(cudaEventRecord(ev0, st));
+  double* U = d_U[0];
+  double* Up = d_U[1];
+  const bool ionic = pr.n_comp > 0 || c.stim_kind != PDG_STIM_NONE;
+  if (ionic) {
+    IonicArgs a{};
+    a.b = b;
+    a.p = pr.p;
+    a.ncells = ncells;
+    a.n_comp = pr.n_comp;
+    a.ngl = static_cast<int>(pr.gl_x.size());
+    a.has_prev = has_prev ? 1 : 0;
+    a.model = c.ionic_model;
+    a.stim = c.stim_kind;
+    a.bbox = d_bbox;
+    a.tri_ptr = d_tri_ptr;
+    a.tri = d_tri;
+    a.U = U;
+    a.Up = Up;
+    a.Y = d_Y[0];
+    a.Yp = d_Y[1];
+    a.Ynext = d_Y[2];
+    a.Minv = d_Minv;
+    a.ion = d_ion;
+    a.n = n;
+    a.chi = c.chi_m;
+    a.dt = c.dt;
+    a.t_mid = t + 0.5 * c.dt;
+    std::memcpy(a.fhn, c.fhn, sizeof a.fhn);
+    std::memcpy(a.stim_p, c.stim_params, sizeof a.stim_p);
+    a.flags = d_ionflags;
+    launch_ionic(a, st);
+  }
+  reset_scalars(c.tol, maxit);
+  halo_exchange(U);
+  launch_rhs(b, ncells, d_ptr, d_col, d_kval, d_M, 2.0 * c.C_m * c.chi_m, U, ionic ? d_ion : nullptr,
+             c.warm_start, d_rhs, d_x, d_r, rctx(kFinDenom), st);
+  PDG_CUDA(cudaEventRecord(ev1, st));
+  PcgResult res;
+  run_solve(maxit, res);
+  PDG_CUDA(cudaEventRecord(ev2, st));
+  int ionflags = 0;
+  if (ionic) {
+    PDG_CUDA(cudaMemcpyAsync(&ionflags, d_ionflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
+  }
+  PDG_CUDA(cudaStreamSynchronize(st));
+  if (ionflags & 2) throw SolverError("fhn: non-finite state in current evaluation");
+  if (ionflags & 1)
+    std::fprintf(stderr,
+                 "polydg: warning: membrane potential left the admissible range by more than 10x "
+                 "the model span\n");
+  if (!res.converged) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "time step %d: PCG did not converge within %d iterations (residual %f)",
+                  k + 1, maxit, res.resid.empty() ? 1.0 : res.resid.back());
+    throw SolverError(buf);
+  }
+  // shift: U_prev <- U_curr, U_curr <- x ; Y_prev <- Y_curr, Y_curr <- Y_next
+  std::swap(d_U[0], d_U[1]);
+  PDG_CUDA(cudaMemcpyAsync(d_U[0], d_x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (pr.n_comp > 0) {
+    double* old_prev = d_Y[1];
+    d_Y[1] = d_Y[0];
+    d_Y[0] = d_Y[2];
+    d_Y[2] = old_prev;
+  }
+  k += 1;
+  t = k * c.dt;
+  float ms_all = 0.f, ms_solve = 0.f;
+  cudaEventElapsedTime(&ms_all, ev0, ev2);
+  cudaEventElapsedTime(&ms_solve, ev1, ev2);
+  out.iterations = res.iterations;
+  out.converged = res.converged;
+  out.final_residual = res.resid.empty() ? 0.0 : res.resid.back();
+  out.alpha = std::move(res.alpha);
+  out.beta = std::move(res.beta);
+  out.step_ms = ms_all;
+  out.solve_ms = ms_solve;
+  return out;
+}
+
+}  // namespace pdg

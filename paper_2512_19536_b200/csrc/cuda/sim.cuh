@@ -1,0 +1,112 @@
+// DeviceSim: one rank's device-resident state and solver (see sim.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "../host/problem.hpp"
+#include "kernels.cuh"
+
+namespace pdg {
+
+struct PcgResult {
+  int iterations = 0;
+  int converged = 0;
+  int error = 0;
+  double denom = 0.0;
+  std::vector<double> resid, alpha, beta;
+};
+
+struct StepResult {
+  int iterations = 0;
+  int converged = 0;
+  double final_residual = 0.0;
+  std::vector<double> alpha, beta;
+  double step_ms = 0.0, solve_ms = 0.0;
+};
+
+void set_sweep_smem(int bytes);
+// Extreme-eigenvalue ratio of the Lanczos tridiagonal (krylov.cpp:85-103).
+bool lanczos_condition(const double* alpha, const double* beta, int m, double* kappa);
+
+class DeviceSim {
+ public:
+  explicit DeviceSim(std::unique_ptr<Problem> prob);
+  virtual ~DeviceSim();
+
+  std::unique_ptr<Problem> P;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  int b = 0, bq = 0, ncells = 0, n_comp = 0, n_tasks = 0;
+  long long n = 0, n_ext = 0;
+  int maxit_default = 0;
+  int k = 0;
+  double t = 0.0;
+  std::vector<int> halo_cells;  // global internal cells appended after the local ones
+
+  // operator
+  int *d_ptr = nullptr, *d_col = nullptr;
+  double *d_kval = nullptr, *d_M = nullptr, *d_Minv = nullptr;
+  // state and work vectors (internal order)
+  double* d_U[2] = {nullptr, nullptr};  // curr, prev
+  double* d_Y[3] = {nullptr, nullptr, nullptr};  // curr, prev, next
+  double *d_x = nullptr, *d_p = nullptr, *d_r = nullptr, *d_z = nullptr, *d_q = nullptr;
+  double *d_rhs = nullptr, *d_ion = nullptr, *d_tmp = nullptr, *d_tmp2 = nullptr, *d_scratch = nullptr;
+  // coarse
+  double *d_E = nullptr, *d_r0 = nullptr, *d_y0 = nullptr;
+  int *d_cell_agg = nullptr, *d_agg_ptr = nullptr, *d_agg_cells = nullptr;
+  // sweep
+  DevTask* d_tasks = nullptr;
+  int *d_fwd_order = nullptr, *d_bwd_order = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;
+  double *d_vals = nullptr, *d_ubuf = nullptr;
+  long long *d_row_dof = nullptr, *d_in_idx = nullptr;
+  int* d_flags = nullptr;
+  unsigned int* d_ticket = nullptr;
+  int smem_fwd = 0, smem_bwd = 0;
+  // ionic
+  double *d_bbox = nullptr, *d_tri = nullptr;
+  int *d_tri_ptr = nullptr, *d_ionflags = nullptr;
+  // pcg bookkeeping
+  Reducer red{};
+  PcgScalars* d_S = nullptr;
+  PcgScalars* h_S = nullptr;
+  double* d_hist = nullptr;
+  int hist_cap = 0;
+  PcgHist H{};
+  int* d_perm = nullptr;
+
+  struct Graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~Graph();
+    void reset();
+  };
+  Graph graphs[2];
+  bool plain_cg = false;  // run pcg_solve with precond = nullptr
+  bool use_pc() const { return P->has_precond && !plain_cg; }
+
+  PcgResult pcg(const double* d_b, const double* d_x0, double* d_xout, double tol, int maxit);
+  void apply_K(const double* x, double* y);
+  void apply_precond(const double* r, double* z);
+  StepResult step();
+
+  // multi-rank hooks (no-ops on one GPU)
+  virtual void halo_exchange(double* v);
+  virtual void coarse_reduce_hook();
+  virtual void dot_reduce_hook(int finish);
+
+ protected:
+  void upload_tasks();
+  void alloc_history(int cap);
+  ReduceCtx rctx(int finish, double* out = nullptr);
+  SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);
+  void precond_apply(const double* r, double* z, int finish, bool honor);
+  double* z_of(double* r);
+  void record_iteration();
+  void record_solve_tail();
+  void build_solve_graph(Graph& g);
+  void reset_scalars(double tol, int maxit);
+  void run_solve(int maxit, PcgResult& res);
+};
+
+}  // namespace pdg
