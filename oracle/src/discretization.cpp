@@ -1,0 +1,598 @@
+// TEST INFRASTRUCTURE ONLY (see oracle.hpp).
+// Restates quadrature.cpp:19-198, dg_space.cpp:17-84, mesh.cpp:17-106,
+// assembly.cpp:13-242 and ionics.cpp:20-113 of /root/reference/proj/src.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <numeric>
+#include <random>
+#include <thread>
+
+#include "oracle.hpp"
+
+namespace orc {
+
+// parallel.cpp:13-41
+int thread_count() {
+  int n = static_cast<int>(std::thread::hardware_concurrency());
+  if (n < 1) n = 1;
+  if (const char* env = std::getenv("POLYDG_THREADS")) {
+    const int cap = std::atoi(env);
+    if (cap >= 1) n = std::min(n, cap);
+  }
+  return n;
+}
+
+void parallel_for(std::size_t n, const std::function<void(std::size_t)>& fn) {
+  const int workers = thread_count();
+  if (workers <= 1 || n < 2) {
+    for (std::size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  const std::size_t chunk = (n + workers - 1) / workers;
+  std::vector<std::thread> pool;
+  for (int w = 0; w < workers; ++w) {
+    const std::size_t b = static_cast<std::size_t>(w) * chunk;
+    if (b >= n) break;
+    const std::size_t e = std::min(n, b + chunk);
+    pool.emplace_back([&fn, b, e] {
+      for (std::size_t i = b; i < e; ++i) fn(i);
+    });
+  }
+  for (auto& t : pool) t.join();
+}
+
+// ---------------- CSR ----------------
+void Csr::apply(const Vec& x, Vec& y) const {
+  y.assign(rows, 0.0);
+  for (int64_t r = 0; r < rows; ++r) {
+    double s = 0.0;
+    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) s += val[k] * x[idx[k]];
+    y[r] = s;
+  }
+}
+
+double Csr::at(int64_t r, int64_t c) const {
+  const auto b = idx.begin() + ptr[r], e = idx.begin() + ptr[r + 1];
+  const auto it = std::lower_bound(b, e, c);
+  return (it != e && *it == c) ? val[it - idx.begin()] : 0.0;
+}
+
+Csr from_triplets(int64_t rows, int64_t cols, std::vector<Triplet>& t) {
+  // stable order by (row, col); duplicates summed in insertion order
+  std::vector<int64_t> order(t.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return t[a].r < t[b].r || (t[a].r == t[b].r && t[a].c < t[b].c);
+  });
+  Csr A;
+  A.rows = rows;
+  A.cols = cols;
+  A.ptr.assign(rows + 1, 0);
+  int64_t pr = -1, pc = -1;
+  for (int64_t o : order) {
+    const Triplet& e = t[o];
+    if (e.r == pr && e.c == pc) {
+      A.val.back() += e.v;
+    } else {
+      A.idx.push_back(e.c);
+      A.val.push_back(e.v);
+      ++A.ptr[e.r + 1];
+      pr = e.r;
+      pc = e.c;
+    }
+  }
+  for (int64_t r = 0; r < rows; ++r) A.ptr[r + 1] += A.ptr[r];
+  return A;
+}
+
+Csr transpose(const Csr& A) {
+  std::vector<Triplet> t;
+  t.reserve(A.val.size());
+  for (int64_t r = 0; r < A.rows; ++r)
+    for (int64_t k = A.ptr[r]; k < A.ptr[r + 1]; ++k) t.push_back({A.idx[k], r, A.val[k]});
+  return from_triplets(A.cols, A.rows, t);
+}
+
+Csr multiply(const Csr& A, const Csr& B) {
+  Csr C;
+  C.rows = A.rows;
+  C.cols = B.cols;
+  C.ptr.assign(A.rows + 1, 0);
+  std::vector<double> acc(B.cols, 0.0);
+  std::vector<int64_t> mark(B.cols, -1), used;
+  for (int64_t r = 0; r < A.rows; ++r) {
+    used.clear();
+    for (int64_t k = A.ptr[r]; k < A.ptr[r + 1]; ++k) {
+      const int64_t j = A.idx[k];
+      for (int64_t l = B.ptr[j]; l < B.ptr[j + 1]; ++l) {
+        const int64_t c = B.idx[l];
+        if (mark[c] != r) {
+          mark[c] = r;
+          acc[c] = 0.0;
+          used.push_back(c);
+        }
+        acc[c] += A.val[k] * B.val[l];
+      }
+    }
+    std::sort(used.begin(), used.end());
+    for (int64_t c : used) {
+      C.idx.push_back(c);
+      C.val.push_back(acc[c]);
+    }
+    C.ptr[r + 1] = static_cast<int64_t>(C.idx.size());
+  }
+  return C;
+}
+
+Csr combine(const Csr& A, double a, const Csr& B, double b) {
+  Csr C;
+  C.rows = A.rows;
+  C.cols = A.cols;
+  C.ptr.assign(A.rows + 1, 0);
+  for (int64_t r = 0; r < A.rows; ++r) {
+    int64_t i = A.ptr[r], j = B.ptr[r];
+    while (i < A.ptr[r + 1] || j < B.ptr[r + 1]) {
+      const int64_t ca = i < A.ptr[r + 1] ? A.idx[i] : INT64_MAX;
+      const int64_t cb = j < B.ptr[r + 1] ? B.idx[j] : INT64_MAX;
+      if (ca == cb) {
+        C.idx.push_back(ca);
+        C.val.push_back(a * A.val[i++] + b * B.val[j++]);
+      } else if (ca < cb) {
+        C.idx.push_back(ca);
+        C.val.push_back(a * A.val[i++]);
+      } else {
+        C.idx.push_back(cb);
+        C.val.push_back(b * B.val[j++]);
+      }
+    }
+    C.ptr[r + 1] = static_cast<int64_t>(C.idx.size());
+  }
+  return C;
+}
+
+// ---------------- quadrature ----------------
+void gauss_legendre(int n, Vec& x, Vec& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  auto leg = [n](double t, double& p0, double& p1) {
+    p0 = 1.0;
+    p1 = t;
+    for (int k = 2; k <= n; ++k) {
+      const double p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+  };
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double t = std::cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 0.0, p0, p1;
+    for (int it = 0; it < 100; ++it) {
+      leg(t, p0, p1);
+      dp = n * (t * p1 - p0) / (t * t - 1.0);
+      const double dx = p1 / dp;
+      t -= dx;
+      if (std::abs(dx) < 1e-15) {
+        leg(t, p0, p1);
+        dp = n * (t * p1 - p0) / (t * t - 1.0);
+        t -= p1 / dp;
+        break;
+      }
+    }
+    const double wt = 2.0 / ((1.0 - t * t) * dp * dp);
+    x[i] = -std::abs(t);
+    x[n - 1 - i] = std::abs(t);
+    w[i] = w[n - 1 - i] = wt;
+  }
+  if (n % 2 == 1) x[n / 2] = 0.0;
+}
+
+static void tri_rule(P2 a, P2 b, P2 c, int order, Rule& r) {
+  const int n = (order + 3) / 2;
+  Vec gx, gw;
+  gauss_legendre(n, gx, gw);
+  const double area2 = cross(b - a, c - a);
+  for (int i = 0; i < n; ++i) {
+    const double s = 0.5 * (gx[i] + 1.0);
+    for (int j = 0; j < n; ++j) {
+      const double t = 0.5 * (gx[j] + 1.0);
+      r.pts.push_back(a + (b - a) * s + (c - a) * (t * (1.0 - s)));
+      r.w.push_back(gw[i] * gw[j] * 0.25 * (1.0 - s) * area2);
+    }
+  }
+}
+
+static double signed_area(const std::vector<P2>& p) {
+  double s = 0.0;
+  for (std::size_t i = 0; i < p.size(); ++i) s += cross(p[i], p[(i + 1) % p.size()]);
+  return 0.5 * s;
+}
+
+static P2 centroid(const std::vector<P2>& p) {
+  double tw = 0, cx = 0, cy = 0;
+  for (std::size_t i = 0; i < p.size(); ++i) {
+    const P2 a = p[i], b = p[(i + 1) % p.size()];
+    const double w = cross(a, b);
+    tw += w;
+    cx += (a.x + b.x) * w;
+    cy += (a.y + b.y) * w;
+  }
+  return {cx / (3.0 * tw), cy / (3.0 * tw)};
+}
+
+Rule polygon_rule(const std::vector<P2>& poly, int order) {
+  order = std::max(order, 1);
+  const std::size_t n = poly.size();
+  const P2 c = centroid(poly);
+  const double area = signed_area(poly);
+  bool fan = true;
+  for (std::size_t i = 0; i < n; ++i)
+    if (cross(poly[i] - c, poly[(i + 1) % n] - c) <= 1e-14 * std::abs(area)) fan = false;
+  Rule r;
+  if (fan) {
+    for (std::size_t i = 0; i < n; ++i) tri_rule(c, poly[i], poly[(i + 1) % n], order, r);
+    return r;
+  }
+  // ear clipping (quadrature.cpp:91-142)
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  while (idx.size() > 3) {
+    const int m = static_cast<int>(idx.size());
+    bool clipped = false;
+    for (int e = 0; e < m && !clipped; ++e) {
+      const int i = idx[(e + m - 1) % m], j = idx[e], k = idx[(e + 1) % m];
+      if (cross(poly[j] - poly[i], poly[k] - poly[i]) <= 0.0) continue;
+      bool ear = true;
+      for (int q : idx) {
+        if (q == i || q == j || q == k) continue;
+        const P2 p = poly[q];
+        if (cross(poly[j] - poly[i], p - poly[i]) >= 0 && cross(poly[k] - poly[j], p - poly[j]) >= 0 &&
+            cross(poly[i] - poly[k], p - poly[k]) >= 0) {
+          ear = false;
+          break;
+        }
+      }
+      if (!ear) continue;
+      tri_rule(poly[i], poly[j], poly[k], order, r);
+      idx.erase(idx.begin() + e);
+      clipped = true;
+    }
+    if (!clipped) throw std::runtime_error("ear_clip: no ear found");
+  }
+  tri_rule(poly[idx[0]], poly[idx[1]], poly[idx[2]], order, r);
+  return r;
+}
+
+Rule segment_rule(P2 a, P2 b, int order) {
+  const int n = (std::max(order, 1) + 2) / 2;
+  Vec gx, gw;
+  gauss_legendre(n, gx, gw);
+  Rule r;
+  const double half = 0.5 * std::hypot(a.x - b.x, a.y - b.y);
+  const P2 mid = (a + b) * 0.5, dir = (b - a) * 0.5;
+  for (int i = 0; i < n; ++i) {
+    r.pts.push_back(mid + dir * gx[i]);
+    r.w.push_back(gw[i] * half);
+  }
+  return r;
+}
+
+int n_modes(int p) { return (p + 1) * (p + 2) / 2; }
+
+void eval_basis(const Box& box, int p, const std::vector<P2>& pts, Vec& val, Vec* gx, Vec* gy) {
+  const int nl = n_modes(p);
+  const std::size_t np = pts.size();
+  val.assign(np * nl, 0.0);
+  if (gx) gx->assign(np * nl, 0.0);
+  if (gy) gy->assign(np * nl, 0.0);
+  Vec px(p + 1), dpx(p + 1), py(p + 1), dpy(p + 1);
+  auto leg = [p](double t, Vec& v, Vec& d) {
+    v[0] = 1.0;
+    d[0] = 0.0;
+    if (p == 0) return;
+    v[1] = t;
+    d[1] = 1.0;
+    for (int k = 1; k < p; ++k) {
+      v[k + 1] = ((2 * k + 1) * t * v[k] - k * v[k - 1]) / (k + 1);
+      d[k + 1] = d[k - 1] + (2 * k + 1) * v[k];
+    }
+  };
+  const double wx = box.w(), wy = box.h();
+  for (std::size_t q = 0; q < np; ++q) {
+    leg((2.0 * pts[q].x - box.x0 - box.x1) / wx, px, dpx);
+    leg((2.0 * pts[q].y - box.y0 - box.y1) / wy, py, dpy);
+    const double inv = 1.0 / std::sqrt(wx * wy);
+    int m = 0;
+    for (int d = 0; d <= p; ++d)
+      for (int ax = d; ax >= 0; --ax, ++m) {
+        const int ay = d - ax;
+        const double sx = std::sqrt(2.0 * ax + 1.0), sy = std::sqrt(2.0 * ay + 1.0);
+        const double fx = sx * px[ax], fy = sy * py[ay];
+        val[q * nl + m] = inv * fx * fy;
+        if (gx) (*gx)[q * nl + m] = inv * sx * dpx[ax] * (2.0 / wx) * fy;
+        if (gy) (*gy)[q * nl + m] = inv * fx * sy * dpy[ay] * (2.0 / wy);
+      }
+  }
+}
+
+// ---------------- mesh view ----------------
+std::vector<P2> MeshView::cell(int c) const {
+  std::vector<P2> p;
+  for (int k = off[c]; k < off[c + 1]; ++k) p.push_back(verts[idx[k]]);
+  return p;
+}
+
+void MeshView::build() {
+  const int nc = n_cells();
+  diam.resize(nc);
+  bbox.resize(nc);
+  for (int c = 0; c < nc; ++c) {
+    const auto p = cell(c);
+    double d2 = 0.0;
+    Box b{1e300, 1e300, -1e300, -1e300};
+    for (std::size_t i = 0; i < p.size(); ++i) {
+      for (std::size_t j = i + 1; j < p.size(); ++j) {
+        const P2 d = p[i] - p[j];
+        d2 = std::max(d2, d.x * d.x + d.y * d.y);
+      }
+      b.x0 = std::min(b.x0, p[i].x);
+      b.x1 = std::max(b.x1, p[i].x);
+      b.y0 = std::min(b.y0, p[i].y);
+      b.y1 = std::max(b.y1, p[i].y);
+    }
+    diam[c] = std::sqrt(d2);
+    bbox[c] = b;
+  }
+  // faces in first-occurrence order of the (min,max) vertex key
+  std::map<std::pair<int, int>, int> key;
+  struct Use {
+    int cell, va, vb, n = 0, other = -1;
+  };
+  std::vector<Use> uses;
+  for (int c = 0; c < nc; ++c) {
+    const int k = off[c + 1] - off[c];
+    for (int e = 0; e < k; ++e) {
+      const int va = idx[off[c] + e], vb = idx[off[c] + (e + 1) % k];
+      auto [it, ins] = key.try_emplace({std::min(va, vb), std::max(va, vb)}, static_cast<int>(uses.size()));
+      if (ins) uses.push_back({c, va, vb, 1, -1});
+      else {
+        uses[it->second].other = c;
+        uses[it->second].n++;
+      }
+    }
+  }
+  faces.clear();
+  for (const Use& u : uses) {
+    if (u.n != 2) continue;
+    Face f;
+    f.a = verts[u.va];
+    f.b = verts[u.vb];
+    f.in = u.cell;
+    f.out = u.other;
+    f.len = std::hypot(f.a.x - f.b.x, f.a.y - f.b.y);
+    f.n = {(f.b.y - f.a.y) / f.len, -(f.b.x - f.a.x) / f.len};
+    faces.push_back(f);
+  }
+}
+
+// ---------------- assembly ----------------
+namespace {
+struct Tensor {
+  double a00, a01, a10, a11;
+};
+Tensor tensor(double sl, double sn, P2 f) {
+  const double len = std::hypot(f.x, f.y);
+  if (!(len > 0.0)) throw ConfigError("conductivity: zero fiber direction");
+  const double nx = -f.y / len, ny = f.x / len;
+  return {sl + (sn - sl) * nx * nx, (sn - sl) * nx * ny, (sn - sl) * ny * nx, sl + (sn - sl) * ny * ny};
+}
+void push_diag(std::vector<Triplet>& t, int64_t r0, const Vec& L, int n) {  // upper triangle mirrored
+  for (int i = 0; i < n; ++i) {
+    t.push_back({r0 + i, r0 + i, L[i * n + i]});
+    for (int j = i + 1; j < n; ++j) {
+      t.push_back({r0 + i, r0 + j, L[i * n + j]});
+      t.push_back({r0 + j, r0 + i, L[i * n + j]});
+    }
+  }
+}
+void dense_llt(int n, const double* a, double* L) {  // row-major
+  std::fill(L, L + n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= L[j * n + k] * L[j * n + k];
+    if (!(d > 0.0)) throw SolverError("dense block is not positive definite");
+    L[j * n + j] = std::sqrt(d);
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[i * n + j];
+      for (int k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+      L[i * n + j] = s / L[j * n + j];
+    }
+  }
+}
+void dense_llt_solve(int n, const double* L, double* x) {
+  for (int i = 0; i < n; ++i) {
+    double s = x[i];
+    for (int k = 0; k < i; ++k) s -= L[i * n + k] * x[k];
+    x[i] = s / L[i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = x[i];
+    for (int k = i + 1; k < n; ++k) s -= L[k * n + i] * x[k];
+    x[i] = s / L[i * n + i];
+  }
+}
+}  // namespace
+
+void Discretization::build(const MeshView& m, const Config& c) {
+  mesh = &m;
+  p = c.degree;
+  nloc = n_modes(p);
+  const int nc = m.n_cells(), order = 2 * p + 2;
+  const int64_t n = static_cast<int64_t>(nc) * nloc;
+  if (!(c.sgl > 0 && c.sgn > 0 && c.swl > 0 && c.swn > 0))
+    throw ConfigError("conductivity: all sigma values must be positive");
+  std::vector<Tensor> sig(nc);
+  std::vector<double> snorm(nc);
+  for (int e = 0; e < nc; ++e) {
+    const bool grey = m.region[e] == 0;
+    const double sl = grey ? c.sgl : c.swl, sn = grey ? c.sgn : c.swn;
+    P2 fib = grey ? c.fiber_grey : c.fiber_white;
+    sig[e] = tensor(sl, sn, fib);
+    snorm[e] = std::max(sl, sn);
+  }
+  if (c.fiber_random) {
+    // ext: theta_K = pi * (rng()>>11) * 2^-53 from mt19937_64(fiber_seed), cell order
+    std::mt19937_64 rng(c.fiber_seed);
+    for (int e = 0; e < nc; ++e) {
+      const double th = M_PI * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+      const bool grey = m.region[e] == 0;
+      sig[e] = tensor(grey ? c.sgl : c.swl, grey ? c.sgn : c.swn, {std::cos(th), std::sin(th)});
+    }
+  }
+  std::vector<Triplet> tm, ta;
+  Vec val, gx, gy;
+  Mchol.assign(nc, Vec());
+  for (int e = 0; e < nc; ++e) {
+    const Rule r = polygon_rule(m.cell(e), order);
+    eval_basis(m.bbox[e], p, r.pts, val, &gx, &gy);
+    Vec lm(nloc * nloc, 0.0), la(nloc * nloc, 0.0);
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      const double* v = &val[q * nloc];
+      for (int i = 0; i < nloc; ++i)
+        for (int j = i; j < nloc; ++j) lm[i * nloc + j] += r.w[q] * v[i] * v[j];
+    }
+    const Tensor& s = sig[e];
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      const double* X = &gx[q * nloc];
+      const double* Y = &gy[q * nloc];
+      for (int j = 0; j < nloc; ++j) {
+        const double sx = s.a00 * X[j] + s.a01 * Y[j], sy = s.a10 * X[j] + s.a11 * Y[j];
+        for (int i = 0; i <= j; ++i) la[i * nloc + j] += r.w[q] * (X[i] * sx + Y[i] * sy);
+      }
+    }
+    push_diag(tm, static_cast<int64_t>(e) * nloc, lm, nloc);
+    push_diag(ta, static_cast<int64_t>(e) * nloc, la, nloc);
+    Vec full(nloc * nloc);
+    for (int i = 0; i < nloc; ++i)
+      for (int j = 0; j < nloc; ++j) full[i * nloc + j] = lm[std::min(i, j) * nloc + std::max(i, j)];
+    Mchol[e].resize(nloc * nloc);
+    dense_llt(nloc, full.data(), Mchol[e].data());
+  }
+  Vec vk, vl, gxk, gyk, gxl, gyl;
+  for (const Face& f : m.faces) {
+    const int K = f.in, L = f.out;
+    const double hk = m.diam[K], hl = m.diam[L];
+    const double eta = c.eta0 * (0.5 * (snorm[K] + snorm[L])) * p * p / (2.0 * hk * hl / (hk + hl));
+    const Rule r = segment_rule(f.a, f.b, order);
+    eval_basis(m.bbox[K], p, r.pts, vk, &gxk, &gyk);
+    eval_basis(m.bbox[L], p, r.pts, vl, &gxl, &gyl);
+    Vec kk(nloc * nloc, 0.0), ll(nloc * nloc, 0.0), kl(nloc * nloc, 0.0), ak(nloc), al(nloc);
+    const Tensor &sk = sig[K], &sl = sig[L];
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      const double w = r.w[q];
+      const double *VK = &vk[q * nloc], *VL = &vl[q * nloc];
+      for (int mm = 0; mm < nloc; ++mm) {
+        const double xk = gxk[q * nloc + mm], yk = gyk[q * nloc + mm];
+        const double xl = gxl[q * nloc + mm], yl = gyl[q * nloc + mm];
+        ak[mm] = (sk.a00 * xk + sk.a01 * yk) * f.n.x + (sk.a10 * xk + sk.a11 * yk) * f.n.y;
+        al[mm] = (sl.a00 * xl + sl.a01 * yl) * f.n.x + (sl.a10 * xl + sl.a11 * yl) * f.n.y;
+      }
+      for (int i = 0; i < nloc; ++i) {
+        for (int j = i; j < nloc; ++j) {
+          kk[i * nloc + j] += w * (-0.5 * (ak[j] * VK[i] + ak[i] * VK[j]) + eta * VK[j] * VK[i]);
+          ll[i * nloc + j] += w * (0.5 * (al[j] * VL[i] + al[i] * VL[j]) + eta * VL[j] * VL[i]);
+        }
+        for (int j = 0; j < nloc; ++j)
+          kl[i * nloc + j] += w * (-0.5 * al[j] * VK[i] + 0.5 * ak[i] * VL[j] - eta * VL[j] * VK[i]);
+      }
+    }
+    push_diag(ta, static_cast<int64_t>(K) * nloc, kk, nloc);
+    push_diag(ta, static_cast<int64_t>(L) * nloc, ll, nloc);
+    for (int i = 0; i < nloc; ++i)
+      for (int j = 0; j < nloc; ++j) {
+        ta.push_back({static_cast<int64_t>(K) * nloc + i, static_cast<int64_t>(L) * nloc + j, kl[i * nloc + j]});
+        ta.push_back({static_cast<int64_t>(L) * nloc + j, static_cast<int64_t>(K) * nloc + i, kl[i * nloc + j]});
+      }
+  }
+  M = from_triplets(n, n, tm);
+  A = from_triplets(n, n, ta);
+  K = combine(M, c.C_m * c.chi_m, A, 0.5 * c.dt);
+  Krhs = combine(M, c.chi_m * c.C_m, A, -0.5 * c.dt);
+}
+
+Vec Discretization::mass_solve(const Vec& rhs) const {
+  Vec x(rhs.size());
+  for (int e = 0; e < mesh->n_cells(); ++e) {
+    double* xe = &x[static_cast<int64_t>(e) * nloc];
+    std::copy(rhs.begin() + static_cast<int64_t>(e) * nloc, rhs.begin() + static_cast<int64_t>(e + 1) * nloc, xe);
+    dense_llt_solve(nloc, Mchol[e].data(), xe);
+  }
+  return x;
+}
+
+Vec Discretization::l2_project(const std::function<double(P2)>& g) const {
+  Vec rhs(static_cast<int64_t>(mesh->n_cells()) * nloc, 0.0), val;
+  for (int e = 0; e < mesh->n_cells(); ++e) {
+    const Rule r = polygon_rule(mesh->cell(e), 2 * p + 2);
+    eval_basis(mesh->bbox[e], p, r.pts, val, nullptr, nullptr);
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      const double wg = r.w[q] * g(r.pts[q]);
+      for (int i = 0; i < nloc; ++i) rhs[static_cast<int64_t>(e) * nloc + i] += wg * val[q * nloc + i];
+    }
+  }
+  return mass_solve(rhs);
+}
+
+// ---------------- ionics ----------------
+double fhn_current(const double* P, double u, double w) {
+  if (!std::isfinite(u) || !std::isfinite(w)) throw SolverError("fhn: non-finite state in current evaluation");
+  const double span = P[6] - P[5];
+  const double v = (u - P[5]) / span;
+  return P[7] * (P[2] * v * (v - P[0]) * (v - 1.0) + P[3] * v * w) * span;
+}
+
+double fhn_rate(const double* P, double u, double w) {
+  if (!std::isfinite(u) || !std::isfinite(w)) throw SolverError("fhn: non-finite state in rate evaluation");
+  const double v = (u - P[5]) / (P[6] - P[5]);
+  return -P[1] * (v - P[4] * w);
+}
+
+IonicTerms ionic_terms(const Discretization& D, const Vec& U, const std::vector<Vec>& Y, const double* P,
+                       bool* out_of_box) {
+  const int nl = D.nloc, nc = D.mesh->n_cells();
+  IonicTerms out;
+  out.I.assign(U.size(), 0.0);
+  out.G.assign(Y.size(), Vec(U.size(), 0.0));
+  const double slack = 10.0 * (P[6] - P[5]);
+  std::vector<char> oob(nc, 0);
+  std::vector<std::string> err(nc);
+  parallel_for(nc, [&](std::size_t ci) {
+    const int e = static_cast<int>(ci);
+    try {
+      const Rule r = polygon_rule(D.mesh->cell(e), 2 * D.p + 2);
+      Vec val;
+      eval_basis(D.mesh->bbox[e], D.p, r.pts, val, nullptr, nullptr);
+      const int64_t b0 = static_cast<int64_t>(e) * nl;
+      for (std::size_t q = 0; q < r.w.size(); ++q) {
+        double u = 0.0, y = 0.0;
+        for (int i = 0; i < nl; ++i) u += val[q * nl + i] * U[b0 + i];
+        if (!Y.empty())
+          for (int i = 0; i < nl; ++i) y += val[q * nl + i] * Y[0][b0 + i];
+        if (u < P[5] - slack || u > P[6] + slack) oob[e] = 1;
+        const double f = fhn_current(P, u, y), m = fhn_rate(P, u, y);
+        const double wf = r.w[q] * f, wm = r.w[q] * m;
+        for (int i = 0; i < nl; ++i) {
+          out.I[b0 + i] += wf * val[q * nl + i];
+          if (!Y.empty()) out.G[0][b0 + i] += wm * val[q * nl + i];
+        }
+      }
+    } catch (const std::exception& ex) {
+      err[e] = ex.what();
+    }
+  });
+  for (const auto& s : err)
+    if (!s.empty()) throw SolverError(s);
+  if (out_of_box) *out_of_box = std::any_of(oob.begin(), oob.end(), [](char c) { return c != 0; });
+  return out;
+}
+
+}  // namespace orc

@@ -188,6 +188,10 @@ pdg_status pdg_sim_pcg(pdg_sim* s, const double* b, const double* x0, double tol
   });
 }
 
+pdg_status pdg_sim_attach_comm(pdg_sim* s, const void* id128, int rank, int world) {
+  return pdg::guarded([&] { S(s).attach_comm(id128, rank, world); });
+}
+
 pdg_status pdg_sim_pcg_device(pdg_sim* s, const double* d_b, const double* d_x0, double tol, int maxit,
                               double* d_x, pdg_pcg_report* rep) {
   return pdg::guarded([&] {

@@ -594,6 +594,23 @@ __global__ void scatter_perm_kernel(const double* __restrict__ src, double* __re
   }
 }
 
+// Multi-rank: the producing kernel stored its local sum; after the NCCL
+// all-reduce this applies the finish on every rank identically.
+__global__ void finish_kernel(ReduceCtx rc, const double* sum, int honor) {
+  if (honor && rc.S->stop) return;
+  apply_finish(rc, *sum);
+}
+
+__global__ void pack_kernel(const double* __restrict__ v, const int* __restrict__ cells, int ncells, int b,
+                            double* __restrict__ out) {
+  const long long n = static_cast<long long>(ncells) * b;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = i / b;
+    out[i] = v[static_cast<long long>(cells[k]) * b + (i - k * b)];
+  }
+}
+
 int vec_grid(long long n) {
   long long g = (n + kVecThreads - 1) / kVecThreads;
   if (g > 148 * 16) g = 148 * 16;
@@ -714,6 +731,15 @@ void launch_sweep_fwd(const SweepArgs& a, int smem, cudaStream_t st) {
 void launch_sweep_bwd(const SweepArgs& a, int smem, cudaStream_t st) {
   if (a.n_tasks == 0) return;
   sweep_bwd_kernel<<<a.n_tasks, kSweepThreads, smem, st>>>(a);
+}
+
+void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st) {
+  finish_kernel<<<1, 1, 0, st>>>(rc, sum, honor ? 1 : 0);
+}
+
+void launch_pack(const double* v, const int* cells, int ncells, int b, double* out, cudaStream_t st) {
+  if (ncells == 0) return;
+  pack_kernel<<<vec_grid(static_cast<long long>(ncells) * b), kVecThreads, 0, st>>>(v, cells, ncells, b, out);
 }
 
 void set_sweep_smem(int bytes) {

@@ -102,6 +102,10 @@ struct IonicArgs {
 void set_gauss_nodes(const double* x, const double* w, int n);
 void launch_ionic(const IonicArgs& a, cudaStream_t st);
 
+// multi-rank helpers: apply a finish to an all-reduced sum; pack halo cells
+void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st);
+void launch_pack(const double* v, const int* cells, int ncells, int b, double* out, cudaStream_t st);
+
 // dst_int[i*b + r] = src_ref[perm[i]*b + r] and the inverse
 void launch_gather_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nfields,
                         long long stride_src, long long stride_dst, cudaStream_t st);

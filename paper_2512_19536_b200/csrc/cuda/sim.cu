@@ -63,24 +63,26 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   ncells = pr.cell_end - pr.cell_begin;
   n = static_cast<long long>(ncells) * b;
   n_comp = pr.n_comp;
+  rank = pr.cfg.rank;
+  world = pr.cfg.world;
   maxit_default = pr.cfg.maxit > 0 ? pr.cfg.maxit : pdg_default_max_iterations(pr.n_global_dofs());
 
   // ---- operator: columns remapped to local positions (halo appended, multi-rank) ----
+  // Halo cells sorted by global internal index: ranks own contiguous ranges,
+  // so the halo is grouped by source rank, in the order the sender packs it.
   std::vector<int> col(pr.K.col.size());
   halo_cells.clear();
   {
-    std::vector<int> halo_slot(pr.mesh.n_cells(), -1);
+    for (int g : pr.K.col)
+      if (g < pr.cell_begin || g >= pr.cell_end) halo_cells.push_back(g);
+    std::sort(halo_cells.begin(), halo_cells.end());
+    halo_cells.erase(std::unique(halo_cells.begin(), halo_cells.end()), halo_cells.end());
     for (std::size_t k = 0; k < pr.K.col.size(); ++k) {
       const int g = pr.K.col[k];
-      if (g >= pr.cell_begin && g < pr.cell_end) {
-        col[k] = g - pr.cell_begin;
-      } else {
-        if (halo_slot[g] < 0) {
-          halo_slot[g] = static_cast<int>(halo_cells.size());
-          halo_cells.push_back(g);
-        }
-        col[k] = ncells + halo_slot[g];
-      }
+      col[k] = (g >= pr.cell_begin && g < pr.cell_end)
+                   ? g - pr.cell_begin
+                   : ncells + static_cast<int>(std::lower_bound(halo_cells.begin(), halo_cells.end(), g) -
+                                               halo_cells.begin());
     }
   }
   n_ext = n + static_cast<long long>(halo_cells.size()) * b;
@@ -156,7 +158,20 @@ void DeviceSim::alloc_history(int cap) {
   for (auto& g : graphs) g.reset();
 }
 
+void DeviceSim::release_tasks() {
+  void* ptrs[] = {d_tasks, d_fwd_order, d_bwd_order, d_task_child, d_vals, d_row_dof, d_in_ptr, d_in_idx,
+                  d_ubuf, d_flags, d_ticket};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  d_tasks = nullptr;
+  d_fwd_order = d_bwd_order = d_task_child = d_in_ptr = d_flags = nullptr;
+  d_vals = d_ubuf = nullptr;
+  d_row_dof = d_in_idx = nullptr;
+  d_ticket = nullptr;
+}
+
 void DeviceSim::upload_tasks() {
+  release_tasks();
   const Problem& pr = *P;
   n_tasks = static_cast<int>(pr.tasks.size());
   std::vector<DevTask> t(n_tasks);
@@ -211,7 +226,8 @@ DeviceSim::~DeviceSim() {
                   d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_order, d_bwd_order, d_task_child,
                   d_vals, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
-                  d_Y[2], d_scratch};
+                  d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global};
+  comm_destroy();
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_S) cudaFreeHost(h_S);
@@ -260,7 +276,8 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
   const PcgScalars* Sh = honor ? d_S : nullptr;
   if (!use_pc()) {
     // plain CG: z aliases r (krylov.cpp:39-42: out = in)
-    launch_prolong_dot(b, 0, ncells, nullptr, nullptr, nullptr, r, const_cast<double*>(r), rctx(finish), st);
+    launch_prolong_dot(b, 0, ncells, nullptr, nullptr, nullptr, r, const_cast<double*>(r), red_for(finish), st);
+    after_reduce(finish, honor);
     return;
   }
   if (pr.two_level) {
@@ -271,20 +288,48 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
   PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
   launch_sweep_fwd(sweep_args(true, r, z, Sh), smem_fwd, st);
   launch_sweep_bwd(sweep_args(false, r, z, Sh), smem_bwd, st);
-  launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, rctx(finish), st);
+  launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
+  after_reduce(finish, honor);
 }
 
 double* DeviceSim::z_of(double* r) { return use_pc() ? d_z : r; }
 
-void DeviceSim::halo_exchange(double* v) { (void)v; }
-void DeviceSim::coarse_reduce_hook() {}
+ReduceCtx DeviceSim::red_for(int finish) {
+  if (world == 1 || finish == kFinNone || finish == kFinStore) return rctx(finish);
+  return rctx(kFinStore, d_dot_local);
+}
+
+// Multi-rank: sum the per-rank partial over NCCL, then apply the finish on
+// every rank (identical inputs, so every rank takes identical decisions).
+void DeviceSim::after_reduce(int finish, bool honor) {
+  if (world == 1 || finish == kFinNone || finish == kFinStore) return;
+  comm_allreduce(d_dot_local, d_dot_global, 1);
+  launch_finish(rctx(finish), d_dot_global, honor, st);
+}
+
+// p-halo for the SpMV: pack the cells each peer needs, grouped send/recv
+// straight into the halo tail of v.
+void DeviceSim::halo_exchange(double* v) {
+  if (world == 1 || halo_peers.empty()) return;
+  for (const HaloPeer& h : halo_peers)
+    launch_pack(v, d_send_cells + h.send_off, h.send_count, b, d_sendbuf + static_cast<long long>(h.send_off) * b, st);
+  comm_exchange(v);
+}
+
+// every rank solves the coarse problem redundantly on the summed r0 (C3)
+void DeviceSim::coarse_reduce_hook() {
+  if (world == 1) return;
+  comm_allreduce(d_r0, d_r0, static_cast<long long>(P->n_agg) * P->bq);
+}
 void DeviceSim::dot_reduce_hook(int) {}
 
 // The body of one PCG iteration (krylov.cpp:49-73), every kernel gated on S->stop.
 void DeviceSim::record_iteration() {
   halo_exchange(d_p);
-  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rctx(kFinPq), true, st);
-  launch_update(n, d_x, d_r, d_p, d_q, rctx(kFinRr), st);
+  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
+  after_reduce(kFinPq, true);
+  launch_update(n, d_x, d_r, d_p, d_q, red_for(kFinRr), st);
+  after_reduce(kFinRr, true);
   precond_apply(d_r, z_of(d_r), kFinRz, true);
   launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
 }
@@ -343,11 +388,26 @@ void DeviceSim::reset_scalars(double tol, int maxit) {
 // Runs the device loop on (d_r, d_x) prepared by the caller; fills rep.
 void DeviceSim::run_solve(int maxit, PcgResult& res) {
   if (maxit + 2 > hist_cap) alloc_history(maxit + 2);
-  Graph& g = graphs[use_pc() ? 1 : 0];
-  if (!g.exec) build_solve_graph(g);
-  PDG_CUDA(cudaGraphLaunch(g.exec, st));
-  PDG_CUDA(cudaMemcpyAsync(h_S, d_S, sizeof(PcgScalars), cudaMemcpyDeviceToHost, st));
-  PDG_CUDA(cudaStreamSynchronize(st));
+  if (world == 1) {
+    Graph& g = graphs[use_pc() ? 1 : 0];
+    if (!g.exec) build_solve_graph(g);
+    PDG_CUDA(cudaGraphLaunch(g.exec, st));
+    PDG_CUDA(cudaMemcpyAsync(h_S, d_S, sizeof(PcgScalars), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+  } else {
+    // multi-rank: host-driven loop (NCCL calls stay outside conditional
+    // graphs); every rank sees the same all-reduced scalars, so all ranks
+    // stop after the same iteration and issue the same collectives.
+    if (!comm) throw SolverError("multi-rank simulation: call pdg_sim_attach_comm first");
+    record_solve_tail();
+    constexpr int kPoll = 4;
+    for (int it = 0; it < maxit;) {
+      for (int j = 0; j < kPoll && it < maxit; ++j, ++it) record_iteration();
+      PDG_CUDA(cudaMemcpyAsync(h_S, d_S, sizeof(PcgScalars), cudaMemcpyDeviceToHost, st));
+      PDG_CUDA(cudaStreamSynchronize(st));
+      if (h_S->stop) break;
+    }
+  }
   res.iterations = h_S->iter;
   res.converged = h_S->converged;
   res.error = h_S->error;
@@ -386,7 +446,8 @@ PcgResult DeviceSim::pcg(const double* d_b, const double* d_x0, double* d_xout, 
   reset_scalars(tol, maxit);
   if (d_x0 != d_x) PDG_CUDA(cudaMemcpyAsync(d_x, d_x0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   halo_exchange(d_x);
-  launch_residual(b, ncells, d_ptr, d_col, d_kval, d_x, d_b, d_r, rctx(kFinDenom), st);
+  launch_residual(b, ncells, d_ptr, d_col, d_kval, d_x, d_b, d_r, red_for(kFinDenom), st);
+  after_reduce(kFinDenom, false);
   run_solve(maxit, res);
   if (d_xout != d_x) PDG_CUDA(cudaMemcpyAsync(d_xout, d_x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   PDG_CUDA(cudaStreamSynchronize(st));
@@ -455,7 +516,8 @@ StepResult DeviceSim::step() {
   reset_scalars(c.tol, maxit);
   halo_exchange(U);
   launch_rhs(b, ncells, d_ptr, d_col, d_kval, d_M, 2.0 * c.C_m * c.chi_m, U, ionic ? d_ion : nullptr,
-             c.warm_start, d_rhs, d_x, d_r, rctx(kFinDenom), st);
+             c.warm_start, d_rhs, d_x, d_r, red_for(kFinDenom), st);
+  after_reduce(kFinDenom, false);
   PDG_CUDA(cudaEventRecord(ev1, st));
   PcgResult res;
   run_solve(maxit, res);

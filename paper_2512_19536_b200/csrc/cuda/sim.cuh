@@ -95,7 +95,27 @@ class DeviceSim {
   virtual void coarse_reduce_hook();
   virtual void dot_reduce_hook(int finish);
 
+  // ---- multi-rank state (comm.cu) ----
+  int rank = 0, world = 1;
+  void* comm = nullptr;  // ncclComm_t
+  struct HaloPeer {
+    int peer;
+    int send_off, send_count;  // cells in d_send_cells / d_sendbuf
+    int recv_off, recv_count;  // halo slots (after the local cells)
+  };
+  std::vector<HaloPeer> halo_peers;
+  int* d_send_cells = nullptr;
+  double* d_sendbuf = nullptr;
+  double *d_dot_local = nullptr, *d_dot_global = nullptr;
+  void attach_comm(const void* id128, int rank, int world);
+  void comm_allreduce(const double* src, double* dst, long long count);
+  void comm_exchange(double* v);
+  void release_tasks();
+  void comm_destroy();
+
  protected:
+  ReduceCtx red_for(int finish);
+  void after_reduce(int finish, bool honor);
   void upload_tasks();
   void alloc_history(int cap);
   ReduceCtx rctx(int finish, double* out = nullptr);
