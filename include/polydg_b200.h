@@ -173,6 +173,18 @@ pdg_status pdg_sim_pcg(pdg_sim* s, const double* b, const double* x0, double tol
  * internal order. */
 pdg_status pdg_sim_pcg_device(pdg_sim* s, const double* d_b, const double* d_x0, double tol,
                               int maxit, double* d_x, pdg_pcg_report* rep);
+/* ---- measurement (no reference analogue; the reference only times wall
+ * clock, timestepper.cpp:203,227-228) ---- */
+/* stop = 0 records a start event on the solver stream; stop = 1 records the
+ * end event, waits for it and returns the device time between the two */
+pdg_status pdg_sim_timer(pdg_sim* s, int stop, double* elapsed_ms);
+/* kernels issued by pdg_sim_step so far (graph-replayed launches included) */
+int64_t pdg_sim_kernel_launches(const pdg_sim* s);
+/* per-kernel device time (ms, averaged over reps) and algorithmic bytes per
+ * launch, slots: 0 spmv, 1 update, 2 restrict, 3 sweep_fwd, 4 sweep_bwd,
+ * 5 prolong_dot, 6 pupdate, 7 ionic, 8 rhs */
+pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9);
+
 /* default_max_iterations (krylov.cpp:12-15) and condition_estimate (:85-103) */
 int pdg_default_max_iterations(int64_t n);
 int pdg_condition_estimate(const double* alphas, const double* betas, int m, double* kappa);

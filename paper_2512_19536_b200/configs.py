@@ -1,0 +1,61 @@
+"""The BASELINE.json workloads as SimulationConfig factories.
+
+Where BASELINE.json is silent the reference defaults apply:
+unit square, mesh seed 42, chi_m = 1000, C_m = 1, eta0 = 10, warm start, q = p,
+S_H = S (coarse partition = subdomain partition, realised by the reference's
+greedy agglomerator). Builder choices for unstated inputs (documented in
+DESIGN.md): strip-stimulus amplitude STIM_AMP, fibre angle RNG
+mt19937_64(42) with theta = pi*(rng()>>11)*2^-53 in cell order, and FHN in
+place of the unpinned Barreto-Cressman kinetics for every parity run.
+"""
+from __future__ import annotations
+
+from .simulation import SimulationConfig
+
+STIM_AMP = 2.0e4   # uA/cm^3 over the stimulated strip (chi*C_m = 1000 -> ~20 mV/ms)
+GREY_WHITE = dict(sigma_white_l=1.0, sigma_white_n=0.2, sigma_grey_l=0.5, sigma_grey_n=0.5,
+                  fiber_random=True, fiber_seed=42)
+
+
+def config1(**kw) -> SimulationConfig:
+    """1,024 cells, p=1, 16 subdomains / 16 agglomerates, sigma = 1, strip stimulus 1 ms, 100 steps."""
+    base = dict(cells=1024, lloyd=5, degree=1, subdomains=16, coarse=-1, sigma_grey_l=1.0,
+                sigma_grey_n=1.0, sigma_white_l=1.0, sigma_white_n=1.0, initial=("constant", -85.0),
+                stimulus=("strip", STIM_AMP, 0.1, 1.0), dt=0.01, T=1.0, tol=1e-8)
+    base.update(kw)
+    return SimulationConfig(**base)
+
+
+def config2(**kw) -> SimulationConfig:
+    """16,384 cells, p=3, 64 subdomains / 64 agglomerates, grey/white anisotropy, 200 steps."""
+    base = dict(cells=16384, lloyd=5, degree=3, subdomains=64, coarse=-1, dt=0.01, T=2.0, tol=1e-8,
+                **GREY_WHITE)
+    base.update(kw)
+    return SimulationConfig(**base)
+
+
+def config3(p: int, subdomains: int, **kw) -> SimulationConfig:
+    """65,536 cells, p in 1..4, S in {64, 256}, S_H = S, 50 steps."""
+    base = dict(cells=65536, lloyd=5, degree=p, subdomains=subdomains, coarse=-1, dt=0.01, T=0.5,
+                tol=1e-8, **GREY_WHITE)
+    base.update(kw)
+    return SimulationConfig(**base)
+
+
+def config4(**kw) -> SimulationConfig:
+    """1,048,576 cells, p=3, 512 subdomains, travelling-wave stimulus x < 0.05, 100 steps."""
+    base = dict(cells=1048576, lloyd=5, degree=3, subdomains=512, coarse=-1, dt=0.01, T=1.0, tol=1e-8,
+                initial=("constant", -85.0), stimulus=("strip", STIM_AMP, 0.05, 1.0), **GREY_WHITE)
+    base.update(kw)
+    return SimulationConfig(**base)
+
+
+def config5(p: int, **kw) -> SimulationConfig:
+    """config-4 mesh at p in {2, 4}, 1,024 subdomains, one solve to rtol 1e-10 from x0 = 0."""
+    base = dict(cells=1048576, lloyd=5, degree=p, subdomains=1024, coarse=-1, dt=0.01, T=0.01, tol=1e-10,
+                warm_start=False, **GREY_WHITE)
+    base.update(kw)
+    return SimulationConfig(**base)
+
+
+CONFIGS = {"config1": config1, "config2": config2, "config4": config4}

@@ -26,24 +26,19 @@ pdg::DeviceSim& S(pdg_sim* s) { return *s->d; }
 void to_device(pdg::DeviceSim& d, const double* h, double* dst, int nfields = 1) {
   const auto& pr = *d.P;
   const long long N = pr.n_global_dofs();
-  double* stage = nullptr;
-  PDG_CUDA(cudaMalloc(&stage, sizeof(double) * N * nfields));
+  double* stage = d.stage(N * nfields);
   PDG_CUDA(cudaMemcpyAsync(stage, h, sizeof(double) * N * nfields, cudaMemcpyHostToDevice, d.st));
   pdg::launch_gather_perm(stage, dst, d.d_perm, d.ncells, d.b, nfields, N, d.n, d.st);
-  PDG_CUDA(cudaStreamSynchronize(d.st));
-  cudaFree(stage);
 }
 
 void to_host(pdg::DeviceSim& d, const double* src, double* h, int nfields = 1) {
   const auto& pr = *d.P;
   const long long N = pr.n_global_dofs();
-  double* stage = nullptr;
-  PDG_CUDA(cudaMalloc(&stage, sizeof(double) * N * nfields));
-  PDG_CUDA(cudaMemsetAsync(stage, 0, sizeof(double) * N * nfields, d.st));
+  double* stage = d.stage(N * nfields);
+  if (d.world > 1) PDG_CUDA(cudaMemsetAsync(stage, 0, sizeof(double) * N * nfields, d.st));
   pdg::launch_scatter_perm(src, stage, d.d_perm, d.ncells, d.b, nfields, d.n, N, d.st);
   PDG_CUDA(cudaMemcpyAsync(h, stage, sizeof(double) * N * nfields, cudaMemcpyDeviceToHost, d.st));
   PDG_CUDA(cudaStreamSynchronize(d.st));
-  cudaFree(stage);
 }
 
 void fill_report(const pdg::PcgResult& r, pdg_pcg_report* rep) {
@@ -185,6 +180,20 @@ pdg_status pdg_sim_pcg(pdg_sim* s, const double* b, const double* x0, double tol
     const pdg::PcgResult r = d.pcg(d.d_rhs, d.d_x, d.d_x, tol, maxit);
     to_host(d, d.d_x, x);
     fill_report(r, rep);
+  });
+}
+
+pdg_status pdg_sim_timer(pdg_sim* s, int stop, double* elapsed_ms) {
+  return pdg::guarded([&] { S(s).timer(stop, elapsed_ms); });
+}
+
+int64_t pdg_sim_kernel_launches(const pdg_sim* s) { return s->d->launches; }
+
+pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9) {
+  return pdg::guarded([&] {
+    long long b[9];
+    S(s).profile(reps, ms9, b);
+    for (int i = 0; i < 9; ++i) bytes9[i] = b[i];
   });
 }
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -58,6 +59,8 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   PDG_CUDA(cudaEventCreate(&ev0));
   PDG_CUDA(cudaEventCreate(&ev1));
   PDG_CUDA(cudaEventCreate(&ev2));
+  PDG_CUDA(cudaEventCreate(&ev_t0));
+  PDG_CUDA(cudaEventCreate(&ev_t1));
   b = pr.b;
   bq = pr.two_level ? pr.bq : 0;
   ncells = pr.cell_end - pr.cell_begin;
@@ -226,7 +229,9 @@ DeviceSim::~DeviceSim() {
                   d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_order, d_bwd_order, d_task_child,
                   d_vals, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
-                  d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global};
+                  d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage};
+  cudaEventDestroy(ev_t0);
+  cudaEventDestroy(ev_t1);
   comm_destroy();
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -550,6 +555,7 @@ StepResult DeviceSim::step() {
   }
   k += 1;
   t = k * c.dt;
+  launches += (ionic ? 1 : 0) + 1 + precond_launches() + 1 + body_launches() * static_cast<long long>(res.iterations);
   float ms_all = 0.f, ms_solve = 0.f;
   cudaEventElapsedTime(&ms_all, ev0, ev2);
   cudaEventElapsedTime(&ms_solve, ev1, ev2);
@@ -561,6 +567,112 @@ StepResult DeviceSim::step() {
   out.step_ms = ms_all;
   out.solve_ms = ms_solve;
   return out;
+}
+
+}  // namespace pdg
+
+namespace pdg {
+
+// kernels issued by one precond apply (restrict, fwd, bwd sweeps, prolong+dot)
+int DeviceSim::precond_launches() const {
+  if (!use_pc()) return 1;
+  return (P->two_level ? 1 : 0) + (n_tasks > 0 ? 2 : 0) + 1;
+}
+
+// kernels per PCG iteration: spmv, update, precond, pupdate, loop condition
+// (+ finish kernels and halo packs on multi-rank runs)
+int DeviceSim::body_launches() const {
+  int k = 1 + 1 + precond_launches() + 1 + (world == 1 ? 1 : 0);
+  if (world > 1) k += 3 + static_cast<int>(halo_peers.size());
+  return k;
+}
+
+double* DeviceSim::stage(long long len) {
+  if (len > stage_len) {
+    if (d_stage) cudaFree(d_stage);
+    d_stage = dalloc<double>(len);
+    stage_len = len;
+  }
+  return d_stage;
+}
+
+void DeviceSim::timer(int stop, double* ms) {
+  if (!stop) {
+    PDG_CUDA(cudaEventRecord(ev_t0, st));
+    return;
+  }
+  PDG_CUDA(cudaEventRecord(ev_t1, st));
+  PDG_CUDA(cudaEventSynchronize(ev_t1));
+  float f = 0.f;
+  PDG_CUDA(cudaEventElapsedTime(&f, ev_t0, ev_t1));
+  if (ms) *ms = f;
+}
+
+// Times each kernel class in isolation on the live operands (device events on
+// the solver stream) and returns its algorithmic bytes per launch:
+//   0 spmv   8 nnz + 4 nnzb + 4 (rows+1) + 8 n (x) + 8 n (y) + 8 n (dot weight)
+//   1 update 8 n * 5 (x, r, p, q read; x, r written: 6 passes, p/q read once)
+//   2 restrict 8 N b bq (E) + 8 n (r) + 4 N
+//   3 sweep_fwd / 4 sweep_bwd: 8 factor values + 16 n + index arrays
+//   5 prolong_dot 8 N b bq + 24 n + 4 N ; 6 pupdate 24 n ; 7 ionic ; 8 rhs
+void DeviceSim::profile(int reps, double* ms, long long* bytes) {
+  const Problem& pr = *P;
+  reset_scalars(0.5, 1 << 30);
+  h_S->rho = 1e-30;
+  h_S->pq = 1.0;
+  PDG_CUDA(cudaMemcpyAsync(d_S, h_S, sizeof(PcgScalars), cudaMemcpyHostToDevice, st));
+  PDG_CUDA(cudaMemcpyAsync(d_p, d_U[0], n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  PDG_CUDA(cudaMemcpyAsync(d_r, d_U[0], n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const ReduceCtx rs = rctx(kFinStore);
+  cudaEvent_t a, z;
+  PDG_CUDA(cudaEventCreate(&a));
+  PDG_CUDA(cudaEventCreate(&z));
+  const long long N = ncells, nnzb = static_cast<long long>(pr.K.col.size());
+  auto timeit = [&](int slot, long long by, const std::function<void()>& f) {
+    f();
+    PDG_CUDA(cudaEventRecord(a, st));
+    for (int i = 0; i < reps; ++i) f();
+    PDG_CUDA(cudaEventRecord(z, st));
+    PDG_CUDA(cudaEventSynchronize(z));
+    float t = 0.f;
+    PDG_CUDA(cudaEventElapsedTime(&t, a, z));
+    ms[slot] = t / reps;
+    bytes[slot] = by;
+  };
+  for (int i = 0; i < 9; ++i) {
+    ms[i] = 0.0;
+    bytes[i] = 0;
+  }
+  timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 24 * n,
+         [&] { launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rs, false, st); });
+  timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
+  const long long fv = static_cast<long long>(pr.fvals.size());
+  const long long idx_bytes = 8 * static_cast<long long>(pr.row_dof.size() + pr.in_idx.size()) +
+                              4 * static_cast<long long>(pr.in_ptr.size()) + 64LL * n_tasks;
+  if (use_pc()) {
+    if (pr.two_level)
+      timeit(2, 8 * N * b * bq + 8 * n + 4 * N,
+             [&] { launch_restrict(b, bq, pr.n_agg, d_agg_ptr, d_agg_cells, d_E, d_r, d_r0, nullptr, st); });
+    timeit(3, 8 * fv + 16 * n + idx_bytes, [&] {
+      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
+      PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
+      launch_sweep_fwd(sweep_args(true, d_r, d_z, nullptr), smem_fwd, st);
+    });
+    timeit(4, 8 * fv + 16 * n + idx_bytes, [&] {
+      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
+      PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
+      launch_sweep_bwd(sweep_args(false, d_r, d_z, nullptr), smem_bwd, st);
+    });
+    timeit(5, 8 * N * b * bq + 24 * n + 4 * N,
+           [&] { launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st); });
+  }
+  timeit(6, 24 * n, [&] { launch_pupdate(n, d_tmp, d_z, d_S, false, st); });
+  timeit(8, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 8 * N * b * b + 56 * n, [&] {
+    launch_rhs(b, ncells, d_ptr, d_col, d_kval, d_M, 2.0, d_U[0], nullptr, 1, d_tmp, d_tmp2, d_q, rs, st);
+  });
+  cudaEventDestroy(a);
+  cudaEventDestroy(z);
+  PDG_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace pdg

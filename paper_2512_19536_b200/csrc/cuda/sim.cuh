@@ -113,6 +113,17 @@ class DeviceSim {
   void release_tasks();
   void comm_destroy();
 
+  // ---- measurement ----
+  long long launches = 0;  // kernels issued by step()
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  double* d_stage = nullptr;  // host<->device staging (reference order)
+  long long stage_len = 0;
+  int precond_launches() const;
+  int body_launches() const;
+  void timer(int stop, double* ms);
+  void profile(int reps, double* ms, long long* bytes);
+  double* stage(long long len);
+
  protected:
   ReduceCtx red_for(int finish);
   void after_reduce(int finish, bool honor);
