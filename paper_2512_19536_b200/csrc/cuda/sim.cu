@@ -393,7 +393,10 @@ void DeviceSim::reset_scalars(double tol, int maxit) {
 // Runs the device loop on (d_r, d_x) prepared by the caller; fills rep.
 void DeviceSim::run_solve(int maxit, PcgResult& res) {
   if (maxit + 2 > hist_cap) alloc_history(maxit + 2);
-  if (world == 1) {
+  // PDG_NO_GRAPH=1 runs the host-driven loop (kernels inside conditional
+  // graphs are invisible to ncu)
+  static const bool no_graph = std::getenv("PDG_NO_GRAPH") && std::getenv("PDG_NO_GRAPH")[0] == '1';
+  if (world == 1 && !no_graph) {
     Graph& g = graphs[use_pc() ? 1 : 0];
     if (!g.exec) build_solve_graph(g);
     PDG_CUDA(cudaGraphLaunch(g.exec, st));
@@ -403,7 +406,7 @@ void DeviceSim::run_solve(int maxit, PcgResult& res) {
     // multi-rank: host-driven loop (NCCL calls stay outside conditional
     // graphs); every rank sees the same all-reduced scalars, so all ranks
     // stop after the same iteration and issue the same collectives.
-    if (!comm) throw SolverError("multi-rank simulation: call pdg_sim_attach_comm first");
+    if (world > 1 && !comm) throw SolverError("multi-rank simulation: call pdg_sim_attach_comm first");
     record_solve_tail();
     constexpr int kPoll = 4;
     for (int it = 0; it < maxit;) {
