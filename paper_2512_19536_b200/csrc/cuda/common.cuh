@@ -20,8 +20,23 @@ namespace pdg {
 // One supernode of the Schwarz sweep (see host/problem.hpp TaskDesc).
 struct DevTask {
   int coarse, bs, w, nr;
-  long long dof0, val_off, ubuf_off;
+  long long dof0, ubuf_off;
+  int f_tile0, f_ntile, h_tile0, h_ntile;
   int rows_off, in_off, parent, child_off, n_child, pad;
+};
+
+// A CTA's share of one supernode in one sweep direction: row tiles
+// [tile_begin, tile_end) of the task's panel. Big separators are split into
+// many units so the critical path of the elimination tree streams at
+// multi-SM bandwidth.
+struct DevUnit {
+  int task, tile_begin, tile_end, nunit;  // nunit = units of this task (completion count)
+};
+
+// One 32-row tile of a supernode panel (host/problem.hpp Problem::Tile).
+struct DevTile {
+  long long off;
+  int ncol, col0, rows, stride;
 };
 
 // Scalars of one PCG solve, resident in device memory. The iteration index,
@@ -57,7 +72,7 @@ struct Reducer {
   unsigned int* counter;
 };
 
-constexpr int kSweepThreads = 256;
+constexpr int kSweepThreads = 128;
 constexpr int kVecThreads = 256;
 
 }  // namespace pdg

@@ -319,116 +319,7 @@ __global__ void restrict_kernel(const int* __restrict__ agg_ptr, const int* __re
   }
 }
 
-// ---------------- Schwarz supernode sweeps (sync-free, ticketed) ----------------
-
-__device__ __forceinline__ long long col_start(int j, int w) {
-  return static_cast<long long>(j) * w - static_cast<long long>(j) * (j - 1) / 2;
-}
-
-__global__ void __launch_bounds__(kSweepThreads) sweep_fwd_kernel(SweepArgs a) {
-  if (a.S && a.S->stop) return;
-  extern __shared__ double sm[];
-  __shared__ int s_task;
-  if (threadIdx.x == 0) s_task = a.order[atomicAdd(a.ticket, 1u)];
-  __syncthreads();
-  const int tid = s_task;
-  const DevTask T = a.tasks[tid];
-  if (threadIdx.x == 0)
-    for (int k = 0; k < T.n_child; ++k) {
-      const int c = a.task_child[T.child_off + k];
-      while (ld_acquire(a.flags + c) == 0) __nanosleep(64);
-    }
-  __syncthreads();
-  const double* in = T.coarse ? a.r0 : a.r;
-  double* out = T.coarse ? a.y0 : a.z;
-  const int w = T.w, nr = T.nr, bs = T.bs;
-  double* t = sm;
-  double* y = sm + w;
-  for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    const int cell = i / bs, rr = i - cell * bs;
-    double v = in[T.dof0 + i];
-    const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
-    for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
-    t[i] = v;
-  }
-  __syncthreads();
-  const double* Linv = a.vals + T.val_off;
-  for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    double acc0 = 0.0, acc1 = 0.0;
-    long long p = i;  // col_start(0) + i - 0
-    int j = 0;
-    for (; j + 1 <= i; j += 2) {
-      acc0 = fma(__ldg(Linv + p), t[j], acc0);
-      p += w - j - 1;
-      acc1 = fma(__ldg(Linv + p), t[j + 1], acc1);
-      p += w - j - 2;
-    }
-    if (j <= i) acc0 = fma(__ldg(Linv + p), t[j], acc0);
-    const double v = acc0 + acc1;
-    y[i] = v;
-    out[T.dof0 + i] = v;
-  }
-  __syncthreads();
-  if (nr > 0) {
-    const double* Bm = Linv + static_cast<long long>(w) * (w + 1) / 2;
-    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-      double acc0 = 0.0, acc1 = 0.0;
-      int j = 0;
-      for (; j + 1 < w; j += 2) {
-        acc0 = fma(__ldg(Bm + static_cast<long long>(j) * nr + k), y[j], acc0);
-        acc1 = fma(__ldg(Bm + static_cast<long long>(j + 1) * nr + k), y[j + 1], acc1);
-      }
-      if (j < w) acc0 = fma(__ldg(Bm + static_cast<long long>(j) * nr + k), y[j], acc0);
-      a.ubuf[T.ubuf_off + k] = acc0 + acc1;
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release(a.flags + tid, 1);
-}
-
-__global__ void __launch_bounds__(kSweepThreads) sweep_bwd_kernel(SweepArgs a) {
-  if (a.S && a.S->stop) return;
-  extern __shared__ double sm[];
-  __shared__ int s_task;
-  if (threadIdx.x == 0) s_task = a.order[atomicAdd(a.ticket, 1u)];
-  __syncthreads();
-  const int tid = s_task;
-  const DevTask T = a.tasks[tid];
-  if (threadIdx.x == 0 && T.parent >= 0)
-    while (ld_acquire(a.flags + T.parent) == 0) __nanosleep(64);
-  __syncthreads();
-  double* out = T.coarse ? a.y0 : a.z;
-  const int w = T.w, nr = T.nr, bs = T.bs;
-  double* s = sm;
-  double* xr = sm + w;
-  for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-    const int cell = k / bs, rr = k - cell * bs;
-    xr[k] = __ldcg(out + a.row_dof[T.rows_off + cell] + rr);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const double* Linv = a.vals + T.val_off;
-  const double* Bm = Linv + static_cast<long long>(w) * (w + 1) / 2;
-  for (int j = warp; j < w; j += nwarp) {
-    double acc = 0.0;
-    const double* colj = Bm + static_cast<long long>(j) * nr;
-    for (int k = lane; k < nr; k += 32) acc = fma(__ldg(colj + k), xr[k], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) s[j] = __ldcg(out + T.dof0 + j) - acc;
-  }
-  __syncthreads();
-  for (int j = warp; j < w; j += nwarp) {
-    double acc = 0.0;
-    const double* colj = Linv + col_start(j, w);
-    for (int i = j + lane; i < w; i += 32) acc = fma(__ldg(colj + (i - j)), s[i], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) out[T.dof0 + j] = acc;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release(a.flags + tid, 1);
-}
+// Schwarz supernode sweeps: see sweep.cu
 
 // ---------------- ionic terms at quadrature nodes ----------------
 
@@ -724,15 +615,6 @@ void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* ag
 #undef L
 }
 
-void launch_sweep_fwd(const SweepArgs& a, int smem, cudaStream_t st) {
-  if (a.n_tasks == 0) return;
-  sweep_fwd_kernel<<<a.n_tasks, kSweepThreads, smem, st>>>(a);
-}
-void launch_sweep_bwd(const SweepArgs& a, int smem, cudaStream_t st) {
-  if (a.n_tasks == 0) return;
-  sweep_bwd_kernel<<<a.n_tasks, kSweepThreads, smem, st>>>(a);
-}
-
 void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st) {
   finish_kernel<<<1, 1, 0, st>>>(rc, sum, honor ? 1 : 0);
 }
@@ -740,11 +622,6 @@ void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st)
 void launch_pack(const double* v, const int* cells, int ncells, int b, double* out, cudaStream_t st) {
   if (ncells == 0) return;
   pack_kernel<<<vec_grid(static_cast<long long>(ncells) * b), kVecThreads, 0, st>>>(v, cells, ncells, b, out);
-}
-
-void set_sweep_smem(int bytes) {
-  PDG_CUDA(cudaFuncSetAttribute(sweep_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  PDG_CUDA(cudaFuncSetAttribute(sweep_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 void set_gauss_nodes(const double* x, const double* w, int n) {

@@ -61,12 +61,15 @@ void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* ag
 
 struct SweepArgs {
   const DevTask* tasks;
-  const int* order;
+  const DevUnit* units;   // ticket order (topological)
+  int n_units;
+  const int* task_nunit;  // completion count per task in this direction
   int n_tasks;
   unsigned int* ticket;
   int* flags;
   const int* task_child;
-  const double* vals;
+  const double* mat;      // fmat (forward) or hmat (backward)
+  const DevTile* tiles;   // ftiles / htiles
   const long long* row_dof;
   const int* in_ptr;
   const long long* in_idx;

@@ -162,13 +162,15 @@ void DeviceSim::alloc_history(int cap) {
 }
 
 void DeviceSim::release_tasks() {
-  void* ptrs[] = {d_tasks, d_fwd_order, d_bwd_order, d_task_child, d_vals, d_row_dof, d_in_ptr, d_in_idx,
-                  d_ubuf, d_flags, d_ticket};
+  void* ptrs[] = {d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_task_child, d_fmat, d_hmat, d_ftiles, d_htiles,
+                  d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   d_tasks = nullptr;
-  d_fwd_order = d_bwd_order = d_task_child = d_in_ptr = d_flags = nullptr;
-  d_vals = d_ubuf = nullptr;
+  d_nunit = d_task_child = d_in_ptr = d_flags = nullptr;
+  d_fwd_units = d_bwd_units = nullptr;
+  d_fmat = d_hmat = d_ubuf = nullptr;
+  d_ftiles = d_htiles = nullptr;
   d_row_dof = d_in_idx = nullptr;
   d_ticket = nullptr;
 }
@@ -181,8 +183,8 @@ void DeviceSim::upload_tasks() {
   int wmax = 0, nrmax = 0;
   for (int i = 0; i < n_tasks; ++i) {
     const TaskDesc& s = pr.tasks[i];
-    t[i] = DevTask{s.coarse, s.bs, s.w, s.nr, s.dof0, s.val_off, s.ubuf_off,
-                   s.rows_off, s.in_off, s.parent, s.child_off, s.n_child, 0};
+    t[i] = DevTask{s.coarse, s.bs, s.w, s.nr, s.dof0, s.ubuf_off, s.f_tile0, s.f_ntile, s.h_tile0,
+                   s.h_ntile, s.rows_off, s.in_off, s.parent, s.child_off, s.n_child, 0};
     wmax = std::max(wmax, s.w);
     nrmax = std::max(nrmax, s.nr);
   }
@@ -200,18 +202,60 @@ void DeviceSim::upload_tasks() {
     if (A.depth != C.depth) return A.depth < C.depth;
     return A.w * (A.w + A.nr) > C.w * (C.w + C.nr);
   });
-  smem_fwd = 2 * wmax * static_cast<int>(sizeof(double));
-  smem_bwd = (wmax + nrmax) * static_cast<int>(sizeof(double));
+  // inputs + split-column partials (<= kSweepThreads doubles), sweep.cu
+  smem_fwd = (wmax + kSweepThreads) * static_cast<int>(sizeof(double));
+  smem_bwd = (wmax + nrmax + kSweepThreads) * static_cast<int>(sizeof(double));
   const int smem_max = std::max(smem_fwd, smem_bwd);
   if (smem_max > 220 * 1024)
     throw SolverError("schwarz: supernode too large for the device sweep (w=" + std::to_string(wmax) +
                       ", rows=" + std::to_string(nrmax) + ")");
   if (smem_max > 48 * 1024) set_sweep_smem(smem_max);
   d_tasks = dupload(t, st);
-  d_fwd_order = dupload(fo, st);
-  d_bwd_order = dupload(bo, st);
+  // work units: consecutive row tiles of ~kUnitBytes of panel per CTA
+  constexpr long long kUnitBytes = 32 * 1024;
+  auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units,
+                        std::vector<int>& nunit) {
+    nunit.assign(std::max(n_tasks, 1), 0);
+    for (int tk : order) {
+      const TaskDesc& s = pr.tasks[tk];
+      const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
+      const auto& tiles = fwd ? pr.ftiles : pr.htiles;
+      const int first = static_cast<int>(units.size());
+      int b0 = 0;
+      while (b0 < nt) {
+        long long bytes = 0;
+        int e = b0;
+        while (e < nt && (e == b0 || bytes + 8LL * tiles[t0 + e].ncol * tiles[t0 + e].stride <= kUnitBytes)) {
+          bytes += 8LL * tiles[t0 + e].ncol * tiles[t0 + e].stride;
+          ++e;
+        }
+        units.push_back(DevUnit{tk, b0, e, 0});
+        b0 = e;
+      }
+      nunit[tk] = static_cast<int>(units.size()) - first;
+      for (std::size_t u = first; u < units.size(); ++u) units[u].nunit = nunit[tk];
+    }
+  };
+  std::vector<DevUnit> fu, bu;
+  std::vector<int> fn, bn;
+  make_units(fo, true, fu, fn);
+  make_units(bo, false, bu, bn);
+  n_units_f = static_cast<int>(fu.size());
+  n_units_b = static_cast<int>(bu.size());
+  d_fwd_units = dupload(fu, st);
+  d_bwd_units = dupload(bu, st);
+  fn.insert(fn.end(), bn.begin(), bn.end());
+  d_nunit = dupload(fn, st);
   d_task_child = dupload(pr.task_child, st);
-  d_vals = dupload(pr.fvals, st);
+  d_fmat = dupload(pr.fmat, st);
+  d_hmat = dupload(pr.hmat, st);
+  std::vector<DevTile> ft(pr.ftiles.size()), ht(pr.htiles.size());
+  for (std::size_t i = 0; i < ft.size(); ++i)
+    ft[i] = DevTile{pr.ftiles[i].off, pr.ftiles[i].ncol, pr.ftiles[i].col0, pr.ftiles[i].rows, pr.ftiles[i].stride};
+  for (std::size_t i = 0; i < ht.size(); ++i)
+    ht[i] = DevTile{pr.htiles[i].off, pr.htiles[i].ncol, pr.htiles[i].col0, pr.htiles[i].rows, pr.htiles[i].stride};
+  d_ftiles = dupload(ft, st);
+  d_htiles = dupload(ht, st);
   std::vector<long long> rd(pr.row_dof.begin(), pr.row_dof.end());
   d_row_dof = dupload(rd, st);
   d_in_ptr = dupload(pr.in_ptr, st);
@@ -226,8 +270,8 @@ DeviceSim::~DeviceSim() {
   for (auto& g : graphs) g.reset();
   void* ptrs[] = {d_ptr, d_col, d_kval, d_M, d_Minv, d_U[0], d_U[1], d_x, d_p, d_r, d_z, d_q,
                   d_rhs, d_ion, d_tmp, d_tmp2, d_Y[0], d_Y[1], d_E, d_cell_agg, d_agg_ptr,
-                  d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_order, d_bwd_order, d_task_child,
-                  d_vals, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
+                  d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_task_child,
+                  d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
                   d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage};
   cudaEventDestroy(ev_t0);
@@ -256,12 +300,15 @@ ReduceCtx DeviceSim::rctx(int finish, double* out) {
 SweepArgs DeviceSim::sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S) {
   SweepArgs a;
   a.tasks = d_tasks;
-  a.order = fwd ? d_fwd_order : d_bwd_order;
+  a.units = fwd ? d_fwd_units : d_bwd_units;
+  a.n_units = fwd ? n_units_f : n_units_b;
+  a.task_nunit = d_nunit + (fwd ? 0 : std::max(n_tasks, 1));
   a.n_tasks = n_tasks;
   a.ticket = d_ticket + (fwd ? 0 : 1);
   a.flags = d_flags + (fwd ? 0 : std::max(n_tasks, 1));
   a.task_child = d_task_child;
-  a.vals = d_vals;
+  a.mat = fwd ? d_fmat : d_hmat;
+  a.tiles = fwd ? d_ftiles : d_htiles;
   a.row_dof = d_row_dof;
   a.in_ptr = d_in_ptr;
   a.in_idx = d_in_idx;
@@ -649,19 +696,20 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
   timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 24 * n,
          [&] { launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rs, false, st); });
   timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
-  const long long fv = static_cast<long long>(pr.fvals.size());
+  const long long fvf = static_cast<long long>(pr.fmat.size()), fvh = static_cast<long long>(pr.hmat.size());
+  const long long tile_bytes = 24LL * static_cast<long long>(pr.ftiles.size());
   const long long idx_bytes = 8 * static_cast<long long>(pr.row_dof.size() + pr.in_idx.size()) +
                               4 * static_cast<long long>(pr.in_ptr.size()) + 64LL * n_tasks;
   if (use_pc()) {
     if (pr.two_level)
       timeit(2, 8 * N * b * bq + 8 * n + 4 * N,
              [&] { launch_restrict(b, bq, pr.n_agg, d_agg_ptr, d_agg_cells, d_E, d_r, d_r0, nullptr, st); });
-    timeit(3, 8 * fv + 16 * n + idx_bytes, [&] {
+    timeit(3, 8 * fvf + 16 * n + idx_bytes + tile_bytes, [&] {
       PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
       PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
       launch_sweep_fwd(sweep_args(true, d_r, d_z, nullptr), smem_fwd, st);
     });
-    timeit(4, 8 * fv + 16 * n + idx_bytes, [&] {
+    timeit(4, 8 * fvh + 16 * n + idx_bytes + tile_bytes, [&] {
       PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
       PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
       launch_sweep_bwd(sweep_args(false, d_r, d_z, nullptr), smem_bwd, st);

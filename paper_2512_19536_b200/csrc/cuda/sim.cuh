@@ -57,8 +57,11 @@ class DeviceSim {
   int *d_cell_agg = nullptr, *d_agg_ptr = nullptr, *d_agg_cells = nullptr;
   // sweep
   DevTask* d_tasks = nullptr;
-  int *d_fwd_order = nullptr, *d_bwd_order = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;
-  double *d_vals = nullptr, *d_ubuf = nullptr;
+  int *d_nunit = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;
+  DevUnit *d_fwd_units = nullptr, *d_bwd_units = nullptr;
+  int n_units_f = 0, n_units_b = 0;
+  double *d_fmat = nullptr, *d_hmat = nullptr, *d_ubuf = nullptr;
+  DevTile *d_ftiles = nullptr, *d_htiles = nullptr;
   long long *d_row_dof = nullptr, *d_in_idx = nullptr;
   int* d_flags = nullptr;
   unsigned int* d_ticket = nullptr;

@@ -1,0 +1,121 @@
+// Device packing of the exact local factors (see problem.hpp pack_unit_tasks).
+//
+// For a supernode S with w columns and nr below rows (h = w + nr), the sweep
+// reads ONE dense panel per direction:
+//   forward   F = [ inv(L_SS) ; L_RS inv(L_SS) ]     (h x w):   [y_S ; u_S] = F t_S
+//   backward  H = F^T                                 (w x h):   x_S = H [y_S ; -x_R]
+// since x_S = inv(L_SS)^T (y_S - L_RS^T x_R) = inv(L_SS)^T y_S - (L_RS inv(L_SS))^T x_R.
+// Each task is therefore a single independent mat-vec (no intra-task
+// dependency chain). Panels are stored in 32-row tiles (column-major inside a
+// tile, last tile not padded) so a warp reads one coalesced 8*rows-byte row
+// segment per input column; the zero upper triangle of inv(L_SS) is skipped
+// at tile granularity.
+#include <algorithm>
+
+#include "problem.hpp"
+
+namespace pdg {
+
+void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {
+  constexpr int kTile = 32;
+  const int bs = F.bs;
+  const int base = static_cast<int>(pr.tasks.size());
+  const int nsn = static_cast<int>(F.sn.size());
+  std::vector<std::vector<int>> kids(nsn);
+  for (int s = 0; s < nsn; ++s)
+    if (F.sn[s].parent >= 0) kids[F.sn[s].parent].push_back(s);
+  std::vector<int> height(nsn, 0), depth(nsn, 0);
+  for (int s = 0; s < nsn; ++s)
+    for (int c : kids[s]) height[s] = std::max(height[s], height[c] + 1);
+  for (int s = nsn - 1; s >= 0; --s)
+    if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
+
+  std::vector<int> slot(nsn);
+  std::vector<double> G, Fd;
+  for (int s = 0; s < nsn; ++s) {
+    const Supernode& S = F.sn[s];
+    const int w = S.w(bs), nr = static_cast<int>(S.rows.size()) * bs, h = w + nr;
+    // G = L_RS inv(L_SS): G(k, j) = sum_{m >= j} B(k, m) Linv(m, j)
+    G.assign(static_cast<std::size_t>(nr) * w, 0.0);
+    for (int j = 0; j < w; ++j) {
+      const double* lcol = S.Linv.data() + static_cast<std::size_t>(j) * w - static_cast<std::size_t>(j) * (j - 1) / 2;
+      double* g = G.data() + static_cast<std::size_t>(j) * nr;
+      for (int m = j; m < w; ++m) {
+        const double coef = lcol[m - j];
+        if (coef == 0.0) continue;
+        const double* bcol = S.B.data() + static_cast<std::size_t>(m) * nr;
+        for (int k = 0; k < nr; ++k) g[k] += bcol[k] * coef;
+      }
+    }
+    auto Fat = [&](int i, int j) -> double {  // F(i, j)
+      if (i < w) {
+        if (i < j) return 0.0;
+        return S.Linv[static_cast<std::size_t>(j) * w - static_cast<std::size_t>(j) * (j - 1) / 2 + (i - j)];
+      }
+      return G[static_cast<std::size_t>(j) * nr + (i - w)];
+    };
+    TaskDesc t;
+    t.coarse = coarse;
+    t.bs = bs;
+    t.w = w;
+    t.nr = nr;
+    t.dof0 = dof_base + static_cast<std::int64_t>(S.s0) * bs;
+    // forward tiles: output rows of F
+    // tiles start 16-byte aligned and hold an even number of rows (a zero row
+    // pads odd tails) so each lane streams double2 pairs of rows
+    t.f_tile0 = static_cast<int>(pr.ftiles.size());
+    for (int r0 = 0; r0 < h; r0 += kTile) {
+      const int rows = std::min(kTile, h - r0), rs = rows + (rows & 1);
+      const int ncol = std::min(w, r0 + rows);
+      if (pr.fmat.size() & 1) pr.fmat.push_back(0.0);
+      pr.ftiles.push_back({static_cast<std::int64_t>(pr.fmat.size()), ncol, 0, rows, rs});
+      for (int j = 0; j < ncol; ++j)
+        for (int l = 0; l < rs; ++l) pr.fmat.push_back(l < rows ? Fat(r0 + l, j) : 0.0);
+    }
+    t.f_ntile = static_cast<int>(pr.ftiles.size()) - t.f_tile0;
+    // backward tiles: output rows of H = F^T (columns of F), inputs i >= r0
+    t.h_tile0 = static_cast<int>(pr.htiles.size());
+    for (int r0 = 0; r0 < w; r0 += kTile) {
+      const int rows = std::min(kTile, w - r0), rs = rows + (rows & 1);
+      const int ncol = h - r0;
+      if (pr.hmat.size() & 1) pr.hmat.push_back(0.0);
+      pr.htiles.push_back({static_cast<std::int64_t>(pr.hmat.size()), ncol, r0, rows, rs});
+      for (int i = r0; i < h; ++i)
+        for (int l = 0; l < rs; ++l) pr.hmat.push_back(l < rows ? Fat(i, r0 + l) : 0.0);
+    }
+    t.h_ntile = static_cast<int>(pr.htiles.size()) - t.h_tile0;
+    t.rows_off = static_cast<int>(pr.row_dof.size());
+    for (int qpos : S.rows) pr.row_dof.push_back(dof_base + static_cast<std::int64_t>(qpos) * bs);
+    t.ubuf_off = pr.ubuf_size;
+    pr.ubuf_size += nr;
+    t.parent = S.parent >= 0 ? base + S.parent : -1;
+    t.child_off = static_cast<int>(pr.task_child.size());
+    for (int c : kids[s]) pr.task_child.push_back(base + c);
+    t.n_child = static_cast<int>(kids[s].size());
+    t.height = height[s];
+    t.depth = depth[s];
+    slot[s] = static_cast<int>(pr.in_ptr.size()) - 1;
+    t.in_off = slot[s];
+    for (int cc = S.s0; cc < S.s1; ++cc) pr.in_ptr.push_back(pr.in_ptr.back());  // filled below
+    pr.tasks.push_back(t);
+  }
+  // incoming lists: (S, cell) <- ubuf slices of descendants D, in D order
+  std::vector<std::vector<std::int64_t>> inc(F.m);
+  for (int d = 0; d < nsn; ++d) {
+    const Supernode& D = F.sn[d];
+    for (std::size_t k = 0; k < D.rows.size(); ++k)
+      inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
+  }
+  for (int s = 0; s < nsn; ++s) {
+    const Supernode& S = F.sn[s];
+    int at = slot[s];
+    for (int cc = S.s0; cc < S.s1; ++cc) {
+      pr.in_idx.insert(pr.in_idx.end(), inc[cc].begin(), inc[cc].end());
+      pr.in_ptr[at + 1] = static_cast<int>(pr.in_idx.size());
+      ++at;
+    }
+  }
+  pr.factor_values = static_cast<std::int64_t>(pr.fmat.size() + pr.hmat.size());
+}
+
+}  // namespace pdg

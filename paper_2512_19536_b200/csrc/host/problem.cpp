@@ -605,65 +605,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       }, 256);
     }
   }
-  // pack fine tasks
-  auto add_unit_tasks = [&](const SupernodalFactor& F, int coarse, std::int64_t dof_base,
-                            const std::function<std::int64_t(int)>& pos_dof) {
-    const int bs = F.bs;
-    const int base = static_cast<int>(pr.tasks.size());
-    const int nsn = static_cast<int>(F.sn.size());
-    std::vector<std::vector<int>> kids(nsn);
-    for (int s = 0; s < nsn; ++s)
-      if (F.sn[s].parent >= 0) kids[F.sn[s].parent].push_back(s);
-    std::vector<int> height(nsn, 0), depth(nsn, 0);
-    for (int s = 0; s < nsn; ++s)
-      for (int c : kids[s]) height[s] = std::max(height[s], height[c] + 1);
-    for (int s = nsn - 1; s >= 0; --s)
-      if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
-    // in-slot base of each supernode
-    std::vector<int> slot(nsn);
-    for (int s = 0; s < nsn; ++s) {
-      const Supernode& S = F.sn[s];
-      TaskDesc t;
-      t.coarse = coarse;
-      t.bs = bs;
-      t.w = S.w(bs);
-      t.nr = static_cast<int>(S.rows.size()) * bs;
-      t.dof0 = dof_base + pos_dof(S.s0);
-      t.val_off = static_cast<std::int64_t>(pr.fvals.size());
-      pr.fvals.insert(pr.fvals.end(), S.Linv.begin(), S.Linv.end());
-      pr.fvals.insert(pr.fvals.end(), S.B.begin(), S.B.end());
-      t.rows_off = static_cast<int>(pr.row_dof.size());
-      for (int qpos : S.rows) pr.row_dof.push_back(dof_base + pos_dof(qpos));
-      t.ubuf_off = pr.ubuf_size;
-      pr.ubuf_size += t.nr;
-      t.parent = S.parent >= 0 ? base + S.parent : -1;
-      t.child_off = static_cast<int>(pr.task_child.size());
-      for (int c : kids[s]) pr.task_child.push_back(base + c);
-      t.n_child = static_cast<int>(kids[s].size());
-      t.height = height[s];
-      t.depth = depth[s];
-      slot[s] = static_cast<int>(pr.in_ptr.size()) - 1;
-      t.in_off = slot[s];
-      for (int cc = S.s0; cc < S.s1; ++cc) pr.in_ptr.push_back(pr.in_ptr.back());  // filled below
-      pr.tasks.push_back(t);
-    }
-    // incoming lists: (S, cell) <- ubuf slices of descendants D, in D order
-    std::vector<std::vector<std::int64_t>> inc(F.m);
-    for (int d = 0; d < nsn; ++d) {
-      const Supernode& D = F.sn[d];
-      for (std::size_t k = 0; k < D.rows.size(); ++k)
-        inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
-    }
-    for (int s = 0; s < nsn; ++s) {
-      const Supernode& S = F.sn[s];
-      int at = slot[s];
-      for (int cc = S.s0; cc < S.s1; ++cc) {
-        pr.in_idx.insert(pr.in_idx.end(), inc[cc].begin(), inc[cc].end());
-        pr.in_ptr[at + 1] = static_cast<int>(pr.in_idx.size());
-        ++at;
-      }
-    }
-  };
+  // pack fine tasks (host/pack.cpp)
   pr.in_ptr = {0};
   for (const UnitFactor& uf : factors) {
     std::int64_t base;
@@ -671,8 +613,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       base = static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b;
     else
       base = static_cast<std::int64_t>(&uf - factors.data()) * b;
-    add_unit_tasks(uf.F, 0, base, [b](int pos) { return static_cast<std::int64_t>(pos) * b; });
-    pr.factor_values += uf.F.values();
+    pack_unit_tasks(pr, uf.F, 0, base);
   }
   pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
   factors.clear();
@@ -838,61 +779,8 @@ void finish_coarse(Problem& pr) {
   } catch (const SolverError&) {
     throw SolverError("schwarz: coarse operator factorization failed");
   }
-  // pack coarse tasks (vector set 1: r0 -> y0)
-  const int bs = F.bs;
-  const int base = static_cast<int>(pr.tasks.size());
-  const int nsn = static_cast<int>(F.sn.size());
-  std::vector<std::vector<int>> kids(nsn);
-  for (int s = 0; s < nsn; ++s)
-    if (F.sn[s].parent >= 0) kids[F.sn[s].parent].push_back(s);
-  std::vector<int> height(nsn, 0), depth(nsn, 0);
-  for (int s = 0; s < nsn; ++s)
-    for (int c : kids[s]) height[s] = std::max(height[s], height[c] + 1);
-  for (int s = nsn - 1; s >= 0; --s)
-    if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
-  std::vector<int> slot(nsn);
-  for (int s = 0; s < nsn; ++s) {
-    const Supernode& S = F.sn[s];
-    TaskDesc td;
-    td.coarse = 1;
-    td.bs = bs;
-    td.w = S.w(bs);
-    td.nr = static_cast<int>(S.rows.size()) * bs;
-    td.dof0 = static_cast<std::int64_t>(S.s0) * bs;
-    td.val_off = static_cast<std::int64_t>(pr.fvals.size());
-    pr.fvals.insert(pr.fvals.end(), S.Linv.begin(), S.Linv.end());
-    pr.fvals.insert(pr.fvals.end(), S.B.begin(), S.B.end());
-    td.rows_off = static_cast<int>(pr.row_dof.size());
-    for (int qpos : S.rows) pr.row_dof.push_back(static_cast<std::int64_t>(qpos) * bs);
-    td.ubuf_off = pr.ubuf_size;
-    pr.ubuf_size += td.nr;
-    td.parent = S.parent >= 0 ? base + S.parent : -1;
-    td.child_off = static_cast<int>(pr.task_child.size());
-    for (int c : kids[s]) pr.task_child.push_back(base + c);
-    td.n_child = static_cast<int>(kids[s].size());
-    td.height = height[s];
-    td.depth = depth[s];
-    slot[s] = static_cast<int>(pr.in_ptr.size()) - 1;
-    td.in_off = slot[s];
-    for (int cc = S.s0; cc < S.s1; ++cc) pr.in_ptr.push_back(pr.in_ptr.back());
-    pr.tasks.push_back(td);
-  }
-  std::vector<std::vector<std::int64_t>> inc(F.m);
-  for (int d = 0; d < nsn; ++d) {
-    const Supernode& D = F.sn[d];
-    for (std::size_t k = 0; k < D.rows.size(); ++k)
-      inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
-  }
-  for (int s = 0; s < nsn; ++s) {
-    const Supernode& S = F.sn[s];
-    int at = slot[s];
-    for (int cc = S.s0; cc < S.s1; ++cc) {
-      pr.in_idx.insert(pr.in_idx.end(), inc[cc].begin(), inc[cc].end());
-      pr.in_ptr[at + 1] = static_cast<int>(pr.in_idx.size());
-      ++at;
-    }
-  }
-  pr.factor_values += F.values();
+  // coarse tasks use vector set 1 (r0 -> y0) and follow the fine ones
+  pack_unit_tasks(pr, F, 1, 0);
 }
 
 }  // namespace pdg

@@ -34,7 +34,8 @@ struct TaskDesc {
   int w = 0;           // supernode columns (cells * bs)
   int nr = 0;          // below rows (|R| * bs)
   std::int64_t dof0 = 0;    // first dof of the supernode in its vector
-  std::int64_t val_off = 0; // Linv (w(w+1)/2) then B (nr*w)
+  int f_tile0 = 0, f_ntile = 0;  // forward tiles of F = [inv(L_SS); L_RS inv(L_SS)]
+  int h_tile0 = 0, h_ntile = 0;  // backward tiles of H = F^T
   int rows_off = 0;    // R cell dof-starts in row_dof[rows_off .. + nr/bs)
   std::int64_t ubuf_off = 0;  // update buffer slot (nr doubles)
   int in_off = 0;      // incoming CSR: in_ptr[in_off .. in_off + w/bs]
@@ -64,7 +65,14 @@ struct Problem {
   // Schwarz local solves
   std::vector<TaskDesc> tasks;
   std::vector<int> task_child, fwd_order, bwd_order;
-  std::vector<double> fvals;     // all Linv/B values
+  // Row-tiled dense panels: tile t covers output rows [32k, 32k+rows) of its
+  // task; element (row r0+l, input col0+j) at mat[off + j*rows + l].
+  struct Tile {
+    std::int64_t off;
+    int ncol, col0, rows, stride;  // stride = rows rounded up to even
+  };
+  std::vector<double> fmat, hmat;    // forward / backward panels
+  std::vector<Tile> ftiles, htiles;
   std::vector<std::int64_t> row_dof;  // below-row cell dof starts
   std::vector<int> in_ptr;       // incoming CSR (per supernode cell slot)
   std::vector<std::int64_t> in_idx;   // ubuf offsets
@@ -95,6 +103,11 @@ struct Problem {
   std::int64_t n_local_dofs() const { return static_cast<std::int64_t>(cell_end - cell_begin) * b; }
   std::int64_t n_global_dofs() const { return static_cast<std::int64_t>(mesh.n_cells()) * b; }
 };
+
+// Appends the supernodes of one exact local factor (fine subdomain, coarse=0,
+// or the coarse problem, coarse=1) as device tasks: panels, tiles, row maps,
+// incoming update lists and the tree links (host/pack.cpp).
+void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base);
 
 void validate_config(const pdg_config& cfg);
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
