@@ -37,7 +37,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "PCG DOF-iterations/s and solve time per CN step; % of HBM roofline, 1/2/4/8 GPU"
 UNIT = "DOF-iter/s"
-KERNELS = ["spmv", "update", "restrict", "sweep_fwd", "sweep_bwd", "prolong_dot", "pupdate", "ionic", "rhs"]
+KERNELS = ["spmv", "update", "restrict", "sweep", "restrict_combine", "prolong_dot", "pupdate", "ionic", "rhs"]
 REF_BUDGET_S = 150.0
 
 
@@ -265,7 +265,7 @@ def main():
     kby = (C.c_int64 * 9)()
     _lib.check(L.pdg_sim_profile(sim._h, 20, kms, kby))
     per_step = {"spmv": its / args.steps, "update": its / args.steps}
-    for k in ("restrict", "sweep_fwd", "sweep_bwd", "prolong_dot", "pupdate"):
+    for k in ("restrict", "sweep", "restrict_combine", "prolong_dot", "pupdate"):
         per_step[k] = its / args.steps + 1
     per_step["rhs"] = 1
     shares = {k: kms[i] * per_step.get(k, 0) / (elapsed_ms / args.steps) for i, k in enumerate(KERNELS)}
@@ -278,9 +278,9 @@ def main():
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
     # bytes of one whole PCG iteration vs its device time (all kernels of the body)
-    iter_bytes = sum(kby[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep_fwd", "sweep_bwd",
+    iter_bytes = sum(kby[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep", "restrict_combine",
                                                       "prolong_dot", "pupdate"))
-    iter_ms = sum(kms[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep_fwd", "sweep_bwd",
+    iter_ms = sum(kms[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep", "restrict_combine",
                                                    "prolong_dot", "pupdate"))
 
     cpu = None

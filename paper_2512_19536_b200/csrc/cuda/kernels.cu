@@ -485,6 +485,19 @@ __global__ void scatter_perm_kernel(const double* __restrict__ src, double* __re
   }
 }
 
+// r0[node] = sum of the node's chunk partials, fixed order
+__global__ void restrict_combine_kernel(int bq, int n_agg, const int* __restrict__ node_chunk_ptr,
+                                        const double* __restrict__ part, double* __restrict__ r0,
+                                        const PcgScalars* S) {
+  if (S && S->stop) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_agg * bq) return;
+  const int a = i / bq, m = i - a * bq;
+  double s = 0.0;
+  for (int ch = node_chunk_ptr[a]; ch < node_chunk_ptr[a + 1]; ++ch) s += part[static_cast<long long>(ch) * bq + m];
+  r0[i] = s;
+}
+
 // Multi-rank: the producing kernel stored its local sum; after the NCCL
 // all-reduce this applies the finish on every rank identically.
 __global__ void finish_kernel(ReduceCtx rc, const double* sum, int honor) {
@@ -613,6 +626,12 @@ void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* ag
 #define L(B) restrict_dispatch<B>(bq, n_agg, agg_ptr, agg_cells, E, r, r0, S, st)
   PDG_B_DISPATCH(b, L)
 #undef L
+}
+
+void launch_restrict_combine(int bq, int n_agg, const int* node_chunk_ptr, const double* part, double* r0,
+                             const PcgScalars* S, cudaStream_t st) {
+  const int n = n_agg * bq;
+  restrict_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(bq, n_agg, node_chunk_ptr, part, r0, S);
 }
 
 void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st) {

@@ -59,17 +59,25 @@ void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* ag
                      const double* E, const double* r, double* r0, const PcgScalars* S,
                      cudaStream_t st);
 
+// r0 chunk partials -> r0 (one CTA-sized chunk of an agglomerate per restrict CTA)
+void launch_restrict_combine(int bq, int n_agg, const int* node_chunk_ptr, const double* part, double* r0,
+                             const PcgScalars* S, cudaStream_t st);
+
+// One launch runs the forward units (tickets [0, n_units_f)) then the
+// backward units; counters: flags[task] forward, flags[n_tasks + task] backward.
 struct SweepArgs {
   const DevTask* tasks;
-  const DevUnit* units;   // ticket order (topological)
-  int n_units;
-  const int* task_nunit;  // completion count per task in this direction
+  const DevUnit* units;   // ticket order (topological): forward units, then backward units
+  int n_units_f, n_units;
+  const int* task_nunit;  // [fwd n_tasks | bwd n_tasks] completion counts
   int n_tasks;
   unsigned int* ticket;
-  int* flags;
+  int* flags;             // [fwd n_tasks | bwd n_tasks]
   const int* task_child;
-  const double* mat;      // fmat (forward) or hmat (backward)
-  const DevTile* tiles;   // ftiles / htiles
+  const double* fmat;
+  const double* hmat;
+  const DevTile* ftiles;
+  const DevTile* htiles;
   const long long* row_dof;
   const int* in_ptr;
   const long long* in_idx;
@@ -80,8 +88,7 @@ struct SweepArgs {
   double* y0;
   const PcgScalars* S;
 };
-void launch_sweep_fwd(const SweepArgs& a, int smem_bytes, cudaStream_t st);
-void launch_sweep_bwd(const SweepArgs& a, int smem_bytes, cudaStream_t st);
+void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
 
 // Ionic model + stimulus at quadrature nodes (one warp per cell).
 struct IonicArgs {

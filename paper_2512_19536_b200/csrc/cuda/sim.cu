@@ -119,6 +119,17 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     d_agg_cells = dupload(pr.agg_cells, st);
     d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
     d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
+    // restriction chunks: <= 64 cells of one agglomerate per CTA
+    std::vector<int> cptr{0}, nptr{0};
+    for (int a = 0; a < pr.n_agg; ++a) {
+      for (int k = pr.agg_cell_ptr[a]; k < pr.agg_cell_ptr[a + 1]; k += 64)
+        cptr.push_back(std::min(k + 64, pr.agg_cell_ptr[a + 1]));
+      nptr.push_back(static_cast<int>(cptr.size()) - 1);
+    }
+    n_chunks = static_cast<int>(cptr.size()) - 1;
+    d_chunk_ptr = dupload(cptr, st);
+    d_node_chunk_ptr = dupload(nptr, st);
+    d_r0part = dalloc<double>(static_cast<std::size_t>(std::max(n_chunks, 1)) * pr.bq);
   }
   upload_tasks();
 
@@ -240,10 +251,11 @@ void DeviceSim::upload_tasks() {
   std::vector<int> fn, bn;
   make_units(fo, true, fu, fn);
   make_units(bo, false, bu, bn);
+  // one ticket space: forward units, then backward units (sweep.cu)
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
+  fu.insert(fu.end(), bu.begin(), bu.end());
   d_fwd_units = dupload(fu, st);
-  d_bwd_units = dupload(bu, st);
   fn.insert(fn.end(), bn.begin(), bn.end());
   d_nunit = dupload(fn, st);
   d_task_child = dupload(pr.task_child, st);
@@ -273,7 +285,7 @@ DeviceSim::~DeviceSim() {
                   d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_task_child,
                   d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
-                  d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage};
+                  d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage, d_chunk_ptr, d_node_chunk_ptr, d_r0part};
   cudaEventDestroy(ev_t0);
   cudaEventDestroy(ev_t1);
   comm_destroy();
@@ -297,18 +309,21 @@ ReduceCtx DeviceSim::rctx(int finish, double* out) {
   return rc;
 }
 
-SweepArgs DeviceSim::sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S) {
+SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScalars* S) {
   SweepArgs a;
   a.tasks = d_tasks;
-  a.units = fwd ? d_fwd_units : d_bwd_units;
-  a.n_units = fwd ? n_units_f : n_units_b;
-  a.task_nunit = d_nunit + (fwd ? 0 : std::max(n_tasks, 1));
-  a.n_tasks = n_tasks;
-  a.ticket = d_ticket + (fwd ? 0 : 1);
-  a.flags = d_flags + (fwd ? 0 : std::max(n_tasks, 1));
+  a.units = d_fwd_units;
+  a.n_units_f = n_units_f;
+  a.n_units = n_units_f + n_units_b;
+  a.task_nunit = d_nunit;
+  a.n_tasks = std::max(n_tasks, 1);
+  a.ticket = d_ticket;
+  a.flags = d_flags;
   a.task_child = d_task_child;
-  a.mat = fwd ? d_fmat : d_hmat;
-  a.tiles = fwd ? d_ftiles : d_htiles;
+  a.fmat = d_fmat;
+  a.hmat = d_hmat;
+  a.ftiles = d_ftiles;
+  a.htiles = d_htiles;
   a.row_dof = d_row_dof;
   a.in_ptr = d_in_ptr;
   a.in_idx = d_in_idx;
@@ -333,13 +348,13 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
     return;
   }
   if (pr.two_level) {
-    launch_restrict(b, bq, pr.n_agg, d_agg_ptr, d_agg_cells, d_E, r, d_r0, Sh, st);
+    launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, r, d_r0part, Sh, st);
+    launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, Sh, st);
     coarse_reduce_hook();
   }
-  PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
+  PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
   PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-  launch_sweep_fwd(sweep_args(true, r, z, Sh), smem_fwd, st);
-  launch_sweep_bwd(sweep_args(false, r, z, Sh), smem_bwd, st);
+  launch_sweep(sweep_args(true, r, z, Sh), std::max(smem_fwd, smem_bwd), st);
   launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
   after_reduce(finish, honor);
 }
@@ -626,7 +641,7 @@ namespace pdg {
 // kernels issued by one precond apply (restrict, fwd, bwd sweeps, prolong+dot)
 int DeviceSim::precond_launches() const {
   if (!use_pc()) return 1;
-  return (P->two_level ? 1 : 0) + (n_tasks > 0 ? 2 : 0) + 1;
+  return (P->two_level ? 2 : 0) + (n_tasks > 0 ? 1 : 0) + 1;
 }
 
 // kernels per PCG iteration: spmv, update, precond, pupdate, loop condition
@@ -701,18 +716,17 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
   const long long idx_bytes = 8 * static_cast<long long>(pr.row_dof.size() + pr.in_idx.size()) +
                               4 * static_cast<long long>(pr.in_ptr.size()) + 64LL * n_tasks;
   if (use_pc()) {
-    if (pr.two_level)
-      timeit(2, 8 * N * b * bq + 8 * n + 4 * N,
-             [&] { launch_restrict(b, bq, pr.n_agg, d_agg_ptr, d_agg_cells, d_E, d_r, d_r0, nullptr, st); });
-    timeit(3, 8 * fvf + 16 * n + idx_bytes + tile_bytes, [&] {
-      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
+    if (pr.two_level) {
+      timeit(2, 8 * N * b * bq + 8 * n + 4 * N + 8LL * n_chunks * bq,
+             [&] { launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_r, d_r0part, nullptr, st); });
+      timeit(4, 16LL * n_chunks * bq + 8LL * pr.n_agg * bq,
+             [&] { launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, nullptr, st); });
+    }
+    // slot 3: the fused forward + backward sweep (panels F and H once each)
+    timeit(3, 8 * (fvf + fvh) + 32 * n + 2 * (idx_bytes + tile_bytes), [&] {
+      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
       PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-      launch_sweep_fwd(sweep_args(true, d_r, d_z, nullptr), smem_fwd, st);
-    });
-    timeit(4, 8 * fvh + 16 * n + idx_bytes + tile_bytes, [&] {
-      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 2 * sizeof(unsigned int), st));
-      PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-      launch_sweep_bwd(sweep_args(false, d_r, d_z, nullptr), smem_bwd, st);
+      launch_sweep(sweep_args(true, d_r, d_z, nullptr), std::max(smem_fwd, smem_bwd), st);
     });
     timeit(5, 8 * N * b * bq + 24 * n + 4 * N,
            [&] { launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st); });

@@ -55,6 +55,9 @@ class DeviceSim {
   // coarse
   double *d_E = nullptr, *d_r0 = nullptr, *d_y0 = nullptr;
   int *d_cell_agg = nullptr, *d_agg_ptr = nullptr, *d_agg_cells = nullptr;
+  int n_chunks = 0;
+  int *d_chunk_ptr = nullptr, *d_node_chunk_ptr = nullptr;
+  double* d_r0part = nullptr;
   // sweep
   DevTask* d_tasks = nullptr;
   int *d_nunit = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;

@@ -1,20 +1,22 @@
-// Schwarz local solves and the coarse solve as one sync-free supernode sweep
-// per direction (replaces the parallel_for of LLT / SimplicialLLT solves,
-// /root/reference/proj/src/schwarz.cpp:155-167).
+// Schwarz local solves and the coarse solve as ONE sync-free supernode sweep
+// (forward then backward in a single launch), replacing the parallel_for of
+// LLT / SimplicialLLT solves (/root/reference/proj/src/schwarz.cpp:155-167).
 //
-// Every CTA takes a ticket in topological order (forward: children first;
-// backward: parents first), so a CTA only ever waits on tasks whose units all
-// hold smaller tickets, i.e. are already running: deadlock-free without a
-// grid barrier, and subdomains of very different sizes (1.77x at config 4)
-// overlap instead of running in waves.
+// Every CTA takes a ticket; tickets enumerate forward units in topological
+// order (children first) and then backward units (parents first). A CTA only
+// ever waits on units with smaller tickets, which are already running, so the
+// sweep is deadlock-free without a grid barrier, subdomains of very different
+// sizes (1.77x at config 4) overlap instead of running in waves, and the
+// backward sweep of a finished subtree starts while other subtrees are still
+// in their forward sweep.
 // Each supernode is ONE dense mat-vec over its row-tiled panel (host/pack.cpp):
 //   forward : [y_S ; u_S] = F (r_S - sum of incoming descendant updates u_D)
 //   backward: x_S         = H [y_S ; -x_R]
-// and is cut into units of row tiles, one CTA each, so the large separators
-// on the critical path of the elimination tree stream at multi-SM bandwidth.
-// Inside a unit a warp streams a (tile, column-chunk) item: each half-warp
-// takes every other input column and each lane a double2 (two rows), with 8
-// loads in flight per lane.
+// cut into units of row tiles, one CTA each, so the large separators on the
+// critical path of the elimination tree stream at multi-SM bandwidth. Inside
+// a unit a warp streams a (tile, column-chunk) item: each half-warp takes
+// every other input column and each lane a double2 (two rows), 8 loads in
+// flight per lane.
 // Results of other tasks (update slices, ancestor x) are read with ld.cg so a
 // stale L1 line can never be observed; a unit publishes with barrier + fence
 // + a release add on the task's completion counter.
@@ -32,34 +34,33 @@ __device__ __forceinline__ int ld_acquire_s(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void wait_count(const int* flag, int need) {
+  while (ld_acquire_s(flag) < need) __nanosleep(20);
+}
 
 constexpr int kWarps = kSweepThreads / 32;
 constexpr int kMaxSmemTiles = 32;
 
 template <bool FWD>
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
-  if (a.S && a.S->stop) return;
-  extern __shared__ double sm[];
-  __shared__ DevUnit s_unit;
-  __shared__ DevTile s_tiles[kMaxSmemTiles];
-  if (threadIdx.x == 0) s_unit = a.units[atomicAdd(a.ticket, 1u)];
-  __syncthreads();
-  const DevUnit U = s_unit;
+__device__ __forceinline__ void run_unit(const SweepArgs& a, const DevUnit& U, double* sm, DevTile* s_tiles) {
   const DevTask T = a.tasks[U.task];
   const int ntile = U.tile_end - U.tile_begin;
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
+  const DevTile* tiles = FWD ? a.ftiles : a.htiles;
+  const double* mat = FWD ? a.fmat : a.hmat;
   // tile descriptors do not depend on other tasks: fetch them while waiting
-  for (int i = threadIdx.x; i < ntile && i < kMaxSmemTiles; i += blockDim.x) s_tiles[i] = a.tiles[tile0 + i];
+  for (int i = threadIdx.x; i < ntile && i < kMaxSmemTiles; i += blockDim.x) s_tiles[i] = tiles[tile0 + i];
   if (threadIdx.x == 0) {
     if (FWD) {
       for (int k = 0; k < T.n_child; ++k) {
         const int c = a.task_child[T.child_off + k];
-        const int need = a.task_nunit[c];
-        while (ld_acquire_s(a.flags + c) < need) __nanosleep(20);
+        wait_count(a.flags + c, a.task_nunit[c]);
       }
     } else if (T.parent >= 0) {
-      const int need = a.task_nunit[T.parent];
-      while (ld_acquire_s(a.flags + T.parent) < need) __nanosleep(20);
+      wait_count(a.flags + a.n_tasks + T.parent, a.task_nunit[a.n_tasks + T.parent]);
+    } else {
+      // a root's backward needs its own forward result
+      wait_count(a.flags + U.task, a.task_nunit[U.task]);
     }
   }
   __syncthreads();
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
       xin[i] = v;
     }
   } else {
-    // only inputs i >= first row of this unit are touched (H is upper triangular in its first w columns)
+    // only inputs i >= first row of this unit are touched (H's first w columns are upper triangular)
     const int i0 = U.tile_begin * 32;
     for (int i = i0 + threadIdx.x; i < h; i += blockDim.x) {
       if (i < w) {
@@ -95,12 +96,12 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
   const int half = lane >> 4, l2 = lane & 15;
   for (int it = warp; it < items; it += kWarps) {
     const int R = it / split, c = it - R * split;
-    const DevTile tl = R < kMaxSmemTiles ? s_tiles[R] : a.tiles[tile0 + R];
+    const DevTile tl = R < kMaxSmemTiles ? s_tiles[R] : tiles[tile0 + R];
     const int chunk = (((tl.ncol + split - 1) / split) + 1) & ~1;  // even: halves keep their parity
     const int j0 = c * chunk, j1 = min(tl.ncol, j0 + chunk);
     double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
     if (2 * l2 < tl.rows) {
-      const double2* m = reinterpret_cast<const double2*>(a.mat + tl.off) + l2;
+      const double2* m = reinterpret_cast<const double2*>(mat + tl.off) + l2;
       const long long cs = tl.stride >> 1;  // double2 per column
       const double* x = xin + tl.col0;
       int j = j0 + half;
@@ -164,25 +165,36 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    red_release_add(a.flags + U.task, 1);
+    red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, 1);
   }
+}
+
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
+  if (a.S && a.S->stop) return;
+  extern __shared__ double sm[];
+  __shared__ int s_ticket;
+  __shared__ DevUnit s_unit;
+  __shared__ DevTile s_tiles[kMaxSmemTiles];
+  if (threadIdx.x == 0) {
+    const int tk = static_cast<int>(atomicAdd(a.ticket, 1u));
+    s_ticket = tk;
+    s_unit = a.units[tk];
+  }
+  __syncthreads();
+  const DevUnit U = s_unit;
+  if (s_ticket < a.n_units_f) run_unit<true>(a, U, sm, s_tiles);
+  else run_unit<false>(a, U, sm, s_tiles);
 }
 
 }  // namespace
 
-void launch_sweep_fwd(const SweepArgs& a, int smem, cudaStream_t st) {
+void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
   if (a.n_units == 0) return;
-  sweep_kernel<true><<<a.n_units, kSweepThreads, smem, st>>>(a);
-}
-
-void launch_sweep_bwd(const SweepArgs& a, int smem, cudaStream_t st) {
-  if (a.n_units == 0) return;
-  sweep_kernel<false><<<a.n_units, kSweepThreads, smem, st>>>(a);
+  sweep_kernel<<<a.n_units, kSweepThreads, smem, st>>>(a);
 }
 
 void set_sweep_smem(int bytes) {
-  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 }  // namespace pdg
