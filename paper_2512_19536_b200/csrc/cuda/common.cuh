@@ -29,8 +29,15 @@ struct DevTask {
 // [tile_begin, tile_end) of the task's panel. Big separators are split into
 // many units so the critical path of the elimination tree streams at
 // multi-SM bandwidth.
+// Two kinds: whole tiles [tile_begin, tile_end) (nchunk == 1), or one column
+// chunk [c0, c1) of a single wide tile (nchunk > 1) whose partial sums land in
+// part slot part_base + chunk; the last chunk to finish (tile counter) reduces
+// them in chunk order.
 struct DevUnit {
-  int task, tile_begin, tile_end, nunit;  // nunit = units of this task (completion count)
+  int task, tile_begin, tile_end, c0, c1, chunk, nchunk, part_base, tile_ctr, dir, pad0, pad1;
+  long long src_off;  // first panel double staged by TMA
+  int bytes;          // staged bytes (multiple of 16)
+  int pad2;
 };
 
 // One 32-row tile of a supernode panel (host/problem.hpp Problem::Tile).

@@ -69,10 +69,11 @@ struct SweepArgs {
   const DevTask* tasks;
   const DevUnit* units;   // ticket order (topological): forward units, then backward units
   int n_units_f, n_units;
-  const int* task_nunit;  // [fwd n_tasks | bwd n_tasks] completion counts
   int n_tasks;
   unsigned int* ticket;
-  int* flags;             // [fwd n_tasks | bwd n_tasks]
+  int* flags;             // tiles completed: [fwd n_tasks | bwd n_tasks]
+  int* tile_ctr;          // chunks completed per split tile
+  double* part;           // 32 partial sums per column chunk
   const int* task_child;
   const double* fmat;
   const double* hmat;
@@ -88,7 +89,7 @@ struct SweepArgs {
   double* y0;
   const PcgScalars* S;
 };
-void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
+void launch_sweep(const SweepArgs& a, int smem_bytes, int panel_doubles, cudaStream_t st);
 
 // Ionic model + stimulus at quadrature nodes (one warp per cell).
 struct IonicArgs {

@@ -173,14 +173,14 @@ void DeviceSim::alloc_history(int cap) {
 }
 
 void DeviceSim::release_tasks() {
-  void* ptrs[] = {d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_task_child, d_fmat, d_hmat, d_ftiles, d_htiles,
+  void* ptrs[] = {d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_part, d_task_child, d_fmat, d_hmat, d_ftiles, d_htiles,
                   d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   d_tasks = nullptr;
   d_nunit = d_task_child = d_in_ptr = d_flags = nullptr;
   d_fwd_units = d_bwd_units = nullptr;
-  d_fmat = d_hmat = d_ubuf = nullptr;
+  d_fmat = d_hmat = d_ubuf = d_part = nullptr;
   d_ftiles = d_htiles = nullptr;
   d_row_dof = d_in_idx = nullptr;
   d_ticket = nullptr;
@@ -213,51 +213,90 @@ void DeviceSim::upload_tasks() {
     if (A.depth != C.depth) return A.depth < C.depth;
     return A.w * (A.w + A.nr) > C.w * (C.w + C.nr);
   });
-  // inputs + split-column partials (<= kSweepThreads doubles), sweep.cu
-  smem_fwd = (wmax + kSweepThreads) * static_cast<int>(sizeof(double));
-  smem_bwd = (wmax + nrmax + kSweepThreads) * static_cast<int>(sizeof(double));
-  const int smem_max = std::max(smem_fwd, smem_bwd);
-  if (smem_max > 220 * 1024)
-    throw SolverError("schwarz: supernode too large for the device sweep (w=" + std::to_string(wmax) +
-                      ", rows=" + std::to_string(nrmax) + ")");
-  if (smem_max > 48 * 1024) set_sweep_smem(smem_max);
+  (void)wmax;
+  (void)nrmax;
   d_tasks = dupload(t, st);
-  // work units: consecutive row tiles of ~kUnitBytes of panel per CTA
-  constexpr long long kUnitBytes = 32 * 1024;
-  auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units,
-                        std::vector<int>& nunit) {
-    nunit.assign(std::max(n_tasks, 1), 0);
+  // Work units of <= kUnitBytes of panel: runs of whole tiles, or column
+  // chunks of one wide tile (partials reduced by the last chunk, sweep.cu).
+  constexpr long long kUnitBytes = 16 * 1024;
+  int n_parts = 0, n_tile_ctr = 0;
+  long long max_panel = 0, max_in = 0;
+  auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units) {
     for (int tk : order) {
       const TaskDesc& s = pr.tasks[tk];
       const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
-      const int first = static_cast<int>(units.size());
+      auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };
       int b0 = 0;
       while (b0 < nt) {
+        const auto& tb = tiles[t0 + b0];
+        if (tbytes(b0) > kUnitBytes) {
+          // column chunks of an even number of columns
+          long long cols = kUnitBytes / (8LL * tb.stride);
+          cols = std::max<long long>(2, cols & ~1LL);
+          const int nch = static_cast<int>((tb.ncol + cols - 1) / cols);
+          for (int c = 0; c < nch; ++c) {
+            const int c0 = static_cast<int>(c * cols), c1 = std::min<int>(tb.ncol, static_cast<int>((c + 1) * cols));
+            DevUnit u{};
+            u.task = tk;
+            u.tile_begin = b0;
+            u.tile_end = b0 + 1;
+            u.c0 = c0;
+            u.c1 = c1;
+            u.chunk = c;
+            u.nchunk = nch;
+            u.part_base = n_parts;
+            u.tile_ctr = n_tile_ctr;
+            u.dir = fwd ? 0 : 1;
+            u.src_off = tb.off + static_cast<long long>(c0) * tb.stride;
+            u.bytes = static_cast<int>(8LL * (c1 - c0) * tb.stride);
+            max_panel = std::max<long long>(max_panel, u.bytes);
+            max_in = std::max<long long>(max_in, c1 - c0);
+            units.push_back(u);
+          }
+          n_parts += nch;
+          ++n_tile_ctr;
+          ++b0;
+          continue;
+        }
         long long bytes = 0;
         int e = b0;
-        while (e < nt && (e == b0 || bytes + 8LL * tiles[t0 + e].ncol * tiles[t0 + e].stride <= kUnitBytes)) {
-          bytes += 8LL * tiles[t0 + e].ncol * tiles[t0 + e].stride;
+        while (e < nt && tbytes(e) <= kUnitBytes && (e == b0 || bytes + tbytes(e) <= kUnitBytes)) {
+          bytes += tbytes(e);
           ++e;
         }
-        units.push_back(DevUnit{tk, b0, e, 0});
+        DevUnit u{};
+        u.task = tk;
+        u.tile_begin = b0;
+        u.tile_end = e;
+        u.nchunk = 1;
+        u.dir = fwd ? 0 : 1;
+        u.src_off = tb.off;
+        u.bytes = static_cast<int>(bytes);
+        int lo = tiles[t0 + b0].col0, hi = 0;
+        for (int r = b0; r < e; ++r) hi = std::max(hi, tiles[t0 + r].col0 + tiles[t0 + r].ncol);
+        max_panel = std::max(max_panel, bytes);
+        max_in = std::max<long long>(max_in, hi - lo);
+        units.push_back(u);
         b0 = e;
       }
-      nunit[tk] = static_cast<int>(units.size()) - first;
-      for (std::size_t u = first; u < units.size(); ++u) units[u].nunit = nunit[tk];
     }
   };
   std::vector<DevUnit> fu, bu;
-  std::vector<int> fn, bn;
-  make_units(fo, true, fu, fn);
-  make_units(bo, false, bu, bn);
+  make_units(fo, true, fu);
+  make_units(bo, false, bu);
   // one ticket space: forward units, then backward units (sweep.cu)
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
   fu.insert(fu.end(), bu.begin(), bu.end());
   d_fwd_units = dupload(fu, st);
-  fn.insert(fn.end(), bn.begin(), bn.end());
-  d_nunit = dupload(fn, st);
+  n_tile_ctrs = std::max(n_tile_ctr, 1);
+  d_nunit = dalloc<int>(n_tile_ctrs);  // chunk counters of split tiles
+  d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
+  panel_doubles = static_cast<int>((max_panel + 127) / 128 * 16);
+  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (panel_doubles + kSweepThreads + static_cast<int>(max_in) + 2);
+  if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
+  if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   d_task_child = dupload(pr.task_child, st);
   d_fmat = dupload(pr.fmat, st);
   d_hmat = dupload(pr.hmat, st);
@@ -315,7 +354,8 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.units = d_fwd_units;
   a.n_units_f = n_units_f;
   a.n_units = n_units_f + n_units_b;
-  a.task_nunit = d_nunit;
+  a.tile_ctr = d_nunit;
+  a.part = d_part;
   a.n_tasks = std::max(n_tasks, 1);
   a.ticket = d_ticket;
   a.flags = d_flags;
@@ -354,7 +394,8 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
   }
   PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
   PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-  launch_sweep(sweep_args(true, r, z, Sh), std::max(smem_fwd, smem_bwd), st);
+  PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
+  launch_sweep(sweep_args(true, r, z, Sh), smem_fwd, panel_doubles, st);
   launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
   after_reduce(finish, honor);
 }
@@ -726,7 +767,8 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
     timeit(3, 8 * (fvf + fvh) + 32 * n + 2 * (idx_bytes + tile_bytes), [&] {
       PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
       PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-      launch_sweep(sweep_args(true, d_r, d_z, nullptr), std::max(smem_fwd, smem_bwd), st);
+      PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
+      launch_sweep(sweep_args(true, d_r, d_z, nullptr), smem_fwd, panel_doubles, st);
     });
     timeit(5, 8 * N * b * bq + 24 * n + 4 * N,
            [&] { launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st); });
