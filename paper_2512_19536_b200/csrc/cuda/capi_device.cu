@@ -211,3 +211,33 @@ pdg_status pdg_sim_pcg_device(pdg_sim* s, const double* d_b, const double* d_x0,
 }
 
 }  // extern "C"
+
+namespace pdg {
+
+int DeviceSim::trace_sweep(long long* out, int cap) {
+  const int nu = n_units_f + n_units_b;
+  if (!d_trace) PDG_CUDA(cudaMalloc(&d_trace, sizeof(long long) * 4 * std::max(nu, 1)));
+  PDG_CUDA(cudaMemcpyAsync(d_tmp2, d_r, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  apply_precond(d_tmp2, d_z);
+  std::vector<long long> tr(4 * static_cast<std::size_t>(nu));
+  PDG_CUDA(cudaMemcpy(tr.data(), d_trace, tr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  cudaFree(d_trace);
+  d_trace = nullptr;
+  for (int u = 0; u < nu && u < cap; ++u) {
+    long long* o = out + 8LL * u;
+    for (int k = 0; k < 4; ++k) o[k] = tr[4 * u + k];
+    o[4] = h_units[u].task;
+    o[5] = h_units[u].dir;
+    o[6] = h_units[u].bytes;
+    o[7] = h_units[u].nchunk;
+  }
+  return nu;
+}
+
+}  // namespace pdg
+
+extern "C" int pdg_sim_trace_sweep(pdg_sim* s, long long* out, int cap) {
+  int n = -1;
+  pdg::guarded([&] { n = S(s).trace_sweep(out, cap); });
+  return n;
+}

@@ -34,10 +34,13 @@ struct DevTask {
 // part slot part_base + chunk; the last chunk to finish (tile counter) reduces
 // them in chunk order.
 struct DevUnit {
-  int task, tile_begin, tile_end, c0, c1, chunk, nchunk, part_base, tile_ctr, dir, pad0, pad1;
+  int task, tile_begin, tile_end, c0, c1, chunk, nchunk, part_base, tile_ctr, dir;
+  int n_dep;          // flags to wait on (> 2: walk the task's children)
+  int dep[2], need[2];
+  int own_fwd;        // backward: own forward counter index (its y_S), -1 for forward units
   long long src_off;  // first panel double staged by TMA
   int bytes;          // staged bytes (multiple of 16)
-  int pad2;
+  int own_need;
 };
 
 // One 32-row tile of a supernode panel (host/problem.hpp Problem::Tile).

@@ -88,6 +88,8 @@ struct SweepArgs {
   const double* r0;
   double* y0;
   const PcgScalars* S;
+  int stage_meta;  // stage gather maps in smem before the dependency wait
+  long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, int panel_doubles, cudaStream_t st);
 

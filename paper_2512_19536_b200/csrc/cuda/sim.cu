@@ -218,9 +218,37 @@ void DeviceSim::upload_tasks() {
   d_tasks = dupload(t, st);
   // Work units of <= kUnitBytes of panel: runs of whole tiles, or column
   // chunks of one wide tile (partials reduced by the last chunk, sweep.cu).
-  constexpr long long kUnitBytes = 16 * 1024;
+  // unit size (panel bytes per CTA visit); PDG_UNIT_KB overrides
+  static const long long kUnitBytes =
+      1024LL * (std::getenv("PDG_UNIT_KB") ? std::max(2, std::atoi(std::getenv("PDG_UNIT_KB"))) : 32);
   int n_parts = 0, n_tile_ctr = 0;
   long long max_panel = 0, max_in = 0;
+  // dependency counters a unit waits on (sweep.cu): forward = children's
+  // forward tiles, backward = parent's backward tiles (roots: own forward)
+  const int nt_flag = std::max(n_tasks, 1);
+  auto set_deps = [&](DevUnit& u, int tk, bool fwd) {
+    const TaskDesc& s = pr.tasks[tk];
+    u.own_fwd = -1;
+    u.own_need = 0;
+    if (fwd) {
+      u.n_dep = s.n_child;
+      for (int k = 0; k < s.n_child && k < 2; ++k) {
+        const int c = pr.task_child[s.child_off + k];
+        u.dep[k] = c;
+        u.need[k] = pr.tasks[c].f_ntile;
+      }
+    } else if (s.parent >= 0) {
+      u.n_dep = 1;
+      u.dep[0] = nt_flag + s.parent;
+      u.need[0] = pr.tasks[s.parent].h_ntile;
+      u.own_fwd = tk;
+      u.own_need = s.f_ntile;
+    } else {
+      u.n_dep = 1;
+      u.dep[0] = tk;
+      u.need[0] = s.f_ntile;
+    }
+  };
   auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units) {
     for (int tk : order) {
       const TaskDesc& s = pr.tasks[tk];
@@ -252,6 +280,7 @@ void DeviceSim::upload_tasks() {
             u.bytes = static_cast<int>(8LL * (c1 - c0) * tb.stride);
             max_panel = std::max<long long>(max_panel, u.bytes);
             max_in = std::max<long long>(max_in, c1 - c0);
+            set_deps(u, tk, fwd);
             units.push_back(u);
           }
           n_parts += nch;
@@ -277,6 +306,7 @@ void DeviceSim::upload_tasks() {
         for (int r = b0; r < e; ++r) hi = std::max(hi, tiles[t0 + r].col0 + tiles[t0 + r].ncol);
         max_panel = std::max(max_panel, bytes);
         max_in = std::max<long long>(max_in, hi - lo);
+        set_deps(u, tk, fwd);
         units.push_back(u);
         b0 = e;
       }
@@ -289,11 +319,13 @@ void DeviceSim::upload_tasks() {
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
   fu.insert(fu.end(), bu.begin(), bu.end());
+  h_units = fu;
   d_fwd_units = dupload(fu, st);
   n_tile_ctrs = std::max(n_tile_ctr, 1);
   d_nunit = dalloc<int>(n_tile_ctrs);  // chunk counters of split tiles
   d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
-  panel_doubles = static_cast<int>((max_panel + 127) / 128 * 16);
+  (void)max_panel;
+  panel_doubles = 0;  // panels stream from L2 (bulk-prefetched), not staged in smem
   smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (panel_doubles + kSweepThreads + static_cast<int>(max_in) + 2);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
@@ -373,6 +405,9 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.r0 = d_r0;
   a.y0 = d_y0;
   a.S = S;
+  static const int stage_meta = std::getenv("PDG_SWEEP_META") ? std::atoi(std::getenv("PDG_SWEEP_META")) : 1;
+  a.stage_meta = stage_meta;
+  a.trace = d_trace;
   return a;
 }
 

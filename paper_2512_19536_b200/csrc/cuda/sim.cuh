@@ -129,6 +129,11 @@ class DeviceSim {
   int body_launches() const;
   void timer(int stop, double* ms);
   void profile(int reps, double* ms, long long* bytes);
+  // one traced preconditioner sweep: 8 int64 per unit (4 globaltimer stamps,
+  // task, direction, staged bytes, chunks); returns the unit count
+  long long* d_trace = nullptr;
+  std::vector<DevUnit> h_units;
+  int trace_sweep(long long* out, int cap);
   double* stage(long long len);
 
  protected:

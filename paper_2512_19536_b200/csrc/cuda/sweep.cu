@@ -12,10 +12,16 @@
 //   forward : [y_S ; u_S] = F (r_S - sum of incoming descendant updates u_D)
 //   backward: x_S         = H [y_S ; -x_R]
 // cut into units of <= 16 KB of panel: whole 32-row tiles, or column chunks
-// of a wide tile. A unit stages its panel bytes into shared memory with one
-// TMA bulk copy (cp.async.bulk + mbarrier) issued BEFORE it waits for its
-// dependencies, so HBM streaming is taken off the elimination tree's critical
-// path; after the wait only the input gather and an smem mat-vec remain.
+// of a wide tile.
+//
+// The elimination tree's critical path is a chain of dependent memory round
+// trips, so a unit splits its CTA by role: thread 0 starts polling its (at
+// most two, precomputed) dependency counters immediately, while warps 1-3
+// issue the TMA bulk copy of the unit's panel slice into shared memory
+// (cp.async.bulk + mbarrier), stage tile descriptors and the static gather
+// maps, and prefetch every input that does not depend on the awaited tasks.
+// After the wait only one level of dependent loads (descendant update slices
+// or ancestor x) and an smem mat-vec remain on the critical path.
 // Column chunks write 32 partial sums each; the last chunk of a tile to finish
 // (counter) reduces them in chunk order, so results are deterministic.
 // Results of other tasks are read with ld.cg; a unit publishes with barrier +
@@ -41,8 +47,17 @@ __device__ __forceinline__ int atom_acq_rel_add(int* p, int v) {
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void wait_count(const int* flag, int need) {
-  while (ld_acquire_s(flag) < need) __nanosleep(20);
+  while (ld_acquire_s(flag) < need) __nanosleep(16);
+}
+// named barrier for the staging warps (1..kWarps-1) only
+__device__ __forceinline__ void staging_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kSweepThreads - 32) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -74,31 +89,51 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, int phase) {
 
 constexpr int kWarps = kSweepThreads / 32;
 constexpr int kMaxSmemTiles = 32;
+constexpr int kMetaCells = 160;  // staged in_ptr entries per unit
+constexpr int kMetaIdx = 768;    // staged update offsets / row dof starts per unit
 
-// one warp: out rows of tile `tl` restricted to input columns [j0, j1) from the
-// staged panel `m` (tile base in smem); returns (row 2*l2, row 2*l2+1) sums in half 0
+struct UnitSmem {
+  DevUnit u;
+  DevTask t;
+  int col_lo, col_hi, cell_lo, meta, last;
+  DevTile tiles[kMaxSmemTiles];
+  int iptr[kMetaCells];
+  long long idx[kMetaIdx];
+  uint64_t bar;
+};
+
+// one warp: rows of tile `tl` restricted to input columns [j0, j1) of the
+// panel `m` (tile base, global, L2-prefetched); (row 2*l2, row 2*l2+1) sums in half 0
 __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, const double* x, int j0, int j1) {
   const int lane = threadIdx.x & 31, half = lane >> 4, l2 = lane & 15;
-  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
   if (2 * l2 < tl.rows) {
     const double2* mm = reinterpret_cast<const double2*>(m) + l2;
-    const int cs = tl.stride >> 1;
+    const long long cs = tl.stride >> 1;
     int j = j0 + half;
-    for (; j + 2 < j1; j += 4) {
-      const double2 v0 = mm[j * cs], v1 = mm[(j + 2) * cs];
-      const double x0 = x[j], x1 = x[j + 2];
-      acc0.x = fma(v0.x, x0, acc0.x);
-      acc0.y = fma(v0.y, x0, acc0.y);
-      acc1.x = fma(v1.x, x1, acc1.x);
-      acc1.y = fma(v1.y, x1, acc1.y);
+    for (; j + 14 < j1; j += 16) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(mm + (j + 2 * u) * cs);
+#pragma unroll
+      for (int u = 0; u < 8; u += 4) {
+        acc0.x = fma(v[u].x, x[j + 2 * u], acc0.x);
+        acc0.y = fma(v[u].y, x[j + 2 * u], acc0.y);
+        acc1.x = fma(v[u + 1].x, x[j + 2 * u + 2], acc1.x);
+        acc1.y = fma(v[u + 1].y, x[j + 2 * u + 2], acc1.y);
+        acc2.x = fma(v[u + 2].x, x[j + 2 * u + 4], acc2.x);
+        acc2.y = fma(v[u + 2].y, x[j + 2 * u + 4], acc2.y);
+        acc3.x = fma(v[u + 3].x, x[j + 2 * u + 6], acc3.x);
+        acc3.y = fma(v[u + 3].y, x[j + 2 * u + 6], acc3.y);
+      }
     }
     for (; j < j1; j += 2) {
-      const double2 v0 = mm[j * cs];
+      const double2 v0 = __ldg(mm + j * cs);
       acc0.x = fma(v0.x, x[j], acc0.x);
       acc0.y = fma(v0.y, x[j], acc0.y);
     }
   }
-  double vx = acc0.x + acc1.x, vy = acc0.y + acc1.y;
+  double vx = (acc0.x + acc1.x) + (acc2.x + acc3.x), vy = (acc0.y + acc1.y) + (acc2.y + acc3.y);
   vx += __shfl_down_sync(0xffffffffu, vx, 16);
   vy += __shfl_down_sync(0xffffffffu, vy, 16);
   return make_double2(vx, vy);
@@ -110,70 +145,139 @@ __device__ __forceinline__ void store_row(const SweepArgs& a, const DevTask& T, 
   else a.ubuf[T.ubuf_off + (o - T.w)] = v;
 }
 
+// warps 1..3: everything that does not depend on the awaited tasks
 template <bool FWD>
-__device__ __forceinline__ void run_unit(const SweepArgs& a, const DevUnit& U, double* panel, double* xin,
-                                         double* part, DevTile* s_tiles, uint64_t* bar) {
-  const DevTask T = a.tasks[U.task];
+__device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* panel, double* xin) {
+  const int t = threadIdx.x - 32;  // 0 .. kSweepThreads-33
+  const int nst = kSweepThreads - 32;
+  const DevUnit& U = s.u;
+  if (t == 0) {
+    s.t = a.tasks[U.task];
+    // TMA bulk prefetch of the unit's panel into L2 while the unit waits
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((FWD ? a.fmat : a.hmat) + U.src_off),
+                 "r"(U.bytes)
+                 : "memory");
+  }
+  staging_sync();
+  const DevTask& T = s.t;
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
   const int ntile = U.tile_end - U.tile_begin;
   const DevTile* tiles = FWD ? a.ftiles : a.htiles;
-  const double* mat = FWD ? a.fmat : a.hmat;
-  // 1. stage this unit's panel bytes (independent of other tasks) ...
-  if (threadIdx.x == 0) tma_load_1d(panel, mat + U.src_off, U.bytes, bar);
-  for (int i = threadIdx.x; i < ntile && i < kMaxSmemTiles; i += blockDim.x) s_tiles[i] = tiles[tile0 + i];
-  // 2. ... while waiting for the tasks it reads
+  for (int i = t; i < ntile && i < kMaxSmemTiles; i += nst) s.tiles[i] = tiles[tile0 + i];
+  staging_sync();
+  const int bs = T.bs, w = T.w;
+  const DevTile t0 = s.tiles[0];
+  const int col_lo = t0.col0 + (U.nchunk > 1 ? U.c0 : 0);
+  int col_hi = t0.col0 + (U.nchunk > 1 ? U.c1 : t0.ncol);
+  for (int r = 1; r < ntile && r < kMaxSmemTiles; ++r) col_hi = max(col_hi, s.tiles[r].col0 + s.tiles[r].ncol);
+  const int cell_lo = col_lo / bs, cell_hi = (col_hi + bs - 1) / bs;
+  if (t == 0) {
+    s.col_lo = col_lo;
+    s.col_hi = col_hi;
+    s.cell_lo = cell_lo;
+  }
+  int meta = 0;
+  if (FWD) {
+    // independent part of the inputs: r (or r0) itself
+    const double* in = T.coarse ? a.r0 : a.r;
+    for (int i = col_lo + t; i < col_hi; i += nst) xin[i - col_lo] = in[T.dof0 + i];
+    const int nc = cell_hi - cell_lo;
+    if (a.stage_meta && nc + 1 <= kMetaCells) {
+      for (int c = t; c <= nc; c += nst) s.iptr[c] = a.in_ptr[T.in_off + cell_lo + c];
+      staging_sync();
+      const int e0 = s.iptr[0], ne = s.iptr[nc] - e0;
+      if (ne <= kMetaIdx) {
+        for (int k = t; k < ne; k += nst) s.idx[k] = a.in_idx[e0 + k];
+        meta = 1;
+      }
+    }
+  } else {
+    const int r_lo = max(col_lo, w);
+    const int rc0 = (r_lo - w) / bs;
+    const int nr_cells = col_hi > w ? (col_hi - w + bs - 1) / bs - rc0 : 0;
+    if (a.stage_meta && nr_cells <= kMetaIdx) {
+      for (int k = t; k < nr_cells; k += nst) s.idx[k] = a.row_dof[T.rows_off + rc0 + k];
+      meta = 1;
+    }
+    // own y_S (this task's forward result) is independent of the awaited ancestors
+    if (U.own_fwd >= 0 && col_lo < w) {
+      if (t == 0) wait_count(a.flags + U.own_fwd, U.own_need);
+      staging_sync();
+      double* outv = T.coarse ? a.y0 : a.z;
+      for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(outv + T.dof0 + i);
+    }
+  }
+  if (t == 0) s.meta = meta;
+}
+
+template <bool FWD>
+__device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* panel, double* xin, double* part,
+                                         int phase, int tk) {
+  long long* tr = a.trace ? a.trace + 4LL * tk : nullptr;
   if (threadIdx.x == 0) {
-    if (FWD) {
+    if (tr) tr[0] = gtimer();
+    const DevUnit& U = s.u;
+    if (U.n_dep <= 2) {
+      for (int d = 0; d < U.n_dep; ++d) wait_count(a.flags + U.dep[d], U.need[d]);
+    } else {  // many children: walk the task's child list
+      const DevTask T = a.tasks[U.task];
       for (int k = 0; k < T.n_child; ++k) {
         const int c = a.task_child[T.child_off + k];
         wait_count(a.flags + c, a.tasks[c].f_ntile);
       }
-    } else if (T.parent >= 0) {
-      wait_count(a.flags + a.n_tasks + T.parent, a.tasks[T.parent].h_ntile);
-    } else {
-      wait_count(a.flags + U.task, T.f_ntile);  // a root's backward needs its own forward
     }
+    if (tr) tr[1] = gtimer();
+  } else if (threadIdx.x >= 32) {
+    stage<FWD>(a, s, panel, xin);
   }
   __syncthreads();
-  // 3. gather the input columns this unit touches
+  const DevUnit& U = s.u;
+  const DevTask& T = s.t;
   const int w = T.w, bs = T.bs;
+  const int col_lo = s.col_lo, col_hi = s.col_hi, cell_lo = s.cell_lo;
+  const bool meta = s.meta;
   double* outv = T.coarse ? a.y0 : a.z;
-  const DevTile t0 = s_tiles[0];
-  const int col_lo = t0.col0 + (U.nchunk > 1 ? U.c0 : 0);
-  int col_hi = t0.col0 + (U.nchunk > 1 ? U.c1 : t0.ncol);
-  for (int r = 1; r < ntile && r < kMaxSmemTiles; ++r) col_hi = max(col_hi, s_tiles[r].col0 + s_tiles[r].ncol);
+  // the one dependent gather level
   if (FWD) {
-    const double* in = T.coarse ? a.r0 : a.r;
     for (int i = col_lo + threadIdx.x; i < col_hi; i += blockDim.x) {
       const int cell = i / bs, rr = i - cell * bs;
-      double v = in[T.dof0 + i];
-      const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
-      for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
+      double v = xin[i - col_lo];
+      if (meta) {
+        const int e0 = s.iptr[0];
+        for (int k = s.iptr[cell - cell_lo]; k < s.iptr[cell - cell_lo + 1]; ++k)
+          v -= __ldcg(a.ubuf + s.idx[k - e0] + rr);
+      } else {
+        const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
+        for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
+      }
       xin[i - col_lo] = v;
     }
   } else {
-    for (int i = col_lo + threadIdx.x; i < col_hi; i += blockDim.x) {
+    const int rc0 = (max(col_lo, w) - w) / bs;
+    const int i_start = (U.own_fwd >= 0) ? max(col_lo, w) : col_lo;  // own y already staged
+    for (int i = i_start + threadIdx.x; i < col_hi; i += blockDim.x) {
       double v;
       if (i < w) {
         v = __ldcg(outv + T.dof0 + i);
       } else {
         const int k = i - w, cell = k / bs, rr = k - cell * bs;
-        v = -__ldcg(outv + a.row_dof[T.rows_off + cell] + rr);
+        const long long base = meta ? s.idx[cell - rc0] : a.row_dof[T.rows_off + cell];
+        v = -__ldcg(outv + base + rr);
       }
       xin[i - col_lo] = v;
     }
   }
-  mbar_wait(bar, 0);
   __syncthreads();
-  // 4. smem mat-vec
+  if (tr && threadIdx.x == 0) tr[2] = gtimer();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, l2 = lane & 15;
+  const int ntile = U.tile_end - U.tile_begin;
   if (U.nchunk > 1) {
     // one tile, columns [c0, c1): warps split the columns, partials to global
-    const DevTile tl = t0;
+    const DevTile tl = s.tiles[0];
     const int nc = U.c1 - U.c0;
     const int per = (((nc + kWarps - 1) / kWarps) + 1) & ~1;
     const int j0 = warp * per, j1 = min(nc, j0 + per);
-    const double2 v = tile_dot(panel, tl, xin, j0, j1);
+    const double2 v = tile_dot((FWD ? a.fmat : a.hmat) + U.src_off, tl, xin, j0, j1);
     if (lane < 16) {
       part[warp * 32 + 2 * l2] = v.x;
       part[warp * 32 + 2 * l2 + 1] = v.y;
@@ -181,34 +285,36 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, const DevUnit& U, d
     __syncthreads();
     double* gp = a.part + static_cast<long long>(U.part_base + U.chunk) * 32;
     if (threadIdx.x < 32) {
-      double s = 0.0;
-      for (int q = 0; q < kWarps; ++q) s += part[q * 32 + threadIdx.x];
-      __stcg(gp + threadIdx.x, s);
+      double sum = 0.0;
+      for (int q = 0; q < kWarps; ++q) sum += part[q * 32 + threadIdx.x];
+      __stcg(gp + threadIdx.x, sum);
     }
     __syncthreads();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = atom_acq_rel_add(a.tile_ctr + U.tile_ctr, 1) == U.nchunk - 1;
+    if (threadIdx.x == 0) s.last = atom_acq_rel_add(a.tile_ctr + U.tile_ctr, 1) == U.nchunk - 1;
     __syncthreads();
-    if (!s_last) return;
+    if (!s.last) {
+      if (tr && threadIdx.x == 0) tr[3] = gtimer();
+      return;
+    }
     if (threadIdx.x < tl.rows) {
-      double s = 0.0;
+      double sum = 0.0;
       const double* base = a.part + static_cast<long long>(U.part_base) * 32 + threadIdx.x;
-      for (int c = 0; c < U.nchunk; ++c) s += __ldcg(base + c * 32);
-      store_row<FWD>(a, T, outv, U.tile_begin * 32 + threadIdx.x, s);
+      for (int c = 0; c < U.nchunk; ++c) sum += __ldcg(base + c * 32);
+      store_row<FWD>(a, T, outv, U.tile_begin * 32 + threadIdx.x, sum);
     }
     __syncthreads();
     if (threadIdx.x == 0) red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, 1);
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     return;
   }
   // whole tiles: items = (tile, column split) over the warps
   const int split = ntile >= kWarps ? 1 : kWarps / ntile;
   const int items = ntile * split;
-  const double* pbase = panel;
-  // tile R's smem base = sum of previous tile sizes
+  const DevTile* gtiles = (FWD ? a.ftiles : a.htiles) + (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
   for (int it = warp; it < items; it += kWarps) {
     const int R = it / split, c = it - R * split;
-    const DevTile tl = R < kMaxSmemTiles ? s_tiles[R] : tiles[tile0 + R];
-    const double* m = pbase + (tl.off - U.src_off);
+    const DevTile tl = R < kMaxSmemTiles ? s.tiles[R] : gtiles[R];
+    const double* m = (FWD ? a.fmat : a.hmat) + tl.off;
     const int chunk = (((tl.ncol + split - 1) / split) + 1) & ~1;
     const int j0 = c * chunk, j1 = min(tl.ncol, j0 + chunk);
     const double2 v = tile_dot(m, tl, xin + (tl.col0 - col_lo), j0, j1);
@@ -227,7 +333,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, const DevUnit& U, d
     __syncthreads();
     for (int q = threadIdx.x; q < ntile * 32; q += blockDim.x) {
       const int R = q >> 5, l = q & 31;
-      if (l >= s_tiles[R].rows) continue;
+      if (l >= s.tiles[R].rows) continue;
       double v = 0.0;
       for (int c = 0; c < split; ++c) v += part[(R * split + c) * 32 + l];
       store_row<FWD>(a, T, outv, (U.tile_begin + R) * 32 + l, v);
@@ -235,36 +341,55 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, const DevUnit& U, d
   }
   __syncthreads();
   if (threadIdx.x == 0) red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, ntile);
+  if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
+// Persistent: resident CTAs loop over tickets in increasing order, so the
+// lowest unfinished ticket is always being processed and its dependencies
+// (smaller tickets) are finished or in progress — no deadlock, no per-unit
+// CTA launch cost.
 __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a, int panel_doubles) {
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
+  __shared__ UnitSmem s;
   __shared__ int s_ticket;
-  __shared__ DevUnit s_unit;
-  __shared__ DevTile s_tiles[kMaxSmemTiles];
-  __shared__ __align__(8) uint64_t s_bar;
   if (threadIdx.x == 0) {
-    const int tk = static_cast<int>(atomicAdd(a.ticket, 1u));
-    s_ticket = tk;
-    s_unit = a.units[tk];
-    mbar_init(&s_bar, 1);
+    mbar_init(&s.bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  const DevUnit U = s_unit;
   double* panel = sm;
-  double* part = sm + panel_doubles;          // kSweepThreads doubles
+  double* part = sm + panel_doubles;  // kSweepThreads doubles
   double* xin = part + kSweepThreads;
-  if (s_ticket < a.n_units_f) run_unit<true>(a, U, panel, xin, part, s_tiles, &s_bar);
-  else run_unit<false>(a, U, panel, xin, part, s_tiles, &s_bar);
+  for (int phase = 0;; phase ^= 1) {
+    if (threadIdx.x == 0) {
+      const int tk = static_cast<int>(atomicAdd(a.ticket, 1u));
+      s_ticket = tk;
+      if (tk < a.n_units) s.u = a.units[tk];
+    }
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= a.n_units) break;
+    if (tk < a.n_units_f) run_unit<true>(a, s, panel, xin, part, phase, tk);
+    else run_unit<false>(a, s, panel, xin, part, phase, tk);
+    __syncthreads();
+  }
 }
 
 }  // namespace
 
 void launch_sweep(const SweepArgs& a, int smem, int panel_doubles, cudaStream_t st) {
   if (a.n_units == 0) return;
-  sweep_kernel<<<a.n_units, kSweepThreads, smem, st>>>(a, panel_doubles);
+  static int cached_smem = -1, resident = 0;
+  if (cached_smem != smem) {
+    int per_sm = 0, sms = 0, dev = 0;
+    PDG_CUDA(cudaGetDevice(&dev));
+    PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel, kSweepThreads, smem));
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    cached_smem = smem;
+  }
+  const int grid = a.n_units < resident ? a.n_units : resident;
+  sweep_kernel<<<grid, kSweepThreads, smem, st>>>(a, panel_doubles);
 }
 
 void set_sweep_smem(int bytes) {

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <numeric>
@@ -270,7 +271,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
   }
   // ND inside each multi-cell subdomain
-  const int leaf = std::clamp(64 / b, 4, 16);
+  // nested-dissection leaf size (cells): dense leaves of ~64 dofs; PDG_ND_LEAF overrides
+  int leaf = std::clamp(64 / b, 4, 16);
+  if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
   parallel_for(n_units, [&](int u) {
