@@ -124,6 +124,12 @@ int64_t pdg_problem_export(const pdg_problem* p, int which, int64_t* rows, int64
 void pdg_problem_owner(const pdg_problem* p, int which, int* owner);
 /* internal order: perm[i] = reference cell of internal position i */
 void pdg_problem_perm(const pdg_problem* p, int* perm);
+/* multi-rank layout: internal cell range per rank (world+1 entries) and the
+ * SpMV halo against `peer`: send = this rank's local cells (relative to its
+ * first cell), recv = peer's global internal cells; counts = {nsend, nrecv};
+ * NULL arrays query the sizes */
+void pdg_problem_rank_cells(const pdg_problem* p, int* starts);
+void pdg_problem_halo(const pdg_problem* p, int peer, int* send, int* recv, int counts[2]);
 
 /* ---- simulation on the device (Simulation, timestepper.hpp:109-152) ---- */
 typedef struct pdg_sim pdg_sim;
@@ -184,6 +190,10 @@ int64_t pdg_sim_kernel_launches(const pdg_sim* s);
  * launch, slots: 0 spmv, 1 update, 2 restrict, 3 sweep_fwd, 4 sweep_bwd,
  * 5 prolong_dot, 6 pupdate, 7 ionic, 8 rhs */
 pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9);
+/* one traced Schwarz sweep: 8 int64 per work unit (globaltimer at start, deps
+ * met, inputs staged, published; task, direction, panel bytes, chunks);
+ * returns the unit count (scripts/sweep_trace.py) */
+int pdg_sim_trace_sweep(pdg_sim* s, long long* out, int cap);
 
 /* default_max_iterations (krylov.cpp:12-15) and condition_estimate (:85-103) */
 int pdg_default_max_iterations(int64_t n);

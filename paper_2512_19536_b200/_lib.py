@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
             "pdg_problem_export": (i64, [vp, i32, P(i64), P(i64), P(dbl)]),
             "pdg_problem_owner": (None, [vp, i32, P(i32)]),
             "pdg_problem_perm": (None, [vp, P(i32)]),
+            "pdg_problem_rank_cells": (None, [vp, P(i32)]),
+            "pdg_problem_halo": (None, [vp, i32, P(i32), P(i32), P(i32)]),
             "pdg_default_max_iterations": (i32, [i64]),
         }
         for name, (res, args) in sig.items():
@@ -131,6 +133,7 @@ def _bind_device(L):
         "pdg_sim_timer": (i32, [vp, i32, P(dbl)]),
         "pdg_sim_kernel_launches": (i64, [vp]),
         "pdg_sim_profile": (i32, [vp, i32, P(dbl), P(i64)]),
+        "pdg_sim_trace_sweep": (i32, [vp, P(i64), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -266,3 +266,24 @@ int64_t problem_export(const Problem& pr, int which, int64_t* rows, int64_t* col
 }
 
 }  // namespace pdg
+
+extern "C" {
+
+// SpMV halo of this rank against `peer` (host/pack.cpp halo_plan): send = local
+// internal cells (relative to the rank's first cell), recv = global internal
+// cells; counts[0..1] = sizes. Arrays may be NULL to query the sizes.
+void pdg_problem_halo(const pdg_problem* h, int peer, int* send, int* recv, int counts[2]) {
+  std::vector<std::vector<int>> s, r;
+  pdg::halo_plan(*h->p, s, r);
+  counts[0] = static_cast<int>(s[peer].size());
+  counts[1] = static_cast<int>(r[peer].size());
+  if (send) std::copy(s[peer].begin(), s[peer].end(), send);
+  if (recv) std::copy(r[peer].begin(), r[peer].end(), recv);
+}
+
+// internal cell range of every rank: world+1 entries
+void pdg_problem_rank_cells(const pdg_problem* h, int* starts) {
+  std::copy(h->p->rank_cell_start.begin(), h->p->rank_cell_start.end(), starts);
+}
+
+}  // extern "C"

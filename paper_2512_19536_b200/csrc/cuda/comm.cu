@@ -117,32 +117,23 @@ void DeviceSim::attach_comm(const void* id128, int r, int w) {
   d_dot_local = dmalloc<double>(1);
   d_dot_global = dmalloc<double>(1);
 
-  // halo plan from the global mesh adjacency (identical on every rank)
-  auto owner_rank = [&](int g) {
-    return static_cast<int>(std::upper_bound(pr.rank_cell_start.begin(), pr.rank_cell_start.end(), g) -
-                            pr.rank_cell_start.begin()) - 1;
-  };
-  std::vector<std::vector<int>> send(w);
-  for (const Face& f : pr.mesh.interior_faces()) {
-    const int a = pr.iperm[f.cell_in], c2 = pr.iperm[f.cell_out];
-    const int ra = owner_rank(a), rc = owner_rank(c2);
-    if (ra == rc) continue;
-    if (ra == r) send[rc].push_back(a - pr.cell_begin);
-    if (rc == r) send[ra].push_back(c2 - pr.cell_begin);
-  }
+  // halo plan from the global mesh adjacency (identical on every rank, host/pack.cpp)
+  std::vector<std::vector<int>> send, recv;
+  halo_plan(pr, send, recv);
   std::vector<int> send_cells;
   halo_peers.clear();
   for (int peer = 0; peer < w; ++peer) {
     if (peer == r) continue;
-    auto& s = send[peer];
-    std::sort(s.begin(), s.end());
-    s.erase(std::unique(s.begin(), s.end()), s.end());
+    const auto& s = send[peer];
     HaloPeer h{peer, static_cast<int>(send_cells.size()), static_cast<int>(s.size()), 0, 0};
     send_cells.insert(send_cells.end(), s.begin(), s.end());
     const auto lo = std::lower_bound(halo_cells.begin(), halo_cells.end(), pr.rank_cell_start[peer]);
     const auto hi = std::lower_bound(halo_cells.begin(), halo_cells.end(), pr.rank_cell_start[peer + 1]);
     h.recv_off = static_cast<int>(lo - halo_cells.begin());
     h.recv_count = static_cast<int>(hi - lo);
+    if (h.recv_count != static_cast<int>(recv[peer].size()) ||
+        !std::equal(recv[peer].begin(), recv[peer].end(), lo))
+      throw CudaError("attach_comm: halo plan disagrees with the operator's column set");
     if (h.send_count || h.recv_count) halo_peers.push_back(h);
   }
   d_send_cells = dmalloc<int>(send_cells.size());

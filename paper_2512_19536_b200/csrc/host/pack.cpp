@@ -119,3 +119,36 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
 }
 
 }  // namespace pdg
+
+namespace pdg {
+
+void halo_plan(const Problem& pr, std::vector<std::vector<int>>& send, std::vector<std::vector<int>>& recv) {
+  const int w = pr.cfg.world, r = pr.cfg.rank;
+  auto owner_rank = [&](int g) {
+    return static_cast<int>(std::upper_bound(pr.rank_cell_start.begin(), pr.rank_cell_start.end(), g) -
+                            pr.rank_cell_start.begin()) - 1;
+  };
+  send.assign(w, {});
+  recv.assign(w, {});
+  for (const Face& f : pr.mesh.interior_faces()) {
+    const int a = pr.iperm[f.cell_in], c = pr.iperm[f.cell_out];
+    const int ra = owner_rank(a), rc = owner_rank(c);
+    if (ra == rc) continue;
+    if (ra == r) {
+      send[rc].push_back(a - pr.cell_begin);
+      recv[rc].push_back(c);
+    }
+    if (rc == r) {
+      send[ra].push_back(c - pr.cell_begin);
+      recv[ra].push_back(a);
+    }
+  }
+  for (int p = 0; p < w; ++p) {
+    for (auto* v : {&send[p], &recv[p]}) {
+      std::sort(v->begin(), v->end());
+      v->erase(std::unique(v->begin(), v->end()), v->end());
+    }
+  }
+}
+
+}  // namespace pdg

@@ -109,6 +109,11 @@ struct Problem {
 // incoming update lists and the tree links (host/pack.cpp).
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base);
 
+// Multi-rank SpMV halo, identical on every rank:
+// send[peer] = this rank's local cells adjacent to peer's cells (ascending),
+// recv[peer] = peer's global internal cells this rank's rows touch (ascending).
+void halo_plan(const Problem& pr, std::vector<std::vector<int>>& send, std::vector<std::vector<int>>& recv);
+
 void validate_config(const pdg_config& cfg);
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
 // coarse factorisation + task packing; split out so a multi-rank run can sum
