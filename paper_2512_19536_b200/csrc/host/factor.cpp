@@ -19,6 +19,7 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
   t.order.reserve(m);
   t.sn_start.push_back(0);
   std::vector<int> side(m, -1);
+  constexpr int n_dirs = 4;
   auto emit = [&](const std::vector<int>& nodes) {
     for (int v : nodes) t.order.push_back(v);
     t.sn_start.push_back(static_cast<int>(t.order.size()));
@@ -33,34 +34,41 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
           roots.push_back(emit(nodes));
           return;
         }
-        double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
-        for (int v : nodes) {
-          x0 = std::min(x0, pos[v].x);
-          x1 = std::max(x1, pos[v].x);
-          y0 = std::min(y0, pos[v].y);
-          y1 = std::max(y1, pos[v].y);
-        }
-        const bool by_x = (x1 - x0) >= (y1 - y0);
-        std::sort(nodes.begin(), nodes.end(), [&](int a, int b) {
-          const double ca = by_x ? pos[a].x : pos[a].y, cb = by_x ? pos[b].x : pos[b].y;
-          return ca < cb || (ca == cb && a < b);
-        });
+        // median cuts along 4 directions; keep the smallest one-sided separator
         const std::size_t half = nodes.size() / 2;
-        for (std::size_t i = 0; i < nodes.size(); ++i) side[nodes[i]] = i < half ? 0 : 1;
-        std::vector<int> sep_l, sep_r;
-        for (std::size_t i = 0; i < nodes.size(); ++i) {
-          const int v = nodes[i];
-          const int sv = side[v];
-          for (int k = adj_ptr[v]; k < adj_ptr[v + 1]; ++k) {
-            const int u = adj[k];
-            if (side[u] >= 0 && side[u] != sv) {
-              (sv == 0 ? sep_l : sep_r).push_back(v);
-              break;
+        std::vector<int> best_order, sep;
+        bool have = false;
+        static const double kDir[4][2] = {{1, 0}, {0, 1}, {0.7071067811865476, 0.7071067811865476},
+                                          {0.7071067811865476, -0.7071067811865476}};
+        for (int d = 0; d < n_dirs; ++d) {
+          std::vector<int> ord = nodes;
+          const double dx = kDir[d][0], dy = kDir[d][1];
+          std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+            const double ca = pos[a].x * dx + pos[a].y * dy, cb = pos[b].x * dx + pos[b].y * dy;
+            return ca < cb || (ca == cb && a < b);
+          });
+          for (std::size_t i = 0; i < ord.size(); ++i) side[ord[i]] = i < half ? 0 : 1;
+          std::vector<int> sep_l, sep_r;
+          for (std::size_t i = 0; i < ord.size(); ++i) {
+            const int v = ord[i];
+            const int sv = side[v];
+            for (int k = adj_ptr[v]; k < adj_ptr[v + 1]; ++k) {
+              const int u = adj[k];
+              if (side[u] >= 0 && side[u] != sv) {
+                (sv == 0 ? sep_l : sep_r).push_back(v);
+                break;
+              }
             }
           }
+          for (int v : ord) side[v] = -1;
+          std::vector<int>& s = sep_r.size() < sep_l.size() ? sep_r : sep_l;
+          if (!have || s.size() < sep.size()) {
+            have = true;
+            sep = s;
+            best_order = std::move(ord);
+          }
         }
-        for (int v : nodes) side[v] = -1;
-        std::vector<int>& sep = sep_r.size() < sep_l.size() ? sep_r : sep_l;
+        nodes = std::move(best_order);
         if (2 * sep.size() > nodes.size()) {
           roots.push_back(emit(nodes));
           return;
