@@ -140,7 +140,7 @@ def run_reference(args):
     value = n * its / el
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc_lib().orc_threads(), "kind": "port",
                              "sample": f"{done} of {args.steps} requested CN steps timed "
@@ -294,7 +294,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n_global,
                        "steps_timed": args.steps, "pcg_iterations": its,
