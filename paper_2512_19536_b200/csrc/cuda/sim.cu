@@ -13,6 +13,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <queue>
 #include <vector>
 
 #include "../host/problem.hpp"
@@ -186,6 +187,125 @@ void DeviceSim::release_tasks() {
   d_ticket = nullptr;
 }
 
+namespace {
+
+// Orders the sweep's work units by a simulated list schedule on `slots`
+// resident CTAs: a unit is released when its task-level dependencies finish
+// (forward: all children forward; backward: parent backward and own forward),
+// the free CTA takes the released unit with the longest path to the end of
+// the sweep, and tickets follow the simulated start times. A unit's
+// dependencies start strictly earlier, so the ticket order stays topological
+// (the persistent sweep's deadlock-freedom argument, sweep.cu).
+std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& units, int slots) {
+  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;  // ns
+  const int nt = static_cast<int>(pr.tasks.size()), nu = static_cast<int>(units.size());
+  auto cost = [&](const DevUnit& u) { return kFixed + kPerByte * u.bytes; };
+  std::vector<double> cmax_f(nt, 0.0), cmax_b(nt, 0.0);
+  std::vector<int> left_f(nt, 0), left_b(nt, 0);
+  std::vector<std::vector<int>> units_f(nt), units_b(nt);
+  for (int i = 0; i < nu; ++i) {
+    const DevUnit& u = units[i];
+    if (u.dir == 0) {
+      cmax_f[u.task] = std::max(cmax_f[u.task], cost(u));
+      units_f[u.task].push_back(i);
+    } else {
+      cmax_b[u.task] = std::max(cmax_b[u.task], cost(u));
+      units_b[u.task].push_back(i);
+    }
+  }
+  // longest remaining path (bottom level) per task and direction; children
+  // precede parents in task order
+  std::vector<double> Lb(nt, 0.0), Lf(nt, 0.0), kid_b(nt, 0.0);
+  for (int s = 0; s < nt; ++s) {
+    Lb[s] = cmax_b[s] + kPublish + kid_b[s];
+    const int p = pr.tasks[s].parent;
+    if (p >= 0) kid_b[p] = std::max(kid_b[p], Lb[s]);
+  }
+  for (int s = nt - 1; s >= 0; --s) {
+    const int p = pr.tasks[s].parent;
+    Lf[s] = cmax_f[s] + kPublish + std::max(p >= 0 ? Lf[p] : 0.0, Lb[s]);
+  }
+  std::vector<double> prio(nu);
+  for (int i = 0; i < nu; ++i) {
+    const DevUnit& u = units[i];
+    const int s = u.task;
+    prio[i] = u.dir == 0 ? Lf[s] - cmax_f[s] + cost(u) : Lb[s] - cmax_b[s] + cost(u);
+  }
+  // pending dependency counts per task-direction
+  std::vector<int> dep_f(nt), dep_b(nt);
+  for (int s = 0; s < nt; ++s) {
+    dep_f[s] = pr.tasks[s].n_child;
+    dep_b[s] = 1 + (pr.tasks[s].parent >= 0 ? 1 : 0);
+    left_f[s] = static_cast<int>(units_f[s].size());
+    left_b[s] = static_cast<int>(units_b[s].size());
+  }
+  using TI = std::pair<double, int>;
+  std::priority_queue<TI, std::vector<TI>, std::greater<TI>> release, finish, cta;
+  std::priority_queue<TI> ready;  // by priority
+  std::vector<double> task_done_f(nt, 0.0), task_done_b(nt, 0.0), start(nu, 0.0);
+  auto release_dir = [&](int s, bool fwd, double t) {
+    for (int i : fwd ? units_f[s] : units_b[s]) release.push({t, i});
+  };
+  for (int s = 0; s < nt; ++s)
+    if (dep_f[s] == 0) release_dir(s, true, 0.0);
+  for (int c = 0; c < slots; ++c) cta.push({0.0, c});
+  auto complete = [&](int i, double t) {
+    const DevUnit& u = units[i];
+    const int s = u.task;
+    if (u.dir == 0) {
+      task_done_f[s] = std::max(task_done_f[s], t);
+      if (--left_f[s] > 0) return;
+      const double r = task_done_f[s] + kPublish;
+      const int p = pr.tasks[s].parent;
+      if (p >= 0 && --dep_f[p] == 0) release_dir(p, true, r);
+      if (--dep_b[s] == 0) release_dir(s, false, r);
+    } else {
+      task_done_b[s] = std::max(task_done_b[s], t);
+      if (--left_b[s] > 0) return;
+      const double r = task_done_b[s] + kPublish;
+      for (int k = 0; k < pr.tasks[s].n_child; ++k) {
+        const int c = pr.task_child[pr.tasks[s].child_off + k];
+        if (--dep_b[c] == 0) release_dir(c, false, r);
+      }
+    }
+  };
+  int placed = 0;
+  std::vector<int> order;
+  order.reserve(nu);
+  while (placed < nu) {
+    auto [t, c] = cta.top();
+    cta.pop();
+    while (!finish.empty() && finish.top().first <= t) {
+      complete(finish.top().second, finish.top().first);
+      finish.pop();
+    }
+    while (!release.empty() && release.top().first <= t) {
+      ready.push({prio[release.top().second], release.top().second});
+      release.pop();
+    }
+    if (ready.empty()) {
+      // idle until the next completion or release
+      double nxt = 1e300;
+      if (!finish.empty()) nxt = std::min(nxt, finish.top().first);
+      if (!release.empty()) nxt = std::min(nxt, release.top().first);
+      if (nxt >= 1e300) throw SolverError("schwarz: sweep schedule has a dependency cycle");
+      cta.push({std::max(nxt, t), c});
+      continue;
+    }
+    const int i = ready.top().second;
+    ready.pop();
+    start[i] = t;
+    order.push_back(i);
+    ++placed;
+    const double f = t + cost(units[i]);
+    finish.push({f, i});
+    cta.push({f, c});
+  }
+  return order;
+}
+
+}  // namespace
+
 void DeviceSim::upload_tasks() {
   release_tasks();
   const Problem& pr = *P;
@@ -315,10 +435,22 @@ void DeviceSim::upload_tasks() {
   std::vector<DevUnit> fu, bu;
   make_units(fo, true, fu);
   make_units(bo, false, bu);
-  // one ticket space: forward units, then backward units (sweep.cu)
+  // one ticket space (sweep.cu): forward and backward units in the order of a
+  // simulated list schedule (critical path first), or PDG_SWEEP_ORDER=level:
+  // all forward units by height, then all backward units by depth
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
   fu.insert(fu.end(), bu.begin(), bu.end());
+  const char* ord_env = std::getenv("PDG_SWEEP_ORDER");
+  if (!(ord_env && std::strcmp(ord_env, "level") == 0)) {
+    int sms = 148, dev = 0;
+    PDG_CUDA(cudaGetDevice(&dev));
+    PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const std::vector<int> perm = list_schedule(pr, fu, sms * 8);
+    std::vector<DevUnit> o(fu.size());
+    for (std::size_t i = 0; i < perm.size(); ++i) o[i] = fu[perm[i]];
+    fu.swap(o);
+  }
   h_units = fu;
   d_fwd_units = dupload(fu, st);
   n_tile_ctrs = std::max(n_tile_ctr, 1);

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a, int p
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= a.n_units) break;
-    if (tk < a.n_units_f) run_unit<true>(a, s, panel, xin, part, phase, tk);
+    if (s.u.dir == 0) run_unit<true>(a, s, panel, xin, part, phase, tk);
     else run_unit<false>(a, s, panel, xin, part, phase, tk);
     __syncthreads();
   }
