@@ -87,6 +87,8 @@ struct SweepArgs {
   double* z;
   const double* r0;
   double* y0;
+  double* yf;             // forward results y_S (fine / coarse), read by the backward units
+  double* yc;
   const PcgScalars* S;
   int stage_meta;  // stage gather maps in smem before the dependency wait
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)

@@ -175,9 +175,10 @@ void DeviceSim::alloc_history(int cap) {
 
 void DeviceSim::release_tasks() {
   void* ptrs[] = {d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_part, d_task_child, d_fmat, d_hmat, d_ftiles, d_htiles,
-                  d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket};
+                  d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_yfwd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  d_yfwd = nullptr;
   d_tasks = nullptr;
   d_nunit = d_task_child = d_in_ptr = d_flags = nullptr;
   d_fwd_units = d_bwd_units = nullptr;
@@ -477,6 +478,7 @@ void DeviceSim::upload_tasks() {
   std::vector<long long> ii(pr.in_idx.begin(), pr.in_idx.end());
   d_in_idx = dupload(ii, st);
   d_ubuf = dalloc<double>(std::max<std::int64_t>(pr.ubuf_size, 1));
+  d_yfwd = dalloc<double>(n + static_cast<std::size_t>(pr.two_level ? pr.n_agg * pr.bq : 0));
   d_flags = dalloc<int>(2 * std::max(n_tasks, 1));
   d_ticket = dalloc<unsigned int>(2);
 }
@@ -536,6 +538,8 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.z = z;
   a.r0 = d_r0;
   a.y0 = d_y0;
+  a.yf = d_yfwd;
+  a.yc = d_yfwd + n;
   a.S = S;
   static const int stage_meta = std::getenv("PDG_SWEEP_META") ? std::atoi(std::getenv("PDG_SWEEP_META")) : 1;
   a.stage_meta = stage_meta;

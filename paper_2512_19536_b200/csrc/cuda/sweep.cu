@@ -52,8 +52,24 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ int ld_relaxed_s(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin with relaxed loads (each acquire load invalidates the SM's L1, which
+// the other CTAs on the SM are using), then one acquire load for ordering.
+// A count that never arrives is a schedule bug: fail the launch instead of
+// hanging the device.
 __device__ __forceinline__ void wait_count(const int* flag, int need) {
-  while (ld_acquire_s(flag) < need) __nanosleep(16);
+  if (ld_relaxed_s(flag) < need) {
+    const long long t0 = clock64();
+    do {
+      __nanosleep(16);
+      if (clock64() - t0 > (1LL << 33)) __trap();
+    } while (ld_relaxed_s(flag) < need);
+  }
+  (void)ld_acquire_s(flag);
 }
 // named barrier for the staging warps (1..kWarps-1) only
 __device__ __forceinline__ void staging_sync() {
@@ -141,7 +157,10 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
 
 template <bool FWD>
 __device__ __forceinline__ void store_row(const SweepArgs& a, const DevTask& T, double* outv, int o, double v) {
-  if (!FWD || o < T.w) outv[T.dof0 + o] = v;
+  // forward y_S goes to its own buffer: a task's backward units read all of
+  // y_S while their siblings already overwrite the output with x_S
+  if (!FWD) outv[T.dof0 + o] = v;
+  else if (o < T.w) (T.coarse ? a.yc : a.yf)[T.dof0 + o] = v;
   else a.ubuf[T.ubuf_off + (o - T.w)] = v;
 }
 
@@ -203,8 +222,8 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* p
     if (U.own_fwd >= 0 && col_lo < w) {
       if (t == 0) wait_count(a.flags + U.own_fwd, U.own_need);
       staging_sync();
-      double* outv = T.coarse ? a.y0 : a.z;
-      for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(outv + T.dof0 + i);
+      const double* ybuf = T.coarse ? a.yc : a.yf;
+      for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(ybuf + T.dof0 + i);
     }
   }
   if (t == 0) s.meta = meta;
@@ -258,7 +277,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     for (int i = i_start + threadIdx.x; i < col_hi; i += blockDim.x) {
       double v;
       if (i < w) {
-        v = __ldcg(outv + T.dof0 + i);
+        v = __ldcg((T.coarse ? a.yc : a.yf) + T.dof0 + i);
       } else {
         const int k = i - w, cell = k / bs, rr = k - cell * bs;
         const long long base = meta ? s.idx[cell - rc0] : a.row_dof[T.rows_off + cell];

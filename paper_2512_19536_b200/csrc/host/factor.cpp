@@ -14,8 +14,9 @@ std::int64_t SupernodalFactor::values() const {
 }
 
 NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
-                         const std::vector<Pt>& pos, int leaf) {
+                         const std::vector<Pt>& pos, int leaf, int merge) {
   NdTree t;
+  merge = std::max(1, merge);
   t.order.reserve(m);
   t.sn_start.push_back(0);
   std::vector<int> side(m, -1);
@@ -26,9 +27,15 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
     t.parent.push_back(-1);
     return static_cast<int>(t.parent.size()) - 1;
   };
-  std::function<void(std::vector<int>&, std::vector<int>&)> rec =
-      [&](std::vector<int>& nodes, std::vector<int>& roots) {
+  // Separators of `merge` consecutive levels form one supernode (a level
+  // whose depth % merge != 0 hands its separator up as `pending`): the
+  // elimination tree gets `merge` times shallower, which shortens the
+  // dependency chain of the triangular sweeps, at the price of storing the
+  // (zero) couplings between the merged separators.
+  std::function<void(std::vector<int>&, std::vector<int>&, std::vector<int>&, int)> rec =
+      [&](std::vector<int>& nodes, std::vector<int>& roots, std::vector<int>& pending, int depth) {
         roots.clear();
+        pending.clear();
         if (nodes.empty()) return;
         if (static_cast<int>(nodes.size()) <= leaf) {
           roots.push_back(emit(nodes));
@@ -81,24 +88,31 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
           (i < half ? left : right).push_back(v);
         }
         for (int v : sep) side[v] = -1;
-        std::vector<int> rl, rr;
-        rec(left, rl);
-        rec(right, rr);
-        if (sep.empty()) {
-          roots = rl;
-          roots.insert(roots.end(), rr.begin(), rr.end());
+        std::vector<int> rl, rr, pl, pr;
+        rec(left, rl, pl, depth + 1);
+        rec(right, rr, pr, depth + 1);
+        std::vector<int> sep_nodes = pl;
+        sep_nodes.insert(sep_nodes.end(), pr.begin(), pr.end());
+        sep_nodes.insert(sep_nodes.end(), sep.begin(), sep.end());
+        roots = rl;
+        roots.insert(roots.end(), rr.begin(), rr.end());
+        if (depth % merge != 0) {  // defer: the ancestor level emits it
+          pending = sep_nodes;
           return;
         }
-        std::vector<int> sep_nodes = sep;
+        if (sep_nodes.empty()) return;
         const int id = emit(sep_nodes);
-        for (int c : rl) t.parent[c] = id;
-        for (int c : rr) t.parent[c] = id;
-        roots.push_back(id);
+        for (int c : roots) t.parent[c] = id;
+        roots.assign(1, id);
       };
   std::vector<int> all(m);
   for (int i = 0; i < m; ++i) all[i] = i;
-  std::vector<int> roots;
-  rec(all, roots);
+  std::vector<int> roots, pending;
+  rec(all, roots, pending, 0);
+  if (!pending.empty()) {
+    const int id = emit(pending);
+    for (int c : roots) t.parent[c] = id;
+  }
   return t;
 }
 

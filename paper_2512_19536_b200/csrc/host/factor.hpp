@@ -33,9 +33,10 @@ struct NdTree {
 };
 
 // Recursive coordinate bisection; separators are the smaller one-sided
-// boundary of the cut. Deterministic (ties broken by node id).
+// boundary of the cut. Deterministic (ties broken by node id). `merge`
+// consecutive separator levels form one supernode.
 NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
-                         const std::vector<Pt>& pos, int leaf_nodes);
+                         const std::vector<Pt>& pos, int leaf_nodes, int merge = 1);
 
 struct Supernode {
   int s0 = 0, s1 = 0;         // positions

@@ -274,6 +274,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   // nested-dissection leaf size (cells): dense leaves of ~64 dofs; PDG_ND_LEAF overrides
   int leaf = std::clamp(64 / b, 4, 16);
   if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
+  // separator levels merged per supernode (shallower elimination trees); PDG_ND_MERGE overrides
+  int nd_merge = 2;
+  if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
   parallel_for(n_units, [&](int u) {
@@ -295,7 +298,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       ap.push_back(static_cast<int>(aj.size()));
       pos[i] = mesh.centroid(cells[i]);
     }
-    nd[u] = nested_dissection(m, ap, aj, pos, leaf);
+    nd[u] = nested_dissection(m, ap, aj, pos, leaf, nd_merge);
     unit_cells[u].resize(m);
     for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
   });
