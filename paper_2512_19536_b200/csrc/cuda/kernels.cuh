@@ -90,10 +90,10 @@ struct SweepArgs {
   double* yf;             // forward results y_S (fine / coarse), read by the backward units
   double* yc;
   const PcgScalars* S;
-  int stage_meta;  // stage gather maps in smem before the dependency wait
+  int* epoch;        // [0] sweep number (counters wait for (epoch+1) * count), [1] CTAs finished
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)
 };
-void launch_sweep(const SweepArgs& a, int smem_bytes, int panel_doubles, cudaStream_t st);
+void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
 
 // Ionic model + stimulus at quadrature nodes (one warp per cell).
 struct IonicArgs {

@@ -455,11 +455,14 @@ void DeviceSim::upload_tasks() {
   h_units = fu;
   d_fwd_units = dupload(fu, st);
   n_tile_ctrs = std::max(n_tile_ctr, 1);
-  d_nunit = dalloc<int>(n_tile_ctrs);  // chunk counters of split tiles
+  // chunk counters of split tiles; like the task counters they are monotone
+  // across sweeps (sweep.cu), so they are zeroed once here
+  d_nunit = dalloc<int>(n_tile_ctrs);
+  PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
   d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
   (void)max_panel;
-  panel_doubles = 0;  // panels stream from L2 (bulk-prefetched), not staged in smem
-  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (panel_doubles + kSweepThreads + static_cast<int>(max_in) + 2);
+  // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
+  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + static_cast<int>(max_in) + 2);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   d_task_child = dupload(pr.task_child, st);
@@ -480,7 +483,11 @@ void DeviceSim::upload_tasks() {
   d_ubuf = dalloc<double>(std::max<std::int64_t>(pr.ubuf_size, 1));
   d_yfwd = dalloc<double>(n + static_cast<std::size_t>(pr.two_level ? pr.n_agg * pr.bq : 0));
   d_flags = dalloc<int>(2 * std::max(n_tasks, 1));
-  d_ticket = dalloc<unsigned int>(2);
+  PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
+  // [0] next ticket, [1] sweep number, [2] CTAs finished (sweep.cu)
+  d_ticket = dalloc<unsigned int>(4);
+  PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 4 * sizeof(unsigned int), st));
+  PDG_CUDA(cudaStreamSynchronize(st));
 }
 
 DeviceSim::~DeviceSim() {
@@ -541,8 +548,7 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.yf = d_yfwd;
   a.yc = d_yfwd + n;
   a.S = S;
-  static const int stage_meta = std::getenv("PDG_SWEEP_META") ? std::atoi(std::getenv("PDG_SWEEP_META")) : 1;
-  a.stage_meta = stage_meta;
+  a.epoch = reinterpret_cast<int*>(d_ticket) + 1;
   a.trace = d_trace;
   return a;
 }
@@ -563,10 +569,7 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
     launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, Sh, st);
     coarse_reduce_hook();
   }
-  PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
-  PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-  PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
-  launch_sweep(sweep_args(true, r, z, Sh), smem_fwd, panel_doubles, st);
+  launch_sweep(sweep_args(true, r, z, Sh), smem_fwd, st);
   launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
   after_reduce(finish, honor);
 }
@@ -935,12 +938,8 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
              [&] { launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, nullptr, st); });
     }
     // slot 3: the fused forward + backward sweep (panels F and H once each)
-    timeit(3, 8 * (fvf + fvh) + 32 * n + 2 * (idx_bytes + tile_bytes), [&] {
-      PDG_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned int), st));
-      PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
-      PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
-      launch_sweep(sweep_args(true, d_r, d_z, nullptr), smem_fwd, panel_doubles, st);
-    });
+    timeit(3, 8 * (fvf + fvh) + 32 * n + 2 * (idx_bytes + tile_bytes),
+           [&] { launch_sweep(sweep_args(true, d_r, d_z, nullptr), smem_fwd, st); });
     timeit(5, 8 * N * b * bq + 24 * n + 4 * N,
            [&] { launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st); });
   }

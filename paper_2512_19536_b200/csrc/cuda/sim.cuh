@@ -62,7 +62,7 @@ class DeviceSim {
   DevTask* d_tasks = nullptr;
   int *d_nunit = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;
   DevUnit *d_fwd_units = nullptr, *d_bwd_units = nullptr;
-  int n_units_f = 0, n_units_b = 0, n_tile_ctrs = 0, panel_doubles = 0;
+  int n_units_f = 0, n_units_b = 0, n_tile_ctrs = 0;
   double* d_part = nullptr;
   double *d_fmat = nullptr, *d_hmat = nullptr, *d_ubuf = nullptr, *d_yfwd = nullptr;
   DevTile *d_ftiles = nullptr, *d_htiles = nullptr;

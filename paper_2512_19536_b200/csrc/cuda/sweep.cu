@@ -2,30 +2,31 @@
 // (forward then backward in a single launch), replacing the parallel_for of
 // LLT / SimplicialLLT solves (/root/reference/proj/src/schwarz.cpp:155-167).
 //
-// Every CTA takes a ticket; tickets enumerate forward units in topological
-// order (children first) and then backward units (parents first). A CTA only
-// ever waits on units with smaller tickets, which are already running, so the
-// sweep is deadlock-free without a grid barrier, subdomains of very different
-// sizes overlap instead of running in waves, and the backward sweep of a
-// finished subtree starts while other subtrees are still going forward.
 // Each supernode is ONE dense mat-vec over its row-tiled panel (host/pack.cpp):
 //   forward : [y_S ; u_S] = F (r_S - sum of incoming descendant updates u_D)
 //   backward: x_S         = H [y_S ; -x_R]
-// cut into units of <= 16 KB of panel: whole 32-row tiles, or column chunks
-// of a wide tile.
+// cut into work units of <= 32 KB of panel: runs of whole 32-row tiles, or
+// column chunks of one wide tile.
 //
-// The elimination tree's critical path is a chain of dependent memory round
-// trips, so a unit splits its CTA by role: thread 0 starts polling its (at
-// most two, precomputed) dependency counters immediately, while warps 1-3
-// issue the TMA bulk copy of the unit's panel slice into shared memory
-// (cp.async.bulk + mbarrier), stage tile descriptors and the static gather
-// maps, and prefetch every input that does not depend on the awaited tasks.
-// After the wait only one level of dependent loads (descendant update slices
-// or ancestor x) and an smem mat-vec remain on the critical path.
-// Column chunks write 32 partial sums each; the last chunk of a tile to finish
-// (counter) reduces them in chunk order, so results are deterministic.
-// Results of other tasks are read with ld.cg; a unit publishes with barrier +
-// one red.release.gpu (cumulative over the barrier).
+// Scheduling: resident CTAs take tickets; tickets follow a simulated
+// critical-path list schedule (sim.cu), so forward and backward units
+// interleave and a unit's dependencies always hold smaller tickets. A CTA
+// holds up to two tickets (the unit it runs + one of lookahead whose
+// descriptor and task record are fetched while it runs; deeper lookahead
+// reserves critical units too early), and the lowest unfinished ticket is
+// always running, so the sweep is deadlock-free without a grid barrier.
+// A unit's panel is bulk-prefetched into L2 when the unit starts.
+//
+// Per unit the CTA splits by role: thread 0 polls the (at most two,
+// precomputed) dependency counters, lane 1 of warp 0 fetches the lookahead
+// unit, and warps 1-3 stage tile descriptors, gather maps and every input
+// that does not depend on the awaited units. After the wait only one level of
+// dependent loads (descendant update slices or ancestor x) and the mat-vec
+// remain. Column chunks write 32 partial sums; the last chunk to arrive
+// (atom.acq_rel) reduces them in chunk order, so results are deterministic.
+// Results of other units are read with ld.cg; a unit publishes with barrier +
+// one red.release.gpu. Counters are monotone across launches (sweep number
+// `epoch`), so no memsets are needed between sweeps.
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -37,6 +38,11 @@ namespace {
 __device__ __forceinline__ int ld_acquire_s(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_s(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void red_release_add(int* p, int v) {
@@ -51,11 +57,6 @@ __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-__device__ __forceinline__ int ld_relaxed_s(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 // Spin with relaxed loads (each acquire load invalidates the SM's L1, which
 // the other CTAs on the SM are using), then one acquire load for ordering.
@@ -76,47 +77,46 @@ __device__ __forceinline__ void staging_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kSweepThreads - 32) : "memory");
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, int bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, int phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  }
-}
-
 constexpr int kWarps = kSweepThreads / 32;
 constexpr int kMaxSmemTiles = 32;
 constexpr int kMetaCells = 160;  // staged in_ptr entries per unit
 constexpr int kMetaIdx = 768;    // staged update offsets / row dof starts per unit
+constexpr int kAhead = 2;  // ring: running unit + one lookahead unit
 
-struct UnitSmem {
+struct Ahead {
   DevUnit u;
   DevTask t;
-  int col_lo, col_hi, cell_lo, meta, last;
+  int tk;
+};
+
+struct UnitSmem {
+  DevUnit u;  // running unit and its task
+  DevTask t;
+  int col_lo, col_hi, cell_lo, meta, last, ep;
   DevTile tiles[kMaxSmemTiles];
   int iptr[kMetaCells];
   long long idx[kMetaIdx];
-  uint64_t bar;
+  Ahead q[kAhead];
+  int qh;
 };
+
+// takes the next ticket into lookahead slot `q`: descriptor, task record, and
+// an L2 bulk prefetch of the unit's panel
+__device__ __forceinline__ void fetch_ahead(const SweepArgs& a, Ahead& q) {
+  const int tk = static_cast<int>(atomicAdd(a.ticket, 1u));
+  q.tk = tk < a.n_units ? tk : a.n_units;
+  if (tk < a.n_units) {
+    q.u = a.units[tk];
+    q.t = a.tasks[q.u.task];
+  }
+}
+// L2 bulk prefetch of the running unit's panel (issued when the unit starts:
+// prefetching the lookahead units as well overcommits the L2)
+__device__ __forceinline__ void prefetch_panel(const SweepArgs& a, const DevUnit& u) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((u.dir == 0 ? a.fmat : a.hmat) + u.src_off),
+               "r"(u.bytes)
+               : "memory");
+}
 
 // one warp: rows of tile `tl` restricted to input columns [j0, j1) of the
 // panel `m` (tile base, global, L2-prefetched); (row 2*l2, row 2*l2+1) sums in half 0
@@ -164,21 +164,14 @@ __device__ __forceinline__ void store_row(const SweepArgs& a, const DevTask& T, 
   else a.ubuf[T.ubuf_off + (o - T.w)] = v;
 }
 
-// warps 1..3: everything that does not depend on the awaited tasks
+// warps 1..3: everything that does not depend on the awaited units
 template <bool FWD>
-__device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* panel, double* xin) {
+__device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* xin) {
   const int t = threadIdx.x - 32;  // 0 .. kSweepThreads-33
   const int nst = kSweepThreads - 32;
   const DevUnit& U = s.u;
-  if (t == 0) {
-    s.t = a.tasks[U.task];
-    // TMA bulk prefetch of the unit's panel into L2 while the unit waits
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((FWD ? a.fmat : a.hmat) + U.src_off),
-                 "r"(U.bytes)
-                 : "memory");
-  }
-  staging_sync();
   const DevTask& T = s.t;
+  if (t == 0) prefetch_panel(a, U);
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
   const int ntile = U.tile_end - U.tile_begin;
   const DevTile* tiles = FWD ? a.ftiles : a.htiles;
@@ -201,7 +194,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* p
     const double* in = T.coarse ? a.r0 : a.r;
     for (int i = col_lo + t; i < col_hi; i += nst) xin[i - col_lo] = in[T.dof0 + i];
     const int nc = cell_hi - cell_lo;
-    if (a.stage_meta && nc + 1 <= kMetaCells) {
+    if (nc + 1 <= kMetaCells) {
       for (int c = t; c <= nc; c += nst) s.iptr[c] = a.in_ptr[T.in_off + cell_lo + c];
       staging_sync();
       const int e0 = s.iptr[0], ne = s.iptr[nc] - e0;
@@ -214,13 +207,13 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* p
     const int r_lo = max(col_lo, w);
     const int rc0 = (r_lo - w) / bs;
     const int nr_cells = col_hi > w ? (col_hi - w + bs - 1) / bs - rc0 : 0;
-    if (a.stage_meta && nr_cells <= kMetaIdx) {
+    if (nr_cells <= kMetaIdx) {
       for (int k = t; k < nr_cells; k += nst) s.idx[k] = a.row_dof[T.rows_off + rc0 + k];
       meta = 1;
     }
     // own y_S (this task's forward result) is independent of the awaited ancestors
     if (U.own_fwd >= 0 && col_lo < w) {
-      if (t == 0) wait_count(a.flags + U.own_fwd, U.own_need);
+      if (t == 0) wait_count(a.flags + U.own_fwd, (s.ep + 1) * U.own_need);
       staging_sync();
       const double* ybuf = T.coarse ? a.yc : a.yf;
       for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(ybuf + T.dof0 + i);
@@ -230,24 +223,31 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* p
 }
 
 template <bool FWD>
-__device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* panel, double* xin, double* part,
-                                         int phase, int tk) {
+__device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* xin, double* part, int tk) {
   long long* tr = a.trace ? a.trace + 4LL * tk : nullptr;
+  const int ep = s.ep;
   if (threadIdx.x == 0) {
     if (tr) tr[0] = gtimer();
     const DevUnit& U = s.u;
     if (U.n_dep <= 2) {
-      for (int d = 0; d < U.n_dep; ++d) wait_count(a.flags + U.dep[d], U.need[d]);
+      for (int d = 0; d < U.n_dep; ++d) wait_count(a.flags + U.dep[d], (ep + 1) * U.need[d]);
     } else {  // many children: walk the task's child list
-      const DevTask T = a.tasks[U.task];
+      const DevTask& T = s.t;
       for (int k = 0; k < T.n_child; ++k) {
         const int c = a.task_child[T.child_off + k];
-        wait_count(a.flags + c, a.tasks[c].f_ntile);
+        wait_count(a.flags + c, (ep + 1) * a.tasks[c].f_ntile);
       }
     }
     if (tr) tr[1] = gtimer();
+  } else if (threadIdx.x == 1) {
+    // lookahead: q[qh] is the next unit; the slot after it (freed when the
+    // running unit was copied out) takes the next ticket
+    const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
+    Ahead& q = s.q[target];
+    if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
+    else q.tk = a.n_units;
   } else if (threadIdx.x >= 32) {
-    stage<FWD>(a, s, panel, xin);
+    stage<FWD>(a, s, xin);
   }
   __syncthreads();
   const DevUnit& U = s.u;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
       __stcg(gp + threadIdx.x, sum);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s.last = atom_acq_rel_add(a.tile_ctr + U.tile_ctr, 1) == U.nchunk - 1;
+    if (threadIdx.x == 0) s.last = atom_acq_rel_add(a.tile_ctr + U.tile_ctr, 1) + 1 == (ep + 1) * U.nchunk;
     __syncthreads();
     if (!s.last) {
       if (tr && threadIdx.x == 0) tr[3] = gtimer();
@@ -363,40 +363,53 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
-// Persistent: resident CTAs loop over tickets in increasing order, so the
-// lowest unfinished ticket is always being processed and its dependencies
-// (smaller tickets) are finished or in progress — no deadlock, no per-unit
-// CTA launch cost.
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a, int panel_doubles) {
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ UnitSmem s;
-  __shared__ int s_ticket;
-  if (threadIdx.x == 0) {
-    mbar_init(&s.bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  double* panel = sm;
-  double* part = sm + panel_doubles;  // kSweepThreads doubles
+  double* part = sm;  // kSweepThreads doubles
   double* xin = part + kSweepThreads;
-  for (int phase = 0;; phase ^= 1) {
-    if (threadIdx.x == 0) {
-      const int tk = static_cast<int>(atomicAdd(a.ticket, 1u));
-      s_ticket = tk;
-      if (tk < a.n_units) s.u = a.units[tk];
+  if (threadIdx.x == 0) {
+    s.ep = __ldcg(a.epoch);
+    for (int i = 0; i + 1 < kAhead; ++i) {
+      if (i == 0 || s.q[i - 1].tk < a.n_units) fetch_ahead(a, s.q[i]);
+      else s.q[i].tk = a.n_units;
     }
-    __syncthreads();
-    const int tk = s_ticket;
+    s.q[kAhead - 1].tk = a.n_units;
+    s.qh = 0;
+  }
+  __syncthreads();
+  // slot layout: q[qh] running, q[qh+1] next, q[qh+2] fetched during the run
+  for (;;) {
+    const Ahead& cur = s.q[s.qh];
+    const int tk = cur.tk;
     if (tk >= a.n_units) break;
-    if (s.u.dir == 0) run_unit<true>(a, s, panel, xin, part, phase, tk);
-    else run_unit<false>(a, s, panel, xin, part, phase, tk);
+    if (threadIdx.x < 32) reinterpret_cast<int*>(&s.u)[threadIdx.x % (sizeof(DevUnit) / 4)] =
+        reinterpret_cast<const int*>(&cur.u)[threadIdx.x % (sizeof(DevUnit) / 4)];
+    else if (threadIdx.x < 64) reinterpret_cast<int*>(&s.t)[(threadIdx.x - 32) % (sizeof(DevTask) / 4)] =
+        reinterpret_cast<const int*>(&cur.t)[(threadIdx.x - 32) % (sizeof(DevTask) / 4)];
     __syncthreads();
+    if (threadIdx.x == 0) s.qh = s.qh == kAhead - 1 ? 0 : s.qh + 1;
+    // run_unit reads s.qh only from thread 1 after this barrier
+    __syncthreads();
+    if (s.u.dir == 0) run_unit<true>(a, s, xin, part, tk);
+    else run_unit<false>(a, s, xin, part, tk);
+    __syncthreads();
+  }
+  // the last CTA of this sweep resets the tickets and advances the epoch
+  if (threadIdx.x == 0) {
+    if (atomicAdd(a.epoch + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.epoch[1] = 0;
+      *a.ticket = 0u;
+      a.epoch[0] = s.ep + 1;
+      __threadfence();
+    }
   }
 }
 
 }  // namespace
 
-void launch_sweep(const SweepArgs& a, int smem, int panel_doubles, cudaStream_t st) {
+void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
   if (a.n_units == 0) return;
   static int cached_smem = -1, resident = 0;
   if (cached_smem != smem) {
@@ -408,7 +421,7 @@ void launch_sweep(const SweepArgs& a, int smem, int panel_doubles, cudaStream_t 
     cached_smem = smem;
   }
   const int grid = a.n_units < resident ? a.n_units : resident;
-  sweep_kernel<<<grid, kSweepThreads, smem, st>>>(a, panel_doubles);
+  sweep_kernel<<<grid, kSweepThreads, smem, st>>>(a);
 }
 
 void set_sweep_smem(int bytes) {
