@@ -319,6 +319,95 @@ __global__ void restrict_kernel(const int* __restrict__ agg_ptr, const int* __re
   }
 }
 
+// PCG update fused with the coarse restriction (krylov.cpp:54-58 then
+// schwarz.cpp:166): one CTA per restriction chunk (<= 64 cells of one
+// agglomerate) updates x and r for its cells, keeps the new r in shared
+// memory and writes the chunk's E^T r partial (coalesced over the E blocks);
+// ||r||^2 is finished grid-wide as in update_kernel. Deterministic.
+template <int B, int BQ>
+__global__ void __launch_bounds__(256) update_restrict_kernel(const int* __restrict__ chunk_ptr,
+                                                              const int* __restrict__ cells,
+                                                              const double* __restrict__ E, double* __restrict__ x,
+                                                              double* __restrict__ r, const double* __restrict__ p,
+                                                              const double* __restrict__ q,
+                                                              double* __restrict__ r0part, ReduceCtx rc) {
+  PcgScalars* S = rc.S;
+  if (S->stop) return;
+  const double pq = S->pq;
+  const int it = S->iter;
+  if (!isfinite(pq) || pq <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S->error = !isfinite(pq) ? kPcgPqNonFinite : kPcgPqNonPos;
+      S->stop = 1;
+    }
+    return;
+  }
+  const double alpha = S->rho / pq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rc.H.alpha[it] = alpha;
+    S->alpha = alpha;
+  }
+  constexpr int kCells = 64;
+  __shared__ double rs[kCells * B];
+  __shared__ int cl[kCells];
+  __shared__ double wsum[8][BQ];
+  const int c0 = chunk_ptr[blockIdx.x], nc = chunk_ptr[blockIdx.x + 1] - c0;
+  for (int k = threadIdx.x; k < nc; k += blockDim.x) cl[k] = cells[c0 + k];
+  __syncthreads();
+  double contrib = 0.0;
+  for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
+    const int k = e / B, i = e - k * B;
+    const long long d = static_cast<long long>(cl[k]) * B + i;
+    x[d] += alpha * p[d];
+    const double rv = r[d] - alpha * q[d];
+    r[d] = rv;
+    rs[e] = rv;
+    contrib += rv * rv;
+  }
+  __syncthreads();
+  double acc[BQ];
+#pragma unroll
+  for (int m = 0; m < BQ; ++m) acc[m] = 0.0;
+  // 8 E loads in flight per thread before any is consumed
+  const int total = nc * B * BQ;
+  constexpr int kU = 8;
+  for (int e0 = threadIdx.x; e0 < total; e0 += kU * blockDim.x) {
+    double ev[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      ev[u] = 0.0;
+      if (e < total) {
+        const int k = e / (B * BQ), f = e - k * (B * BQ);
+        ev[u] = __ldg(E + static_cast<long long>(cl[k]) * (B * BQ) + f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= total) break;
+      const int k = e / (B * BQ), f = e - k * (B * BQ), m = f / B, i = f - m * B;
+      const double v = ev[u] * rs[k * B + i];
+#pragma unroll
+      for (int mm = 0; mm < BQ; ++mm)
+        if (mm == m) acc[mm] += v;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < BQ; ++m) {
+    const double v = warp_sum(acc[m]);
+    if (lane == 0) wsum[wid][m] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < BQ) {
+    double s = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += wsum[w][threadIdx.x];
+    r0part[static_cast<long long>(blockIdx.x) * BQ + threadIdx.x] = s;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
 // Schwarz supernode sweeps: see sweep.cu
 
 // ---------------- ionic terms at quadrature nodes ----------------
@@ -624,6 +713,32 @@ static void restrict_dispatch(int bq, int n_agg, const int* agg_ptr, const int* 
 void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* agg_cells,
                      const double* E, const double* r, double* r0, const PcgScalars* S, cudaStream_t st) {
 #define L(B) restrict_dispatch<B>(bq, n_agg, agg_ptr, agg_cells, E, r, r0, S, st)
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+template <int B>
+static void update_restrict_dispatch(int bq, int n_chunks, const int* chunk_ptr, const int* cells, const double* E,
+                                     double* x, double* r, const double* p, const double* q, double* r0part,
+                                     ReduceCtx rc, cudaStream_t st) {
+  switch (bq) {
+#define UR(BQ) update_restrict_kernel<B, BQ><<<n_chunks, 256, 0, st>>>(chunk_ptr, cells, E, x, r, p, q, r0part, rc)
+    case 3: UR(3); break;
+    case 6: if constexpr (B >= 6) { UR(6); break; }
+    [[fallthrough]];
+    case 10: if constexpr (B >= 10) { UR(10); break; }
+    [[fallthrough]];
+    case 15: if constexpr (B >= 15) { UR(15); break; }
+    [[fallthrough]];
+#undef UR
+    default: throw CudaError("unsupported coarse block size");
+  }
+}
+
+void launch_update_restrict(int b, int bq, int n_chunks, const int* chunk_ptr, const int* cells, const double* E,
+                            double* x, double* r, const double* p, const double* q, double* r0part, ReduceCtx rc,
+                            cudaStream_t st) {
+#define L(B) update_restrict_dispatch<B>(bq, n_chunks, chunk_ptr, cells, E, x, r, p, q, r0part, rc, st)
   PDG_B_DISPATCH(b, L)
 #undef L
 }

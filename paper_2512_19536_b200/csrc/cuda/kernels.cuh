@@ -59,6 +59,12 @@ void launch_restrict(int b, int bq, int n_agg, const int* agg_ptr, const int* ag
                      const double* E, const double* r, double* r0, const PcgScalars* S,
                      cudaStream_t st);
 
+// update_kernel fused with the restriction: per chunk of <= 64 cells of one
+// agglomerate, x += alpha p, r -= alpha q, r0part[chunk] = E^T r (chunk cells)
+void launch_update_restrict(int b, int bq, int n_chunks, const int* chunk_ptr, const int* cells, const double* E,
+                            double* x, double* r, const double* p, const double* q, double* r0part, ReduceCtx rc,
+                            cudaStream_t st);
+
 // r0 chunk partials -> r0 (one CTA-sized chunk of an agglomerate per restrict CTA)
 void launch_restrict_combine(int bq, int n_agg, const int* node_chunk_ptr, const double* part, double* r0,
                              const PcgScalars* S, cudaStream_t st);
@@ -89,6 +95,8 @@ struct SweepArgs {
   double* y0;
   double* yf;             // forward results y_S (fine / coarse), read by the backward units
   double* yc;
+  const double* r0part;   // non-null: the coarse forward sums r0 from the restriction chunks
+  const int* node_chunk_ptr;
   const PcgScalars* S;
   int* epoch;        // [0] sweep number (counters wait for (epoch+1) * count), [1] CTAs finished
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)

@@ -120,11 +120,13 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     d_agg_cells = dupload(pr.agg_cells, st);
     d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
     d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
-    // restriction chunks: <= 64 cells of one agglomerate per CTA
+    // restriction chunks: <= kChunk (<= 64) cells of one agglomerate per CTA;
+    // small chunks keep the fused update + restriction spread over all SMs
+    const int kChunk = std::getenv("PDG_CHUNK_CELLS") ? std::clamp(std::atoi(std::getenv("PDG_CHUNK_CELLS")), 1, 64) : 32;
     std::vector<int> cptr{0}, nptr{0};
     for (int a = 0; a < pr.n_agg; ++a) {
-      for (int k = pr.agg_cell_ptr[a]; k < pr.agg_cell_ptr[a + 1]; k += 64)
-        cptr.push_back(std::min(k + 64, pr.agg_cell_ptr[a + 1]));
+      for (int k = pr.agg_cell_ptr[a]; k < pr.agg_cell_ptr[a + 1]; k += kChunk)
+        cptr.push_back(std::min(k + kChunk, pr.agg_cell_ptr[a + 1]));
       nptr.push_back(static_cast<int>(cptr.size()) - 1);
     }
     n_chunks = static_cast<int>(cptr.size()) - 1;
@@ -547,6 +549,10 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.y0 = d_y0;
   a.yf = d_yfwd;
   a.yc = d_yfwd + n;
+  // one rank: the coarse forward sums r0 from the restriction chunks itself;
+  // several ranks: r0 is combined and all-reduced first
+  a.r0part = (world == 1 && P->two_level) ? d_r0part : nullptr;
+  a.node_chunk_ptr = d_node_chunk_ptr;
   a.S = S;
   a.epoch = reinterpret_cast<int*>(d_ticket) + 1;
   a.trace = d_trace;
@@ -555,7 +561,7 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
 
 // z = B r with the r.z reduction finished as `finish`. `S_honor` makes every
 // kernel a no-op once the solve has stopped.
-void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor) {
+void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor, bool restricted) {
   const Problem& pr = *P;
   const PcgScalars* Sh = honor ? d_S : nullptr;
   if (!use_pc()) {
@@ -565,9 +571,12 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
     return;
   }
   if (pr.two_level) {
-    launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, r, d_r0part, Sh, st);
-    launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, Sh, st);
-    coarse_reduce_hook();
+    // restricted: the chunk partials came from the fused update (record_iteration)
+    if (!restricted) launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, r, d_r0part, Sh, st);
+    if (world > 1) {
+      launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, Sh, st);
+      coarse_reduce_hook();
+    }
   }
   launch_sweep(sweep_args(true, r, z, Sh), smem_fwd, st);
   launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
@@ -610,9 +619,14 @@ void DeviceSim::record_iteration() {
   halo_exchange(d_p);
   launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
   after_reduce(kFinPq, true);
-  launch_update(n, d_x, d_r, d_p, d_q, red_for(kFinRr), st);
+  const bool fuse = use_pc() && P->two_level && world == 1;
+  if (fuse)
+    launch_update_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q, d_r0part,
+                           red_for(kFinRr), st);
+  else
+    launch_update(n, d_x, d_r, d_p, d_q, red_for(kFinRr), st);
   after_reduce(kFinRr, true);
-  precond_apply(d_r, z_of(d_r), kFinRz, true);
+  precond_apply(d_r, z_of(d_r), kFinRz, true, fuse);
   launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
 }
 
@@ -853,16 +867,19 @@ StepResult DeviceSim::step() {
 
 namespace pdg {
 
-// kernels issued by one precond apply (restrict, fwd, bwd sweeps, prolong+dot)
+// kernels issued by one stand-alone precond apply: restrict (+ combine on
+// several ranks), the sweep, prolong+dot
 int DeviceSim::precond_launches() const {
   if (!use_pc()) return 1;
-  return (P->two_level ? 2 : 0) + (n_tasks > 0 ? 1 : 0) + 1;
+  return (P->two_level ? (world > 1 ? 2 : 1) : 0) + (n_tasks > 0 ? 1 : 0) + 1;
 }
 
 // kernels per PCG iteration: spmv, update, precond, pupdate, loop condition
-// (+ finish kernels and halo packs on multi-rank runs)
+// (+ finish kernels and halo packs on multi-rank runs); on one rank the
+// restriction is fused into the update
 int DeviceSim::body_launches() const {
-  int k = 1 + 1 + precond_launches() + 1 + (world == 1 ? 1 : 0);
+  const int fused = (use_pc() && P->two_level && world == 1) ? 1 : 0;
+  int k = 1 + 1 + precond_launches() - fused + 1 + (world == 1 ? 1 : 0);
   if (world > 1) k += 3 + static_cast<int>(halo_peers.size());
   return k;
 }
@@ -925,13 +942,19 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
   }
   timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 24 * n,
          [&] { launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rs, false, st); });
-  timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
+  const bool fused = use_pc() && pr.two_level && world == 1;
+  if (fused)  // slot 1 = the update fused with the restriction (slots 2, 4 stay 0)
+    timeit(1, 48 * n + 8 * N * b * bq + 4 * N + 8LL * n_chunks * bq, [&] {
+      launch_update_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q, d_r0part, rs, st);
+    });
+  else
+    timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
   const long long fvf = static_cast<long long>(pr.fmat.size()), fvh = static_cast<long long>(pr.hmat.size());
   const long long tile_bytes = 24LL * static_cast<long long>(pr.ftiles.size());
   const long long idx_bytes = 8 * static_cast<long long>(pr.row_dof.size() + pr.in_idx.size()) +
                               4 * static_cast<long long>(pr.in_ptr.size()) + 64LL * n_tasks;
   if (use_pc()) {
-    if (pr.two_level) {
+    if (pr.two_level && !fused) {
       timeit(2, 8 * N * b * bq + 8 * n + 4 * N + 8LL * n_chunks * bq,
              [&] { launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_r, d_r0part, nullptr, st); });
       timeit(4, 16LL * n_chunks * bq + 8LL * pr.n_agg * bq,

@@ -143,7 +143,7 @@ class DeviceSim {
   void alloc_history(int cap);
   ReduceCtx rctx(int finish, double* out = nullptr);
   SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);
-  void precond_apply(const double* r, double* z, int finish, bool honor);
+  void precond_apply(const double* r, double* z, int finish, bool honor, bool restricted = false);
   double* z_of(double* r);
   void record_iteration();
   void record_solve_tail();

@@ -191,8 +191,19 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   int meta = 0;
   if (FWD) {
     // independent part of the inputs: r (or r0) itself
-    const double* in = T.coarse ? a.r0 : a.r;
-    for (int i = col_lo + t; i < col_hi; i += nst) xin[i - col_lo] = in[T.dof0 + i];
+    if (T.coarse && a.r0part) {
+      // r0 = sum of the restriction chunks of each coarse node, in chunk order
+      // (the restrict_combine kernel folded into the coarse forward staging)
+      for (int i = col_lo + t; i < col_hi; i += nst) {
+        const int d = static_cast<int>(T.dof0) + i, node = d / bs, m = d - node * bs;
+        double v = 0.0;
+        for (int c = a.node_chunk_ptr[node]; c < a.node_chunk_ptr[node + 1]; ++c) v += a.r0part[c * bs + m];
+        xin[i - col_lo] = v;
+      }
+    } else {
+      const double* in = T.coarse ? a.r0 : a.r;
+      for (int i = col_lo + t; i < col_hi; i += nst) xin[i - col_lo] = in[T.dof0 + i];
+    }
     const int nc = cell_hi - cell_lo;
     if (nc + 1 <= kMetaCells) {
       for (int c = t; c <= nc; c += nst) s.iptr[c] = a.in_ptr[T.in_off + cell_lo + c];
