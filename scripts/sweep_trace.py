@@ -52,3 +52,9 @@ ch = nchunk > 1
 print(f"  chunked units {int(ch.sum())} ({nbytes[ch].sum() / 1e6:.1f} MB), whole-tile units {int((~ch).sum())}")
 ntask = len(np.unique(task))
 print(f"  tasks {ntask}, units/task {n / ntask:.1f}")
+# the tail of the sweep: which units finish last, and when their dependencies were met
+order = np.argsort(done)[::-1][:25]
+print("  last units to finish (task, dir, chunks, bytes, start, deps met, staged, done; us):")
+for u in order:
+    print(f"    task {int(task[u]):5d} dir {int(direc[u])} nch {int(nchunk[u]):2d} {int(nbytes[u]):6d} B  "
+          f"{st[u] / 1e3:6.1f} {dep[u] / 1e3:6.1f} {stg[u] / 1e3:6.1f} {done[u] / 1e3:6.1f}")
