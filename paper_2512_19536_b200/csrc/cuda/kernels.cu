@@ -141,17 +141,27 @@ __device__ __forceinline__ double bsr_row_dot(int row, int r, const int* __restr
                                               const int* __restrict__ col,
                                               const double* __restrict__ val,
                                               const double* __restrict__ x) {
+  // all 2B loads of a block are issued before its FMAs, and the next block's
+  // column index is loaded one block ahead (memory-level parallelism)
   double acc0 = 0.0, acc1 = 0.0;
   const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  int c = k0 < k1 ? __ldg(col + k0) : 0;
   for (int k = k0; k < k1; ++k) {
-    const int c = __ldg(col + k);
+    const int cn = k + 1 < k1 ? __ldg(col + k + 1) : 0;
     const double* blk = val + static_cast<long long>(k) * (B * B) + r;
     const double* xb = x + static_cast<long long>(c) * B;
+    double v[B], xv[B];
+#pragma unroll
+    for (int cc = 0; cc < B; ++cc) {
+      v[cc] = __ldg(blk + cc * B);
+      xv[cc] = __ldg(xb + cc);
+    }
 #pragma unroll
     for (int cc = 0; cc < B; cc += 2) {
-      acc0 = fma(__ldg(blk + cc * B), __ldg(xb + cc), acc0);
-      if (cc + 1 < B) acc1 = fma(__ldg(blk + (cc + 1) * B), __ldg(xb + cc + 1), acc1);
+      acc0 = fma(v[cc], xv[cc], acc0);
+      if (cc + 1 < B) acc1 = fma(v[cc + 1], xv[cc + 1], acc1);
     }
+    c = cn;
   }
   return acc0 + acc1;
 }

@@ -341,9 +341,16 @@ void DeviceSim::upload_tasks() {
   d_tasks = dupload(t, st);
   // Work units of <= kUnitBytes of panel: runs of whole tiles, or column
   // chunks of one wide tile (partials reduced by the last chunk, sweep.cu).
-  // unit size (panel bytes per CTA visit); PDG_UNIT_KB overrides
-  static const long long kUnitBytes =
-      1024LL * (std::getenv("PDG_UNIT_KB") ? std::max(2, std::atoi(std::getenv("PDG_UNIT_KB"))) : 32);
+  // unit size (panel bytes per CTA visit): a unit's fixed cost (~5 us of
+  // dependent round trips) dominates below ~32 KB, while the separators near
+  // the roots are the critical path; leaves (height 0) and the rest can use
+  // different sizes. PDG_UNIT_KB / PDG_LEAF_KB override.
+  auto env_kb = [](const char* k, int d) {
+    const char* e = std::getenv(k);
+    return 1024LL * (e ? std::max(2, std::atoi(e)) : d);
+  };
+  static const long long kUnitBytes = env_kb("PDG_UNIT_KB", 44);  // best of a 16-96 KB scan on config2
+  static const long long kLeafBytes = env_kb("PDG_LEAF_KB", static_cast<int>(kUnitBytes / 1024));
   int n_parts = 0, n_tile_ctr = 0;
   long long max_panel = 0, max_in = 0;
   // dependency counters a unit waits on (sweep.cu): forward = children's
@@ -378,13 +385,17 @@ void DeviceSim::upload_tasks() {
       const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
       auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };
+      const long long kUnit = s.height == 0 ? kLeafBytes : kUnitBytes;
       int b0 = 0;
       while (b0 < nt) {
         const auto& tb = tiles[t0 + b0];
-        if (tbytes(b0) > kUnitBytes) {
-          // column chunks of an even number of columns
-          long long cols = kUnitBytes / (8LL * tb.stride);
-          cols = std::max<long long>(2, cols & ~1LL);
+        if (tbytes(b0) > kUnit) {
+          // balanced column chunks of an even number of columns (no small
+          // remainder chunk paying a whole unit's fixed cost)
+          const long long max_cols = std::max<long long>(2, (kUnit / (8LL * tb.stride)) & ~1LL);
+          const int nch0 = static_cast<int>((tb.ncol + max_cols - 1) / max_cols);
+          long long cols = (tb.ncol + nch0 - 1) / nch0;
+          cols = std::max<long long>(2, (cols + 1) & ~1LL);
           const int nch = static_cast<int>((tb.ncol + cols - 1) / cols);
           for (int c = 0; c < nch; ++c) {
             const int c0 = static_cast<int>(c * cols), c1 = std::min<int>(tb.ncol, static_cast<int>((c + 1) * cols));
@@ -413,7 +424,7 @@ void DeviceSim::upload_tasks() {
         }
         long long bytes = 0;
         int e = b0;
-        while (e < nt && tbytes(e) <= kUnitBytes && (e == b0 || bytes + tbytes(e) <= kUnitBytes)) {
+        while (e < nt && tbytes(e) <= kUnit && (e == b0 || bytes + tbytes(e) <= kUnit)) {
           bytes += tbytes(e);
           ++e;
         }
