@@ -190,9 +190,10 @@ int64_t pdg_sim_kernel_launches(const pdg_sim* s);
  * launch, slots: 0 spmv, 1 update, 2 restrict, 3 sweep_fwd, 4 sweep_bwd,
  * 5 prolong_dot, 6 pupdate, 7 ionic, 8 rhs */
 pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9);
-/* one traced Schwarz sweep: 8 int64 per work unit (globaltimer at start, deps
- * met, inputs staged, published; task, direction, panel bytes, chunks);
- * returns the unit count (scripts/sweep_trace.py) */
+/* one traced Schwarz sweep: 12 int64 per work unit (globaltimer at start,
+ * deps met, inputs gathered, published, staging done, mat-vec done; task,
+ * direction, panel bytes, chunks, task height, coarse flag); returns the unit
+ * count (scripts/sweep_trace.py) */
 int pdg_sim_trace_sweep(pdg_sim* s, long long* out, int cap);
 
 /* default_max_iterations (krylov.cpp:12-15) and condition_estimate (:85-103) */

@@ -216,20 +216,23 @@ namespace pdg {
 
 int DeviceSim::trace_sweep(long long* out, int cap) {
   const int nu = n_units_f + n_units_b;
-  if (!d_trace) PDG_CUDA(cudaMalloc(&d_trace, sizeof(long long) * 4 * std::max(nu, 1)));
+  if (!d_trace) PDG_CUDA(cudaMalloc(&d_trace, sizeof(long long) * 8 * std::max(nu, 1)));
+  PDG_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(long long) * 8 * std::max(nu, 1), st));
   PDG_CUDA(cudaMemcpyAsync(d_tmp2, d_r, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   apply_precond(d_tmp2, d_z);
-  std::vector<long long> tr(4 * static_cast<std::size_t>(nu));
+  std::vector<long long> tr(8 * static_cast<std::size_t>(nu));
   PDG_CUDA(cudaMemcpy(tr.data(), d_trace, tr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
   cudaFree(d_trace);
   d_trace = nullptr;
   for (int u = 0; u < nu && u < cap; ++u) {
-    long long* o = out + 8LL * u;
-    for (int k = 0; k < 4; ++k) o[k] = tr[4 * u + k];
-    o[4] = h_units[u].task;
-    o[5] = h_units[u].dir;
-    o[6] = h_units[u].bytes;
-    o[7] = h_units[u].nchunk;
+    long long* o = out + 12LL * u;
+    for (int k = 0; k < 6; ++k) o[k] = tr[8 * u + k];
+    o[6] = h_units[u].task;
+    o[7] = h_units[u].dir;
+    o[8] = h_units[u].bytes;
+    o[9] = h_units[u].nchunk;
+    o[10] = P->tasks[h_units[u].task].height;
+    o[11] = P->tasks[h_units[u].task].coarse;
   }
   return nu;
 }

@@ -41,6 +41,8 @@ struct DevUnit {
   long long src_off;  // first panel double staged by TMA
   int bytes;          // staged bytes (multiple of 16)
   int own_need;
+  int col_lo, col_hi;  // input columns [col_lo, col_hi) of the task's panel this unit reads
+  int in_e0, in_n;     // forward: its incoming-update list in_idx[in_e0, in_e0 + in_n)
 };
 
 // One 32-row tile of a supernode panel (host/problem.hpp Problem::Tile).

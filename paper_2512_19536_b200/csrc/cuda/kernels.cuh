@@ -99,6 +99,7 @@ struct SweepArgs {
   const int* node_chunk_ptr;
   const PcgScalars* S;
   int* epoch;        // [0] sweep number (counters wait for (epoch+1) * count), [1] CTAs finished
+  int xcap;          // doubles per unit input buffer (two per CTA, double-buffered staging)
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);

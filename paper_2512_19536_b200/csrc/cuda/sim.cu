@@ -386,6 +386,18 @@ void DeviceSim::upload_tasks() {
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
       auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };
       const long long kUnit = s.height == 0 ? kLeafBytes : kUnitBytes;
+      // input column range and (forward) its incoming-update list, so the
+      // kernel stages without dependent metadata loads
+      auto set_cols = [&](DevUnit& u, int lo, int hi) {
+        u.col_lo = lo;
+        u.col_hi = hi;
+        u.in_e0 = u.in_n = 0;
+        if (fwd) {
+          const int c_lo = lo / s.bs, c_hi = (hi + s.bs - 1) / s.bs;
+          u.in_e0 = pr.in_ptr[s.in_off + c_lo];
+          u.in_n = pr.in_ptr[s.in_off + c_hi] - u.in_e0;
+        }
+      };
       int b0 = 0;
       while (b0 < nt) {
         const auto& tb = tiles[t0 + b0];
@@ -414,6 +426,7 @@ void DeviceSim::upload_tasks() {
             u.bytes = static_cast<int>(8LL * (c1 - c0) * tb.stride);
             max_panel = std::max<long long>(max_panel, u.bytes);
             max_in = std::max<long long>(max_in, c1 - c0);
+            set_cols(u, tb.col0 + c0, tb.col0 + c1);
             set_deps(u, tk, fwd);
             units.push_back(u);
           }
@@ -440,6 +453,7 @@ void DeviceSim::upload_tasks() {
         for (int r = b0; r < e; ++r) hi = std::max(hi, tiles[t0 + r].col0 + tiles[t0 + r].ncol);
         max_panel = std::max(max_panel, bytes);
         max_in = std::max<long long>(max_in, hi - lo);
+        set_cols(u, lo, hi);
         set_deps(u, tk, fwd);
         units.push_back(u);
         b0 = e;
@@ -475,7 +489,9 @@ void DeviceSim::upload_tasks() {
   d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
   (void)max_panel;
   // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
-  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + static_cast<int>(max_in) + 2);
+  // partial sums + the unit's input buffer (sweep.cu)
+  sweep_xcap = static_cast<int>(max_in) + 2;
+  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   d_task_child = dupload(pr.task_child, st);
@@ -566,6 +582,7 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.node_chunk_ptr = d_node_chunk_ptr;
   a.S = S;
   a.epoch = reinterpret_cast<int*>(d_ticket) + 1;
+  a.xcap = sweep_xcap;
   a.trace = d_trace;
   return a;
 }

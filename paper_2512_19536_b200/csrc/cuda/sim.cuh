@@ -69,7 +69,7 @@ class DeviceSim {
   long long *d_row_dof = nullptr, *d_in_idx = nullptr;
   int* d_flags = nullptr;
   unsigned int* d_ticket = nullptr;
-  int smem_fwd = 0, smem_bwd = 0;
+  int smem_fwd = 0, smem_bwd = 0, sweep_xcap = 0;
   // ionic
   double *d_bbox = nullptr, *d_tri = nullptr;
   int *d_tri_ptr = nullptr, *d_ionflags = nullptr;

@@ -92,7 +92,7 @@ struct Ahead {
 struct UnitSmem {
   DevUnit u;  // running unit and its task
   DevTask t;
-  int col_lo, col_hi, cell_lo, meta, last, ep;
+  int col_lo, col_hi, cell_lo, meta, last, ep, tk;
   DevTile tiles[kMaxSmemTiles];
   int iptr[kMetaCells];
   long long idx[kMetaIdx];
@@ -172,16 +172,14 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   const DevUnit& U = s.u;
   const DevTask& T = s.t;
   if (t == 0) prefetch_panel(a, U);
+  // every load below depends only on the (host-precomputed) descriptor, so
+  // the whole staging is one round of independent loads
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
   const int ntile = U.tile_end - U.tile_begin;
   const DevTile* tiles = FWD ? a.ftiles : a.htiles;
   for (int i = t; i < ntile && i < kMaxSmemTiles; i += nst) s.tiles[i] = tiles[tile0 + i];
-  staging_sync();
   const int bs = T.bs, w = T.w;
-  const DevTile t0 = s.tiles[0];
-  const int col_lo = t0.col0 + (U.nchunk > 1 ? U.c0 : 0);
-  int col_hi = t0.col0 + (U.nchunk > 1 ? U.c1 : t0.ncol);
-  for (int r = 1; r < ntile && r < kMaxSmemTiles; ++r) col_hi = max(col_hi, s.tiles[r].col0 + s.tiles[r].ncol);
+  const int col_lo = U.col_lo, col_hi = U.col_hi;
   const int cell_lo = col_lo / bs, cell_hi = (col_hi + bs - 1) / bs;
   if (t == 0) {
     s.col_lo = col_lo;
@@ -205,14 +203,10 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
       for (int i = col_lo + t; i < col_hi; i += nst) xin[i - col_lo] = in[T.dof0 + i];
     }
     const int nc = cell_hi - cell_lo;
-    if (nc + 1 <= kMetaCells) {
+    if (nc + 1 <= kMetaCells && U.in_n <= kMetaIdx) {
       for (int c = t; c <= nc; c += nst) s.iptr[c] = a.in_ptr[T.in_off + cell_lo + c];
-      staging_sync();
-      const int e0 = s.iptr[0], ne = s.iptr[nc] - e0;
-      if (ne <= kMetaIdx) {
-        for (int k = t; k < ne; k += nst) s.idx[k] = a.in_idx[e0 + k];
-        meta = 1;
-      }
+      for (int k = t; k < U.in_n; k += nst) s.idx[k] = a.in_idx[U.in_e0 + k];
+      meta = 1;
     }
   } else {
     const int r_lo = max(col_lo, w);
@@ -230,12 +224,15 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
       for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(ybuf + T.dof0 + i);
     }
   }
-  if (t == 0) s.meta = meta;
+  if (t == 0) {
+    s.meta = meta;
+    if (a.trace) a.trace[8LL * s.tk + 4] = gtimer();
+  }
 }
 
 template <bool FWD>
 __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* xin, double* part, int tk) {
-  long long* tr = a.trace ? a.trace + 4LL * tk : nullptr;
+  long long* tr = a.trace ? a.trace + 8LL * tk : nullptr;
   const int ep = s.ep;
   if (threadIdx.x == 0) {
     if (tr) tr[0] = gtimer();
@@ -312,6 +309,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
       part[warp * 32 + 2 * l2] = v.x;
       part[warp * 32 + 2 * l2 + 1] = v.y;
     }
+    if (tr && threadIdx.x == 0) tr[5] = gtimer();
     __syncthreads();
     double* gp = a.part + static_cast<long long>(U.part_base + U.chunk) * 32;
     if (threadIdx.x < 32) {
@@ -369,6 +367,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
       store_row<FWD>(a, T, outv, (U.tile_begin + R) * 32 + l, v);
     }
   }
+  if (tr && threadIdx.x == 0) tr[5] = gtimer();
   __syncthreads();
   if (threadIdx.x == 0) red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, ntile);
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
@@ -392,17 +391,24 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
   __syncthreads();
   // slot layout: q[qh] running, q[qh+1] next, q[qh+2] fetched during the run
   for (;;) {
-    const Ahead& cur = s.q[s.qh];
-    const int tk = cur.tk;
+    // warp 0 copies the descriptor and task record out of the ring and
+    // advances the ring head; one barrier publishes both
+    if (threadIdx.x < 32) {
+      const Ahead& cur = s.q[s.qh];
+      constexpr int nu = sizeof(DevUnit) / 4, nt = sizeof(DevTask) / 4;
+      for (int i = threadIdx.x; i < nu + nt; i += 32) {
+        if (i < nu) reinterpret_cast<int*>(&s.u)[i] = reinterpret_cast<const int*>(&cur.u)[i];
+        else reinterpret_cast<int*>(&s.t)[i - nu] = reinterpret_cast<const int*>(&cur.t)[i - nu];
+      }
+      __syncwarp();
+      if (threadIdx.x == 0) {
+        s.tk = cur.tk;
+        s.qh = s.qh == kAhead - 1 ? 0 : s.qh + 1;
+      }
+    }
+    __syncthreads();
+    const int tk = s.tk;
     if (tk >= a.n_units) break;
-    if (threadIdx.x < 32) reinterpret_cast<int*>(&s.u)[threadIdx.x % (sizeof(DevUnit) / 4)] =
-        reinterpret_cast<const int*>(&cur.u)[threadIdx.x % (sizeof(DevUnit) / 4)];
-    else if (threadIdx.x < 64) reinterpret_cast<int*>(&s.t)[(threadIdx.x - 32) % (sizeof(DevTask) / 4)] =
-        reinterpret_cast<const int*>(&cur.t)[(threadIdx.x - 32) % (sizeof(DevTask) / 4)];
-    __syncthreads();
-    if (threadIdx.x == 0) s.qh = s.qh == kAhead - 1 ? 0 : s.qh + 1;
-    // run_unit reads s.qh only from thread 1 after this barrier
-    __syncthreads();
     if (s.u.dir == 0) run_unit<true>(a, s, xin, part, tk);
     else run_unit<false>(a, s, xin, part, tk);
     __syncthreads();

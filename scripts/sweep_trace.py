@@ -22,17 +22,24 @@ L = _lib.lib()
 L.pdg_sim_trace_sweep.restype = C.c_int
 L.pdg_sim_trace_sweep.argtypes = [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]
 cap = 400000
-buf = np.zeros(cap * 8, np.int64)
+F = 12
+buf = np.zeros(cap * F, np.int64)
 for rep in range(3):
     n = L.pdg_sim_trace_sweep(sim._h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), cap)
-t = buf[:n * 8].reshape(n, 8).astype(np.float64)
+t = buf[:n * F].reshape(n, F).astype(np.float64)
 t0 = t[:, 0].min()
-st, dep, stg, done = (t[:, i] - t0 for i in range(4))
-task, direc, nbytes, nchunk = t[:, 4], t[:, 5], t[:, 6], t[:, 7]
+st, dep, stg, done, staged, comp = (t[:, i] - t0 for i in range(6))
+task, direc, nbytes, nchunk, height, coarse = (t[:, i] for i in range(6, 12))
 span = done.max()
 print(f"units {n}: span {span / 1e3:.1f} us; fwd {int((direc == 0).sum())} bwd {int((direc == 1).sum())}")
-for lab, v in (("wait", dep - st), ("stage", stg - dep), ("compute+pub", done - stg), ("total", done - st)):
-    print(f"  {lab:12s} mean {v.mean() / 1e3:6.2f} us  p50 {np.median(v) / 1e3:6.2f}  p90 {np.percentile(v, 90) / 1e3:6.2f}"
+ready = dep <= st + 300  # dependencies already met when the unit started
+print(f"  units whose dependencies were met at start: {int(ready.sum())}")
+for lab, v in (("wait", dep - st), ("staging", staged - st), ("deps->gathered", stg - dep),
+               ("mat-vec", comp - stg), ("publish", done - comp), ("total", done - st),
+               ("total|ready", (done - st)[ready]), ("staging|ready", (staged - st)[ready]),
+               ("gather|ready", (stg - dep)[ready]), ("matvec|ready", (comp - stg)[ready]),
+               ("publish|ready", (done - comp)[ready])):
+    print(f"  {lab:15s} mean {v.mean() / 1e3:6.2f} us  p50 {np.median(v) / 1e3:6.2f}  p90 {np.percentile(v, 90) / 1e3:6.2f}"
           f"  max {v.max() / 1e3:6.2f}")
 print(f"  sum unit time / span = mean concurrency {((done - st).sum() / span):.0f}")
 print(f"  last forward unit done at {done[direc == 0].max() / 1e3:.1f} us, first backward start {st[direc == 1].min() / 1e3:.1f} us")
