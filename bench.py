@@ -268,6 +268,7 @@ def main():
     for k in ("restrict", "sweep", "restrict_combine", "prolong_dot", "pupdate"):
         per_step[k] = its / args.steps + 1
     per_step["rhs"] = 1
+    per_step["ionic"] = 1
     shares = {k: kms[i] * per_step.get(k, 0) / (elapsed_ms / args.steps) for i, k in enumerate(KERNELS)}
     dom = max(shares, key=shares.get)
     di = KERNELS.index(dom)

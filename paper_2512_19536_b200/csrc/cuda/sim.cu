@@ -801,6 +801,40 @@ void DeviceSim::apply_precond(const double* r, double* z) {
 }
 
 // Simulation::step (timestepper.cpp:144-200)
+// ionic terms, stimulus and Y update of one step (ionics.cpp:61-113,
+// timestepper.cpp:128-186) on the current state
+IonicArgs DeviceSim::ionic_args(bool has_prev) const {
+  const Problem& pr = *P;
+  const pdg_config& c = pr.cfg;
+  IonicArgs a{};
+  a.b = b;
+  a.p = pr.p;
+  a.ncells = ncells;
+  a.n_comp = pr.n_comp;
+  a.ngl = static_cast<int>(pr.gl_x.size());
+  a.has_prev = has_prev ? 1 : 0;
+  a.model = c.ionic_model;
+  a.stim = c.stim_kind;
+  a.bbox = d_bbox;
+  a.tri_ptr = d_tri_ptr;
+  a.tri = d_tri;
+  a.U = d_U[0];
+  a.Up = d_U[1];
+  a.Y = d_Y[0];
+  a.Yp = d_Y[1];
+  a.Ynext = d_Y[2];
+  a.Minv = d_Minv;
+  a.ion = d_ion;
+  a.n = n;
+  a.chi = c.chi_m;
+  a.dt = c.dt;
+  a.t_mid = t + 0.5 * c.dt;
+  std::memcpy(a.fhn, c.fhn, sizeof a.fhn);
+  std::memcpy(a.stim_p, c.stim_params, sizeof a.stim_p);
+  a.flags = d_ionflags;
+  return a;
+}
+
 StepResult DeviceSim::step() {
   const Problem& pr = *P;
   const pdg_config& c = pr.cfg;
@@ -812,33 +846,7 @@ StepResult DeviceSim::step() {
   double* Up = d_U[1];
   const bool ionic = pr.n_comp > 0 || c.stim_kind != PDG_STIM_NONE;
   if (ionic) {
-    IonicArgs a{};
-    a.b = b;
-    a.p = pr.p;
-    a.ncells = ncells;
-    a.n_comp = pr.n_comp;
-    a.ngl = static_cast<int>(pr.gl_x.size());
-    a.has_prev = has_prev ? 1 : 0;
-    a.model = c.ionic_model;
-    a.stim = c.stim_kind;
-    a.bbox = d_bbox;
-    a.tri_ptr = d_tri_ptr;
-    a.tri = d_tri;
-    a.U = U;
-    a.Up = Up;
-    a.Y = d_Y[0];
-    a.Yp = d_Y[1];
-    a.Ynext = d_Y[2];
-    a.Minv = d_Minv;
-    a.ion = d_ion;
-    a.n = n;
-    a.chi = c.chi_m;
-    a.dt = c.dt;
-    a.t_mid = t + 0.5 * c.dt;
-    std::memcpy(a.fhn, c.fhn, sizeof a.fhn);
-    std::memcpy(a.stim_p, c.stim_params, sizeof a.stim_p);
-    a.flags = d_ionflags;
-    launch_ionic(a, st);
+    launch_ionic(ionic_args(has_prev), st);
   }
   reset_scalars(c.tol, maxit);
   halo_exchange(U);
@@ -998,6 +1006,11 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
   timeit(8, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 8 * N * b * b + 56 * n, [&] {
     launch_rhs(b, ncells, d_ptr, d_col, d_kval, d_M, 2.0, d_U[0], nullptr, 1, d_tmp, d_tmp2, d_q, rs, st);
   });
+  // slot 7: ionic terms (FP64-FMA bound: the basis is evaluated at every
+  // quadrature point); bytes = states in, ion + Y_next out, M^-1 blocks, geometry
+  if (pr.n_comp > 0 || pr.cfg.stim_kind != PDG_STIM_NONE)
+    timeit(7, 8 * (6 * n + N * b * b + 4 * N) + 48 * static_cast<long long>(pr.tri.size() / 6),
+           [&] { launch_ionic(ionic_args(k > 0), st); });
   cudaEventDestroy(a);
   cudaEventDestroy(z);
   PDG_CUDA(cudaStreamSynchronize(st));

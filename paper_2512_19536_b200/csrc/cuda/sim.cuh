@@ -144,6 +144,7 @@ class DeviceSim {
   ReduceCtx rctx(int finish, double* out = nullptr);
   SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);
   void precond_apply(const double* r, double* z, int finish, bool honor, bool restricted = false);
+  IonicArgs ionic_args(bool has_prev) const;
   double* z_of(double* r);
   void record_iteration();
   void record_solve_tail();
