@@ -5,8 +5,8 @@
 // Each supernode is ONE dense mat-vec over its row-tiled panel (host/pack.cpp):
 //   forward : [y_S ; u_S] = F (r_S - sum of incoming descendant updates u_D)
 //   backward: x_S         = H [y_S ; -x_R]
-// cut into work units of <= 32 KB of panel: runs of whole 32-row tiles, or
-// column chunks of one wide tile.
+// cut into work units of <= 44 KB of panel: runs of whole 32-row tiles, or
+// balanced column chunks of one wide tile.
 //
 // Scheduling: resident CTAs take tickets; tickets follow a simulated
 // critical-path list schedule (sim.cu), so forward and backward units
