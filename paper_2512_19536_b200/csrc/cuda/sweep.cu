@@ -31,6 +31,10 @@
 
 #include "kernels.cuh"
 
+#ifndef PDG_DOT_DEPTH
+#define PDG_DOT_DEPTH 8
+#endif
+
 namespace pdg {
 
 namespace {
@@ -127,12 +131,13 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
     const double2* mm = reinterpret_cast<const double2*>(m) + l2;
     const long long cs = tl.stride >> 1;
     int j = j0 + half;
-    for (; j + 14 < j1; j += 16) {
-      double2 v[8];
+    constexpr int D = PDG_DOT_DEPTH;  // double2 loads in flight per lane
+    for (; j + 2 * D - 2 < j1; j += 2 * D) {
+      double2 v[D];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(mm + (j + 2 * u) * cs);
+      for (int u = 0; u < D; ++u) v[u] = __ldg(mm + (j + 2 * u) * cs);
 #pragma unroll
-      for (int u = 0; u < 8; u += 4) {
+      for (int u = 0; u < D; u += 4) {
         acc0.x = fma(v[u].x, x[j + 2 * u], acc0.x);
         acc0.y = fma(v[u].y, x[j + 2 * u], acc0.y);
         acc1.x = fma(v[u + 1].x, x[j + 2 * u + 2], acc1.x);
