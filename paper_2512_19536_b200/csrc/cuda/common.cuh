@@ -87,4 +87,28 @@ struct Reducer {
 constexpr int kSweepThreads = 128;
 constexpr int kVecThreads = 256;
 
+// Programmatic dependent launch: the PCG body kernels are launched so that a
+// kernel's CTAs can be scheduled while its predecessor in the stream drains;
+// every such kernel calls pdl_wait() before touching anything the predecessor
+// wrote (a no-op for ordinary launches). PDG_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PDG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 }  // namespace pdg

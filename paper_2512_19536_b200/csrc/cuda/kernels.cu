@@ -10,6 +10,7 @@
 // order by the last CTA to arrive, so reruns are bit-identical (the
 // reference's determinism contract, parallel.hpp:14-16).
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
     spmv_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
                 const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+  pdl_wait();
   if (honor_stop && rc.S->stop) return;
   const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
   const int row = blockIdx.x * RowGeom<B>::kRows + lr;
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
 __global__ void update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
                               const double* __restrict__ p, const double* __restrict__ q,
                               ReduceCtx rc) {
+  pdl_wait();
   PcgScalars* S = rc.S;
   if (S->stop) return;
   const double pq = S->pq;
@@ -263,6 +266,7 @@ __global__ void update_kernel(long long n, double* __restrict__ x, double* __res
 
 __global__ void pupdate_kernel(long long n, double* __restrict__ p, const double* __restrict__ z,
                                const PcgScalars* S, int first) {
+  pdl_wait();
   if (!first && S->stop) return;
   const double beta = first ? 0.0 : S->beta;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -275,6 +279,7 @@ __global__ void prolong_dot_kernel(int ncells, const double* __restrict__ E,
                                    const int* __restrict__ cell_agg, const double* __restrict__ y0,
                                    const double* __restrict__ r, double* __restrict__ z,
                                    ReduceCtx rc) {
+  pdl_wait();
   if (rc.S->stop) return;
   const long long n = static_cast<long long>(ncells) * B;
   double contrib = 0.0;
@@ -301,6 +306,7 @@ template <int B, int BQ>
 __global__ void restrict_kernel(const int* __restrict__ agg_ptr, const int* __restrict__ agg_cells,
                                 const double* __restrict__ E, const double* __restrict__ r,
                                 double* __restrict__ r0, const PcgScalars* S) {
+  pdl_wait();
   if (S && S->stop) return;
   const int a = blockIdx.x;
   const int c0 = agg_ptr[a], c1 = agg_ptr[a + 1];
@@ -341,6 +347,7 @@ __global__ void __launch_bounds__(256) update_restrict_kernel(const int* __restr
                                                               double* __restrict__ r, const double* __restrict__ p,
                                                               const double* __restrict__ q,
                                                               double* __restrict__ r0part, ReduceCtx rc) {
+  pdl_wait();
   PcgScalars* S = rc.S;
   if (S->stop) return;
   const double pq = S->pq;
@@ -588,6 +595,7 @@ __global__ void scatter_perm_kernel(const double* __restrict__ src, double* __re
 __global__ void restrict_combine_kernel(int bq, int n_agg, const int* __restrict__ node_chunk_ptr,
                                         const double* __restrict__ part, double* __restrict__ r0,
                                         const PcgScalars* S) {
+  pdl_wait();
   if (S && S->stop) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_agg * bq) return;
@@ -614,6 +622,15 @@ __global__ void pack_kernel(const double* __restrict__ v, const int* __restrict_
   }
 }
 
+}  // namespace
+
+bool pdl_enabled() {
+  static const bool on = !(std::getenv("PDG_PDL") && std::atoi(std::getenv("PDG_PDL")) == 0);
+  return on;
+}
+
+namespace {
+
 int vec_grid(long long n) {
   long long g = (n + kVecThreads - 1) / kVecThreads;
   if (g > 148 * 16) g = 148 * 16;
@@ -638,8 +655,8 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
 #define L(B)                                                                                  \
   {                                                                                           \
     const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \
-    spmv_kernel<B><<<g, RowGeom<B>::kThreads, 0, st>>>(rows, ptr, col, val, x, y, dotw, rc,   \
-                                                       honor_stop ? 1 : 0);                   \
+    launch_pdl(spmv_kernel<B>, g, RowGeom<B>::kThreads, 0, st, rows, ptr, col, val, x, y, dotw, rc, \
+               honor_stop ? 1 : 0);                                                           \
   }
   if (rows > 0) PDG_B_DISPATCH(b, L)
 #undef L
@@ -671,12 +688,12 @@ void launch_rhs(int b, int rows, const int* ptr, const int* col, const double* v
 
 void launch_update(long long n, double* x, double* r, const double* p, const double* q, ReduceCtx rc,
                    cudaStream_t st) {
-  update_kernel<<<vec_grid(n), kVecThreads, 0, st>>>(n, x, r, p, q, rc);
+  launch_pdl(update_kernel, vec_grid(n), kVecThreads, 0, st, n, x, r, p, q, rc);
 }
 
 void launch_pupdate(long long n, double* p, const double* z, const PcgScalars* S, bool first,
                     cudaStream_t st) {
-  pupdate_kernel<<<vec_grid(n), kVecThreads, 0, st>>>(n, p, z, S, first ? 1 : 0);
+  launch_pdl(pupdate_kernel, vec_grid(n), kVecThreads, 0, st, n, p, z, S, first ? 1 : 0);
 }
 
 template <int B>
@@ -685,13 +702,13 @@ static void prolong_dispatch(int bq, int ncells, const double* E, const int* cel
                              cudaStream_t st) {
   const int g = vec_grid(static_cast<long long>(ncells) * B);
   switch (bq) {
-    case 0: prolong_dot_kernel<B, 0><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break;
-    case 3: prolong_dot_kernel<B, 3><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break;
-    case 6: if constexpr (B >= 6) { prolong_dot_kernel<B, 6><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    case 0: launch_pdl(prolong_dot_kernel<B, 0>, g, kVecThreads, 0, st, ncells, E, cell_agg, y0, r, z, rc); break;
+    case 3: launch_pdl(prolong_dot_kernel<B, 3>, g, kVecThreads, 0, st, ncells, E, cell_agg, y0, r, z, rc); break;
+    case 6: if constexpr (B >= 6) { launch_pdl(prolong_dot_kernel<B, 6>, g, kVecThreads, 0, st, ncells, E, cell_agg, y0, r, z, rc); break; }
     [[fallthrough]];
-    case 10: if constexpr (B >= 10) { prolong_dot_kernel<B, 10><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    case 10: if constexpr (B >= 10) { launch_pdl(prolong_dot_kernel<B, 10>, g, kVecThreads, 0, st, ncells, E, cell_agg, y0, r, z, rc); break; }
     [[fallthrough]];
-    case 15: if constexpr (B >= 15) { prolong_dot_kernel<B, 15><<<g, kVecThreads, 0, st>>>(ncells, E, cell_agg, y0, r, z, rc); break; }
+    case 15: if constexpr (B >= 15) { launch_pdl(prolong_dot_kernel<B, 15>, g, kVecThreads, 0, st, ncells, E, cell_agg, y0, r, z, rc); break; }
     [[fallthrough]];
     default: throw CudaError("unsupported coarse block size");
   }
@@ -709,12 +726,12 @@ static void restrict_dispatch(int bq, int n_agg, const int* agg_ptr, const int* 
                               const double* E, const double* r, double* r0, const PcgScalars* S,
                               cudaStream_t st) {
   switch (bq) {
-    case 3: restrict_kernel<B, 3><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break;
-    case 6: if constexpr (B >= 6) { restrict_kernel<B, 6><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    case 3: launch_pdl(restrict_kernel<B, 3>, n_agg, 256, 0, st, agg_ptr, agg_cells, E, r, r0, S); break;
+    case 6: if constexpr (B >= 6) { launch_pdl(restrict_kernel<B, 6>, n_agg, 256, 0, st, agg_ptr, agg_cells, E, r, r0, S); break; }
     [[fallthrough]];
-    case 10: if constexpr (B >= 10) { restrict_kernel<B, 10><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    case 10: if constexpr (B >= 10) { launch_pdl(restrict_kernel<B, 10>, n_agg, 256, 0, st, agg_ptr, agg_cells, E, r, r0, S); break; }
     [[fallthrough]];
-    case 15: if constexpr (B >= 15) { restrict_kernel<B, 15><<<n_agg, 256, 0, st>>>(agg_ptr, agg_cells, E, r, r0, S); break; }
+    case 15: if constexpr (B >= 15) { launch_pdl(restrict_kernel<B, 15>, n_agg, 256, 0, st, agg_ptr, agg_cells, E, r, r0, S); break; }
     [[fallthrough]];
     default: throw CudaError("unsupported coarse block size");
   }
@@ -732,7 +749,7 @@ static void update_restrict_dispatch(int bq, int n_chunks, const int* chunk_ptr,
                                      double* x, double* r, const double* p, const double* q, double* r0part,
                                      ReduceCtx rc, cudaStream_t st) {
   switch (bq) {
-#define UR(BQ) update_restrict_kernel<B, BQ><<<n_chunks, 256, 0, st>>>(chunk_ptr, cells, E, x, r, p, q, r0part, rc)
+#define UR(BQ) launch_pdl(update_restrict_kernel<B, BQ>, n_chunks, 256, 0, st, chunk_ptr, cells, E, x, r, p, q, r0part, rc)
     case 3: UR(3); break;
     case 6: if constexpr (B >= 6) { UR(6); break; }
     [[fallthrough]];
@@ -756,7 +773,7 @@ void launch_update_restrict(int b, int bq, int n_chunks, const int* chunk_ptr, c
 void launch_restrict_combine(int bq, int n_agg, const int* node_chunk_ptr, const double* part, double* r0,
                              const PcgScalars* S, cudaStream_t st) {
   const int n = n_agg * bq;
-  restrict_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(bq, n_agg, node_chunk_ptr, part, r0, S);
+  launch_pdl(restrict_combine_kernel, (n + 255) / 256, 256, 0, st, bq, n_agg, node_chunk_ptr, part, r0, S);
 }
 
 void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st) {

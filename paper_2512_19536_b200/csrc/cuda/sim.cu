@@ -50,6 +50,7 @@ static const char* pcg_error_message(int e) {
 }
 
 __global__ void set_condition_kernel(cudaGraphConditionalHandle h, const PcgScalars* S) {
+  pdl_wait();
   cudaGraphSetConditional(h, S->stop ? 0u : 1u);
 }
 
@@ -697,7 +698,7 @@ void DeviceSim::build_solve_graph(Graph& g) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   PDG_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   record_iteration();
-  set_condition_kernel<<<1, 1, 0, st>>>(handle, d_S);
+  launch_pdl(set_condition_kernel, 1, 1, 0, st, handle, d_S);
   PDG_CUDA(cudaStreamEndCapture(st, &body));
   PDG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
 }

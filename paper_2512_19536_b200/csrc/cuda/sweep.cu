@@ -379,6 +379,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
 }
 
 __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
+  pdl_wait();
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ UnitSmem s;
@@ -443,7 +444,7 @@ void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
     cached_smem = smem;
   }
   const int grid = a.n_units < resident ? a.n_units : resident;
-  sweep_kernel<<<grid, kSweepThreads, smem, st>>>(a);
+  launch_pdl(sweep_kernel, grid, kSweepThreads, smem, st, a);
 }
 
 void set_sweep_smem(int bytes) {
