@@ -190,6 +190,9 @@ int64_t pdg_sim_kernel_launches(const pdg_sim* s);
  * launch, slots: 0 spmv, 1 update, 2 restrict, 3 sweep_fwd, 4 sweep_bwd,
  * 5 prolong_dot, 6 pupdate, 7 ionic, 8 rhs */
 pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9);
+/* live timing of the Schwarz sweep inside the solves run so far: launches and
+ * their summed device duration (first CTA start to last CTA end, globaltimer) */
+pdg_status pdg_sim_sweep_live(pdg_sim* s, int64_t* launches, double* total_ms);
 /* one traced Schwarz sweep: 12 int64 per work unit (globaltimer at start,
  * deps met, inputs gathered, published, staging done, mat-vec done; task,
  * direction, panel bytes, chunks, task height, coarse flag); returns the unit

@@ -133,6 +133,7 @@ def _bind_device(L):
         "pdg_sim_timer": (i32, [vp, i32, P(dbl)]),
         "pdg_sim_kernel_launches": (i64, [vp]),
         "pdg_sim_profile": (i32, [vp, i32, P(dbl), P(i64)]),
+        "pdg_sim_sweep_live": (i32, [vp, P(i64), P(dbl)]),
         "pdg_sim_trace_sweep": (i32, [vp, P(i64), i32]),
     }
     for name, (res, args) in sig.items():

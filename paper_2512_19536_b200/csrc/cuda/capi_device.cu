@@ -197,6 +197,17 @@ pdg_status pdg_sim_profile(pdg_sim* s, int reps, double* ms9, int64_t* bytes9) {
   });
 }
 
+pdg_status pdg_sim_sweep_live(pdg_sim* s, int64_t* launches, double* total_ms) {
+  return pdg::guarded([&] {
+    auto& d = S(s);
+    unsigned long long v[3] = {0, 0, 0};
+    PDG_CUDA(cudaStreamSynchronize(d.st));
+    if (d.d_live) PDG_CUDA(cudaMemcpy(v, d.d_live, sizeof v, cudaMemcpyDeviceToHost));
+    if (launches) *launches = static_cast<int64_t>(v[2]);
+    if (total_ms) *total_ms = static_cast<double>(v[1]) * 1e-6;
+  });
+}
+
 pdg_status pdg_sim_attach_comm(pdg_sim* s, const void* id128, int rank, int world) {
   return pdg::guarded([&] { S(s).attach_comm(id128, rank, world); });
 }

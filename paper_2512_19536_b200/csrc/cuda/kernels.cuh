@@ -99,7 +99,8 @@ struct SweepArgs {
   const int* node_chunk_ptr;
   const PcgScalars* S;
   int* epoch;        // [0] sweep number (counters wait for (epoch+1) * count), [1] CTAs finished
-  int xcap;          // doubles per unit input buffer (two per CTA, double-buffered staging)
+  int xcap;          // doubles per unit input buffer
+  unsigned long long* live;  // [0] start of this launch (CTA 0), [1] summed launch ns, [2] launches
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);

@@ -386,6 +386,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
   double* part = sm;  // kSweepThreads doubles
   double* xin = part + kSweepThreads;
   if (threadIdx.x == 0) {
+    // live duration of every launch (first CTA start -> last CTA end, read by
+    // bench.py over its timed region)
+    if (blockIdx.x == 0 && a.live) a.live[0] = static_cast<unsigned long long>(gtimer());
     s.ep = __ldcg(a.epoch);
     for (int i = 0; i + 1 < kAhead; ++i) {
       if (i == 0 || s.q[i - 1].tk < a.n_units) fetch_ahead(a, s.q[i]);
@@ -425,6 +428,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
       a.epoch[1] = 0;
       *a.ticket = 0u;
       a.epoch[0] = s.ep + 1;
+      if (a.live) {
+        a.live[1] += static_cast<unsigned long long>(gtimer()) - __ldcg(a.live);
+        a.live[2] += 1;
+      }
       __threadfence();
     }
   }
