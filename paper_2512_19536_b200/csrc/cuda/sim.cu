@@ -522,6 +522,14 @@ void DeviceSim::upload_tasks() {
     PDG_CUDA(cudaMemsetAsync(d_live, 0, 3 * sizeof(unsigned long long), st));
   }
   PDG_CUDA(cudaStreamSynchronize(st));
+  panel_values = static_cast<long long>(pr.fmat.size() + pr.hmat.size());
+  // one rank: the panels live on the device from now on (config 4: ~40 GB of
+  // host memory back); several ranks re-pack after the coarse all-reduce
+  if (pr.cfg.world == 1) {
+    Problem& mp = *P;
+    std::vector<double>().swap(mp.fmat);
+    std::vector<double>().swap(mp.hmat);
+  }
 }
 
 DeviceSim::~DeviceSim() {
@@ -1006,7 +1014,7 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
     });
   else
     timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
-  const long long fvf = static_cast<long long>(pr.fmat.size()), fvh = static_cast<long long>(pr.hmat.size());
+  const long long fvf = panel_values, fvh = 0;  // F + H values (host copies released after upload)
   const long long tile_bytes = 24LL * static_cast<long long>(pr.ftiles.size());
   const long long idx_bytes = 8 * static_cast<long long>(pr.row_dof.size() + pr.in_idx.size()) +
                               4 * static_cast<long long>(pr.in_ptr.size()) + 64LL * n_tasks;

@@ -71,6 +71,7 @@ class DeviceSim {
   unsigned int* d_ticket = nullptr;
   int smem_fwd = 0, smem_bwd = 0, sweep_xcap = 0;
   unsigned long long* d_live = nullptr;  // live sweep timing (sweep.cu)
+  long long panel_values = 0;            // F + H doubles on the device
   // ionic
   double *d_bbox = nullptr, *d_tri = nullptr;
   int *d_tri_ptr = nullptr, *d_ionflags = nullptr;

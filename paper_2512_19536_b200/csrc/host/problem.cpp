@@ -547,11 +547,22 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   for (int k = 0; k < n_units; ++k)
     if (unit_rank[unit_order[k]] == cfg.rank) my_units.push_back(unit_order[k]);
   std::vector<UnitFactor> factors;
+  pr.in_ptr = {0};
+  bool packed = false;
   if (pr.has_precond) {
     if (multi_sub) {
-      factors.resize(my_units.size());
-      parallel_for(static_cast<int>(my_units.size()), [&](int k) {
-        const int u = my_units[k];
+      // factor a batch of subdomains in parallel, pack it (in subdomain
+      // order) and free it: only one batch of unpacked factors is alive, so
+      // the host peak is the packed panels plus a batch (config 4: ~40 GB of
+      // panels instead of twice that)
+      const int n_my = static_cast<int>(my_units.size());
+      const int batch = std::max(1, 4 * setup_threads());
+      for (int b0 = 0; b0 < n_my; b0 += batch) {
+      const int b1 = std::min(n_my, b0 + batch);
+      factors.assign(b1 - b0, UnitFactor{});
+      parallel_for(b1 - b0, [&](int kb) {
+        const int k = kb;
+        const int u = my_units[b0 + kb];
         const int m = static_cast<int>(unit_cells[u].size());
         const int s0 = unit_start[u];
         BlockMatrix Bm;
@@ -582,6 +593,11 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
                             " factorization failed (not positive definite)");
         }
       });
+      for (const UnitFactor& uf : factors)
+        pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b);
+      factors.clear();
+      }
+      packed = true;
     } else {
       // one element per subdomain: dense b x b Cholesky (schwarz.cpp:103-112)
       factors.resize(nloc);
@@ -611,16 +627,11 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       }, 256);
     }
   }
-  // pack fine tasks (host/pack.cpp)
-  pr.in_ptr = {0};
-  for (const UnitFactor& uf : factors) {
-    std::int64_t base;
-    if (multi_sub)
-      base = static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b;
-    else
-      base = static_cast<std::int64_t>(&uf - factors.data()) * b;
-    pack_unit_tasks(pr, uf.F, 0, base);
-  }
+  // pack fine tasks (host/pack.cpp); the multi-cell subdomains were packed
+  // batch by batch above
+  if (!packed)
+    for (const UnitFactor& uf : factors)
+      pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(&uf - factors.data()) * b);
   pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
   factors.clear();
 
