@@ -425,6 +425,151 @@ __global__ void __launch_bounds__(256) update_restrict_kernel(const int* __restr
   grid_finish(block_sum(contrib), rc);
 }
 
+// ---- coarse-space kernels with the chunk's E blocks staged by TMA ----
+// When every restriction chunk is a run of consecutive cells (the coarse
+// partition is the subdomain partition, so agglomerates are contiguous in the
+// internal order), a chunk's E blocks are one contiguous byte range: one bulk
+// copy (cp.async.bulk + mbarrier) brings it into shared memory while the CTA
+// does its vector work, instead of strided per-thread E loads.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Thread 0 starts the copy of the (16-byte widened) range [lo, hi) into dst;
+// returns the offset of lo inside dst. Call __syncthreads() before waiting.
+__device__ __forceinline__ int stage_bytes(const void* lo, const void* hi, unsigned char* dst, uint64_t* bar) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(lo), b = reinterpret_cast<unsigned long long>(hi);
+  const unsigned long long alo = a & ~15ull, ahi = (b + 15) & ~15ull;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(static_cast<unsigned>(ahi - alo))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(alo), "r"(static_cast<unsigned>(ahi - alo)), "r"(smem_addr(bar))
+        : "memory");
+  }
+  return static_cast<int>(a - alo);
+}
+
+__device__ __forceinline__ void wait_bytes(uint64_t* bar) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(bar))
+        : "memory");
+  }
+}
+
+template <int B, int BQ>
+__global__ void __launch_bounds__(256) update_restrict_tma_kernel(const int* __restrict__ chunk_ptr,
+                                                                  const int* __restrict__ cells,
+                                                                  const double* __restrict__ E,
+                                                                  double* __restrict__ x, double* __restrict__ r,
+                                                                  const double* __restrict__ p,
+                                                                  const double* __restrict__ q,
+                                                                  double* __restrict__ r0part, ReduceCtx rc) {
+  pdl_wait();
+  PcgScalars* S = rc.S;
+  if (S->stop) return;
+  const double pq = S->pq;
+  const int it = S->iter;
+  if (!isfinite(pq) || pq <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S->error = !isfinite(pq) ? kPcgPqNonFinite : kPcgPqNonPos;
+      S->stop = 1;
+    }
+    return;
+  }
+  const double alpha = S->rho / pq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rc.H.alpha[it] = alpha;
+    S->alpha = alpha;
+  }
+  extern __shared__ __align__(128) unsigned char dyn[];
+  __shared__ uint64_t bar;
+  __shared__ double rs[64 * B];
+  __shared__ double red[B * BQ];
+  const int c0 = chunk_ptr[blockIdx.x], nc = chunk_ptr[blockIdx.x + 1] - c0;
+  const long long cell0 = cells[c0];
+  const double* Eg = E + cell0 * (B * BQ);
+  const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
+  const double* Es = reinterpret_cast<const double*>(dyn + off);
+  // the x / r update overlaps the copy (consecutive dofs: coalesced)
+  double contrib = 0.0;
+  const long long d0 = cell0 * B;
+  for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
+    const long long d = d0 + e;
+    x[d] += alpha * p[d];
+    const double rv = r[d] - alpha * q[d];
+    r[d] = rv;
+    rs[e] = rv;
+    contrib += rv * rv;
+  }
+  __syncthreads();
+  wait_bytes(&bar);
+  // r0part[m] = sum_i sum_k E_k(i, m) r_k(i): thread f = (m, i) sums over cells
+  for (int f = threadIdx.x; f < B * BQ; f += blockDim.x) {
+    const int i = f % B;
+    double acc = 0.0;
+    for (int k = 0; k < nc; ++k) acc = fma(Es[k * (B * BQ) + f], rs[k * B + i], acc);
+    red[f] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < BQ) {
+    double s = 0.0;
+    for (int i = 0; i < B; ++i) s += red[threadIdx.x * B + i];
+    r0part[static_cast<long long>(blockIdx.x) * BQ + threadIdx.x] = s;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
+// z += E y0 for one chunk (all its cells share the agglomerate) and r.z
+template <int B, int BQ>
+__global__ void __launch_bounds__(256) prolong_dot_tma_kernel(const int* __restrict__ chunk_ptr,
+                                                              const int* __restrict__ cells,
+                                                              const int* __restrict__ cell_agg,
+                                                              const double* __restrict__ E,
+                                                              const double* __restrict__ y0,
+                                                              const double* __restrict__ r, double* __restrict__ z,
+                                                              ReduceCtx rc) {
+  pdl_wait();
+  if (rc.S->stop) return;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  __shared__ uint64_t bar;
+  __shared__ double ys[BQ];
+  const int c0 = chunk_ptr[blockIdx.x], nc = chunk_ptr[blockIdx.x + 1] - c0;
+  const long long cell0 = cells[c0];
+  const double* Eg = E + cell0 * (B * BQ);
+  const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
+  const double* Es = reinterpret_cast<const double*>(dyn + off);
+  if (threadIdx.x < BQ) ys[threadIdx.x] = y0[static_cast<long long>(cell_agg[cell0]) * BQ + threadIdx.x];
+  __syncthreads();
+  wait_bytes(&bar);
+  double contrib = 0.0;
+  const long long d0 = cell0 * B;
+  for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
+    const int k = e / B, i = e - k * B;
+    const long long d = d0 + e;
+    const double* ek = Es + k * (B * BQ) + i;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < BQ; ++m) acc = fma(ek[m * B], ys[m], acc);
+    const double zi = z[d] + acc;
+    z[d] = zi;
+    contrib += r[d] * zi;
+  }
+  grid_finish(block_sum(contrib), rc);
+}
+
 // Schwarz supernode sweeps: see sweep.cu
 
 // ---------------- ionic terms at quadrature nodes ----------------
@@ -766,6 +911,65 @@ void launch_update_restrict(int b, int bq, int n_chunks, const int* chunk_ptr, c
                             double* x, double* r, const double* p, const double* q, double* r0part, ReduceCtx rc,
                             cudaStream_t st) {
 #define L(B) update_restrict_dispatch<B>(bq, n_chunks, chunk_ptr, cells, E, x, r, p, q, r0part, rc, st)
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+template <int B, int BQ>
+static void coarse_tma_launch(bool update, int n_chunks, int max_nc, const int* chunk_ptr, const int* cells,
+                              const int* cell_agg, const double* E, double* x, double* r, const double* p,
+                              const double* q, double* r0part, const double* y0, double* z, ReduceCtx rc,
+                              cudaStream_t st) {
+  const int smem = max_nc * B * BQ * 8 + 32;  // + widening of the range to 16-byte ends
+  static int set_u = 0, set_p = 0;
+  if (update) {
+    if (smem > set_u) {
+      PDG_CUDA(cudaFuncSetAttribute(update_restrict_tma_kernel<B, BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      set_u = smem;
+    }
+    launch_pdl(update_restrict_tma_kernel<B, BQ>, n_chunks, 256, smem, st, chunk_ptr, cells, E, x, r, p, q, r0part, rc);
+  } else {
+    if (smem > set_p) {
+      PDG_CUDA(cudaFuncSetAttribute(prolong_dot_tma_kernel<B, BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      set_p = smem;
+    }
+    launch_pdl(prolong_dot_tma_kernel<B, BQ>, n_chunks, 256, smem, st, chunk_ptr, cells, cell_agg, E, y0, r, z, rc);
+  }
+}
+
+template <int B>
+static void coarse_tma_dispatch(bool update, int bq, int n_chunks, int max_nc, const int* chunk_ptr,
+                                const int* cells, const int* cell_agg, const double* E, double* x, double* r,
+                                const double* p, const double* q, double* r0part, const double* y0, double* z,
+                                ReduceCtx rc, cudaStream_t st) {
+#define CT(BQ) coarse_tma_launch<B, BQ>(update, n_chunks, max_nc, chunk_ptr, cells, cell_agg, E, x, r, p, q, r0part, y0, z, rc, st)
+  switch (bq) {
+    case 3: CT(3); break;
+    case 6: if constexpr (B >= 6) { CT(6); break; }
+    [[fallthrough]];
+    case 10: if constexpr (B >= 10) { CT(10); break; }
+    [[fallthrough]];
+    case 15: if constexpr (B >= 15) { CT(15); break; }
+    [[fallthrough]];
+    default: throw CudaError("unsupported coarse block size");
+  }
+#undef CT
+}
+
+void launch_update_restrict_tma(int b, int bq, int n_chunks, int max_chunk_cells, const int* chunk_ptr,
+                                const int* cells, const double* E, double* x, double* r, const double* p,
+                                const double* q, double* r0part, ReduceCtx rc, cudaStream_t st) {
+#define L(B) coarse_tma_dispatch<B>(true, bq, n_chunks, max_chunk_cells, chunk_ptr, cells, nullptr, E, x, r, p, q, \
+                                    r0part, nullptr, nullptr, rc, st)
+  PDG_B_DISPATCH(b, L)
+#undef L
+}
+
+void launch_prolong_dot_tma(int b, int bq, int n_chunks, int max_chunk_cells, const int* chunk_ptr, const int* cells,
+                            const int* cell_agg, const double* E, const double* y0, const double* r, double* z,
+                            ReduceCtx rc, cudaStream_t st) {
+#define L(B) coarse_tma_dispatch<B>(false, bq, n_chunks, max_chunk_cells, chunk_ptr, cells, cell_agg, E, nullptr, \
+                                    const_cast<double*>(r), nullptr, nullptr, nullptr, y0, z, rc, st)
   PDG_B_DISPATCH(b, L)
 #undef L
 }

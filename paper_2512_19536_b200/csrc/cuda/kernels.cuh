@@ -65,6 +65,15 @@ void launch_update_restrict(int b, int bq, int n_chunks, const int* chunk_ptr, c
                             double* x, double* r, const double* p, const double* q, double* r0part, ReduceCtx rc,
                             cudaStream_t st);
 
+// the same two coarse-space steps when every chunk is a run of consecutive
+// cells: the chunk's E blocks are brought into shared memory by one bulk copy
+void launch_update_restrict_tma(int b, int bq, int n_chunks, int max_chunk_cells, const int* chunk_ptr,
+                                const int* cells, const double* E, double* x, double* r, const double* p,
+                                const double* q, double* r0part, ReduceCtx rc, cudaStream_t st);
+void launch_prolong_dot_tma(int b, int bq, int n_chunks, int max_chunk_cells, const int* chunk_ptr, const int* cells,
+                            const int* cell_agg, const double* E, const double* y0, const double* r, double* z,
+                            ReduceCtx rc, cudaStream_t st);
+
 // r0 chunk partials -> r0 (one CTA-sized chunk of an agglomerate per restrict CTA)
 void launch_restrict_combine(int bq, int n_agg, const int* node_chunk_ptr, const double* part, double* r0,
                              const PcgScalars* S, cudaStream_t st);

@@ -131,6 +131,15 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
       nptr.push_back(static_cast<int>(cptr.size()) - 1);
     }
     n_chunks = static_cast<int>(cptr.size()) - 1;
+    // chunks of consecutive cells -> the coarse kernels stage E by bulk copy
+    chunks_contiguous = true;
+    max_chunk_cells = 1;
+    for (int c = 0; c < n_chunks; ++c) {
+      max_chunk_cells = std::max(max_chunk_cells, cptr[c + 1] - cptr[c]);
+      for (int k = cptr[c]; k < cptr[c + 1]; ++k)
+        if (pr.agg_cells[k] != pr.agg_cells[cptr[c]] + (k - cptr[c])) chunks_contiguous = false;
+    }
+    if (std::getenv("PDG_COARSE_TMA") && std::atoi(std::getenv("PDG_COARSE_TMA")) == 0) chunks_contiguous = false;
     d_chunk_ptr = dupload(cptr, st);
     d_node_chunk_ptr = dupload(nptr, st);
     d_r0part = dalloc<double>(static_cast<std::size_t>(std::max(n_chunks, 1)) * pr.bq);
@@ -622,7 +631,11 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
     }
   }
   launch_sweep(sweep_args(true, r, z, Sh), smem_fwd, st);
-  launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
+  if (pr.two_level && chunks_contiguous)
+    launch_prolong_dot_tma(b, bq, n_chunks, max_chunk_cells, d_chunk_ptr, d_agg_cells, d_cell_agg, d_E, d_y0, r, z,
+                           red_for(finish), st);
+  else
+    launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, r, z, red_for(finish), st);
   after_reduce(finish, honor);
 }
 
@@ -663,7 +676,10 @@ void DeviceSim::record_iteration() {
   launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
   after_reduce(kFinPq, true);
   const bool fuse = use_pc() && P->two_level && world == 1;
-  if (fuse)
+  if (fuse && chunks_contiguous)
+    launch_update_restrict_tma(b, bq, n_chunks, max_chunk_cells, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q,
+                               d_r0part, red_for(kFinRr), st);
+  else if (fuse)
     launch_update_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q, d_r0part,
                            red_for(kFinRr), st);
   else
@@ -1010,7 +1026,11 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
   const bool fused = use_pc() && pr.two_level && world == 1;
   if (fused)  // slot 1 = the update fused with the restriction (slots 2, 4 stay 0)
     timeit(1, 48 * n + 8 * N * b * bq + 4 * N + 8LL * n_chunks * bq, [&] {
-      launch_update_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q, d_r0part, rs, st);
+      if (chunks_contiguous)
+        launch_update_restrict_tma(b, bq, n_chunks, max_chunk_cells, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p,
+                                   d_q, d_r0part, rs, st);
+      else
+        launch_update_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, d_p, d_q, d_r0part, rs, st);
     });
   else
     timeit(1, 48 * n, [&] { launch_update(n, d_x, d_r, d_p, d_q, rs, st); });
@@ -1029,7 +1049,13 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
     timeit(3, 8 * (fvf + fvh) + 32 * n + 2 * (idx_bytes + tile_bytes),
            [&] { launch_sweep(sweep_args(true, d_r, d_z, nullptr), smem_fwd, st); });
     timeit(5, 8 * N * b * bq + 24 * n + 4 * N,
-           [&] { launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st); });
+           [&] {
+             if (pr.two_level && chunks_contiguous)
+               launch_prolong_dot_tma(b, bq, n_chunks, max_chunk_cells, d_chunk_ptr, d_agg_cells, d_cell_agg, d_E,
+                                      d_y0, d_r, d_z, rs, st);
+             else
+               launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st);
+           });
   }
   timeit(6, 24 * n, [&] { launch_pupdate(n, d_tmp, d_z, d_S, false, st); });
   timeit(8, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 8 * N * b * b + 56 * n, [&] {

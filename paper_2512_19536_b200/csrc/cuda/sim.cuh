@@ -55,7 +55,8 @@ class DeviceSim {
   // coarse
   double *d_E = nullptr, *d_r0 = nullptr, *d_y0 = nullptr;
   int *d_cell_agg = nullptr, *d_agg_ptr = nullptr, *d_agg_cells = nullptr;
-  int n_chunks = 0;
+  int n_chunks = 0, max_chunk_cells = 0;
+  bool chunks_contiguous = false;
   int *d_chunk_ptr = nullptr, *d_node_chunk_ptr = nullptr;
   double* d_r0part = nullptr;
   // sweep

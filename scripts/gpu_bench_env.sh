@@ -8,7 +8,7 @@ for e in "$@"; do
 import json, sys
 try:
     d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1]); r = d["roofline"]
-    print(f"{sys.argv[1]:60s} value {d['value']:.4g} sweep_us {r['launch_ms']*1e3:.1f} GB/s {r['kernels']['sweep']['GB/s']:.0f}")
+    print(f"{sys.argv[1]:60s} value {d['value']:.4g} sweep_us {r['launch_ms']*1e3:.1f} GB/s {r['kernels']['sweep']['GB/s']:.0f} update_us {r['kernels']['update']['ms']*1e3:.1f} prolong_us {r['kernels']['prolong_dot']['ms']*1e3:.1f}")
 except Exception as ex:
     print(sys.argv[1], "FAILED", ex)
 PY
