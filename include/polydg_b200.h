@@ -129,6 +129,8 @@ void pdg_problem_perm(const pdg_problem* p, int* perm);
  * first cell), recv = peer's global internal cells; counts = {nsend, nrecv};
  * NULL arrays query the sizes */
 void pdg_problem_rank_cells(const pdg_problem* p, int* starts);
+/* copy of the problem's mesh (reference cell order) as an owning pdg_mesh */
+pdg_status pdg_problem_mesh(const pdg_problem* p, pdg_mesh** out);
 void pdg_problem_halo(const pdg_problem* p, int peer, int* send, int* recv, int counts[2]);
 
 /* ---- simulation on the device (Simulation, timestepper.hpp:109-152) ---- */
@@ -175,6 +177,14 @@ pdg_status pdg_sim_apply_precond(pdg_sim* s, const double* r, double* z);
  * gives plain CG. maxit <= 0 -> default_max_iterations. */
 pdg_status pdg_sim_pcg(pdg_sim* s, const double* b, const double* x0, double tol, int maxit,
                        int use_precond, double* x, pdg_pcg_report* rep);
+/* cell_means (snapshot.cpp:13-28) of the current potential U^k, computed on
+ * the device at the order-2p+2 rule; `means` holds n_cells doubles in
+ * reference cell order (cells of other ranks are left 0). */
+pdg_status pdg_sim_cell_means(pdg_sim* s, double* means);
+/* export_snapshot (snapshot.cpp:30-75) of U^k at the simulation time:
+ * format "vtk-legacy" or "csv-cellmeans"; PDG_ERR_CONFIG on an unknown
+ * format, PDG_ERR_IO when the file cannot be written. */
+pdg_status pdg_sim_export_snapshot(pdg_sim* s, const char* path, const char* format);
 /* device-resident variants for benchmarking: vectors already on the device,
  * internal order. */
 pdg_status pdg_sim_pcg_device(pdg_sim* s, const double* d_b, const double* d_x0, double tol,

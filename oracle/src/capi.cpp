@@ -262,6 +262,14 @@ int orc_sim_ionic_terms(void* h, const double* U, const double* Y, double* I, do
   });
 }
 
+int orc_sim_cell_means(void* h, const double* U, double* means) {
+  return guarded([&] {
+    auto& s = *static_cast<orc::Simulation*>(h);
+    const orc::Vec m = orc::cell_means(s.D, orc::Vec(U, U + s.U.size()));
+    std::memcpy(means, m.data(), m.size() * sizeof(double));
+  });
+}
+
 int orc_pcg_dense(int n, const double* A, const double* b, const double* Pm, double tol, int maxit,
                   const double* x0, double* x, orc_report* rep) {
   return guarded([&] {

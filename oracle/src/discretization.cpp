@@ -542,6 +542,26 @@ Vec Discretization::l2_project(const std::function<double(P2)>& g) const {
   return mass_solve(rhs);
 }
 
+// cell_means (snapshot.cpp:13-28): (1/|K|) sum_q w_q (Phi U_K)_q at order 2p+2,
+// |K| the shoelace area of the cell (mesh.cpp:36, geometry.cpp:11-20)
+Vec cell_means(const Discretization& D, const Vec& U) {
+  const int nl = D.nloc, nc = D.mesh->n_cells();
+  Vec means(nc, 0.0), val;
+  for (int e = 0; e < nc; ++e) {
+    const std::vector<P2> poly = D.mesh->cell(e);
+    const Rule r = polygon_rule(poly, 2 * D.p + 2);
+    eval_basis(D.mesh->bbox[e], D.p, r.pts, val, nullptr, nullptr);
+    double acc = 0.0;
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      double u = 0.0;
+      for (int i = 0; i < nl; ++i) u += val[q * nl + i] * U[static_cast<int64_t>(e) * nl + i];
+      acc += r.w[q] * u;
+    }
+    means[e] = acc / signed_area(poly);
+  }
+  return means;
+}
+
 // ---------------- ionics ----------------
 double fhn_current(const double* P, double u, double w) {
   if (!std::isfinite(u) || !std::isfinite(w)) throw SolverError("fhn: non-finite state in current evaluation");

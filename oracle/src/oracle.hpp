@@ -134,6 +134,9 @@ struct Discretization {
   Vec l2_project(const std::function<double(P2)>& g) const;
 };
 
+// ---- snapshot.cpp:13-28 ----
+Vec cell_means(const Discretization& D, const Vec& U);
+
 // ---- ionics (ionics.cpp:20-113) ----
 double fhn_current(const double* prm, double u, double w);
 double fhn_rate(const double* prm, double u, double w);

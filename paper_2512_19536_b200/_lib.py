@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
             "pdg_problem_perm": (None, [vp, P(i32)]),
             "pdg_problem_rank_cells": (None, [vp, P(i32)]),
             "pdg_problem_halo": (None, [vp, i32, P(i32), P(i32), P(i32)]),
+            "pdg_problem_mesh": (i32, [vp, P(vp)]),
             "pdg_default_max_iterations": (i32, [i64]),
         }
         for name, (res, args) in sig.items():
@@ -124,6 +125,8 @@ def _bind_device(L):
         "pdg_sim_set_state": (i32, [vp, i32, P(dbl), P(dbl), P(dbl), P(dbl)]),
         "pdg_sim_apply_K": (i32, [vp, P(dbl), P(dbl)]),
         "pdg_sim_apply_precond": (i32, [vp, P(dbl), P(dbl)]),
+        "pdg_sim_cell_means": (i32, [vp, P(dbl)]),
+        "pdg_sim_export_snapshot": (i32, [vp, C.c_char_p, C.c_char_p]),
         "pdg_sim_pcg": (i32, [vp, P(dbl), P(dbl), dbl, i32, i32, P(dbl), P(PcgReport)]),
         "pdg_sim_pcg_device": (i32, [vp, vp, vp, dbl, i32, vp, P(PcgReport)]),
         "pdg_condition_estimate": (i32, [P(dbl), P(dbl), i32, P(dbl)]),

@@ -272,6 +272,10 @@ extern "C" {
 // SpMV halo of this rank against `peer` (host/pack.cpp halo_plan): send = local
 // internal cells (relative to the rank's first cell), recv = global internal
 // cells; counts[0..1] = sizes. Arrays may be NULL to query the sizes.
+pdg_status pdg_problem_mesh(const pdg_problem* h, pdg_mesh** out) {
+  return pdg::guarded([&] { *out = new pdg_mesh{h->p->mesh}; });
+}
+
 void pdg_problem_halo(const pdg_problem* h, int peer, int* send, int* recv, int counts[2]) {
   std::vector<std::vector<int>> s, r;
   pdg::halo_plan(*h->p, s, r);

@@ -5,8 +5,12 @@
 
 #include <cstring>
 #include <memory>
+#include <string>
+#include <vector>
+#include <algorithm>
 
 #include "../capi_internal.hpp"
+#include "../host/snapshot.hpp"
 #include "sim.cuh"
 
 struct pdg_problem {
@@ -63,6 +67,15 @@ void fill_report(const pdg::PcgResult& r, pdg_pcg_report* rep) {
   cp(r.beta, rep->betas);
 }
 
+// device cell means scattered to reference cell order (other ranks' cells 0)
+void cell_means_ref(pdg::DeviceSim& d, double* means) {
+  const pdg::Problem& pr = *d.P;
+  std::vector<double> local;
+  d.cell_means(local);
+  std::fill(means, means + pr.mesh.n_cells(), 0.0);
+  for (int i = 0; i < d.ncells; ++i) means[pr.perm[pr.cell_begin + i]] = local[i];
+}
+
 }  // namespace
 
 extern "C" {
@@ -114,6 +127,22 @@ pdg_status pdg_sim_step(pdg_sim* s, pdg_step_stats* stats) {
       stats->solve_ms = r.solve_ms;
       stats->step_ms = r.step_ms;
     }
+  });
+}
+
+pdg_status pdg_sim_cell_means(pdg_sim* s, double* means) {
+  return pdg::guarded([&] { cell_means_ref(S(s), means); });
+}
+
+pdg_status pdg_sim_export_snapshot(pdg_sim* s, const char* path, const char* format) {
+  return pdg::guarded([&] {
+    pdg::DeviceSim& d = S(s);
+    const pdg::Problem& pr = *d.P;
+    if (std::string(format) != "vtk-legacy" && std::string(format) != "csv-cellmeans")
+      throw pdg::ConfigError("unknown snapshot format '" + std::string(format) + "'");
+    std::vector<double> means(pr.mesh.n_cells());
+    cell_means_ref(d, means.data());
+    pdg::write_snapshot(pr.mesh, means, d.t, path, format);
   });
 }
 

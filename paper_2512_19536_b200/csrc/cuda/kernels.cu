@@ -989,6 +989,52 @@ void launch_pack(const double* v, const int* cells, int ncells, int b, double* o
   pack_kernel<<<vec_grid(static_cast<long long>(ncells) * b), kVecThreads, 0, st>>>(v, cells, ncells, b, out);
 }
 
+// ---------------- per-cell means (snapshot.cpp:13-28) ----------------
+// mean_K = (1/|K|) sum_q w_q (Phi U_K)_q over the order-2p+2 rule, one warp
+// per cell; the quadrature points are generated exactly like the ionic ones.
+template <int P>
+__global__ void __launch_bounds__(256) cell_means_kernel(int ncells, int ngl, const double* __restrict__ bbox,
+                                                         const int* __restrict__ tri_ptr,
+                                                         const double* __restrict__ tri,
+                                                         const double* __restrict__ U,
+                                                         const double* __restrict__ area,
+                                                         double* __restrict__ out) {
+  constexpr int B = (P + 1) * (P + 2) / 2;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= ncells) return;
+  const long long o = static_cast<long long>(c) * B;
+  double Uc[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) Uc[k] = U[o + k];
+  const double bx0 = bbox[4 * c], by0 = bbox[4 * c + 1], bx1 = bbox[4 * c + 2], by1 = bbox[4 * c + 3];
+  const double wx = bx1 - bx0, wy = by1 - by0;
+  const double inv = 1.0 / sqrt(wx * wy);
+  const int t0 = tri_ptr[c], t1 = tri_ptr[c + 1];
+  const int npt = (t1 - t0) * ngl * ngl;
+  double acc = 0.0;
+  for (int pidx = lane; pidx < npt; pidx += 32) {
+    const int tr = pidx / (ngl * ngl), rem = pidx - tr * ngl * ngl;
+    const int i = rem / ngl, j = rem - i * ngl;
+    const double* T = tri + static_cast<long long>(t0 + tr) * 6;
+    const double ax = T[0], ay = T[1], bxx = T[2], byy = T[3], cx = T[4], cy = T[5];
+    const double s = 0.5 * (c_glx[i] + 1.0), tt = 0.5 * (c_glx[j] + 1.0);
+    const double eta = tt * (1.0 - s);
+    const double area2 = (bxx - ax) * (cy - ay) - (byy - ay) * (cx - ax);
+    const double px = ax + (bxx - ax) * s + (cx - ax) * eta;
+    const double py = ay + (byy - ay) * s + (cy - ay) * eta;
+    const double w = c_glw[i] * c_glw[j] * 0.25 * (1.0 - s) * area2;
+    double phi[B];
+    basis_eval<P>((2.0 * px - bx0 - bx1) / wx, (2.0 * py - by0 - by1) / wy, inv, phi);
+    double u = 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) u = fma(phi[k], Uc[k], u);
+    acc = fma(w, u, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[c] = acc / area[c];
+}
+
 void set_gauss_nodes(const double* x, const double* w, int n) {
   PDG_CUDA(cudaMemcpyToSymbol(c_glx, x, sizeof(double) * n));
   PDG_CUDA(cudaMemcpyToSymbol(c_glw, w, sizeof(double) * n));
@@ -1006,6 +1052,23 @@ void launch_ionic(const IonicArgs& a, cudaStream_t st) {
     case 6: ionic_kernel<6><<<g, 256, 0, st>>>(a); break;
     default: throw CudaError("unsupported degree for the ionic kernel");
   }
+}
+
+void launch_cell_means(int p, int ncells, int ngl, const double* bbox, const int* tri_ptr, const double* tri,
+                       const double* U, const double* area, double* out, cudaStream_t st) {
+  const int g = (ncells + 7) / 8;
+  if (ncells == 0) return;
+#define PDG_CM(P) cell_means_kernel<P><<<g, 256, 0, st>>>(ncells, ngl, bbox, tri_ptr, tri, U, area, out)
+  switch (p) {
+    case 1: PDG_CM(1); break;
+    case 2: PDG_CM(2); break;
+    case 3: PDG_CM(3); break;
+    case 4: PDG_CM(4); break;
+    case 5: PDG_CM(5); break;
+    case 6: PDG_CM(6); break;
+    default: throw CudaError("unsupported degree for the cell-means kernel");
+  }
+#undef PDG_CM
 }
 
 void launch_gather_perm(const double* src, double* dst, const int* perm, int ncells, int b, int nf,

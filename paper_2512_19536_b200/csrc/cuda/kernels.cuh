@@ -135,6 +135,9 @@ struct IonicArgs {
 };
 void set_gauss_nodes(const double* x, const double* w, int n);
 void launch_ionic(const IonicArgs& a, cudaStream_t st);
+// per-cell means of U over the order-2p+2 rule (snapshot.cpp:13-28)
+void launch_cell_means(int p, int ncells, int ngl, const double* bbox, const int* tri_ptr, const double* tri,
+                       const double* U, const double* area, double* out, cudaStream_t st);
 
 // multi-rank helpers: apply a finish to an all-reduced sum; pack halo cells
 void launch_finish(ReduceCtx rc, const double* sum, bool honor, cudaStream_t st);

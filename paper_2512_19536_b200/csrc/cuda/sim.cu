@@ -549,7 +549,7 @@ DeviceSim::~DeviceSim() {
                   d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
                   d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage, d_chunk_ptr, d_node_chunk_ptr, d_r0part,
-                  d_live};
+                  d_live, d_area, d_means};
   cudaEventDestroy(ev_t0);
   cudaEventDestroy(ev_t1);
   comm_destroy();
@@ -864,6 +864,23 @@ IonicArgs DeviceSim::ionic_args(bool has_prev) const {
   std::memcpy(a.stim_p, c.stim_params, sizeof a.stim_p);
   a.flags = d_ionflags;
   return a;
+}
+
+// cell_means (snapshot.cpp:13-28) of U^k on the device
+void DeviceSim::cell_means(std::vector<double>& out) {
+  const Problem& pr = *P;
+  if (!d_area) {
+    std::vector<double> area(ncells);
+    for (int i = 0; i < ncells; ++i) area[i] = pr.mesh.area(pr.perm[pr.cell_begin + i]);
+    d_area = dupload(area, st);
+    d_means = dalloc<double>(ncells);
+  }
+  launch_cell_means(pr.p, ncells, static_cast<int>(pr.gl_x.size()), d_bbox, d_tri_ptr, d_tri, d_U[0], d_area,
+                    d_means, st);
+  PDG_CUDA(cudaGetLastError());
+  out.resize(ncells);
+  PDG_CUDA(cudaMemcpyAsync(out.data(), d_means, sizeof(double) * ncells, cudaMemcpyDeviceToHost, st));
+  PDG_CUDA(cudaStreamSynchronize(st));
 }
 
 StepResult DeviceSim::step() {

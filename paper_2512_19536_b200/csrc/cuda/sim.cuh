@@ -76,6 +76,7 @@ class DeviceSim {
   // ionic
   double *d_bbox = nullptr, *d_tri = nullptr;
   int *d_tri_ptr = nullptr, *d_ionflags = nullptr;
+  double *d_area = nullptr, *d_means = nullptr;  // cell means (snapshot.cpp:13-28), lazy
   // pcg bookkeeping
   Reducer red{};
   PcgScalars* d_S = nullptr;
@@ -99,6 +100,8 @@ class DeviceSim {
   void apply_K(const double* x, double* y);
   void apply_precond(const double* r, double* z);
   StepResult step();
+  // per-cell means of the current potential, this rank's cells, internal order
+  void cell_means(std::vector<double>& out);
 
   // multi-rank hooks (no-ops on one GPU)
   virtual void halo_exchange(double* v);

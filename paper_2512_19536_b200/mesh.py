@@ -46,6 +46,12 @@ class Mesh:
         split = -1e300 if split_y is None else float(split_y)
         check(L.pdg_mesh_generate(int(n_cells), d, C.c_uint64(seed), int(lloyd), split, C.byref(self._h)))
 
+    @classmethod
+    def _adopt(cls, handle):
+        obj = cls.__new__(cls)
+        obj._h = handle
+        return obj
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib().pdg_mesh_free(self._h)

@@ -228,6 +228,13 @@ class Problem:
         lib().pdg_problem_owner(self._h, 0 if which == "subdomain" else 1, _lib.iptr(o))
         return o
 
+    def mesh(self):
+        """The problem's mesh (reference cell order) as an owning mesh.Mesh."""
+        from .mesh import Mesh
+        h = C.c_void_p()
+        check(lib().pdg_problem_mesh(self._h, C.byref(h)))
+        return Mesh._adopt(h)
+
     def perm(self) -> np.ndarray:
         p = np.zeros(self.n_cells, np.int32)
         lib().pdg_problem_perm(self._h, _lib.iptr(p))
@@ -285,6 +292,17 @@ class Simulation:
         keep = [np.ascontiguousarray(a, dtype=np.float64).ravel() if a is not None else None
                 for a in (U_curr, U_prev, Y_curr, Y_prev)]
         check(lib().pdg_sim_set_state(self._h, int(k), *[dptr(a) if a is not None else None for a in keep]))
+
+    # --- snapshot.hpp:13-22 (means on the device, file written by the library) ---
+    def cell_means(self) -> np.ndarray:
+        """Per-cell means of U^k (snapshot.cpp:13-28), reference cell order."""
+        m = np.zeros(self.problem.n_cells)
+        check(lib().pdg_sim_cell_means(self._h, dptr(m)))
+        return m
+
+    def export_snapshot(self, path: str, fmt: str = "vtk-legacy") -> None:
+        """export_snapshot (snapshot.cpp:30-75) of U^k at the current time."""
+        check(lib().pdg_sim_export_snapshot(self._h, str(path).encode(), fmt.encode()))
 
     # --- LinearOperator::apply (krylov.hpp:15-30, schwarz.hpp:47-72) ---
     def apply_K(self, x: np.ndarray) -> np.ndarray:

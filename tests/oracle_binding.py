@@ -60,6 +60,7 @@ def lib():
             "orc_sim_pcg": (i32, [vp, P(dbl), P(dbl), dbl, i32, i32, P(dbl), P(OrcReport)]),
             "orc_sim_export": (i64, [vp, i32, P(i64), P(i64), P(dbl)]),
             "orc_sim_ionic_terms": (i32, [vp, P(dbl), P(dbl), P(dbl), P(dbl)]),
+            "orc_sim_cell_means": (i32, [vp, P(dbl), P(dbl)]),
             "orc_pcg_dense": (i32, [i32, P(dbl), P(dbl), P(dbl), dbl, i32, P(dbl), P(dbl), P(OrcReport)]),
             "orc_condition_estimate": (i32, [P(dbl), P(dbl), i32, P(dbl)]),
             "orc_fhn": (i32, [P(dbl), dbl, dbl, P(dbl), P(dbl)]),
@@ -152,6 +153,7 @@ class OracleSim:
                                     None if co is None else _i(co), int(n_coarse), C.byref(self._h)))
         self.dimension = lib().orc_sim_dimension(self._h)
         self.n_comp = 1 if config.ionic_model == "fhn" else 0
+        self.regions = reg
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -218,6 +220,13 @@ class OracleSim:
         I, G = np.zeros(self.dimension), np.zeros(self.dimension)
         _check(lib().orc_sim_ionic_terms(self._h, _d(U), _d(Y), _d(I), _d(G)))
         return I, G
+
+    def cell_means(self, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        nc = len(self.regions)
+        m = np.zeros(nc)
+        _check(lib().orc_sim_cell_means(self._h, _d(U), _d(m)))
+        return m
 
 
 def oracle_for(config: SimulationConfig, mesh=None):
