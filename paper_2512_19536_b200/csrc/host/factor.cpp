@@ -1,6 +1,9 @@
 #include "factor.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <string>
@@ -13,14 +16,109 @@ std::int64_t SupernodalFactor::values() const {
   return n;
 }
 
+namespace {
+
+bool separator_cover() {
+  static const bool on = [] {
+    const char* e = std::getenv("PDG_ND_COVER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Minimum vertex cover of the bipartite graph of edges between side 0 and
+// side 1 (nodes of `ord`, side[] in {0,1}): maximum matching by augmenting
+// paths (Kuhn, sides scanned in `ord` order, so deterministic), then Koenig's
+// construction: Z = nodes reachable from unmatched side-0 nodes by
+// alternating paths; cover = (side0 \ Z) u (side1 n Z). Returned in `ord` order.
+std::vector<int> min_cut_cover(const std::vector<int>& ord, const std::vector<int>& side,
+                               const std::vector<int>& ap, const std::vector<int>& aj, std::vector<int>& mate,
+                               std::vector<int>& seen, std::vector<int>& par) {
+  std::vector<int> L;
+  for (int v : ord) {
+    if (side[v] != 0) continue;
+    for (int k = ap[v]; k < ap[v + 1]; ++k)
+      if (side[aj[k]] == 1) {
+        L.push_back(v);
+        break;
+      }
+  }
+  int stamp = 0;
+  // BFS for an augmenting path from the free side-0 node u; par[w] = side-0
+  // node that reached side-1 node w
+  std::vector<int> q;
+  auto augment = [&](int u) -> bool {
+    ++stamp;
+    q.assign(1, u);
+    for (std::size_t h = 0; h < q.size(); ++h) {
+      const int x = q[h];
+      for (int k = ap[x]; k < ap[x + 1]; ++k) {
+        int w = aj[k];
+        if (side[w] != 1 || seen[w] == stamp) continue;
+        seen[w] = stamp;
+        par[w] = x;
+        if (mate[w] < 0) {
+          while (w >= 0) {  // flip the alternating path back to u
+            const int y = par[w], next = mate[y];
+            mate[y] = w;
+            mate[w] = y;
+            w = next;
+          }
+          return true;
+        }
+        q.push_back(mate[w]);
+      }
+    }
+    return false;
+  };
+  for (int u : L) augment(u);
+  // Koenig: alternating BFS from unmatched left nodes
+  ++stamp;
+  q.clear();
+  std::vector<char> inZ;
+  for (int u : L)
+    if (mate[u] < 0) {
+      q.push_back(u);
+      seen[u] = stamp;
+    }
+  for (std::size_t h = 0; h < q.size(); ++h) {
+    const int u = q[h];
+    if (side[u] == 0) {
+      for (int k = ap[u]; k < ap[u + 1]; ++k) {
+        const int w = aj[k];
+        if (side[w] == 1 && seen[w] != stamp && mate[u] != w) {
+          seen[w] = stamp;
+          q.push_back(w);
+        }
+      }
+    } else if (mate[u] >= 0 && seen[mate[u]] != stamp) {
+      seen[mate[u]] = stamp;
+      q.push_back(mate[u]);
+    }
+  }
+  std::vector<int> cover;
+  for (int v : ord) {
+    if (side[v] == 0) {
+      if (mate[v] >= 0 && seen[v] != stamp) cover.push_back(v);
+    } else if (side[v] == 1 && mate[v] >= 0 && seen[v] == stamp) {
+      cover.push_back(v);
+    }
+  }
+  for (int v : ord) mate[v] = seen[v] = -1;
+  return cover;
+}
+
+}  // namespace
+
 NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
                          const std::vector<Pt>& pos, int leaf, int merge) {
   NdTree t;
   merge = std::max(1, merge);
   t.order.reserve(m);
   t.sn_start.push_back(0);
-  std::vector<int> side(m, -1);
+  std::vector<int> side(m, -1), mate(m, -1), seen(m, -1), par(m, -1);
   constexpr int n_dirs = 4;
+  const bool mvc = separator_cover();
   auto emit = [&](const std::vector<int>& nodes) {
     for (int v : nodes) t.order.push_back(v);
     t.sn_start.push_back(static_cast<int>(t.order.size()));
@@ -66,6 +164,12 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
                 break;
               }
             }
+          }
+          if (mvc) {
+            // minimum vertex cover of the cut edges (Koenig): the smallest
+            // separator whose removal disconnects the two halves
+            std::vector<int> cover = min_cut_cover(ord, side, adj_ptr, adj, mate, seen, par);
+            if (cover.size() < sep_l.size() && cover.size() < sep_r.size()) sep_l = std::move(cover);
           }
           for (int v : ord) side[v] = -1;
           std::vector<int>& s = sep_r.size() < sep_l.size() ? sep_r : sep_l;
@@ -252,6 +356,15 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
         double* ck = P.data() + static_cast<std::size_t>(k) * H;
         for (int i = k; i < H; ++i) ck[i] -= cj[i] * lkj;
       }
+    }
+    if (std::getenv("PDG_FILL_STATS")) {
+      static std::atomic<long long> dense{0}, lnz{0}, sky{0}, diag{0};
+      static std::atomic<int> cnt{0};
+      long long d = (long long)w * (w + 1) / 2 + (long long)r * bs * w, l = 0, sk = 0;
+      for (int j = 0; j < w; ++j) for (int i = j; i < H; ++i) if (P[(size_t)j * H + i] != 0.0) ++l;
+      for (int i = w; i < H; ++i) { int f = w; for (int j = 0; j < w; ++j) if (P[(size_t)j * H + i] != 0.0) { f = j; break; } sk += w - f; }
+      dense += d; lnz += l; sky += sk; diag += (long long)w * (w + 1) / 2;
+      if (++cnt % 500 == 0) fprintf(stderr, "fill: dense %lld lnz %lld diag+skyline %lld diag %lld\n", dense.load(), lnz.load(), diag.load() + sky.load(), diag.load());
     }
     // inv(L_SS), packed column-major lower
     S.Linv.assign(static_cast<std::size_t>(w) * (w + 1) / 2, 0.0);

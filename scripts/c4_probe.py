@@ -1,7 +1,7 @@
 """Config 4 (1,048,576 cells, p=3, 512 subdomains) on one GPU: host setup time
 and peak memory, device footprint, a few CN steps with live sweep timing.
 
-    python scripts/c4_probe.py [steps] [config4]
+    python scripts/c4_probe.py [steps] [config4 | config3:P:S | config5:P]
 """
 import ctypes as C
 import json
@@ -16,7 +16,11 @@ from paper_2512_19536_b200.simulation import Simulation  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 name = sys.argv[2] if len(sys.argv) > 2 else "config4"
-cfg = getattr(configs, name)()
+if ":" in name:  # e.g. config3:3:64 or config5:2
+    parts = name.split(":")
+    cfg = getattr(configs, parts[0])(*[int(a) for a in parts[1:]])
+else:
+    cfg = getattr(configs, name)()
 t0 = time.time()
 sim = Simulation(cfg)
 setup_s = time.time() - t0
