@@ -359,8 +359,21 @@ void DeviceSim::upload_tasks() {
     const char* e = std::getenv(k);
     return 1024LL * (e ? std::max(2, std::atoi(e)) : d);
   };
-  static const long long kUnitBytes = env_kb("PDG_UNIT_KB", 44);  // best of a 16-96 KB scan on config2
-  static const long long kLeafBytes = env_kb("PDG_LEAF_KB", static_cast<int>(kUnitBytes / 1024));
+  // Default: ~20 units per resident CTA per sweep, clamped to [44, 88] KB.
+  // Small problems (config2: 351 KB of panel per CTA) are critical-path
+  // bound and want small units (44 KB was the best of a 16-96 KB scan);
+  // large ones (config3 p=3: 1.9 MB per CTA) are bandwidth bound and want
+  // the per-unit round trips amortised over more bytes (88 KB: +8.5%).
+  long long panel_bytes = 0;
+  for (const auto& tl : pr.ftiles) panel_bytes += 8LL * tl.ncol * tl.stride;
+  for (const auto& tl : pr.htiles) panel_bytes += 8LL * tl.ncol * tl.stride;
+  int sms_u = 148, dev_u = 0;
+  PDG_CUDA(cudaGetDevice(&dev_u));
+  PDG_CUDA(cudaDeviceGetAttribute(&sms_u, cudaDevAttrMultiProcessorCount, dev_u));
+  const int max_kb = std::getenv("PDG_UNIT_MAX_KB") ? std::max(44, std::atoi(std::getenv("PDG_UNIT_MAX_KB"))) : 88;
+  const int auto_kb = static_cast<int>(std::clamp<long long>(panel_bytes / (20LL * sms_u * 8) / 1024, 44, max_kb));
+  const long long kUnitBytes = env_kb("PDG_UNIT_KB", auto_kb);
+  const long long kLeafBytes = env_kb("PDG_LEAF_KB", static_cast<int>(kUnitBytes / 1024));
   int n_parts = 0, n_tile_ctr = 0;
   long long max_panel = 0, max_in = 0;
   // dependency counters a unit waits on (sweep.cu): forward = children's
@@ -479,12 +492,18 @@ void DeviceSim::upload_tasks() {
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
   fu.insert(fu.end(), bu.begin(), bu.end());
+  // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
+  // partial sums + the unit's input buffer (sweep.cu)
+  sweep_xcap = static_cast<int>(max_in) + 2;
+  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
+  if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
+  if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   const char* ord_env = std::getenv("PDG_SWEEP_ORDER");
   if (!(ord_env && std::strcmp(ord_env, "level") == 0)) {
     int sms = 148, dev = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const std::vector<int> perm = list_schedule(pr, fu, sms * 8);
+    const std::vector<int> perm = list_schedule(pr, fu, sms * sweep_ctas_per_sm(smem_fwd));
     std::vector<DevUnit> o(fu.size());
     for (std::size_t i = 0; i < perm.size(); ++i) o[i] = fu[perm[i]];
     fu.swap(o);
@@ -498,12 +517,6 @@ void DeviceSim::upload_tasks() {
   PDG_CUDA(cudaMemsetAsync(d_nunit, 0, n_tile_ctrs * sizeof(int), st));
   d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
   (void)max_panel;
-  // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
-  // partial sums + the unit's input buffer (sweep.cu)
-  sweep_xcap = static_cast<int>(max_in) + 2;
-  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
-  if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
-  if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   d_task_child = dupload(pr.task_child, st);
   d_fmat = dupload(pr.fmat, st);
   d_hmat = dupload(pr.hmat, st);

@@ -34,6 +34,10 @@
 #ifndef PDG_DOT_DEPTH
 #define PDG_DOT_DEPTH 8
 #endif
+// minimum resident CTAs per SM the register allocation must allow
+#ifndef PDG_SWEEP_MINB
+#define PDG_SWEEP_MINB 1
+#endif
 
 namespace pdg {
 
@@ -378,7 +382,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, PDG_SWEEP_MINB) sweep_kernel(SweepArgs a) {
   pdl_wait();
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
@@ -452,6 +456,12 @@ void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
   }
   const int grid = a.n_units < resident ? a.n_units : resident;
   launch_pdl(sweep_kernel, grid, kSweepThreads, smem, st, a);
+}
+
+int sweep_ctas_per_sm(int smem) {
+  int per_sm = 0;
+  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel, kSweepThreads, smem));
+  return per_sm > 0 ? per_sm : 1;
 }
 
 void set_sweep_smem(int bytes) {

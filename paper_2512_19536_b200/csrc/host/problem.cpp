@@ -7,6 +7,8 @@
 //   L2 projection              assembly.cpp:228-242
 //   coarse embedding E         schwarz.cpp:13-77, K0 = E^T K E :138-146
 //   subdomain factors          schwarz.cpp:99-136
+#include <chrono>
+#include <cstdio>
 #include "problem.hpp"
 
 #include <algorithm>
@@ -186,11 +188,21 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   auto P = std::make_unique<Problem>();
   Problem& pr = *P;
   pr.cfg = cfg;
+  // PDG_SETUP_TIMES=1: wall time of each setup phase on stderr
+  static const bool times = std::getenv("PDG_SETUP_TIMES") && std::getenv("PDG_SETUP_TIMES")[0] == '1';
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!times) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "setup %-14s %8.2f s\n", name, std::chrono::duration<double>(now - t_last).count());
+    t_last = now;
+  };
   const Box dom{cfg.domain[0], cfg.domain[1], cfg.domain[2], cfg.domain[3]};
   {
     Mesh m = generate_mesh(cfg.mesh_cells, dom, cfg.mesh_seed, cfg.mesh_lloyd);
     pr.mesh = (cfg.split_y > dom.ymin && cfg.split_y < dom.ymax) ? assign_regions(m, cfg.split_y) : std::move(m);
   }
+  phase("mesh");
   const Mesh& mesh = pr.mesh;
   const int N = mesh.n_cells();
   pr.p = cfg.degree;
@@ -215,6 +227,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
   }
 
+  phase("partitions");
   // ---- adjacency (reference cell ids) ----
   std::vector<std::vector<int>> nbr(N);
   for (const Face& f : mesh.interior_faces()) {
@@ -320,6 +333,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   pr.cell_end = pr.rank_cell_start[cfg.rank + 1];
   const int nloc = pr.cell_end - pr.cell_begin;
 
+  phase("ordering");
   // ---- assembly of local rows (assembly.cpp:89-183) ----
   pr.keep_matrices = static_cast<std::int64_t>(N) * b <= 2000000;
   Bsr& A = pr.A;
@@ -538,6 +552,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
   }
 
+  phase("assembly");
   // ---- Schwarz local factors (schwarz.cpp:99-136) ----
   struct UnitFactor {
     int unit;
@@ -635,6 +650,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
   factors.clear();
 
+  phase("factor+pack");
   // ---- coarse embedding E (schwarz.cpp:13-77) and local K0 contribution ----
   if (pr.two_level) {
     const int na = pr.coarse.count;
@@ -773,7 +789,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
           }
       }
     }
+    phase("coarse E,K0");
     if (cfg.world == 1) finish_coarse(pr);
+    phase("coarse factor");
   }
   return P;
 }
