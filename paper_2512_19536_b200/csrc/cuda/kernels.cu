@@ -186,6 +186,107 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
   if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
 }
 
+// Warp per block-row SpMV for even B (p = 2, 3): the row's blocks are
+// contiguous in `val`, so lane l streams double2 j = l + 32t of every block
+// (fully used sectors, 2 blocks in flight per iteration). With B even a
+// double2 never straddles a column, so lane l always accumulates the fixed
+// row pair r = (2l + 64t) % B of column (2j)/B; lanes l = k (mod B/2) share a
+// pair and are summed by a shuffle tree in a fixed order (deterministic).
+template <int B>
+__global__ void __launch_bounds__(256)
+    spmv_warp_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
+                     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+  static_assert(B % 2 == 0, "even block size");
+  constexpr int H = B * B / 2, NT = (H + 31) / 32, S = B / 2;
+  pdl_wait();
+  if (honor_stop && rc.S->stop) return;
+  __shared__ double ys[8][B];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int row = blockIdx.x * 8 + wl;
+  double contrib = 0.0;
+  if (row < rows) {
+    const double2* __restrict__ v2 = reinterpret_cast<const double2*>(val);
+    double2 acc[NT];
+    int cj[NT];
+    bool on[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int j = lane + 32 * t;
+      on[t] = j < H;
+      cj[t] = (2 * j) / B;
+      acc[t] = make_double2(0.0, 0.0);
+    }
+    const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+    int k = k0;
+    for (; k + 1 < k1; k += 2) {
+      const int ca = __ldg(col + k), cb = __ldg(col + k + 1);
+      double2 va[NT], vb[NT];
+      double xa[NT], xb[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (on[t]) {
+          va[t] = __ldg(v2 + static_cast<long long>(k) * H + lane + 32 * t);
+          vb[t] = __ldg(v2 + static_cast<long long>(k + 1) * H + lane + 32 * t);
+          xa[t] = __ldg(x + static_cast<long long>(ca) * B + cj[t]);
+          xb[t] = __ldg(x + static_cast<long long>(cb) * B + cj[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (on[t]) {
+          acc[t].x = fma(va[t].x, xa[t], acc[t].x);
+          acc[t].y = fma(va[t].y, xa[t], acc[t].y);
+          acc[t].x = fma(vb[t].x, xb[t], acc[t].x);
+          acc[t].y = fma(vb[t].y, xb[t], acc[t].y);
+        }
+      }
+    }
+    if (k < k1) {
+      const int ca = __ldg(col + k);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (on[t]) {
+          const double2 va = __ldg(v2 + static_cast<long long>(k) * H + lane + 32 * t);
+          const double xa = __ldg(x + static_cast<long long>(ca) * B + cj[t]);
+          acc[t].x = fma(va.x, xa, acc[t].x);
+          acc[t].y = fma(va.y, xa, acc[t].y);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+#pragma unroll
+      for (int off = S; off < 32; off *= 2) {
+        const double sx = __shfl_down_sync(0xffffffffu, acc[t].x, off);
+        const double sy = __shfl_down_sync(0xffffffffu, acc[t].y, off);
+        if (lane + off < 32) {
+          acc[t].x += sx;
+          acc[t].y += sy;
+        }
+      }
+      if (lane < S) {
+        const int r = (2 * lane + 64 * t) % B;
+        if (t == 0) {
+          ys[wl][r] = acc[t].x;
+          ys[wl][r + 1] = acc[t].y;
+        } else {
+          ys[wl][r] += acc[t].x;
+          ys[wl][r + 1] += acc[t].y;
+        }
+      }
+      __syncwarp();
+    }
+    if (lane < B) {
+      const double yv = ys[wl][lane];
+      const long long i = static_cast<long long>(row) * B + lane;
+      y[i] = yv;
+      if (dotw) contrib = dotw[i] * yv;
+    }
+  }
+  if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
+}
+
 template <int B>
 __global__ void __launch_bounds__(RowGeom<B>::kThreads)
     residual_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
@@ -797,6 +898,17 @@ int vec_grid(long long n) {
 
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val, const double* x,
                  double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
+  // even B (p = 2, 3): warp per block row; PDG_SPMV_WARP=0 selects the
+  // thread-per-row kernel
+  static const bool warp_rows = !(std::getenv("PDG_SPMV_WARP") && std::getenv("PDG_SPMV_WARP")[0] == '0');
+  if (rows > 0 && warp_rows && (b == 6 || b == 10)) {
+    const int g = (rows + 7) / 8;
+    if (b == 6)
+      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+    else
+      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+    return;
+  }
 #define L(B)                                                                                  \
   {                                                                                           \
     const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \

@@ -34,10 +34,15 @@
 #ifndef PDG_DOT_DEPTH
 #define PDG_DOT_DEPTH 8
 #endif
-// minimum resident CTAs per SM the register allocation must allow
-#ifndef PDG_SWEEP_MINB
-#define PDG_SWEEP_MINB 1
+// PDG_SWEEP_MINB (build knob): minimum resident CTAs per SM the register
+// allocation must allow. Unset = the compiler's own choice (58 registers,
+// 8 CTAs/SM), which measured best; an explicit 1 lets it take 102.
+#ifdef PDG_SWEEP_MINB
+#define PDG_SWEEP_BOUNDS __launch_bounds__(kSweepThreads, PDG_SWEEP_MINB)
+#else
+#define PDG_SWEEP_BOUNDS __launch_bounds__(kSweepThreads)
 #endif
+static_assert(PDG_DOT_DEPTH % 4 == 0, "tile_dot consumes loads four at a time");
 
 namespace pdg {
 
@@ -382,7 +387,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
-__global__ void __launch_bounds__(kSweepThreads, PDG_SWEEP_MINB) sweep_kernel(SweepArgs a) {
+__global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
   pdl_wait();
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
