@@ -898,9 +898,12 @@ int vec_grid(long long n) {
 
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val, const double* x,
                  double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
-  // even B (p = 2, 3): warp per block row; PDG_SPMV_WARP=0 selects the
-  // thread-per-row kernel
-  static const bool warp_rows = !(std::getenv("PDG_SPMV_WARP") && std::getenv("PDG_SPMV_WARP")[0] == '0');
+  // even B (p = 2, 3) on small row counts: warp per block row. The
+  // thread-per-row kernel fills only ~half the GPU below ~30K block rows
+  // (config2: 656 CTAs) but streams better once every SM holds several of its
+  // CTAs (config5 p=2: 4.5 vs 2.2 TB/s). PDG_SPMV_WARP=0/1 forces either.
+  static const char* wenv = std::getenv("PDG_SPMV_WARP");
+  const bool warp_rows = wenv ? wenv[0] == '1' : rows <= 32768;
   if (rows > 0 && warp_rows && (b == 6 || b == 10)) {
     const int g = (rows + 7) / 8;
     if (b == 6)
