@@ -518,8 +518,6 @@ void DeviceSim::upload_tasks() {
   d_part = dalloc<double>(static_cast<std::size_t>(std::max(n_parts, 1)) * 32);
   (void)max_panel;
   d_task_child = dupload(pr.task_child, st);
-  d_fmat = dupload(pr.fmat, st);
-  d_hmat = dupload(pr.hmat, st);
   std::vector<DevTile> ft(pr.ftiles.size()), ht(pr.htiles.size());
   for (std::size_t i = 0; i < ft.size(); ++i)
     ft[i] = DevTile{pr.ftiles[i].off, pr.ftiles[i].ncol, pr.ftiles[i].col0, pr.ftiles[i].rows, pr.ftiles[i].stride};
@@ -527,6 +525,7 @@ void DeviceSim::upload_tasks() {
     ht[i] = DevTile{pr.htiles[i].off, pr.htiles[i].ncol, pr.htiles[i].col0, pr.htiles[i].rows, pr.htiles[i].stride};
   d_ftiles = dupload(ft, st);
   d_htiles = dupload(ht, st);
+  build_panels();  // F and H from the factor values (panels.cu)
   std::vector<long long> rd(pr.row_dof.begin(), pr.row_dof.end());
   d_row_dof = dupload(rd, st);
   d_in_ptr = dupload(pr.in_ptr, st);
@@ -544,13 +543,13 @@ void DeviceSim::upload_tasks() {
     PDG_CUDA(cudaMemsetAsync(d_live, 0, 3 * sizeof(unsigned long long), st));
   }
   PDG_CUDA(cudaStreamSynchronize(st));
-  panel_values = static_cast<long long>(pr.fmat.size() + pr.hmat.size());
-  // one rank: the panels live on the device from now on (config 4: ~40 GB of
-  // host memory back); several ranks re-pack after the coarse all-reduce
+  panel_values = static_cast<long long>(pr.fmat_len + pr.hmat_len);
+  // one rank: the panels live on the device from now on (config 4: ~20 GB of
+  // factor values back to the host); several ranks re-pack after the coarse
+  // all-reduce
   if (pr.cfg.world == 1) {
     Problem& mp = *P;
-    std::vector<double>().swap(mp.fmat);
-    std::vector<double>().swap(mp.hmat);
+    std::vector<double>().swap(mp.lval);
   }
 }
 

@@ -147,6 +147,7 @@ class DeviceSim {
   ReduceCtx red_for(int finish);
   void after_reduce(int finish, bool honor);
   void upload_tasks();
+  void build_panels();  // panels.cu
   void alloc_history(int cap);
   ReduceCtx rctx(int finish, double* out = nullptr);
   SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);

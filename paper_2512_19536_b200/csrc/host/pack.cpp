@@ -9,7 +9,8 @@
 // dependency chain). Panels are stored in 32-row tiles (column-major inside a
 // tile, last tile not padded) so a warp reads one coalesced 8*rows-byte row
 // segment per input column; the zero upper triangle of inv(L_SS) is skipped
-// at tile granularity.
+// at tile granularity. This file only lays the tiles out; F and H are formed
+// on the device from inv(L_SS) and L_RS (cuda/panels.cu).
 #include <algorithm>
 
 #include "problem.hpp"
@@ -31,35 +32,20 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
 
   std::vector<int> slot(nsn);
-  std::vector<double> G, Fd;
   for (int s = 0; s < nsn; ++s) {
     const Supernode& S = F.sn[s];
     const int w = S.w(bs), nr = static_cast<int>(S.rows.size()) * bs, h = w + nr;
-    // G = L_RS inv(L_SS): G(k, j) = sum_{m >= j} B(k, m) Linv(m, j)
-    G.assign(static_cast<std::size_t>(nr) * w, 0.0);
-    for (int j = 0; j < w; ++j) {
-      const double* lcol = S.Linv.data() + static_cast<std::size_t>(j) * w - static_cast<std::size_t>(j) * (j - 1) / 2;
-      double* g = G.data() + static_cast<std::size_t>(j) * nr;
-      for (int m = j; m < w; ++m) {
-        const double coef = lcol[m - j];
-        if (coef == 0.0) continue;
-        const double* bcol = S.B.data() + static_cast<std::size_t>(m) * nr;
-        for (int k = 0; k < nr; ++k) g[k] += bcol[k] * coef;
-      }
-    }
-    auto Fat = [&](int i, int j) -> double {  // F(i, j)
-      if (i < w) {
-        if (i < j) return 0.0;
-        return S.Linv[static_cast<std::size_t>(j) * w - static_cast<std::size_t>(j) * (j - 1) / 2 + (i - j)];
-      }
-      return G[static_cast<std::size_t>(j) * nr + (i - w)];
-    };
     TaskDesc t;
     t.coarse = coarse;
     t.bs = bs;
     t.w = w;
     t.nr = nr;
     t.dof0 = dof_base + static_cast<std::int64_t>(S.s0) * bs;
+    // factor values for the device panel builder (cuda/panels.cu)
+    t.linv_off = static_cast<std::int64_t>(pr.lval.size());
+    pr.lval.insert(pr.lval.end(), S.Linv.begin(), S.Linv.end());
+    t.b_off = static_cast<std::int64_t>(pr.lval.size());
+    pr.lval.insert(pr.lval.end(), S.B.begin(), S.B.end());
     // forward tiles: output rows of F
     // tiles start 16-byte aligned and hold an even number of rows (a zero row
     // pads odd tails) so each lane streams double2 pairs of rows
@@ -67,10 +53,9 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     for (int r0 = 0; r0 < h; r0 += kTile) {
       const int rows = std::min(kTile, h - r0), rs = rows + (rows & 1);
       const int ncol = std::min(w, r0 + rows);
-      if (pr.fmat.size() & 1) pr.fmat.push_back(0.0);
-      pr.ftiles.push_back({static_cast<std::int64_t>(pr.fmat.size()), ncol, 0, rows, rs});
-      for (int j = 0; j < ncol; ++j)
-        for (int l = 0; l < rs; ++l) pr.fmat.push_back(l < rows ? Fat(r0 + l, j) : 0.0);
+      pr.fmat_len += pr.fmat_len & 1;
+      pr.ftiles.push_back({pr.fmat_len, ncol, 0, rows, rs});
+      pr.fmat_len += static_cast<std::int64_t>(ncol) * rs;
     }
     t.f_ntile = static_cast<int>(pr.ftiles.size()) - t.f_tile0;
     // backward tiles: output rows of H = F^T (columns of F), inputs i >= r0
@@ -78,10 +63,9 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     for (int r0 = 0; r0 < w; r0 += kTile) {
       const int rows = std::min(kTile, w - r0), rs = rows + (rows & 1);
       const int ncol = h - r0;
-      if (pr.hmat.size() & 1) pr.hmat.push_back(0.0);
-      pr.htiles.push_back({static_cast<std::int64_t>(pr.hmat.size()), ncol, r0, rows, rs});
-      for (int i = r0; i < h; ++i)
-        for (int l = 0; l < rs; ++l) pr.hmat.push_back(l < rows ? Fat(i, r0 + l) : 0.0);
+      pr.hmat_len += pr.hmat_len & 1;
+      pr.htiles.push_back({pr.hmat_len, ncol, r0, rows, rs});
+      pr.hmat_len += static_cast<std::int64_t>(ncol) * rs;
     }
     t.h_ntile = static_cast<int>(pr.htiles.size()) - t.h_tile0;
     t.rows_off = static_cast<int>(pr.row_dof.size());
@@ -115,7 +99,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
       ++at;
     }
   }
-  pr.factor_values = static_cast<std::int64_t>(pr.fmat.size() + pr.hmat.size());
+  pr.factor_values = pr.fmat_len + pr.hmat_len;
 }
 
 }  // namespace pdg

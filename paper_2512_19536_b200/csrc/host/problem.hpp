@@ -42,6 +42,7 @@ struct TaskDesc {
   int parent = -1;     // task id (ND parent), -1 = root
   int child_off = 0, n_child = 0;  // children ids in task_child[]
   int height = 0, depth = 0;
+  std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
 };
 
 struct Problem {
@@ -66,12 +67,15 @@ struct Problem {
   std::vector<TaskDesc> tasks;
   std::vector<int> task_child, fwd_order, bwd_order;
   // Row-tiled dense panels: tile t covers output rows [32k, 32k+rows) of its
-  // task; element (row r0+l, input col0+j) at mat[off + j*rows + l].
+  // task; element (row r0+l, input col0+j) at mat[off + j*stride + l]. The
+  // panels themselves are formed on the device (cuda/panels.cu) from the
+  // factor values in lval; the host only lays the tiles out.
   struct Tile {
     std::int64_t off;
     int ncol, col0, rows, stride;  // stride = rows rounded up to even
   };
-  std::vector<double> fmat, hmat;    // forward / backward panels
+  std::int64_t fmat_len = 0, hmat_len = 0;  // forward / backward panel doubles
+  std::vector<double> lval;          // per task: inv(L_SS) packed lower, then L_RS (column-major)
   std::vector<Tile> ftiles, htiles;
   std::vector<std::int64_t> row_dof;  // below-row cell dof starts
   std::vector<int> in_ptr;       // incoming CSR (per supernode cell slot)
