@@ -284,12 +284,17 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
   }
   // ND inside each multi-cell subdomain
-  // nested-dissection leaf size (cells): dense leaves of ~64 dofs; PDG_ND_LEAF overrides
-  int leaf = std::clamp(64 / b, 4, 16);
-  if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
-  // separator levels merged per supernode (shallower elimination trees); PDG_ND_MERGE overrides
-  int nd_merge = 2;
+  // Nested-dissection shape. Merging two separator levels per supernode
+  // halves the elimination-tree depth (the sweep's critical path) at ~20%
+  // more panel bytes; it pays while the sweep is latency bound (config2,
+  // config3 p=3: +2-9%) and costs once it streams (config3 p=4: -9%). Leaf
+  // size: dense leaves of ~64 dofs (4 cells unmerged). PDG_ND_MERGE /
+  // PDG_ND_LEAF override.
+  const bool big = static_cast<std::int64_t>(N) * b > 800000;
+  int nd_merge = big ? 1 : 2;
   if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
+  int leaf = nd_merge == 1 ? 4 : std::clamp(64 / b, 4, 16);
+  if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
   parallel_for(n_units, [&](int u) {
