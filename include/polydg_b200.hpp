@@ -184,6 +184,21 @@ class Simulation {
     check(pdg_sim_get_state(h_.get(), k, t, U_curr ? U_curr->data() : nullptr, U_prev ? U_prev->data() : nullptr,
                             Y_curr && nc ? Y_curr->data() : nullptr, Y_prev && nc ? Y_prev->data() : nullptr));
   }
+  // cell_means (snapshot.cpp:13-28), computed on the device: n_cells means of
+  // U^k in reference cell order
+  Vector cell_means() const {
+    const pdg_problem* p = pdg_sim_problem(h_.get());
+    std::int64_t info[12];
+    pdg_problem_info(p, info);
+    Vector m(static_cast<std::size_t>(info[0]));
+    check(pdg_sim_cell_means(h_.get(), m.data()));
+    return m;
+  }
+  // export_snapshot (snapshot.cpp:30-75): "vtk-legacy" or "csv-cellmeans";
+  // ConfigError on an unknown format, IoError when the file cannot be written
+  void export_snapshot(const std::string& path, const std::string& format) const {
+    check(pdg_sim_export_snapshot(h_.get(), path.c_str(), format.c_str()));
+  }
   pdg_sim* handle() const { return h_.get(); }
 
  private:

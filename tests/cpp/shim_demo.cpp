@@ -35,5 +35,15 @@ int main() {
     return 1;
   } catch (const SolverError&) {
   }
+  // snapshot.hpp: device cell means + the reference's writers and errors
+  const Vector means = sim.cell_means();
+  std::printf("cell_means %zu first %.6f\n", means.size(), means.empty() ? 0.0 : means[0]);
+  sim.export_snapshot("/tmp/pdg_shim_snapshot.csv", "csv-cellmeans");
+  try {
+    sim.export_snapshot("/tmp/pdg_shim_snapshot.x", "png");
+    return 3;
+  } catch (const ConfigError&) {
+  }
+  if (means.size() != 256) return 4;
   return (res.converged_all && rep.converged && std::sqrt(rr / bb) < 1e-9) ? 0 : 2;
 }
