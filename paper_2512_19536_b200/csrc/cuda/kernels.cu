@@ -14,6 +14,10 @@
 
 #include "kernels.cuh"
 
+#ifndef PDG_SPMV_UNROLL
+#define PDG_SPMV_UNROLL 2
+#endif
+
 namespace pdg {
 
 namespace {
@@ -219,30 +223,35 @@ __global__ void __launch_bounds__(256)
     }
     const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
     int k = k0;
-    for (; k + 1 < k1; k += 2) {
-      const int ca = __ldg(col + k), cb = __ldg(col + k + 1);
-      double2 va[NT], vb[NT];
-      double xa[NT], xb[NT];
+    // PDG_SPMV_UNROLL blocks in flight per iteration; the accumulation order
+    // is block order whatever the unroll, so results do not depend on it
+    constexpr int U = PDG_SPMV_UNROLL;
+    for (; k + U - 1 < k1; k += U) {
+      int cu[U];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        if (on[t]) {
-          va[t] = __ldg(v2 + static_cast<long long>(k) * H + lane + 32 * t);
-          vb[t] = __ldg(v2 + static_cast<long long>(k + 1) * H + lane + 32 * t);
-          xa[t] = __ldg(x + static_cast<long long>(ca) * B + cj[t]);
-          xb[t] = __ldg(x + static_cast<long long>(cb) * B + cj[t]);
-        }
-      }
+      for (int u = 0; u < U; ++u) cu[u] = __ldg(col + k + u);
+      double2 va[U][NT];
+      double xa[U][NT];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        if (on[t]) {
-          acc[t].x = fma(va[t].x, xa[t], acc[t].x);
-          acc[t].y = fma(va[t].y, xa[t], acc[t].y);
-          acc[t].x = fma(vb[t].x, xb[t], acc[t].x);
-          acc[t].y = fma(vb[t].y, xb[t], acc[t].y);
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (on[t]) {
+            va[u][t] = __ldg(v2 + static_cast<long long>(k + u) * H + lane + 32 * t);
+            xa[u][t] = __ldg(x + static_cast<long long>(cu[u]) * B + cj[t]);
+          }
         }
-      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (on[t]) {
+            acc[t].x = fma(va[u][t].x, xa[u][t], acc[t].x);
+            acc[t].y = fma(va[u][t].y, xa[u][t], acc[t].y);
+          }
+        }
     }
-    if (k < k1) {
+    for (; k < k1; ++k) {
       const int ca = __ldg(col + k);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
