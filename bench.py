@@ -49,9 +49,16 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def workload_config(name, rank=0, world=1, device=0):
+def workload_config(name, rank=0, world=1, device=0, scaling="weak"):
+    """The BASELINE workload. Weak scaling (default) keeps the per-GPU problem
+    at the config's size: N GPUs solve one coupled mesh of N x cells with
+    N x subdomains (one halo exchange + all-reduces per PCG iteration);
+    strong scaling shards the config's own mesh over the N GPUs."""
     from paper_2512_19536_b200 import configs
     cfg = getattr(configs, name)()
+    if scaling == "weak" and world > 1:
+        cfg.cells *= world
+        cfg.subdomains *= world
     cfg.rank, cfg.world, cfg.device = rank, world, device
     return cfg
 
@@ -124,7 +131,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = workload_config(args.config)
+    # the arm's own workload (weak scaling: N x the config's mesh), solved by
+    # the single-process CPU oracle
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    cfg = workload_config(args.config, 0, world, 0, args.scaling)
+    cfg.rank, cfg.world = 0, 1
     from tests.oracle_binding import lib as orc_lib, oracle_for
     orc, _ = oracle_for(cfg)
     n = orc.dimension
@@ -140,7 +151,7 @@ def run_reference(args):
     value = n * its / el
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc_lib().orc_threads(), "kind": "port",
                              "sample": f"{done} of {args.steps} requested CN steps timed "
@@ -157,6 +168,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -176,7 +188,7 @@ def main():
     from paper_2512_19536_b200 import _lib
     from paper_2512_19536_b200.simulation import Simulation
     L = _lib.lib()
-    cfg = workload_config(args.config, rank, world, local)
+    cfg = workload_config(args.config, rank, world, local, args.scaling)
     sim = Simulation(cfg)
     if world > 1:
         nb = L.pdg_nccl_unique_id_bytes()
@@ -311,7 +323,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n_global,
                        "steps_timed": args.steps, "pcg_iterations": its,
@@ -319,7 +331,9 @@ def main():
                        "solve_ms_per_step": solve_ms / args.steps,
                        "l2": "operands (K 91 MB + Schwarz panels 408 MB) exceed the 126 MB L2; "
                              "per-kernel profile times flush L2 before each launch",
-                       "parallelism": f"subdomains sharded over {world} GPU(s)"},
+                       "parallelism": f"subdomains sharded over {world} GPU(s)" + (
+                           f" ({args.config} per GPU: {cfg.cells} cells, {cfg.subdomains} subdomains in total)"
+                           if args.scaling == "weak" and world > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(kby[di]),
