@@ -140,7 +140,14 @@ void DeviceSim::build_panels() {
   auto* d_pt = static_cast<PanelTask*>(up(pt.data(), pt.size() * sizeof(PanelTask)));
   auto* d_ftt = static_cast<int*>(up(ft_task.data(), ft_task.size() * sizeof(int)));
   auto* d_htt = static_cast<int*>(up(ht_task.data(), ht_task.size() * sizeof(int)));
-  auto* d_lval = static_cast<double*>(up(pr.lval.data(), pr.lval.size() * sizeof(double)));
+  // factor values: host-computed ones (all tasks, or the coarse tail when the
+  // device factors the subdomains) at lval_host0, then the device factor
+  double* d_lval = nullptr;
+  PDG_CUDA(cudaMalloc(&d_lval, std::max<std::int64_t>(pr.lval_len, 1) * sizeof(double)));
+  if (!pr.lval.empty())
+    PDG_CUDA(cudaMemcpyAsync(d_lval + pr.lval_host0, pr.lval.data(), pr.lval.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, st));
+  if (pr.device_factor) device_factor(d_lval);
   PDG_CUDA(cudaMalloc(&d_fmat, std::max<std::int64_t>(pr.fmat_len, 1) * sizeof(double)));
   PDG_CUDA(cudaMalloc(&d_hmat, std::max<std::int64_t>(pr.hmat_len, 1) * sizeof(double)));
   // alignment gaps between tiles stay zero

@@ -550,6 +550,10 @@ void DeviceSim::upload_tasks() {
   if (pr.cfg.world == 1) {
     Problem& mp = *P;
     std::vector<double>().swap(mp.lval);
+    std::vector<Problem::FactorSn>().swap(mp.fsn);
+    std::vector<Problem::FactorUpd>().swap(mp.fupd);
+    std::vector<int>().swap(mp.frows);
+    std::vector<int>().swap(mp.fmap);
   }
 }
 

@@ -148,6 +148,7 @@ class DeviceSim {
   void after_reduce(int finish, bool honor);
   void upload_tasks();
   void build_panels();  // panels.cu
+  void device_factor(double* d_lval);  // factor.cu: numeric subdomain factors into d_lval
   void alloc_history(int cap);
   ReduceCtx rctx(int finish, double* out = nullptr);
   SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);

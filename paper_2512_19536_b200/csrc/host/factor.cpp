@@ -249,7 +249,7 @@ BlockMatrix permute(const BlockMatrix& A, const std::vector<int>& order) {
   return P;
 }
 
-SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
+SupernodalFactor symbolic_factor(const BlockMatrix& A, const NdTree& nd, std::vector<std::vector<int>>& upd) {
   const int m = A.m, bs = A.bs;
   const int nsn = static_cast<int>(nd.sn_start.size()) - 1;
   SupernodalFactor F;
@@ -282,7 +282,7 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
     std::sort(S.rows.begin(), S.rows.end());
   }
   // updaters of S: descendants D whose rows touch S (ascending D)
-  std::vector<std::vector<int>> upd(nsn);
+  upd.assign(nsn, {});
   std::vector<int> last(nsn, -1);
   for (int d = 0; d < nsn; ++d)
     for (int q : F.sn[d].rows) {
@@ -292,6 +292,14 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
         upd[s].push_back(d);
       }
     }
+  return F;
+}
+
+SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
+  const int m = A.m, bs = A.bs;
+  const int nsn = static_cast<int>(nd.sn_start.size()) - 1;
+  std::vector<std::vector<int>> upd;
+  SupernodalFactor F = symbolic_factor(A, nd, upd);
 
   std::vector<int> rowcell(m, -1);
   std::vector<double> P, x;

@@ -58,6 +58,11 @@ struct SupernodalFactor {
 // Throws SolverError("... not positive definite") on a non-positive pivot.
 SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd);
 
+// The symbolic half: supernode ranges, below rows and, per supernode, the
+// descendants whose rows touch it (ascending; the left-looking update order).
+// No values (A.val may be empty); Linv and B stay empty.
+SupernodalFactor symbolic_factor(const BlockMatrix& A, const NdTree& nd, std::vector<std::vector<int>>& upd);
+
 // Permutes a block matrix: out node i = in node order[i].
 BlockMatrix permute(const BlockMatrix& A, const std::vector<int>& order);
 

@@ -41,11 +41,20 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     t.w = w;
     t.nr = nr;
     t.dof0 = dof_base + static_cast<std::int64_t>(S.s0) * bs;
-    // factor values for the device panel builder (cuda/panels.cu)
-    t.linv_off = static_cast<std::int64_t>(pr.lval.size());
-    pr.lval.insert(pr.lval.end(), S.Linv.begin(), S.Linv.end());
-    t.b_off = static_cast<std::int64_t>(pr.lval.size());
-    pr.lval.insert(pr.lval.end(), S.B.begin(), S.B.end());
+    // factor values for the device panel builder (cuda/panels.cu); a
+    // symbolic-only factor (device factorisation, cuda/factor.cu) reserves
+    // the space
+    t.linv_off = pr.lval_len;
+    pr.lval_len += static_cast<std::int64_t>(w) * (w + 1) / 2;
+    t.b_off = pr.lval_len;
+    pr.lval_len += static_cast<std::int64_t>(nr) * w;
+    if (!S.Linv.empty()) {
+      if (pr.lval.empty()) pr.lval_host0 = t.linv_off;
+      if (pr.lval_host0 + static_cast<std::int64_t>(pr.lval.size()) != t.linv_off)
+        throw SolverError("pack: host factor values must follow the device-factored tasks");
+      pr.lval.insert(pr.lval.end(), S.Linv.begin(), S.Linv.end());
+      pr.lval.insert(pr.lval.end(), S.B.begin(), S.B.end());
+    }
     // forward tiles: output rows of F
     // tiles start 16-byte aligned and hold an even number of rows (a zero row
     // pads odd tails) so each lane streams double2 pairs of rows

@@ -183,6 +183,57 @@ void validate_config(const pdg_config& c) {
   if (c.world < 1 || c.rank < 0 || c.rank >= c.world) throw ConfigError("invalid rank/world");
 }
 
+// Device factorisation plan of one unit (see Problem::FactorSn): tasks
+// [base, base + nsn) were just packed from the symbolic factor F.
+static void add_factor_plan(Problem& pr, const SupernodalFactor& F, const std::vector<std::vector<int>>& upd,
+                            int base, int cell0) {
+  const int bs = F.bs;
+  for (int s = 0; s < static_cast<int>(F.sn.size()); ++s) {
+    const Supernode& S = F.sn[s];
+    const TaskDesc& t = pr.tasks[base + s];
+    Problem::FactorSn f{};
+    f.p_off = pr.fp_len;
+    f.cell0 = cell0;
+    f.ucells = F.m;
+    f.s0 = S.s0;
+    f.s1 = S.s1;
+    f.w = t.w;
+    f.H = t.w + t.nr;
+    pr.fp_len += static_cast<std::int64_t>(f.H) * f.w;
+    pr.fp_len += pr.fp_len & 1;
+    f.rows_off = static_cast<int>(pr.frows.size());
+    f.nrows = static_cast<int>(S.rows.size());
+    pr.frows.insert(pr.frows.end(), S.rows.begin(), S.rows.end());
+    f.upd_off = static_cast<int>(pr.fupd.size());
+    f.nupd = static_cast<int>(upd[s].size());
+    f.height = t.height;
+    for (int d : upd[s]) {
+      const Supernode& D = F.sn[d];
+      Problem::FactorUpd u{};
+      u.d = base + d;
+      u.a = static_cast<int>(std::lower_bound(D.rows.begin(), D.rows.end(), S.s0) - D.rows.begin());
+      u.ce = static_cast<int>(std::lower_bound(D.rows.begin(), D.rows.end(), S.s1) - D.rows.begin());
+      u.nrd = static_cast<int>(D.rows.size());
+      u.map_off = static_cast<std::int64_t>(pr.fmap.size());
+      for (int k = u.a; k < u.nrd; ++k) {
+        const int q = D.rows[k];
+        int rc;
+        if (q < S.s1) {
+          rc = q - S.s0;
+        } else {
+          const auto it = std::lower_bound(S.rows.begin(), S.rows.end(), q);
+          if (it == S.rows.end() || *it != q) throw SolverError("factor plan: descendant row outside the supernode");
+          rc = (S.s1 - S.s0) + static_cast<int>(it - S.rows.begin());
+        }
+        pr.fmap.push_back(rc);
+      }
+      pr.fupd.push_back(u);
+    }
+    pr.fsn.push_back(f);
+  }
+  (void)bs;
+}
+
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   validate_config(cfg);
   auto P = std::make_unique<Problem>();
@@ -564,7 +615,13 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   struct UnitFactor {
     int unit;
     SupernodalFactor F;
+    std::vector<std::vector<int>> upd;  // device factorisation: left-looking updaters
   };
+  // one rank, multi-cell subdomains: the GPU computes the numeric factor
+  // (cuda/factor.cu) from a host symbolic plan; PDG_HOST_FACTOR=1 keeps the
+  // host supernodal Cholesky
+  pr.device_factor = multi_sub && cfg.world == 1 && pr.has_precond &&
+                     !(std::getenv("PDG_HOST_FACTOR") && std::getenv("PDG_HOST_FACTOR")[0] == '1');
   std::vector<int> my_units;
   for (int k = 0; k < n_units; ++k)
     if (unit_rank[unit_order[k]] == cfg.rank) my_units.push_back(unit_order[k]);
@@ -597,8 +654,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
             const int j = pr.K.col[kk];
             if (j < s0 || j >= s0 + m) continue;
             Bm.col.push_back(j - s0);
-            Bm.val.insert(Bm.val.end(), pr.K.val.begin() + static_cast<std::size_t>(kk) * b2,
-                          pr.K.val.begin() + static_cast<std::size_t>(kk + 1) * b2);
+            if (!pr.device_factor)
+              Bm.val.insert(Bm.val.end(), pr.K.val.begin() + static_cast<std::size_t>(kk) * b2,
+                            pr.K.val.begin() + static_cast<std::size_t>(kk + 1) * b2);
           }
           Bm.ptr[i + 1] = static_cast<int>(Bm.col.size());
         }
@@ -608,6 +666,10 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
         t.sn_start = nd[u].sn_start;
         t.parent = nd[u].parent;
         factors[k].unit = u;
+        if (pr.device_factor) {
+          factors[k].F = symbolic_factor(Bm, t, factors[k].upd);
+          return;
+        }
         try {
           factors[k].F = supernodal_cholesky(Bm, t);
         } catch (const SolverError&) {
@@ -615,8 +677,11 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
                             " factorization failed (not positive definite)");
         }
       });
-      for (const UnitFactor& uf : factors)
+      for (const UnitFactor& uf : factors) {
+        const int base = static_cast<int>(pr.tasks.size());
         pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b);
+        if (pr.device_factor) add_factor_plan(pr, uf.F, uf.upd, base, unit_start[uf.unit] - pr.cell_begin);
+      }
       factors.clear();
       }
       packed = true;

@@ -75,7 +75,32 @@ struct Problem {
     int ncol, col0, rows, stride;  // stride = rows rounded up to even
   };
   std::int64_t fmat_len = 0, hmat_len = 0;  // forward / backward panel doubles
-  std::vector<double> lval;          // per task: inv(L_SS) packed lower, then L_RS (column-major)
+  // Factor values, per task: inv(L_SS) packed lower, then L_RS (column-major),
+  // at TaskDesc::linv_off / b_off of a device buffer of lval_len doubles.
+  // Host-computed values cover [lval_host0, lval_len) (all tasks when the
+  // host factors; only the coarse tasks when the device does, cuda/factor.cu).
+  std::int64_t lval_len = 0, lval_host0 = 0;
+  std::vector<double> lval;
+
+  // Device factorisation plan of the fine supernodes (one per fine task, same
+  // index): scratch panel P (H x w, column-major, ld H) at p_off, its unit's
+  // first internal local cell and size, position range, below rows
+  // (unit-relative positions) and the descendants that update it.
+  struct FactorSn {
+    std::int64_t p_off;
+    int cell0, ucells, s0, s1, w, H, rows_off, nrows, upd_off, nupd, height, pad;
+  };
+  // One left-looking update of S by descendant d (a task id): D's below rows
+  // [a, ce) are columns of S; rows [a, nrd) map to P_S row cells map[map_off + k - a].
+  struct FactorUpd {
+    int d, a, ce, nrd;
+    std::int64_t map_off;
+  };
+  bool device_factor = false;
+  std::vector<FactorSn> fsn;
+  std::vector<int> frows, fmap;
+  std::vector<FactorUpd> fupd;
+  std::int64_t fp_len = 0;
   std::vector<Tile> ftiles, htiles;
   std::vector<std::int64_t> row_dof;  // below-row cell dof starts
   std::vector<int> in_ptr;       // incoming CSR (per supernode cell slot)
