@@ -201,3 +201,19 @@ def test_config3_solve_property(p, S):
     rng = np.random.default_rng(1)
     u, v = rng.uniform(-1, 1, sim.dimension), rng.uniform(-1, 1, sim.dimension)
     assert abs(u @ sim.apply_precond(v) - v @ sim.apply_precond(u)) <= 1e-10 * abs(u @ sim.apply_precond(v))
+
+
+def test_device_factor_matches_host_factor(monkeypatch):
+    """The subdomain Cholesky computed on the device (cuda/factor.cu) and on
+    the host (host/factor.cpp, PDG_HOST_FACTOR=1) give the same preconditioner
+    to rounding, and the same PCG iteration counts."""
+    cfg = SimulationConfig(cells=2048, degree=3, lloyd=5, subdomains=16, coarse=-1, fiber_random=True)
+    dev = Simulation(cfg)
+    monkeypatch.setenv("PDG_HOST_FACTOR", "1")
+    host = Simulation(cfg)
+    r = np.random.default_rng(8).uniform(-1, 1, dev.dimension)
+    zd, zh = dev.apply_precond(r), host.apply_precond(r)
+    assert rel(zd, zh) <= 1e-12
+    xd, rd = dev.pcg_solve(r, 1e-10)
+    xh, rh = host.pcg_solve(r, 1e-10)
+    assert rd.iterations == rh.iterations and rel(xd, xh) <= 1e-11
