@@ -31,6 +31,9 @@
 
 #include "kernels.cuh"
 
+#ifndef PDG_SPIN_NS
+#define PDG_SPIN_NS 16  // back-off between dependency polls
+#endif
 #ifndef PDG_DOT_DEPTH
 #define PDG_DOT_DEPTH 8
 #endif
@@ -79,7 +82,7 @@ __device__ __forceinline__ void wait_count(const int* flag, int need) {
   if (ld_relaxed_s(flag) < need) {
     const long long t0 = clock64();
     do {
-      __nanosleep(16);
+      __nanosleep(PDG_SPIN_NS);
       if (clock64() - t0 > (1LL << 33)) __trap();
     } while (ld_relaxed_s(flag) < need);
   }
