@@ -22,7 +22,7 @@ struct DevTask {
   int coarse, bs, w, nr;
   long long dof0, ubuf_off;
   int f_tile0, f_ntile, h_tile0, h_ntile;
-  int rows_off, in_off, parent, child_off, n_child, pad;
+  int rows_off, in_off, parent, child_off, n_child, pad;  // pad = 1: dense root (TaskDesc::root_dense)
 };
 
 // A CTA's share of one supernode in one sweep direction: row tiles

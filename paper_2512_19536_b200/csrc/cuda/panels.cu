@@ -22,7 +22,7 @@ namespace {
 
 struct PanelTask {
   long long linv_off, b_off;
-  int w, nr, f_tile0, pad;
+  int w, nr, f_tile0, dense;  // dense: root panel G = inv(L_SS)^T inv(L_SS) (full w x w)
 };
 
 __device__ __forceinline__ double linv_at(const double* L, int w, int m, int j) {
@@ -48,14 +48,18 @@ __global__ void __launch_bounds__(256) forward_panel_kernel(const PanelTask* __r
   double* out = fmat + tl.off;
   for (int jb = 0; jb < tl.ncol; jb += 32) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const bool any_g = r0 + tl.rows > w;
+    const bool any_g = T.dense || r0 + tl.rows > w;
     if (any_g) {
-      // G rows of this tile: sum over m >= j of B(i - w, m) inv(L)(m, j)
-      for (int mb = jb; mb < w; mb += 32) {
+      // G rows of this tile: sum over m >= j of B(i - w, m) inv(L)(m, j);
+      // dense root: sum over m >= max(i, j) of inv(L)(m, i) inv(L)(m, j)
+      for (int mb = T.dense ? (min(r0, jb) & ~31) : jb; mb < w; mb += 32) {
         for (int e = tid; e < 32 * 32; e += 256) {
-          const int l = e & 31, mm = e >> 5;  // Bs[l][mm] = B(r0 + l - w, mb + mm)
+          const int l = e & 31, mm = e >> 5;  // Bs[l][mm] = B(r0 + l - w, mb + mm) or inv(L)(mb + mm, r0 + l)
           const int i = r0 + l, m = mb + mm;
-          Bs[l][mm] = (i >= w && l < tl.rows && m < w) ? B[static_cast<long long>(m) * nr + (i - w)] : 0.0;
+          if (T.dense)
+            Bs[l][mm] = (l < tl.rows && i < w && m < w && m >= i) ? linv_at(L, w, m, i) : 0.0;
+          else
+            Bs[l][mm] = (i >= w && l < tl.rows && m < w) ? B[static_cast<long long>(m) * nr + (i - w)] : 0.0;
           const int m2 = mb + l, j2 = jb + mm;  // Ls[l][mm] = inv(L)(mb + l, jb + mm)
           Ls[l][mm] = (m2 < w && j2 < w && m2 >= j2) ? linv_at(L, w, m2, j2) : 0.0;
         }
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(256) forward_panel_kernel(const PanelTask* __r
         if (l >= tl.stride) continue;
         const int i = r0 + l;
         double v = 0.0;
-        if (l < tl.rows) v = i < w ? (i >= j ? linv_at(L, w, i, j) : 0.0) : acc[q];
+        if (l < tl.rows) v = T.dense ? acc[q] : i < w ? (i >= j ? linv_at(L, w, i, j) : 0.0) : acc[q];
         out[static_cast<long long>(j) * tl.stride + l] = v;
       }
     }
@@ -127,7 +131,7 @@ void DeviceSim::build_panels() {
   std::vector<int> ft_task(pr.ftiles.size()), ht_task(pr.htiles.size());
   for (int i = 0; i < nt; ++i) {
     const TaskDesc& s = pr.tasks[i];
-    pt[i] = PanelTask{s.linv_off, s.b_off, s.w, s.nr, s.f_tile0, 0};
+    pt[i] = PanelTask{s.linv_off, s.b_off, s.w, s.nr, s.f_tile0, s.root_dense};
     for (int k = 0; k < s.f_ntile; ++k) ft_task[s.f_tile0 + k] = i;
     for (int k = 0; k < s.h_ntile; ++k) ht_task[s.h_tile0 + k] = i;
   }

@@ -262,6 +262,12 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   for (int s = 0; s < nt; ++s)
     if (dep_f[s] == 0) release_dir(s, true, 0.0);
   for (int c = 0; c < slots; ++c) cta.push({0.0, c});
+  auto release_children_bwd = [&](int s, double r) {
+    for (int k = 0; k < pr.tasks[s].n_child; ++k) {
+      const int c = pr.task_child[pr.tasks[s].child_off + k];
+      if (--dep_b[c] == 0) release_dir(c, false, r);
+    }
+  };
   auto complete = [&](int i, double t) {
     const DevUnit& u = units[i];
     const int s = u.task;
@@ -271,15 +277,12 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
       const double r = task_done_f[s] + kPublish;
       const int p = pr.tasks[s].parent;
       if (p >= 0 && --dep_f[p] == 0) release_dir(p, true, r);
-      if (--dep_b[s] == 0) release_dir(s, false, r);
+      if (pr.tasks[s].root_dense) release_children_bwd(s, r);  // x_S is final after the forward
+      else if (--dep_b[s] == 0) release_dir(s, false, r);
     } else {
       task_done_b[s] = std::max(task_done_b[s], t);
       if (--left_b[s] > 0) return;
-      const double r = task_done_b[s] + kPublish;
-      for (int k = 0; k < pr.tasks[s].n_child; ++k) {
-        const int c = pr.task_child[pr.tasks[s].child_off + k];
-        if (--dep_b[c] == 0) release_dir(c, false, r);
-      }
+      release_children_bwd(s, task_done_b[s] + kPublish);
     }
   };
   int placed = 0;
@@ -328,7 +331,7 @@ void DeviceSim::upload_tasks() {
   for (int i = 0; i < n_tasks; ++i) {
     const TaskDesc& s = pr.tasks[i];
     t[i] = DevTask{s.coarse, s.bs, s.w, s.nr, s.dof0, s.ubuf_off, s.f_tile0, s.f_ntile, s.h_tile0,
-                   s.h_ntile, s.rows_off, s.in_off, s.parent, s.child_off, s.n_child, 0};
+                   s.h_ntile, s.rows_off, s.in_off, s.parent, s.child_off, s.n_child, s.root_dense};
     wmax = std::max(wmax, s.w);
     nrmax = std::max(nrmax, s.nr);
   }
@@ -391,9 +394,11 @@ void DeviceSim::upload_tasks() {
         u.need[k] = pr.tasks[c].f_ntile;
       }
     } else if (s.parent >= 0) {
+      // the parent's x_S: its backward tiles, or a dense root's forward ones
+      const TaskDesc& ps = pr.tasks[s.parent];
       u.n_dep = 1;
-      u.dep[0] = nt_flag + s.parent;
-      u.need[0] = pr.tasks[s.parent].h_ntile;
+      u.dep[0] = ps.root_dense ? s.parent : nt_flag + s.parent;
+      u.need[0] = ps.root_dense ? ps.f_ntile : ps.h_ntile;
       u.own_fwd = tk;
       u.own_need = s.f_ntile;
     } else {

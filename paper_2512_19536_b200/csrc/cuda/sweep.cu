@@ -177,6 +177,7 @@ __device__ __forceinline__ void store_row(const SweepArgs& a, const DevTask& T, 
   // forward y_S goes to its own buffer: a task's backward units read all of
   // y_S while their siblings already overwrite the output with x_S
   if (!FWD) outv[T.dof0 + o] = v;
+  else if (T.pad) (T.coarse ? a.y0 : a.z)[T.dof0 + o] = v;  // dense root: x_S = inv(K_SS) t_S
   else if (o < T.w) (T.coarse ? a.yc : a.yf)[T.dof0 + o] = v;
   else a.ubuf[T.ubuf_off + (o - T.w)] = v;
 }

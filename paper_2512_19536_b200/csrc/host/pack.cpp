@@ -12,6 +12,7 @@
 // at tile granularity. This file only lays the tiles out; F and H are formed
 // on the device from inv(L_SS) and L_RS (cuda/panels.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "problem.hpp"
 
@@ -55,13 +56,17 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
       pr.lval.insert(pr.lval.end(), S.Linv.begin(), S.Linv.end());
       pr.lval.insert(pr.lval.end(), S.B.begin(), S.B.end());
     }
+    // a root with no below rows takes one dense symmetric panel
+    // (PDG_DENSE_ROOT=0 keeps the forward/backward pair)
+    static const bool dense_roots = !(std::getenv("PDG_DENSE_ROOT") && std::getenv("PDG_DENSE_ROOT")[0] == '0');
+    t.root_dense = dense_roots && S.parent < 0 && nr == 0 ? 1 : 0;
     // forward tiles: output rows of F
     // tiles start 16-byte aligned and hold an even number of rows (a zero row
     // pads odd tails) so each lane streams double2 pairs of rows
     t.f_tile0 = static_cast<int>(pr.ftiles.size());
     for (int r0 = 0; r0 < h; r0 += kTile) {
       const int rows = std::min(kTile, h - r0), rs = rows + (rows & 1);
-      const int ncol = std::min(w, r0 + rows);
+      const int ncol = t.root_dense ? w : std::min(w, r0 + rows);
       pr.fmat_len += pr.fmat_len & 1;
       pr.ftiles.push_back({pr.fmat_len, ncol, 0, rows, rs});
       pr.fmat_len += static_cast<std::int64_t>(ncol) * rs;
@@ -69,7 +74,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     t.f_ntile = static_cast<int>(pr.ftiles.size()) - t.f_tile0;
     // backward tiles: output rows of H = F^T (columns of F), inputs i >= r0
     t.h_tile0 = static_cast<int>(pr.htiles.size());
-    for (int r0 = 0; r0 < w; r0 += kTile) {
+    for (int r0 = 0; r0 < (t.root_dense ? 0 : w); r0 += kTile) {
       const int rows = std::min(kTile, w - r0), rs = rows + (rows & 1);
       const int ncol = h - r0;
       pr.hmat_len += pr.hmat_len & 1;

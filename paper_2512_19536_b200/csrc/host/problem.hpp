@@ -42,6 +42,10 @@ struct TaskDesc {
   int parent = -1;     // task id (ND parent), -1 = root
   int child_off = 0, n_child = 0;  // children ids in task_child[]
   int height = 0, depth = 0;
+  // root supernode applied as ONE dense symmetric mat-vec x_S = inv(K_SS) t_S
+  // (G = inv(L_SS)^T inv(L_SS) in the forward tiles, no backward tiles): its
+  // forward and backward solves collapse into one level of the sweep
+  int root_dense = 0;
   std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
 };
 
