@@ -111,9 +111,10 @@ std::vector<int> min_cut_cover(const std::vector<int>& ord, const std::vector<in
 }  // namespace
 
 NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
-                         const std::vector<Pt>& pos, int leaf, int merge) {
+                         const std::vector<Pt>& pos, int leaf, int merge, int top) {
   NdTree t;
   merge = std::max(1, merge);
+  top = top > 0 ? top : merge;
   t.order.reserve(m);
   t.sn_start.push_back(0);
   std::vector<int> side(m, -1), mate(m, -1), seen(m, -1), par(m, -1);
@@ -200,7 +201,9 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
         sep_nodes.insert(sep_nodes.end(), sep.begin(), sep.end());
         roots = rl;
         roots.insert(roots.end(), rr.begin(), rr.end());
-        if (depth % merge != 0) {  // defer: the ancestor level emits it
+        // defer: the ancestor level emits it (the top `top` levels form the
+        // root supernode, below that every `merge` levels form one)
+        if (depth < top ? depth != 0 : (depth - top) % merge != 0) {
           pending = sep_nodes;
           return;
         }

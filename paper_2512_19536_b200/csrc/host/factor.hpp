@@ -35,8 +35,10 @@ struct NdTree {
 // Recursive coordinate bisection; separators are the smaller one-sided
 // boundary of the cut. Deterministic (ties broken by node id). `merge`
 // consecutive separator levels form one supernode.
+// consecutive separator levels form one supernode; the root supernode takes
+// the top `top` levels (0: same as merge).
 NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
-                         const std::vector<Pt>& pos, int leaf_nodes, int merge = 1);
+                         const std::vector<Pt>& pos, int leaf_nodes, int merge = 1, int top = 0);
 
 struct Supernode {
   int s0 = 0, s1 = 0;         // positions

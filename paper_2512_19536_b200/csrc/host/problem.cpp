@@ -348,6 +348,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
   int leaf = nd_merge == 1 ? 4 : std::clamp(64 / b, 4, 16);
   if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
+  // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
+  int nd_top = nd_merge;
+  if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
   parallel_for(n_units, [&](int u) {
@@ -369,7 +372,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       ap.push_back(static_cast<int>(aj.size()));
       pos[i] = mesh.centroid(cells[i]);
     }
-    nd[u] = nested_dissection(m, ap, aj, pos, leaf, nd_merge);
+    nd[u] = nested_dissection(m, ap, aj, pos, leaf, nd_merge, nd_top);
     unit_cells[u].resize(m);
     for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
   });
