@@ -18,6 +18,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__maximum_warps_per_active_cycle_pct"]
 
 
+SETUP = {"factor_level_kernel", "assemble_kernel", "forward_panel_kernel", "backward_panel_kernel"}
+
+
 def rep(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -45,10 +48,19 @@ def launches(path):
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").split("::")[-1]
         tot[name] += float(r[hdr.index("Metric Value")]) / 1e3
         cnt[name] += 1
-    total = sum(tot.values())
-    lines = [f"{'kernel':28s} {'launches':>8s} {'total_us':>10s} {'avg_us':>8s} {'share':>6s}"]
+    # one-time setup kernels (device factorisation / panel formation) are
+    # listed apart; shares are of the time-step kernels only
+    setup = {k for k in tot if k in SETUP}
+    total = sum(v for k, v in tot.items() if k not in setup)
+    lines = [f"{'kernel':28s} {'launches':>8s} {'total_us':>10s} {'avg_us':>8s} {'share of steps':>14s}"]
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-        lines.append(f"{k:28s} {cnt[k]:8d} {v:10.1f} {v / cnt[k]:8.2f} {v / total:6.1%}")
+        if k in setup:
+            continue
+        lines.append(f"{k:28s} {cnt[k]:8d} {v:10.1f} {v / cnt[k]:8.2f} {v / total:14.1%}")
+    if setup:
+        lines.append("setup (once per simulation, not in the steps):")
+        for k in sorted(setup, key=lambda k: -tot[k]):
+            lines.append(f"  {k:26s} {cnt[k]:8d} {tot[k]:10.1f} {tot[k] / cnt[k]:8.2f}")
     return "\n".join(lines)
 
 
