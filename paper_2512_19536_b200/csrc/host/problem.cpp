@@ -341,12 +341,12 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   // config3 p=3: +2-9%) and costs once it streams with wide blocks (config3
   // p=4: -9%, config4: -11%, config5 p=4: -35%). With p <= 2 the unmerged
   // tree of small blocks is latency bound even on the 1M-cell mesh (config5
-  // p=2: -9%). Leaf size: dense leaves of ~64 dofs (4 cells unmerged).
+  // p=2: -9%). Leaf size: dense leaves of ~64 dofs.
   // PDG_ND_MERGE / PDG_ND_LEAF override.
   const bool big = static_cast<std::int64_t>(N) * b > 800000 && b >= 10;
   int nd_merge = big ? 1 : 2;
   if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
-  int leaf = nd_merge == 1 ? 4 : std::clamp(64 / b, 4, 16);
+  int leaf = std::clamp(64 / b, 4, 16);  // config4: 6-cell leaves +3.8% over 4
   if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
   // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
   int nd_top = nd_merge;
