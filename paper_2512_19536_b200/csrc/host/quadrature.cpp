@@ -61,10 +61,25 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
   if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
+// The Newton-iterated nodes are the same for every cell and face of a given
+// order: compute each n once (thread-safe static init), same bits as before.
+const std::pair<std::vector<double>, std::vector<double>>& gauss_legendre_cached(int n) {
+  static const auto table = [] {
+    std::vector<std::pair<std::vector<double>, std::vector<double>>> t(33);
+    for (int k = 1; k < 33; ++k) gauss_legendre(k, t[k].first, t[k].second);
+    return t;
+  }();
+  static thread_local std::pair<std::vector<double>, std::vector<double>> big;
+  if (n > 0 && n < 33) return table[n];
+  gauss_legendre(n, big.first, big.second);
+  return big;
+}
+
 void triangle_rule(Pt a, Pt b, Pt c, int order, Rule& out) {
   const int n = (order + 3) / 2;
-  std::vector<double> gx, gw;
-  gauss_legendre(n, gx, gw);
+  const auto& gl = gauss_legendre_cached(n);
+  const std::vector<double>& gx = gl.first;
+  const std::vector<double>& gw = gl.second;
   const double area2 = cross(b - a, c - a);
   for (int i = 0; i < n; ++i) {
     const double s = 0.5 * (gx[i] + 1.0);
@@ -146,8 +161,9 @@ Rule polygon_rule(const std::vector<Pt>& poly, int order) {
 
 Rule segment_rule(Pt p0, Pt p1, int order) {
   const int n = (std::max(order, 1) + 2) / 2;
-  std::vector<double> gx, gw;
-  gauss_legendre(n, gx, gw);
+  const auto& gl = gauss_legendre_cached(n);
+  const std::vector<double>& gx = gl.first;
+  const std::vector<double>& gw = gl.second;
   Rule r;
   const double half = 0.5 * dist(p0, p1);
   const Pt mid = (p0 + p1) * 0.5;
