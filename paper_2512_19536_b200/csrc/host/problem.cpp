@@ -836,9 +836,12 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
     const int bq2 = bq * bq;
     K0.val.assign(static_cast<std::size_t>(K0.col.size()) * bq2, 0.0);
+    // one coarse row per task: its cells in increasing local index, which is
+    // the order a serial sweep over all local rows would add them (same bits)
+    parallel_for(na, [&](int ai) {
     std::vector<double> KE(static_cast<std::size_t>(b) * bq);
-    for (int i = 0; i < nloc; ++i) {
-      const int ai = pr.cell_agg[i];
+    for (int ci = pr.agg_cell_ptr[ai]; ci < pr.agg_cell_ptr[ai + 1]; ++ci) {
+      const int i = pr.agg_cells[ci];
       const double* Ei = &pr.E[static_cast<std::size_t>(i) * b * bq];
       for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1]; ++k) {
         const int j = pr.K.col[k];
@@ -864,6 +867,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
           }
       }
     }
+    }, 1);
     phase("coarse E,K0");
     if (cfg.world == 1) finish_coarse(pr);
     phase("coarse factor");
