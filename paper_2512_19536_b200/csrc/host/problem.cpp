@@ -560,36 +560,52 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
         }
       }
     }, 64);
+    // scatter per local cell, its faces in face order: each diagonal block
+    // sums its face terms in the serial order and every off-diagonal block
+    // has one face, so the parallel scatter gives the serial bits
+    std::vector<int> tptr(nloc + 1, 0), tent;
     for (int t = 0; t < nt; ++t) {
       const Face& f = faces[touched[t]];
       const int iK = pr.iperm[f.cell_in], iL = pr.iperm[f.cell_out];
-      const double* kk = &blocks[static_cast<std::size_t>(t) * 3 * b2];
-      const double* lL = kk + b2;
-      const double* kl = lL + b2;
-      if (iK >= pr.cell_begin && iK < pr.cell_end) {
-        const int li = iK - pr.cell_begin;
-        double* D = &A.val[static_cast<std::size_t>(find_block(li, iK)) * b2];
-        for (int jj = 0; jj < b; ++jj)
-          for (int ii = 0; ii <= jj; ++ii) {
-            D[jj * b + ii] += kk[jj * b + ii];
-            if (ii != jj) D[ii * b + jj] += kk[jj * b + ii];
-          }
-        double* O = &A.val[static_cast<std::size_t>(find_block(li, iL)) * b2];
-        for (int k = 0; k < b2; ++k) O[k] += kl[k];
-      }
-      if (iL >= pr.cell_begin && iL < pr.cell_end) {
-        const int li = iL - pr.cell_begin;
-        double* D = &A.val[static_cast<std::size_t>(find_block(li, iL)) * b2];
-        for (int jj = 0; jj < b; ++jj)
-          for (int ii = 0; ii <= jj; ++ii) {
-            D[jj * b + ii] += lL[jj * b + ii];
-            if (ii != jj) D[ii * b + jj] += lL[jj * b + ii];
-          }
-        double* O = &A.val[static_cast<std::size_t>(find_block(li, iK)) * b2];
-        for (int jj = 0; jj < b; ++jj)
-          for (int ii = 0; ii < b; ++ii) O[jj * b + ii] += kl[ii * b + jj];
+      if (iK >= pr.cell_begin && iK < pr.cell_end) ++tptr[iK - pr.cell_begin + 1];
+      if (iL >= pr.cell_begin && iL < pr.cell_end) ++tptr[iL - pr.cell_begin + 1];
+    }
+    for (int i = 0; i < nloc; ++i) tptr[i + 1] += tptr[i];
+    tent.resize(tptr[nloc]);
+    {
+      std::vector<int> fill(tptr.begin(), tptr.end() - 1);
+      for (int t = 0; t < nt; ++t) {  // entry = 2 t + side (0: cell_in, 1: cell_out)
+        const Face& f = faces[touched[t]];
+        const int iK = pr.iperm[f.cell_in], iL = pr.iperm[f.cell_out];
+        if (iK >= pr.cell_begin && iK < pr.cell_end) tent[fill[iK - pr.cell_begin]++] = 2 * t;
+        if (iL >= pr.cell_begin && iL < pr.cell_end) tent[fill[iL - pr.cell_begin]++] = 2 * t + 1;
       }
     }
+    parallel_for(nloc, [&](int li) {
+      for (int e = tptr[li]; e < tptr[li + 1]; ++e) {
+        const int t = tent[e] >> 1, side = tent[e] & 1;
+        const Face& f = faces[touched[t]];
+        const int iK = pr.iperm[f.cell_in], iL = pr.iperm[f.cell_out];
+        const double* kk = &blocks[static_cast<std::size_t>(t) * 3 * b2];
+        const double* lL = kk + b2;
+        const double* kl = lL + b2;
+        const double* dd = side == 0 ? kk : lL;
+        const int self = side == 0 ? iK : iL, other = side == 0 ? iL : iK;
+        double* D = &A.val[static_cast<std::size_t>(find_block(li, self)) * b2];
+        for (int jj = 0; jj < b; ++jj)
+          for (int ii = 0; ii <= jj; ++ii) {
+            D[jj * b + ii] += dd[jj * b + ii];
+            if (ii != jj) D[ii * b + jj] += dd[jj * b + ii];
+          }
+        double* O = &A.val[static_cast<std::size_t>(find_block(li, other)) * b2];
+        if (side == 0) {
+          for (int k = 0; k < b2; ++k) O[k] += kl[k];
+        } else {
+          for (int jj = 0; jj < b; ++jj)
+            for (int ii = 0; ii < b; ++ii) O[jj * b + ii] += kl[ii * b + jj];
+        }
+      }
+    }, 256);
   }
   // K = C_m chi_m M + dt/2 A (assembly.cpp:197-202)
   {
@@ -599,7 +615,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     pr.K.ptr = A.ptr;
     pr.K.col = A.col;
     pr.K.val.resize(A.val.size());
-    for (int i = 0; i < nloc; ++i)
+    parallel_for(nloc, [&](int i) {
       for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
         const bool diag = A.col[k] == pr.cell_begin + i;
         const double* a_ = &A.val[static_cast<std::size_t>(k) * b2];
@@ -607,6 +623,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
         const double* m_ = &pr.M[static_cast<std::size_t>(i) * b2];
         for (int e = 0; e < b2; ++e) kv[e] = diag ? a * m_[e] + hb * a_[e] : hb * a_[e];
       }
+    }, 256);
     if (!pr.keep_matrices) {
       A.val.clear();
       A.val.shrink_to_fit();
