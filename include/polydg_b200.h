@@ -37,6 +37,18 @@ enum { PDG_PRECOND_NONE = 0, PDG_PRECOND_BLOCK_JACOBI = 1, PDG_PRECOND_TWO_LEVEL
 enum { PDG_IONIC_NONE = 0, PDG_IONIC_FHN = 1, PDG_IONIC_BARRETO_CRESSMAN = 2 };
 enum { PDG_INIT_DISC = 0, PDG_INIT_CONSTANT = 1, PDG_INIT_COSINE = 2, PDG_INIT_BILINEAR = 3 };
 enum { PDG_STIM_NONE = 0, PDG_STIM_STRIP = 1, PDG_STIM_COSINE = 2 };
+/* ext: Barreto-Cressman kinetics (Cressman et al. 2009, J Comput Neurosci 26:159;
+ * the reference registers the model name but ships no kinetics, ionics.cpp:52-57).
+ * State y = (n, h, [K]o, [Na]i); indices into pdg_config.bc: */
+enum {
+  PDG_BC_G_NA = 0, PDG_BC_G_K, PDG_BC_G_NAL, PDG_BC_G_KL, PDG_BC_G_CLL, /* mS/cm^2 */
+  PDG_BC_PHI,                                                         /* gating time scale, 1/ms */
+  PDG_BC_RHO, PDG_BC_G_GLIA, PDG_BC_EPS, PDG_BC_K_BATH,               /* mM/s, mM/s, 1/s, mM */
+  PDG_BC_GAMMA, PDG_BC_BETA, PDG_BC_TAU,                              /* mM cm^2/uC, -, ms/s */
+  PDG_BC_RTF, PDG_BC_CL_I, PDG_BC_CL_O,                               /* mV, mM, mM */
+  PDG_BC_NA_I0, PDG_BC_K_I0, PDG_BC_NA_O0, PDG_BC_AMP,                /* mM, mM, mM, - */
+  PDG_BC_NPARAM
+};
 
 /*
  * Mirrors polydg::SimulationConfig (/root/reference/proj/include/polydg/
@@ -86,9 +98,17 @@ typedef struct pdg_config {
   int coarse_count; /* ext: 0 = hierarchy; -1 = same partition as the subdomains; >0 = agglomerate(mesh,n) */
   /* placement */
   int rank, world, device;
+  /* ext: Barreto-Cressman parameters (PDG_BC_* above); appended so the
+   * earlier layout is unchanged */
+  double bc[PDG_BC_NPARAM];
 } pdg_config;
 
 void pdg_config_default(pdg_config* cfg);
+/* IonicModel::state_dim / resting_potential / resting_state (ionics.hpp:25-31) of
+ * cfg->ionic_model: n_comp = 0 (none), 1 (FHN: u_min, y = 0) or 4 (Barreto-Cressman:
+ * the fixed point of the membrane + concentration equations, found by Newton);
+ * y_rest holds up to 4 values */
+pdg_status pdg_ionic_rest(const pdg_config* cfg, int* n_comp, double* u_rest, double* y_rest);
 const char* pdg_last_error(void);
 
 /* ---- mesh level (host setup; bit-exact with the reference generator) ---- */

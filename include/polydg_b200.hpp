@@ -176,7 +176,8 @@ class Simulation {
   // TimeStepState (timestepper.hpp:82-87): U_curr, U_prev and n_comp Y fields
   void state(int* k, double* t, Vector* U_curr, Vector* U_prev, Vector* Y_curr, Vector* Y_prev) const {
     const std::size_t n = static_cast<std::size_t>(dimension());
-    const int nc = cfg_.ionic_model == PDG_IONIC_NONE ? 0 : 1;
+    int nc = 0;  // IonicModel::state_dim (ionics.hpp:25): 1 FHN, 4 Barreto-Cressman
+    check(pdg_ionic_rest(&cfg_, &nc, nullptr, nullptr));
     if (U_curr) U_curr->resize(n);
     if (U_prev) U_prev->resize(n);
     if (Y_curr) Y_curr->resize(n * nc);

@@ -37,6 +37,7 @@ typedef struct orc_config {
   int subdomains;
   int coarse_count;
   int rank, world, device;
+  double bc[20];
 } orc_config;
 
 typedef struct orc_report {
@@ -85,8 +86,9 @@ orc::Config convert(const orc_config& c) {
   o.fiber_random = c.fiber_random;
   o.fiber_seed = c.fiber_seed;
   o.ionic = c.ionic_model;
-  if (o.ionic > 1) throw orc::ConfigError("oracle: only the FHN model is pinned");
+  if (o.ionic > 2) throw orc::ConfigError("oracle: unknown ionic model");
   std::memcpy(o.fhn, c.fhn, sizeof o.fhn);
+  std::memcpy(o.bc, c.bc, sizeof o.bc);
   o.init_kind = c.init_kind;
   o.u_rest = c.u_rest;
   o.u_patch = c.u_patch;
@@ -255,10 +257,10 @@ int orc_sim_ionic_terms(void* h, const double* U, const double* Y, double* I, do
     auto& s = *static_cast<orc::Simulation*>(h);
     const std::size_t n = s.U.size();
     std::vector<orc::Vec> yv;
-    if (s.cfg.ionic == 1) yv.emplace_back(Y, Y + n);
-    const orc::IonicTerms t = orc::ionic_terms(s.D, orc::Vec(U, U + n), yv, s.cfg.fhn, nullptr);
+    for (std::size_t l = 0; l < s.Y.size(); ++l) yv.emplace_back(Y + l * n, Y + (l + 1) * n);
+    const orc::IonicTerms t = orc::ionic_terms(s.D, orc::Vec(U, U + n), yv, s.cfg, nullptr);
     std::memcpy(I, t.I.data(), n * sizeof(double));
-    if (!t.G.empty()) std::memcpy(G, t.G[0].data(), n * sizeof(double));
+    for (std::size_t l = 0; l < t.G.size(); ++l) std::memcpy(G + l * n, t.G[l].data(), n * sizeof(double));
   });
 }
 
@@ -309,6 +311,17 @@ int orc_fhn(const double* prm, double u, double w, double* f, double* m) {
     *f = orc::fhn_current(prm, u, w);
     *m = orc::fhn_rate(prm, u, w);
   });
+}
+
+int orc_bc(const double* prm, double u, const double* y, double* f, double* m) {
+  return guarded([&] {
+    *f = orc::bc_current(prm, u, y);
+    orc::bc_rates(prm, u, y, m);
+  });
+}
+
+int orc_ionic_rest(const orc_config* c, int* n_comp, double* u, double* y) {
+  return guarded([&] { *n_comp = orc::model_rest(convert(*c), u, y); });
 }
 
 int orc_polygon_quadrature(const double* poly, int n, int order, double* pts, double* w, int cap) {

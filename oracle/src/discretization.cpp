@@ -576,13 +576,141 @@ double fhn_rate(const double* P, double u, double w) {
   return -P[1] * (v - P[4] * w);
 }
 
-IonicTerms ionic_terms(const Discretization& D, const Vec& U, const std::vector<Vec>& Y, const double* P,
+// ---- Barreto-Cressman (Cressman et al. 2009, J Comput Neurosci 26:159-170) ----
+namespace {
+double x_over_1mexp(double x) { return x == 0.0 ? 1.0 : x / (1.0 - std::exp(-x)); }
+struct BcParts {
+  double i_na, i_k, i_cl;
+};
+BcParts bc_parts(const double* P, double u, const double* y) {
+  const double n = y[0], h = y[1], ko = y[2], nai = y[3];
+  if (!std::isfinite(u) || !std::isfinite(n) || !std::isfinite(h) || !std::isfinite(ko) || !std::isfinite(nai))
+    throw SolverError("barreto-cressman: non-finite state in current evaluation");
+  const double alpha_m = x_over_1mexp(0.1 * (u + 30.0)), beta_m = 4.0 * std::exp(-(u + 55.0) / 18.0);
+  const double m_inf = alpha_m / (alpha_m + beta_m);
+  const double k_in = P[17] + (P[16] - nai);            // [K]i
+  const double na_out = P[18] - P[11] * (nai - P[16]);  // [Na]o
+  const double e_na = P[13] * std::log(na_out / nai);
+  const double e_k = P[13] * std::log(ko / k_in);
+  const double e_cl = P[13] * std::log(P[14] / P[15]);
+  BcParts r;
+  r.i_na = P[0] * m_inf * m_inf * m_inf * h * (u - e_na) + P[2] * (u - e_na);
+  r.i_k = P[1] * std::pow(n, 4) * (u - e_k) + P[3] * (u - e_k);
+  r.i_cl = P[4] * (u - e_cl);
+  return r;
+}
+}  // namespace
+
+double bc_current(const double* P, double u, const double* y) {
+  const BcParts c = bc_parts(P, u, y);
+  const double f = P[19] * (c.i_na + c.i_k + c.i_cl);
+  if (!std::isfinite(f)) throw SolverError("barreto-cressman: non-finite state in current evaluation");
+  return f;
+}
+
+void bc_rates(const double* P, double u, const double* y, double* m) {
+  const BcParts c = bc_parts(P, u, y);
+  const double alpha_n = 0.1 * x_over_1mexp(0.1 * (u + 34.0)), beta_n = 0.125 * std::exp(-(u + 44.0) / 80.0);
+  const double alpha_h = 0.07 * std::exp(-(u + 44.0) / 20.0), beta_h = 1.0 / (1.0 + std::exp(-0.1 * (u + 14.0)));
+  const double pump = P[6] / ((1.0 + std::exp((25.0 - y[3]) / 3.0)) * (1.0 + std::exp(5.5 - y[2])));
+  const double glia = P[7] / (1.0 + std::exp((18.0 - y[2]) / 2.5));
+  const double diff = P[8] * (y[2] - P[9]);
+  const double dn = P[5] * (alpha_n * (1.0 - y[0]) - beta_n * y[0]);
+  const double dh = P[5] * (alpha_h * (1.0 - y[1]) - beta_h * y[1]);
+  const double dko = (P[10] * P[11] * c.i_k - 2.0 * P[11] * pump - glia - diff) / P[12];
+  const double dnai = (-P[10] * c.i_na - 3.0 * pump) / P[12];
+  m[0] = -dn;
+  m[1] = -dh;
+  m[2] = -dko;
+  m[3] = -dnai;
+  for (int l = 0; l < 4; ++l)
+    if (!std::isfinite(m[l])) throw SolverError("barreto-cressman: non-finite state in rate evaluation");
+}
+
+int model_rest(const Config& c, double* u, double* y) {
+  if (c.ionic == 1) {
+    *u = c.fhn[5];
+    y[0] = 0.0;
+    return 1;
+  }
+  if (c.ionic != 2) return 0;
+  // Newton on F(u, Ko, Nai) = (I, dKo/dt, dNai/dt) with n, h at steady state;
+  // central-difference Jacobian, partial-pivot elimination
+  auto gates = [](double v, double* g) {
+    const double an = 0.1 * x_over_1mexp(0.1 * (v + 34.0)), bn = 0.125 * std::exp(-(v + 44.0) / 80.0);
+    const double ah = 0.07 * std::exp(-(v + 44.0) / 20.0), bh = 1.0 / (1.0 + std::exp(-0.1 * (v + 14.0)));
+    g[0] = an / (an + bn);
+    g[1] = ah / (ah + bh);
+  };
+  auto F = [&](const double* z, double* f) {
+    double yy[4];
+    gates(z[0], yy);
+    yy[2] = z[1];
+    yy[3] = z[2];
+    double m[4];
+    bc_rates(c.bc, z[0], yy, m);
+    f[0] = bc_current(c.bc, z[0], yy);
+    f[1] = m[2] * c.bc[12];
+    f[2] = m[3] * c.bc[12];
+  };
+  double z[3] = {-68.0, c.bc[9], c.bc[16]};
+  for (int it = 0; it < 100; ++it) {
+    double f[3], J[3][4];
+    F(z, f);
+    for (int j = 0; j < 3; ++j) {
+      double zp[3] = {z[0], z[1], z[2]}, zm[3] = {z[0], z[1], z[2]}, fp[3], fm[3];
+      const double h = 1e-6 * std::max(1.0, std::fabs(z[j]));
+      zp[j] += h;
+      zm[j] -= h;
+      F(zp, fp);
+      F(zm, fm);
+      for (int i = 0; i < 3; ++i) J[i][j] = (fp[i] - fm[i]) / (2.0 * h);
+    }
+    for (int i = 0; i < 3; ++i) J[i][3] = -f[i];
+    for (int col = 0; col < 3; ++col) {
+      int piv = col;
+      for (int r = col + 1; r < 3; ++r)
+        if (std::fabs(J[r][col]) > std::fabs(J[piv][col])) piv = r;
+      for (int k = 0; k < 4; ++k) std::swap(J[col][k], J[piv][k]);
+      for (int r = col + 1; r < 3; ++r) {
+        const double l = J[r][col] / J[col][col];
+        for (int k = col; k < 4; ++k) J[r][k] -= l * J[col][k];
+      }
+    }
+    double dz[3];
+    for (int i = 2; i >= 0; --i) {
+      double s = J[i][3];
+      for (int k = i + 1; k < 3; ++k) s -= J[i][k] * dz[k];
+      dz[i] = s / J[i][i];
+    }
+    double step = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      z[j] += dz[j];
+      step = std::max(step, std::fabs(dz[j]) / std::max(1.0, std::fabs(z[j])));
+    }
+    if (!std::isfinite(step)) break;
+    if (step < 1e-14) {
+      *u = z[0];
+      gates(z[0], y);
+      y[2] = z[1];
+      y[3] = z[2];
+      return 4;
+    }
+  }
+  throw ConfigError("barreto-cressman: no resting state found for these parameters");
+}
+
+IonicTerms ionic_terms(const Discretization& D, const Vec& U, const std::vector<Vec>& Y, const Config& cfg,
                        bool* out_of_box) {
   const int nl = D.nloc, nc = D.mesh->n_cells();
+  const int ncomp = static_cast<int>(Y.size());
+  const bool bc = cfg.ionic == 2;
+  const double* P = cfg.fhn;
   IonicTerms out;
   out.I.assign(U.size(), 0.0);
   out.G.assign(Y.size(), Vec(U.size(), 0.0));
-  const double slack = 10.0 * (P[6] - P[5]);
+  const double umin = bc ? -100.0 : P[5], umax = bc ? 60.0 : P[6];
+  const double slack = 10.0 * (umax - umin);
   std::vector<char> oob(nc, 0);
   std::vector<std::string> err(nc);
   parallel_for(nc, [&](std::size_t ci) {
@@ -593,16 +721,24 @@ IonicTerms ionic_terms(const Discretization& D, const Vec& U, const std::vector<
       eval_basis(D.mesh->bbox[e], D.p, r.pts, val, nullptr, nullptr);
       const int64_t b0 = static_cast<int64_t>(e) * nl;
       for (std::size_t q = 0; q < r.w.size(); ++q) {
-        double u = 0.0, y = 0.0;
+        double u = 0.0, y[4] = {0.0, 0.0, 0.0, 0.0}, m[4] = {0.0, 0.0, 0.0, 0.0};
         for (int i = 0; i < nl; ++i) u += val[q * nl + i] * U[b0 + i];
-        if (!Y.empty())
-          for (int i = 0; i < nl; ++i) y += val[q * nl + i] * Y[0][b0 + i];
-        if (u < P[5] - slack || u > P[6] + slack) oob[e] = 1;
-        const double f = fhn_current(P, u, y), m = fhn_rate(P, u, y);
-        const double wf = r.w[q] * f, wm = r.w[q] * m;
-        for (int i = 0; i < nl; ++i) {
-          out.I[b0 + i] += wf * val[q * nl + i];
-          if (!Y.empty()) out.G[0][b0 + i] += wm * val[q * nl + i];
+        for (int l = 0; l < ncomp; ++l)
+          for (int i = 0; i < nl; ++i) y[l] += val[q * nl + i] * Y[l][b0 + i];
+        if (u < umin - slack || u > umax + slack) oob[e] = 1;
+        double f;
+        if (bc) {
+          f = bc_current(cfg.bc, u, y);
+          bc_rates(cfg.bc, u, y, m);
+        } else {
+          f = fhn_current(P, u, y[0]);
+          m[0] = fhn_rate(P, u, y[0]);
+        }
+        const double wf = r.w[q] * f;
+        for (int i = 0; i < nl; ++i) out.I[b0 + i] += wf * val[q * nl + i];
+        for (int l = 0; l < ncomp; ++l) {
+          const double wm = r.w[q] * m[l];
+          for (int i = 0; i < nl; ++i) out.G[l][b0 + i] += wm * val[q * nl + i];
         }
       }
     } catch (const std::exception& ex) {

@@ -107,8 +107,10 @@ struct Config {
   P2 fiber_grey{0, 1}, fiber_white{0, 1};
   int fiber_random = 0;
   uint64_t fiber_seed = 42;
-  int ionic = 1;  // 0 none, 1 fhn
+  int ionic = 1;  // 0 none, 1 fhn, 2 barreto-cressman (ext, unpinned)
   double fhn[8] = {0.13, 0.013, 0.26, 0.1, 1.0, -85.0, 20.0, 1.0};
+  // g_Na g_K g_NaL g_KL g_ClL phi rho G_glia eps k_bath gamma beta tau RT/F Cl_i Cl_o Na_i0 K_i0 Na_o0 amp
+  double bc[20] = {100, 40, 0.0175, 0.05, 0.05, 3, 1.25, 66, 1.2, 4, 0.0445, 7, 1000, 26.64, 6, 130, 18, 140, 144, 1};
   int init_kind = 0;
   double u_rest = -67, u_patch = -50;
   P2 omega0{0.5, 1.0};
@@ -144,8 +146,15 @@ struct IonicTerms {
   Vec I;
   std::vector<Vec> G;
 };
+// Barreto-Cressman (ext): Cressman et al. 2009 kinetics in the IonicModel
+// convention (dy/dt = -m), state (n, h, [K]o, [Na]i); parity unpinned (the
+// reference ships no kinetics, ionics.cpp:52-57)
+double bc_current(const double* prm, double u, const double* y);
+void bc_rates(const double* prm, double u, const double* y, double* m);
+// resting_potential / resting_state (ionics.hpp:29-30); returns state_dim
+int model_rest(const Config& c, double* u, double* y);
 IonicTerms ionic_terms(const Discretization& D, const Vec& U, const std::vector<Vec>& Y,
-                       const double* fhn, bool* out_of_box);
+                       const Config& cfg, bool* out_of_box);
 
 // ---- linear algebra: operators, PCG, Lanczos (krylov.cpp) ----
 struct Operator {

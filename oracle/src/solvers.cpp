@@ -390,7 +390,12 @@ void Simulation::build(const Config& c, MeshView m, const std::vector<int>& sub_
   U = D.l2_project([this](P2 x) { return initial(x); });
   Up = U;
   Y.clear();
-  if (cfg.ionic == 1) Y.push_back(D.l2_project([](P2) { return 0.0; }));
+  double u_rest = 0.0, y_rest[4] = {0.0, 0.0, 0.0, 0.0};
+  const int ncomp = model_rest(cfg, &u_rest, y_rest);
+  for (int l = 0; l < ncomp; ++l) {  // timestepper.cpp:116-123
+    const double v = y_rest[l];
+    Y.push_back(D.l2_project([v](P2) { return v; }));
+  }
   Yp = Y;
   k = 0;
   t = 0.0;
@@ -421,7 +426,7 @@ StepStats Simulation::step() {
   const int64_t n = static_cast<int64_t>(U.size());
   Vec rhs;
   D.Krhs.apply(U, rhs);
-  if (cfg.ionic == 1) {
+  if (cfg.ionic != 0) {
     Vec us = U;
     std::vector<Vec> ys = Y;
     if (has_prev) {
@@ -430,7 +435,7 @@ StepStats Simulation::step() {
         for (int64_t i = 0; i < n; ++i) ys[l][i] = 2.0 * Y[l][i] - Yp[l][i];
     }
     bool oob = false;
-    const IonicTerms at_star = ionic_terms(D, us, ys, cfg.fhn, &oob);
+    const IonicTerms at_star = ionic_terms(D, us, ys, cfg, &oob);
     if (oob) std::fprintf(stderr, "oracle: warning: membrane potential left the admissible range\n");
     for (int64_t i = 0; i < n; ++i) rhs[i] -= (cfg.chi_m * dt) * at_star.I[i];
   }
@@ -450,8 +455,8 @@ StepStats Simulation::step() {
                   k + 1, maxit, rep.resid.empty() ? 1.0 : rep.resid.back());
     throw SolverError(buf);
   }
-  if (cfg.ionic == 1 && !Y.empty()) {
-    const IonicTerms at_curr = ionic_terms(D, U, Y, cfg.fhn, nullptr);
+  if (cfg.ionic != 0 && !Y.empty()) {
+    const IonicTerms at_curr = ionic_terms(D, U, Y, cfg, nullptr);
     std::vector<Vec> ynext = Y;
     for (std::size_t l = 0; l < ynext.size(); ++l) {
       const Vec s = D.mass_solve(at_curr.G[l]);

@@ -43,6 +43,7 @@ class PdgConfig(C.Structure):
         ("precond_kind", C.c_int), ("h_ratio", C.c_int), ("q", C.c_int),
         ("subdomains", C.c_int), ("coarse_count", C.c_int),
         ("rank", C.c_int), ("world", C.c_int), ("device", C.c_int),
+        ("bc", C.c_double * 20),
     ]
 
 
@@ -83,6 +84,7 @@ def lib() -> C.CDLL:
         sig = {
             "pdg_config_default": (None, [P(PdgConfig)]),
             "pdg_last_error": (C.c_char_p, []),
+            "pdg_ionic_rest": (i32, [P(PdgConfig), P(i32), P(dbl), P(dbl)]),
             "pdg_mesh_generate": (i32, [i32, P(dbl), C.c_uint64, i32, dbl, P(vp)]),
             "pdg_mesh_free": (None, [vp]),
             "pdg_mesh_counts": (None, [vp, P(i32)]),

@@ -5,8 +5,10 @@ unit square, mesh seed 42, chi_m = 1000, C_m = 1, eta0 = 10, warm start, q = p,
 S_H = S (coarse partition = subdomain partition, realised by the reference's
 greedy agglomerator). Builder choices for unstated inputs (documented in
 DESIGN.md): strip-stimulus amplitude STIM_AMP, fibre angle RNG
-mt19937_64(42) with theta = pi*(rng()>>11)*2^-53 in cell order, and FHN in
-place of the unpinned Barreto-Cressman kinetics for every parity run.
+mt19937_64(42) with theta = pi*(rng()>>11)*2^-53 in cell order, and FHN as the
+pinned ionic model of the parity runs. config1_bc() is BASELINE config 1 with
+the Barreto-Cressman kinetics (ext, Cressman et al. 2009; parity oracle-vs-GPU
+only, since the reference ships no kinetics) started from its resting state.
 """
 from __future__ import annotations
 
@@ -24,6 +26,17 @@ def config1(**kw) -> SimulationConfig:
                 stimulus=("strip", STIM_AMP, 0.1, 1.0), dt=0.01, T=1.0, tol=1e-8)
     base.update(kw)
     return SimulationConfig(**base)
+
+
+def config1_bc(**kw) -> SimulationConfig:
+    """config 1 with the Barreto-Cressman model (u, n, h, [K]o, [Na]i) from its resting state."""
+    from .simulation import ionic_rest
+    base = dict(ionic_model="barreto-cressman")
+    base.update(kw)
+    cfg = config1(**base)
+    if "initial" not in kw:
+        cfg.initial = ("constant", ionic_rest(cfg)[1])
+    return cfg
 
 
 def config2(**kw) -> SimulationConfig:

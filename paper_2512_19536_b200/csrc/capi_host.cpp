@@ -71,6 +71,26 @@ void pdg_config_default(pdg_config* c) {
   c->rank = 0;
   c->world = 1;
   c->device = 0;
+  // Barreto-Cressman (ext): Cressman et al. 2009 values, k_bath = 4 mM
+  const double bc[PDG_BC_NPARAM] = {100.0, 40.0, 0.0175, 0.05, 0.05,  // g_Na g_K g_NaL g_KL g_ClL
+                                    3.0,                             // phi
+                                    1.25, 66.0, 1.2, 4.0,            // rho G_glia eps k_bath
+                                    0.0445, 7.0, 1000.0,             // gamma beta tau
+                                    26.64, 6.0, 130.0,               // RT/F, [Cl]i, [Cl]o
+                                    18.0, 140.0, 144.0, 1.0};        // Na_i0 K_i0 Na_o0 amp
+  std::memcpy(c->bc, bc, sizeof bc);
+}
+
+pdg_status pdg_ionic_rest(const pdg_config* cfg, int* n_comp, double* u_rest, double* y_rest) {
+  return pdg::guarded([&] {
+    pdg::validate_config(*cfg);
+    double u = 0.0, y[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nc = pdg::ionic_rest(*cfg, u, y);
+    if (n_comp) *n_comp = nc;
+    if (u_rest) *u_rest = u;
+    if (y_rest)
+      for (int l = 0; l < nc; ++l) y_rest[l] = y[l];
+  });
 }
 
 int pdg_default_max_iterations(int64_t n) {

@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "../host/bc_model.hpp"
 
 #ifndef PDG_SPMV_UNROLL
 #define PDG_SPMV_UNROLL 2
@@ -709,27 +710,31 @@ __device__ __forceinline__ void basis_eval(double xi, double eta, double inv, do
     }
 }
 
-template <int P>
+// NC = state components of the model: 1 (FHN, or no model with a stimulus), 4 (Barreto-Cressman)
+template <int P, int NC>
 __global__ void __launch_bounds__(256) ionic_kernel(IonicArgs a) {
   constexpr int B = (P + 1) * (P + 2) / 2;
-  __shared__ double sc[8][4 * B];
+  __shared__ double sc[8][(2 + 2 * NC) * B];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int c = blockIdx.x * 8 + wl;
   if (c >= a.ncells) return;
   const long long o = static_cast<long long>(c) * B;
-  double* Us = sc[wl];          // extrapolated U*
-  double* Ys = sc[wl] + B;      // extrapolated Y*
-  double* Uc = sc[wl] + 2 * B;  // current U
-  double* Yc = sc[wl] + 3 * B;  // current Y
+  double* Us = sc[wl];                // extrapolated U*
+  double* Uc = sc[wl] + B;            // current U
+  double* Ys = sc[wl] + 2 * B;        // extrapolated Y*, NC fields
+  double* Yc = sc[wl] + (2 + NC) * B; // current Y, NC fields
   const bool model = a.model != 0 && a.n_comp > 0;
   for (int k = lane; k < B; k += 32) {
     const double u = a.U[o + k];
     Uc[k] = u;
     Us[k] = a.has_prev ? 2.0 * u - a.Up[o + k] : u;
     if (model) {
-      const double y = a.Y[o + k];
-      Yc[k] = y;
-      Ys[k] = a.has_prev ? 2.0 * y - a.Yp[o + k] : y;
+#pragma unroll
+      for (int l = 0; l < NC; ++l) {
+        const double y = a.Y[l * a.n + o + k];
+        Yc[l * B + k] = y;
+        Ys[l * B + k] = a.has_prev ? 2.0 * y - a.Yp[l * a.n + o + k] : y;
+      }
     }
   }
   __syncwarp();
@@ -738,10 +743,14 @@ __global__ void __launch_bounds__(256) ionic_kernel(IonicArgs a) {
   const double inv = 1.0 / sqrt(wx * wy);
   const int t0 = a.tri_ptr[c], t1 = a.tri_ptr[c + 1];
   const int ng = a.ngl, npt = (t1 - t0) * ng * ng;
-  double accI[B], accF[B], accG[B];
+  double accI[B], accF[B], accG[NC][B];
 #pragma unroll
-  for (int k = 0; k < B; ++k) accI[k] = accF[k] = accG[k] = 0.0;
-  const double span = a.fhn[6] - a.fhn[5];
+  for (int k = 0; k < B; ++k) {
+    accI[k] = accF[k] = 0.0;
+#pragma unroll
+    for (int l = 0; l < NC; ++l) accG[l][k] = 0.0;
+  }
+  const double span = a.ubounds[1] - a.ubounds[0];
   int flag = 0;
   for (int pidx = lane; pidx < npt; pidx += 32) {
     const int tri = pidx / (ng * ng), rem = pidx - tri * ng * ng;
@@ -757,28 +766,50 @@ __global__ void __launch_bounds__(256) ionic_kernel(IonicArgs a) {
     double phi[B];
     basis_eval<P>((2.0 * px - bx0 - bx1) / wx, (2.0 * py - by0 - by1) / wy, inv, phi);
     if (model) {
-      double us = 0.0, ys = 0.0, uc = 0.0, yc = 0.0;
+      double us = 0.0, uc = 0.0, ys[NC], yc[NC];
+#pragma unroll
+      for (int l = 0; l < NC; ++l) ys[l] = yc[l] = 0.0;
 #pragma unroll
       for (int k = 0; k < B; ++k) {
         us = fma(Us[k], phi[k], us);
-        ys = fma(Ys[k], phi[k], ys);
         uc = fma(Uc[k], phi[k], uc);
-        yc = fma(Yc[k], phi[k], yc);
-      }
-      if (!isfinite(us) || !isfinite(ys) || !isfinite(uc) || !isfinite(yc)) flag |= 2;
-      const double slack = 10.0 * span;
-      if (us < a.fhn[5] - slack || us > a.fhn[6] + slack || uc < a.fhn[5] - slack || uc > a.fhn[6] + slack)
-        flag |= 1;
-      // FitzHugh-Nagumo, Rogers-McCulloch form (ionics.cpp:20-33)
-      const double v = (us - a.fhn[5]) / span;
-      const double f = a.fhn[7] * (a.fhn[2] * v * (v - a.fhn[0]) * (v - 1.0) + a.fhn[3] * v * ys) * span;
-      const double vc = (uc - a.fhn[5]) / span;
-      const double m = -a.fhn[1] * (vc - a.fhn[4] * yc);
-      const double wf = w * f, wm = w * m;
 #pragma unroll
-      for (int k = 0; k < B; ++k) {
-        accI[k] = fma(wf, phi[k], accI[k]);
-        accG[k] = fma(wm, phi[k], accG[k]);
+        for (int l = 0; l < NC; ++l) {
+          ys[l] = fma(Ys[l * B + k], phi[k], ys[l]);
+          yc[l] = fma(Yc[l * B + k], phi[k], yc[l]);
+        }
+      }
+      bool finite = isfinite(us) && isfinite(uc);
+#pragma unroll
+      for (int l = 0; l < NC; ++l) finite = finite && isfinite(ys[l]) && isfinite(yc[l]);
+      const double slack = 10.0 * span;
+      if (us < a.ubounds[0] - slack || us > a.ubounds[1] + slack || uc < a.ubounds[0] - slack ||
+          uc > a.ubounds[1] + slack)
+        flag |= 1;
+      double f, m[NC];
+      if constexpr (NC == 4) {
+        // Barreto-Cressman (bc_model.hpp): current at the extrapolated state, rates at the current one
+        f = bc::current(a.bc, us, ys);
+        bc::rates(a.bc, uc, yc, m);
+        finite = finite && isfinite(f);
+#pragma unroll
+        for (int l = 0; l < NC; ++l) finite = finite && isfinite(m[l]);
+      } else {
+        // FitzHugh-Nagumo, Rogers-McCulloch form (ionics.cpp:20-33)
+        const double v = (us - a.fhn[5]) / span;
+        f = a.fhn[7] * (a.fhn[2] * v * (v - a.fhn[0]) * (v - 1.0) + a.fhn[3] * v * ys[0]) * span;
+        const double vc = (uc - a.fhn[5]) / span;
+        m[0] = -a.fhn[1] * (vc - a.fhn[4] * yc[0]);
+      }
+      if (!finite) flag |= 2;
+      const double wf = w * f;
+#pragma unroll
+      for (int k = 0; k < B; ++k) accI[k] = fma(wf, phi[k], accI[k]);
+#pragma unroll
+      for (int l = 0; l < NC; ++l) {
+        const double wm = w * m[l];
+#pragma unroll
+        for (int k = 0; k < B; ++k) accG[l][k] = fma(wm, phi[k], accG[l][k]);
       }
     }
     if (a.stim != 0) {
@@ -797,25 +828,29 @@ __global__ void __launch_bounds__(256) ionic_kernel(IonicArgs a) {
   for (int k = 0; k < B; ++k) {
     accI[k] = warp_sum(accI[k]);
     accF[k] = warp_sum(accF[k]);
-    accG[k] = warp_sum(accG[k]);
+#pragma unroll
+    for (int l = 0; l < NC; ++l) accG[l][k] = warp_sum(accG[l][k]);
   }
   flag = __reduce_or_sync(0xffffffffu, flag);
+  __syncwarp();
   if (lane == 0) {
     if (flag) atomicOr(a.flags, flag);
 #pragma unroll
-    for (int k = 0; k < B; ++k) {
-      a.ion[o + k] = -(a.chi * a.dt) * accI[k] + a.dt * accF[k];
-      Us[k] = accG[k];  // reuse as G
-    }
+    for (int k = 0; k < B; ++k) a.ion[o + k] = -(a.chi * a.dt) * accI[k] + a.dt * accF[k];
+#pragma unroll
+    for (int l = 0; l < NC; ++l)
+#pragma unroll
+      for (int k = 0; k < B; ++k) Ys[l * B + k] = accG[l][k];  // reuse as G
   }
   __syncwarp();
   if (model) {
     const double* Mi = a.Minv + static_cast<long long>(c) * B * B;
-    for (int k = lane; k < B; k += 32) {
+    for (int idx = lane; idx < NC * B; idx += 32) {
+      const int l = idx / B, k = idx - l * B;
       double acc = 0.0;
 #pragma unroll
-      for (int jj = 0; jj < B; ++jj) acc = fma(Mi[jj * B + k], Us[jj], acc);
-      a.Ynext[o + k] = Yc[k] - a.dt * acc;
+      for (int jj = 0; jj < B; ++jj) acc = fma(Mi[jj * B + k], Ys[l * B + jj], acc);
+      a.Ynext[l * a.n + o + k] = Yc[l * B + k] - a.dt * acc;
     }
   }
 }
@@ -1167,15 +1202,20 @@ void set_gauss_nodes(const double* x, const double* w, int n) {
 void launch_ionic(const IonicArgs& a, cudaStream_t st) {
   const int g = (a.ncells + 7) / 8;
   if (a.ncells == 0) return;
+  const bool bcm = a.model == PDG_IONIC_BARRETO_CRESSMAN && a.n_comp == 4;
+#define PDG_ION(P)                                  \
+  (bcm ? ionic_kernel<P, 4><<<g, 256, 0, st>>>(a)   \
+       : ionic_kernel<P, 1><<<g, 256, 0, st>>>(a))
   switch (a.p) {
-    case 1: ionic_kernel<1><<<g, 256, 0, st>>>(a); break;
-    case 2: ionic_kernel<2><<<g, 256, 0, st>>>(a); break;
-    case 3: ionic_kernel<3><<<g, 256, 0, st>>>(a); break;
-    case 4: ionic_kernel<4><<<g, 256, 0, st>>>(a); break;
-    case 5: ionic_kernel<5><<<g, 256, 0, st>>>(a); break;
-    case 6: ionic_kernel<6><<<g, 256, 0, st>>>(a); break;
+    case 1: PDG_ION(1); break;
+    case 2: PDG_ION(2); break;
+    case 3: PDG_ION(3); break;
+    case 4: PDG_ION(4); break;
+    case 5: PDG_ION(5); break;
+    case 6: PDG_ION(6); break;
     default: throw CudaError("unsupported degree for the ionic kernel");
   }
+#undef PDG_ION
 }
 
 void launch_cell_means(int p, int ncells, int ngl, const double* bbox, const int* tri_ptr, const double* tri,

@@ -130,6 +130,8 @@ struct IonicArgs {
   long long n;
   double chi, dt, t_mid;
   double fhn[8];
+  double bc[PDG_BC_NPARAM];  // Barreto-Cressman parameters (bc_model.hpp)
+  double ubounds[2];         // admissible potential range of the model (diagnostic only)
   double stim_p[4];
   int* flags;         // bit0 out-of-range warning, bit1 non-finite state
 };

@@ -18,6 +18,7 @@
 
 #include "../host/problem.hpp"
 #include "kernels.cuh"
+#include "../host/bc_model.hpp"
 #include "sim.cuh"
 
 namespace pdg {
@@ -882,6 +883,14 @@ IonicArgs DeviceSim::ionic_args(bool has_prev) const {
   a.dt = c.dt;
   a.t_mid = t + 0.5 * c.dt;
   std::memcpy(a.fhn, c.fhn, sizeof a.fhn);
+  std::memcpy(a.bc, c.bc, sizeof a.bc);
+  if (c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN) {
+    a.ubounds[0] = bc::kUMin;
+    a.ubounds[1] = bc::kUMax;
+  } else {
+    a.ubounds[0] = c.fhn[5];
+    a.ubounds[1] = c.fhn[6];
+  }
   std::memcpy(a.stim_p, c.stim_params, sizeof a.stim_p);
   a.flags = d_ionflags;
   return a;
@@ -932,7 +941,10 @@ StepResult DeviceSim::step() {
     PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
   }
   PDG_CUDA(cudaStreamSynchronize(st));
-  if (ionflags & 2) throw SolverError("fhn: non-finite state in current evaluation");
+  if (ionflags & 2)
+    throw SolverError(c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN
+                          ? "barreto-cressman: non-finite state in current evaluation"
+                          : "fhn: non-finite state in current evaluation");
   if (ionflags & 1)
     std::fprintf(stderr,
                  "polydg: warning: membrane potential left the admissible range by more than 10x "

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstdio>
 #include "problem.hpp"
+#include "bc_model.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -145,6 +146,73 @@ double init_value(const pdg_config& c, Pt x) {
 
 }  // namespace
 
+int ionic_rest(const pdg_config& c, double& u, double* y) {
+  if (c.ionic_model == PDG_IONIC_FHN) {  // ionics.hpp:56-57
+    u = c.fhn[5];
+    y[0] = 0.0;
+    return 1;
+  }
+  if (c.ionic_model != PDG_IONIC_BARRETO_CRESSMAN) {
+    u = c.u_rest;
+    return 0;
+  }
+  // Barreto-Cressman rest: gates at their steady state n_inf(u), h_inf(u) and
+  // (u, [K]o, [Na]i) solving I = 0, d[K]o/dt = 0, d[Na]i/dt = 0 (Newton with a
+  // forward-difference Jacobian from u = -68 mV, [K]o = k_bath, [Na]i = Na_i0)
+  const double* P = c.bc;
+  auto full = [&](const double* z, double* yy) {
+    double an, bn, ah, bh;
+    bc::gating_rates(z[0], an, bn, ah, bh);
+    yy[0] = an / (an + bn);
+    yy[1] = ah / (ah + bh);
+    yy[2] = z[1];
+    yy[3] = z[2];
+  };
+  auto resid = [&](const double* z, double* f) {
+    double yy[4], m[4];
+    full(z, yy);
+    bc::rates(P, z[0], yy, m);
+    f[0] = bc::current(P, z[0], yy);
+    f[1] = m[2] * P[PDG_BC_TAU];
+    f[2] = m[3] * P[PDG_BC_TAU];
+  };
+  double z[3] = {-68.0, P[PDG_BC_K_BATH], P[PDG_BC_NA_I0]};
+  bool ok = false;
+  for (int it = 0; it < 100 && !ok; ++it) {
+    double f[3], J[3][3];
+    resid(z, f);
+    for (int j = 0; j < 3; ++j) {
+      double zz[3] = {z[0], z[1], z[2]}, g[3];
+      const double h = 1e-7 * std::max(1.0, std::fabs(z[j]));
+      zz[j] += h;
+      resid(zz, g);
+      for (int i = 0; i < 3; ++i) J[i][j] = (g[i] - f[i]) / h;
+    }
+    // Cramer's rule on the 3x3 system J dz = -f
+    auto det3 = [](double a[3][3]) {
+      return a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) - a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
+             a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+    };
+    const double d = det3(J);
+    if (!std::isfinite(d) || d == 0.0) break;
+    double step = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      double a[3][3];
+      for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) a[r][k] = k == j ? -f[r] : J[r][k];
+      const double dz = det3(a) / d;
+      z[j] += dz;
+      step = std::max(step, std::fabs(dz) / std::max(1.0, std::fabs(z[j])));
+    }
+    ok = step < 1e-14;
+  }
+  if (!ok || !(z[1] > 0.0) || !(z[2] > 0.0))
+    throw ConfigError("barreto-cressman: no resting state found for these parameters");
+  u = z[0];
+  full(z, y);
+  return 4;
+}
+
 void validate_config(const pdg_config& c) {
   if (!(c.dt > 0.0)) throw ConfigError("time.dt must be positive");
   if (!(c.T >= c.dt)) throw ConfigError("time.T must be at least one step");
@@ -174,9 +242,13 @@ void validate_config(const pdg_config& c) {
     if (!(c.fhn[6] > c.fhn[5])) throw ConfigError("fhn: u_max must exceed u_min");
     if (!(c.fhn[1] >= 0.0 && c.fhn[2] > 0.0)) throw ConfigError("fhn: invalid rate constants");
   } else if (c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN) {
-    throw ConfigError(
-        "ionic model 'barreto-cressman': the kinetics are not distributed with the reference; "
-        "parity is unpinned (SURVEY.md 8(c))");
+    for (int k = 0; k < PDG_BC_NPARAM; ++k)
+      if (!std::isfinite(c.bc[k]) || c.bc[k] < 0.0)
+        throw ConfigError("barreto-cressman: parameters must be finite and non-negative");
+    if (!(c.bc[PDG_BC_TAU] > 0.0 && c.bc[PDG_BC_RTF] > 0.0 && c.bc[PDG_BC_CL_I] > 0.0 &&
+          c.bc[PDG_BC_CL_O] > 0.0 && c.bc[PDG_BC_NA_I0] > 0.0 && c.bc[PDG_BC_K_I0] > 0.0 &&
+          c.bc[PDG_BC_NA_O0] > 0.0))
+      throw ConfigError("barreto-cressman: tau, RTF and the reference concentrations must be positive");
   } else if (c.ionic_model != PDG_IONIC_NONE) {
     throw ConfigError("unknown ionic model");
   }
@@ -262,7 +334,8 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   pr.bq = n_modes(pr.q);
   pr.has_precond = cfg.precond_kind != PDG_PRECOND_NONE;
   pr.two_level = cfg.precond_kind == PDG_PRECOND_TWO_LEVEL;
-  pr.n_comp = cfg.ionic_model == PDG_IONIC_FHN ? 1 : 0;
+  double u_model_rest = 0.0, y_rest[4] = {0.0, 0.0, 0.0, 0.0};
+  pr.n_comp = ionic_rest(cfg, u_model_rest, y_rest);
   const int b = pr.b, b2 = b * b;
 
   // ---- partitions (timestepper.cpp:92-102 + ext) ----
@@ -505,6 +578,18 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       double acc = 0.0;
       for (int jj = 0; jj < b; ++jj) acc += Mi[jj * b + ii] * rhs[jj];
       pr.U0[static_cast<std::size_t>(i) * b + ii] = acc;
+    }
+    // Y: l2 projection of the model's constant resting state (timestepper.cpp:116-123)
+    for (int l = 0; l < pr.n_comp; ++l) {
+      if (y_rest[l] == 0.0) continue;
+      std::vector<double> ry(b, 0.0);
+      for (int k = 0; k < nq; ++k)
+        for (int ii = 0; ii < b; ++ii) ry[ii] += rule.w[k] * y_rest[l] * val[k * b + ii];
+      for (int ii = 0; ii < b; ++ii) {
+        double acc = 0.0;
+        for (int jj = 0; jj < b; ++jj) acc += Mi[jj * b + ii] * ry[jj];
+        pr.Y0[static_cast<std::size_t>(l) * nloc * b + static_cast<std::size_t>(i) * b + ii] = acc;
+      }
     }
   }, 16);
   for (int i = 0; i < nloc; ++i) pr.tri_ptr[i + 1] = pr.tri_ptr[i] + static_cast<int>(tri_loc[i].size() / 6);

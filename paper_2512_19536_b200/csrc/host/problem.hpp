@@ -148,6 +148,8 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
 void halo_plan(const Problem& pr, std::vector<std::vector<int>>& send, std::vector<std::vector<int>>& recv);
 
 void validate_config(const pdg_config& cfg);
+// IonicModel::state_dim / resting_potential / resting_state (ionics.hpp:25-31)
+int ionic_rest(const pdg_config& cfg, double& u_rest, double* y_rest);
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
 // coarse factorisation + task packing; split out so a multi-rank run can sum
 // K0 partials before factorising.

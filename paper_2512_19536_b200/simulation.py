@@ -28,6 +28,9 @@ PRECOND = {"none": _lib.PRECOND_NONE, "block-jacobi": _lib.PRECOND_BLOCK_JACOBI,
            "two-level": _lib.PRECOND_TWO_LEVEL}
 IONIC = {"none": _lib.IONIC_NONE, "fhn": _lib.IONIC_FHN, "barreto-cressman": _lib.IONIC_BC}
 FHN_KEYS = ["a", "b", "c1", "c2", "d", "u_min", "u_max", "amp"]
+# Barreto-Cressman (ext; PDG_BC_* in include/polydg_b200.h)
+BC_KEYS = ["g_na", "g_k", "g_nal", "g_kl", "g_cll", "phi", "rho", "g_glia", "eps", "k_bath",
+           "gamma", "beta", "tau", "rtf", "cl_i", "cl_o", "na_i0", "k_i0", "na_o0", "amp"]
 
 
 @dataclass
@@ -94,10 +97,13 @@ class SimulationConfig:
         if self.ionic_model not in IONIC:
             raise _lib.PdgError(2, f"unknown ionic model '{self.ionic_model}'")
         c.ionic_model = IONIC[self.ionic_model]
+        bc = self.ionic_model == "barreto-cressman"
+        keys, arr = (BC_KEYS, c.bc) if bc else (FHN_KEYS, c.fhn)
         for k, v in self.ionic_params.items():
-            if k not in FHN_KEYS:
-                raise _lib.PdgError(2, f"unknown fhn parameter 'ionic.params.{k}'")
-            c.fhn[FHN_KEYS.index(k)] = v
+            if k not in keys:
+                name = "barreto-cressman" if bc else "fhn"
+                raise _lib.PdgError(2, f"unknown {name} parameter 'ionic.params.{k}'")
+            arr[keys.index(k)] = v
         kind = self.initial[0]
         kinds = {"disc": _lib.INIT_DISC, "constant": _lib.INIT_CONSTANT,
                  "cosine": _lib.INIT_COSINE, "bilinear": _lib.INIT_BILINEAR}
@@ -118,6 +124,15 @@ class SimulationConfig:
         c.h_ratio, c.q, c.subdomains, c.coarse_count = self.h_ratio, self.q, self.subdomains, self.coarse
         c.rank, c.world, c.device = self.rank, self.world, self.device
         return c
+
+
+def ionic_rest(config: "SimulationConfig"):
+    """IonicModel::state_dim / resting_potential / resting_state (ionics.hpp:25-31)
+    of config.ionic_model: (n_comp, u_rest, [y_rest...])."""
+    c = config.to_c()
+    nc, u, y = C.c_int(), C.c_double(), (C.c_double * 4)()
+    check(lib().pdg_ionic_rest(C.byref(c), C.byref(nc), C.byref(u), y))
+    return nc.value, u.value, list(y[:nc.value])
 
 
 @dataclass

@@ -64,6 +64,8 @@ def lib():
             "orc_pcg_dense": (i32, [i32, P(dbl), P(dbl), P(dbl), dbl, i32, P(dbl), P(dbl), P(OrcReport)]),
             "orc_condition_estimate": (i32, [P(dbl), P(dbl), i32, P(dbl)]),
             "orc_fhn": (i32, [P(dbl), dbl, dbl, P(dbl), P(dbl)]),
+            "orc_bc": (i32, [P(dbl), dbl, P(dbl), P(dbl), P(dbl)]),
+            "orc_ionic_rest": (i32, [P(PdgConfig), P(i32), P(dbl), P(dbl)]),
             "orc_polygon_quadrature": (i32, [P(dbl), i32, i32, P(dbl), P(dbl), i32]),
         }
         for k, (r, a) in sigs.items():
@@ -128,6 +130,23 @@ def fhn(u, w, params=None):
     return f.value, m.value
 
 
+def barreto_cressman(u, y, params=None):
+    """Pointwise (current, rates) of the oracle's Barreto-Cressman restatement."""
+    from paper_2512_19536_b200._lib import default_config
+    prm = np.array(params if params is not None else list(default_config().bc))
+    ya = np.ascontiguousarray(y, dtype=np.float64)
+    f, m = C.c_double(), np.zeros(4)
+    _check(lib().orc_bc(_d(prm), u, _d(ya), C.byref(f), _d(m)))
+    return f.value, m
+
+
+def ionic_rest(config):
+    cfg = config.to_c()
+    nc, u, y = C.c_int(), C.c_double(), np.zeros(4)
+    _check(lib().orc_ionic_rest(C.byref(cfg), C.byref(nc), C.byref(u), _d(y)))
+    return nc.value, u.value, list(y[:nc.value])
+
+
 def polygon_quadrature(poly, order):
     poly = np.ascontiguousarray(poly, dtype=np.float64)
     pts, w = np.zeros((4096, 2)), np.zeros(4096)
@@ -152,7 +171,7 @@ class OracleSim:
                                     reg.ctypes.data_as(C.POINTER(C.c_uint8)), _i(so), int(n_sub),
                                     None if co is None else _i(co), int(n_coarse), C.byref(self._h)))
         self.dimension = lib().orc_sim_dimension(self._h)
-        self.n_comp = 1 if config.ionic_model == "fhn" else 0
+        self.n_comp = {"fhn": 1, "barreto-cressman": 4}.get(config.ionic_model, 0)
         self.regions = reg
 
     def __del__(self):
@@ -217,9 +236,9 @@ class OracleSim:
     def ionic_terms(self, U, Y):
         U = np.ascontiguousarray(U, dtype=np.float64)
         Y = np.ascontiguousarray(Y, dtype=np.float64)
-        I, G = np.zeros(self.dimension), np.zeros(self.dimension)
+        I, G = np.zeros(self.dimension), np.zeros(max(self.n_comp, 1) * self.dimension)
         _check(lib().orc_sim_ionic_terms(self._h, _d(U), _d(Y), _d(I), _d(G)))
-        return I, G
+        return I, (G if self.n_comp <= 1 else G.reshape(self.n_comp, self.dimension))
 
     def cell_means(self, U):
         U = np.ascontiguousarray(U, dtype=np.float64)
