@@ -197,15 +197,29 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
 // double2 never straddles a column, so lane l always accumulates the fixed
 // row pair r = (2l + 64t) % B of column (2j)/B; lanes l = k (mod B/2) share a
 // pair and are summed by a shuffle tree in a fixed order (deterministic).
-template <int B>
+//
+// FUSE: the CG direction update p' = z + beta p (krylov.cpp:70-72) is folded
+// in: every gathered operand is formed as fma(beta, p, z), the row's own p' is
+// written to `pnew` and weighs the fused p'.q. x = p (previous direction) and
+// pnew are distinct buffers (alternated by the caller), so no CTA reads a
+// value another CTA overwrites. Same bits as pupdate_kernel + plain SpMV.
+template <int B, bool FUSE = false>
 __global__ void __launch_bounds__(256)
     spmv_warp_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                      const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop,
+                     const double* __restrict__ zv = nullptr, double* __restrict__ pnew = nullptr) {
   static_assert(B % 2 == 0, "even block size");
   constexpr int H = B * B / 2, NT = (H + 31) / 32, S = B / 2;
   pdl_wait();
   if (honor_stop && rc.S->stop) return;
+  const double beta = FUSE ? rc.S->beta : 0.0;
+  auto operand = [&](long long idx) {
+    if constexpr (FUSE)
+      return fma(beta, __ldg(x + idx), __ldg(zv + idx));
+    else
+      return __ldg(x + idx);
+  };
   __shared__ double ys[8][B];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int row = blockIdx.x * 8 + wl;
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(256)
         for (int t = 0; t < NT; ++t) {
           if (on[t]) {
             va[u][t] = __ldg(v2 + static_cast<long long>(k + u) * H + lane + 32 * t);
-            xa[u][t] = __ldg(x + static_cast<long long>(cu[u]) * B + cj[t]);
+            xa[u][t] = operand(static_cast<long long>(cu[u]) * B + cj[t]);
           }
         }
 #pragma unroll
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(256)
       for (int t = 0; t < NT; ++t) {
         if (on[t]) {
           const double2 va = __ldg(v2 + static_cast<long long>(k) * H + lane + 32 * t);
-          const double xa = __ldg(x + static_cast<long long>(ca) * B + cj[t]);
+          const double xa = operand(static_cast<long long>(ca) * B + cj[t]);
           acc[t].x = fma(va.x, xa, acc[t].x);
           acc[t].y = fma(va.y, xa, acc[t].y);
         }
@@ -291,7 +305,13 @@ __global__ void __launch_bounds__(256)
       const double yv = ys[wl][lane];
       const long long i = static_cast<long long>(row) * B + lane;
       y[i] = yv;
-      if (dotw) contrib = dotw[i] * yv;
+      if constexpr (FUSE) {
+        const double pv = operand(i);
+        pnew[i] = pv;
+        contrib = pv * yv;
+      } else if (dotw) {
+        contrib = dotw[i] * yv;
+      }
     }
   }
   if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
@@ -376,13 +396,15 @@ __global__ void update_kernel(long long n, double* __restrict__ x, double* __res
 }
 
 __global__ void pupdate_kernel(long long n, double* __restrict__ p, const double* __restrict__ z,
-                               const PcgScalars* S, int first) {
+                               PcgScalars* S, int first) {
   pdl_wait();
   if (!first && S->stop) return;
   const double beta = first ? 0.0 : S->beta;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride)
-    p[i] = first ? z[i] : z[i] + beta * p[i];
+    p[i] = first ? z[i] : fma(beta, p[i], z[i]);
+  // p = z also for a following direction-fused SpMV, which forms fma(beta, p, z)
+  if (first && blockIdx.x == 0 && threadIdx.x == 0) S->beta = 0.0;
 }
 
 template <int B, int BQ>
@@ -951,9 +973,11 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
   if (rows > 0 && warp_rows && (b == 6 || b == 10)) {
     const int g = (rows + 7) / 8;
     if (b == 6)
-      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
+                 nullptr, nullptr);
     else
-      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
+                 nullptr, nullptr);
     return;
   }
 #define L(B)                                                                                  \
@@ -964,6 +988,27 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
   }
   if (rows > 0) PDG_B_DISPATCH(b, L)
 #undef L
+}
+
+bool spmv_fuses_pupdate(int b, int rows) {
+  static const char* wenv = std::getenv("PDG_SPMV_WARP");
+  static const char* fenv = std::getenv("PDG_FUSE_P");
+  const bool warp_rows = wenv ? wenv[0] == '1' : rows <= 32768;
+  // opt-in: measured 1.7 % slower at config2 on B200 (the doubled operand gathers
+  // cost more than the pupdate launch they save, tried and reverted)
+  return (fenv ? fenv[0] == '1' : false) && rows > 0 && warp_rows && (b == 6 || b == 10);
+}
+
+void launch_spmv_pfused(int b, int rows, const int* ptr, const int* col, const double* val, const double* pold,
+                        const double* z, double* pnew, double* q, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
+  const int hs = honor_stop ? 1 : 0;
+  const int g = (rows + 7) / 8;
+  if (b == 6)
+    launch_pdl(spmv_warp_kernel<6, true>, g, 256, 0, st, rows, ptr, col, val, pold, q, nullptr, rc, hs, z, pnew);
+  else if (b == 10)
+    launch_pdl(spmv_warp_kernel<10, true>, g, 256, 0, st, rows, ptr, col, val, pold, q, nullptr, rc, hs, z, pnew);
+  else
+    throw CudaError("direction-fused SpMV needs the warp-row kernel (b = 6 or 10)");
 }
 
 void launch_residual(int b, int rows, const int* ptr, const int* col, const double* val,
@@ -995,7 +1040,7 @@ void launch_update(long long n, double* x, double* r, const double* p, const dou
   launch_pdl(update_kernel, vec_grid(n), kVecThreads, 0, st, n, x, r, p, q, rc);
 }
 
-void launch_pupdate(long long n, double* p, const double* z, const PcgScalars* S, bool first,
+void launch_pupdate(long long n, double* p, const double* z, PcgScalars* S, bool first,
                     cudaStream_t st) {
   launch_pdl(pupdate_kernel, vec_grid(n), kVecThreads, 0, st, n, p, z, S, first ? 1 : 0);
 }

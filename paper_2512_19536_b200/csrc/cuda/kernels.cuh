@@ -33,6 +33,12 @@ struct ReduceCtx {
 };
 
 // y = K x (+ grid dot with `dotw`), BSR rows [0, rows). Early-exits when S->stop.
+// q = K p' with the direction update p' = z + beta p folded into the gather
+// (single rank, warp-row SpMV); p' goes to pnew (!= pold), p'.q is reduced
+bool spmv_fuses_pupdate(int b, int rows);
+void launch_spmv_pfused(int b, int rows, const int* ptr, const int* col, const double* val, const double* pold,
+                        const double* z, double* pnew, double* q, ReduceCtx rc, bool honor_stop,
+                        cudaStream_t st);
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val,
                  const double* x, double* y, const double* dotw, ReduceCtx rc, bool honor_stop,
                  cudaStream_t st);
@@ -48,7 +54,7 @@ void launch_rhs(int b, int rows, const int* ptr, const int* col, const double* v
 void launch_update(long long n, double* x, double* r, const double* p, const double* q,
                    ReduceCtx rc, cudaStream_t st);
 // p = z + beta p  (beta from S) ; or p = z when first
-void launch_pupdate(long long n, double* p, const double* z, const PcgScalars* S, bool first,
+void launch_pupdate(long long n, double* p, const double* z, PcgScalars* S, bool first,
                     cudaStream_t st);
 // z += E y0 (coarse prolongation, optional) ; sum r.z -> kFinRzInit / kFinRz
 void launch_prolong_dot(int b, int bq, int ncells, const double* E, const int* cell_agg,
