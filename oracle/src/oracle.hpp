@@ -14,6 +14,11 @@
 // exact local solvers (RCM + envelope Cholesky instead of the product's
 // nested-dissection supernodal factor), PCG loop and a QL tridiagonal
 // eigensolver for the Lanczos estimate (the product uses bisection).
+//
+// Barreto-Cressman (ionic == 2): PARITY UNPINNED against the reference, which
+// ships no kinetics (ionics.cpp:52-57). bc_current / bc_rates / model_rest
+// restate Cressman et al. 2009 independently of the product's bc_model.hpp and
+// are cross-checked against a numpy restatement (tests/test_barreto_cressman.py).
 #pragma once
 
 #include <cmath>
