@@ -189,7 +189,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   const int nst = kSweepThreads - 32;
   const DevUnit& U = s.u;
   const DevTask& T = s.t;
-  if (t == 0) prefetch_panel(a, U);
+  if (t == 0 && a.prefetch) prefetch_panel(a, U);
   // every load below depends only on the (host-precomputed) descriptor, so
   // the whole staging is one round of independent loads
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
