@@ -229,6 +229,11 @@ pdg_status pdg_sim_sweep_live(pdg_sim* s, int64_t* launches, double* total_ms);
  * count (scripts/sweep_trace.py) */
 int pdg_sim_trace_sweep(pdg_sim* s, long long* out, int cap);
 
+/* BASELINE config-5 input: b_i = 2 (rng()>>11) 2^-53 - 1 drawn from
+ * std::mt19937_64(seed) in dof order, the reference's seeded uniform [-1, 1)
+ * pattern (proj/tests/acceptance.cpp:285-286) */
+void pdg_uniform_rhs(uint64_t seed, int64_t n, double* out);
+
 /* default_max_iterations (krylov.cpp:12-15) and condition_estimate (:85-103) */
 int pdg_default_max_iterations(int64_t n);
 int pdg_condition_estimate(const double* alphas, const double* betas, int m, double* kappa);

@@ -4,6 +4,7 @@
 // here so the oracle does not compile against product headers.
 #include <cstring>
 #include <memory>
+#include <random>
 #include <string>
 
 #include "oracle.hpp"
@@ -129,6 +130,61 @@ extern "C" {
 const char* orc_last_error() { return g_err.c_str(); }
 int orc_config_size() { return static_cast<int>(sizeof(orc_config)); }
 int orc_threads() { return orc::thread_count(); }
+void orc_set_parallel(int on) { orc::set_parallel_ops(on != 0); }
+void orc_set_lean(int level) { orc::set_lean(level); }
+
+// SimulationConfig defaults (timestepper.hpp:21-80, ionics.hpp:42-51), so the
+// oracle can be configured without loading the product library
+void orc_config_default(orc_config* c) {
+  std::memset(c, 0, sizeof *c);
+  const orc::Config d;
+  c->mesh_cells = 512;
+  c->mesh_seed = 42;
+  c->mesh_lloyd = 20;
+  c->domain[2] = c->domain[3] = 1.0;
+  c->split_y = 0.5;
+  c->degree = d.degree;
+  c->eta0 = d.eta0;
+  c->chi_m = d.chi_m;
+  c->C_m = d.C_m;
+  c->dt = d.dt;
+  c->T = d.T;
+  c->sigma_grey_l = d.sgl;
+  c->sigma_grey_n = d.sgn;
+  c->sigma_white_l = d.swl;
+  c->sigma_white_n = d.swn;
+  c->fiber_grey[1] = c->fiber_white[1] = 1.0;
+  c->fiber_seed = 42;
+  c->ionic_model = 1;
+  std::memcpy(c->fhn, d.fhn, sizeof d.fhn);
+  std::memcpy(c->bc, d.bc, sizeof d.bc);
+  c->init_kind = 0;
+  c->u_rest = d.u_rest;
+  c->u_patch = d.u_patch;
+  c->omega0[0] = d.omega0.x;
+  c->omega0[1] = d.omega0.y;
+  c->omega0_r2 = d.omega0_r2;
+  c->tol = d.tol;
+  c->warm_start = 1;
+  c->precond_kind = 2;
+  c->h_ratio = 2;
+  c->world = 1;
+}
+
+// b_i = 2 (rng()>>11) 2^-53 - 1 with mt19937_64(seed) (acceptance.cpp:285-286)
+void orc_uniform_rhs(uint64_t seed, int64_t n, double* out) {
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
+}
+
+// stored blocks of the local factors (sum over subdomains) and of the coarse factor
+int64_t orc_sim_factor_blocks(void* h, int which) {
+  const auto& s = *static_cast<orc::Simulation*>(h);
+  if (which == 1) return s.S.coarse.blocks();
+  int64_t t = 0;
+  for (const auto& f : s.S.local) t += f.blocks();
+  return t;
+}
 
 int orc_sim_create(const orc_config* cfg, const double* verts, int nv, const int* off, const int* idx,
                    int nc, const uint8_t* regions, const int* sub_owner, int n_sub,

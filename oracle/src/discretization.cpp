@@ -43,13 +43,62 @@ void parallel_for(std::size_t n, const std::function<void(std::size_t)>& fn) {
 }
 
 // ---------------- CSR ----------------
+// Row-parallel kernels give the same bits as the serial loops (every row is
+// computed by one thread in the serial order). Csr::apply stays single-threaded
+// like Eigen's SpMV unless parallel operators are switched on (large parity
+// runs; the timed CPU baseline keeps the reference's threading).
+namespace {
+bool g_parallel_ops = false;
+int g_lean = 0;  // 1: drop M and A after K / K_rhs; 2: also skip K_rhs (single solves)
+
+void parallel_rows(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+  const int workers = thread_count();
+  if (workers <= 1 || n < 64) {
+    fn(0, n);
+    return;
+  }
+  const int64_t parts = std::min<int64_t>(n, static_cast<int64_t>(workers) * 8);
+  const int64_t chunk = (n + parts - 1) / parts;
+  parallel_for(static_cast<std::size_t>(parts), [&](std::size_t w) {
+    const int64_t b = static_cast<int64_t>(w) * chunk, e = std::min(n, b + chunk);
+    if (b < e) fn(b, e);
+  });
+}
+
+// builds ptr from per-row counts, then fills rows in parallel
+template <class Count, class Fill>
+Csr build_rows(int64_t rows, int64_t cols, Count count, Fill fill) {
+  Csr C;
+  C.rows = rows;
+  C.cols = cols;
+  C.ptr.assign(rows + 1, 0);
+  parallel_rows(rows, [&](int64_t b, int64_t e) {
+    for (int64_t r = b; r < e; ++r) C.ptr[r + 1] = count(r);
+  });
+  for (int64_t r = 0; r < rows; ++r) C.ptr[r + 1] += C.ptr[r];
+  C.idx.resize(C.ptr[rows]);
+  C.val.resize(C.ptr[rows]);
+  parallel_rows(rows, [&](int64_t b, int64_t e) {
+    for (int64_t r = b; r < e; ++r) fill(r, &C.idx[C.ptr[r]], &C.val[C.ptr[r]]);
+  });
+  return C;
+}
+}  // namespace
+
+void set_parallel_ops(bool on) { g_parallel_ops = on; }
+void set_lean(int level) { g_lean = level; }
+
 void Csr::apply(const Vec& x, Vec& y) const {
   y.assign(rows, 0.0);
-  for (int64_t r = 0; r < rows; ++r) {
-    double s = 0.0;
-    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) s += val[k] * x[idx[k]];
-    y[r] = s;
-  }
+  auto body = [&](int64_t b, int64_t e) {
+    for (int64_t r = b; r < e; ++r) {
+      double s = 0.0;
+      for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) s += val[k] * x[idx[k]];
+      y[r] = s;
+    }
+  };
+  if (g_parallel_ops) parallel_rows(rows, body);
+  else body(0, rows);
 }
 
 double Csr::at(int64_t r, int64_t c) const {
@@ -60,30 +109,41 @@ double Csr::at(int64_t r, int64_t c) const {
 
 Csr from_triplets(int64_t rows, int64_t cols, std::vector<Triplet>& t) {
   // stable order by (row, col); duplicates summed in insertion order
-  std::vector<int64_t> order(t.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    return t[a].r < t[b].r || (t[a].r == t[b].r && t[a].c < t[b].c);
-  });
-  Csr A;
-  A.rows = rows;
-  A.cols = cols;
-  A.ptr.assign(rows + 1, 0);
-  int64_t pr = -1, pc = -1;
-  for (int64_t o : order) {
-    const Triplet& e = t[o];
-    if (e.r == pr && e.c == pc) {
-      A.val.back() += e.v;
-    } else {
-      A.idx.push_back(e.c);
-      A.val.push_back(e.v);
-      ++A.ptr[e.r + 1];
-      pr = e.r;
-      pc = e.c;
+  // (Eigen's setFromTriplets): bucket by row keeping insertion order, then a
+  // stable sort by column inside each row
+  std::vector<int64_t> start(rows + 1, 0);
+  for (const Triplet& e : t) ++start[e.r + 1];
+  for (int64_t r = 0; r < rows; ++r) start[r + 1] += start[r];
+  std::vector<int64_t> order(t.size()), fillp(start.begin(), start.end() - 1);
+  for (int64_t i = 0; i < static_cast<int64_t>(t.size()); ++i) order[fillp[t[i].r]++] = i;
+  fillp.clear();
+  fillp.shrink_to_fit();
+  std::vector<int64_t> rowlen(rows, 0);
+  parallel_rows(rows, [&](int64_t b, int64_t e) {
+    for (int64_t r = b; r < e; ++r) {
+      auto* o = &order[start[r]];
+      const int64_t m = start[r + 1] - start[r];
+      std::stable_sort(o, o + m, [&](int64_t a, int64_t c) { return t[a].c < t[c].c; });
+      int64_t distinct = 0;
+      for (int64_t i = 0; i < m; ++i)
+        if (i == 0 || t[o[i]].c != t[o[i - 1]].c) ++distinct;
+      rowlen[r] = distinct;
     }
-  }
-  for (int64_t r = 0; r < rows; ++r) A.ptr[r + 1] += A.ptr[r];
-  return A;
+  });
+  return build_rows(rows, cols, [&](int64_t r) { return rowlen[r]; },
+                    [&](int64_t r, int64_t* idx, double* val) {
+                      int64_t w = -1;
+                      for (int64_t i = start[r]; i < start[r + 1]; ++i) {
+                        const Triplet& e = t[order[i]];
+                        if (w >= 0 && idx[w] == e.c) {
+                          val[w] += e.v;
+                        } else {
+                          ++w;
+                          idx[w] = e.c;
+                          val[w] = e.v;
+                        }
+                      }
+                    });
 }
 
 Csr transpose(const Csr& A) {
@@ -95,60 +155,61 @@ Csr transpose(const Csr& A) {
 }
 
 Csr multiply(const Csr& A, const Csr& B) {
-  Csr C;
-  C.rows = A.rows;
-  C.cols = B.cols;
-  C.ptr.assign(A.rows + 1, 0);
-  std::vector<double> acc(B.cols, 0.0);
-  std::vector<int64_t> mark(B.cols, -1), used;
-  for (int64_t r = 0; r < A.rows; ++r) {
-    used.clear();
-    for (int64_t k = A.ptr[r]; k < A.ptr[r + 1]; ++k) {
-      const int64_t j = A.idx[k];
-      for (int64_t l = B.ptr[j]; l < B.ptr[j + 1]; ++l) {
-        const int64_t c = B.idx[l];
-        if (mark[c] != r) {
-          mark[c] = r;
-          acc[c] = 0.0;
-          used.push_back(c);
+  // Gustavson row by row; each row accumulates in A's then B's entry order
+  std::vector<std::vector<int64_t>> rows_cols(A.rows);
+  std::vector<std::vector<double>> rows_vals(A.rows);
+  parallel_rows(A.rows, [&](int64_t b, int64_t e) {
+    std::vector<double> a(B.cols, 0.0);
+    std::vector<int64_t> mk(B.cols, -1);
+    std::vector<int64_t> used;
+    for (int64_t r = b; r < e; ++r) {
+      used.clear();
+      for (int64_t k = A.ptr[r]; k < A.ptr[r + 1]; ++k) {
+        const int64_t j = A.idx[k];
+        for (int64_t l = B.ptr[j]; l < B.ptr[j + 1]; ++l) {
+          const int64_t c = B.idx[l];
+          if (mk[c] != r) {
+            mk[c] = r;
+            a[c] = 0.0;
+            used.push_back(c);
+          }
+          a[c] += A.val[k] * B.val[l];
         }
-        acc[c] += A.val[k] * B.val[l];
       }
+      std::sort(used.begin(), used.end());
+      rows_cols[r] = used;
+      auto& v = rows_vals[r];
+      v.resize(used.size());
+      for (std::size_t i = 0; i < used.size(); ++i) v[i] = a[used[i]];
     }
-    std::sort(used.begin(), used.end());
-    for (int64_t c : used) {
-      C.idx.push_back(c);
-      C.val.push_back(acc[c]);
-    }
-    C.ptr[r + 1] = static_cast<int64_t>(C.idx.size());
-  }
-  return C;
+  });
+  return build_rows(A.rows, B.cols, [&](int64_t r) { return static_cast<int64_t>(rows_cols[r].size()); },
+                    [&](int64_t r, int64_t* idx, double* val) {
+                      std::copy(rows_cols[r].begin(), rows_cols[r].end(), idx);
+                      std::copy(rows_vals[r].begin(), rows_vals[r].end(), val);
+                    });
 }
 
 Csr combine(const Csr& A, double a, const Csr& B, double b) {
-  Csr C;
-  C.rows = A.rows;
-  C.cols = A.cols;
-  C.ptr.assign(A.rows + 1, 0);
-  for (int64_t r = 0; r < A.rows; ++r) {
-    int64_t i = A.ptr[r], j = B.ptr[r];
+  auto merge = [&](int64_t r, int64_t* idx, double* val) {
+    int64_t i = A.ptr[r], j = B.ptr[r], w = 0;
     while (i < A.ptr[r + 1] || j < B.ptr[r + 1]) {
       const int64_t ca = i < A.ptr[r + 1] ? A.idx[i] : INT64_MAX;
       const int64_t cb = j < B.ptr[r + 1] ? B.idx[j] : INT64_MAX;
-      if (ca == cb) {
-        C.idx.push_back(ca);
-        C.val.push_back(a * A.val[i++] + b * B.val[j++]);
-      } else if (ca < cb) {
-        C.idx.push_back(ca);
-        C.val.push_back(a * A.val[i++]);
-      } else {
-        C.idx.push_back(cb);
-        C.val.push_back(b * B.val[j++]);
+      const int64_t c = std::min(ca, cb);
+      if (idx) {
+        idx[w] = c;
+        val[w] = ca == cb ? a * A.val[i] + b * B.val[j] : (ca < cb ? a * A.val[i] : b * B.val[j]);
       }
+      if (ca == cb) ++i, ++j;
+      else if (ca < cb) ++i;
+      else ++j;
+      ++w;
     }
-    C.ptr[r + 1] = static_cast<int64_t>(C.idx.size());
-  }
-  return C;
+    return w;
+  };
+  return build_rows(A.rows, A.cols, [&](int64_t r) { return merge(r, nullptr, nullptr); },
+                    [&](int64_t r, int64_t* idx, double* val) { merge(r, idx, val); });
 }
 
 // ---------------- quadrature ----------------
@@ -385,15 +446,6 @@ Tensor tensor(double sl, double sn, P2 f) {
   const double nx = -f.y / len, ny = f.x / len;
   return {sl + (sn - sl) * nx * nx, (sn - sl) * nx * ny, (sn - sl) * ny * nx, sl + (sn - sl) * ny * ny};
 }
-void push_diag(std::vector<Triplet>& t, int64_t r0, const Vec& L, int n) {  // upper triangle mirrored
-  for (int i = 0; i < n; ++i) {
-    t.push_back({r0 + i, r0 + i, L[i * n + i]});
-    for (int j = i + 1; j < n; ++j) {
-      t.push_back({r0 + i, r0 + j, L[i * n + j]});
-      t.push_back({r0 + j, r0 + i, L[i * n + j]});
-    }
-  }
-}
 void dense_llt(int n, const double* a, double* L) {  // row-major
   std::fill(L, L + n * n, 0.0);
   for (int j = 0; j < n; ++j) {
@@ -448,75 +500,159 @@ void Discretization::build(const MeshView& m, const Config& c) {
       sig[e] = tensor(grey ? c.sgl : c.swl, grey ? c.sgn : c.swn, {std::cos(th), std::sin(th)});
     }
   }
-  std::vector<Triplet> tm, ta;
-  Vec val, gx, gy;
-  Mchol.assign(nc, Vec());
-  for (int e = 0; e < nc; ++e) {
-    const Rule r = polygon_rule(m.cell(e), order);
-    eval_basis(m.bbox[e], p, r.pts, val, &gx, &gy);
-    Vec lm(nloc * nloc, 0.0), la(nloc * nloc, 0.0);
-    for (std::size_t q = 0; q < r.w.size(); ++q) {
-      const double* v = &val[q * nloc];
-      for (int i = 0; i < nloc; ++i)
-        for (int j = i; j < nloc; ++j) lm[i * nloc + j] += r.w[q] * v[i] * v[j];
-    }
-    const Tensor& s = sig[e];
-    for (std::size_t q = 0; q < r.w.size(); ++q) {
-      const double* X = &gx[q * nloc];
-      const double* Y = &gy[q * nloc];
-      for (int j = 0; j < nloc; ++j) {
-        const double sx = s.a00 * X[j] + s.a01 * Y[j], sy = s.a10 * X[j] + s.a11 * Y[j];
-        for (int i = 0; i <= j; ++i) la[i * nloc + j] += r.w[q] * (X[i] * sx + Y[i] * sy);
-      }
-    }
-    push_diag(tm, static_cast<int64_t>(e) * nloc, lm, nloc);
-    push_diag(ta, static_cast<int64_t>(e) * nloc, la, nloc);
-    Vec full(nloc * nloc);
-    for (int i = 0; i < nloc; ++i)
-      for (int j = 0; j < nloc; ++j) full[i * nloc + j] = lm[std::min(i, j) * nloc + std::max(i, j)];
-    Mchol[e].resize(nloc * nloc);
-    dense_llt(nloc, full.data(), Mchol[e].data());
-  }
-  Vec vk, vl, gxk, gyk, gxl, gyl;
+  // Direct CSR assembly with the SAME per-entry summation order as
+  // setFromTriplets over the reference's triplet stream (assembly.cpp:52-84):
+  // all volume blocks first (cell order), then per interior face, in face
+  // order, the K-K block, the L-L block and the K-L / L-K pair. Local blocks
+  // are computed in parallel; accumulation into each entry follows the stream.
+  const int nl = nloc, nl2 = nl * nl;
+  std::vector<std::vector<int>> nbr(nc);
+  for (int e = 0; e < nc; ++e) nbr[e].push_back(e);
   for (const Face& f : m.faces) {
-    const int K = f.in, L = f.out;
-    const double hk = m.diam[K], hl = m.diam[L];
-    const double eta = c.eta0 * (0.5 * (snorm[K] + snorm[L])) * p * p / (2.0 * hk * hl / (hk + hl));
-    const Rule r = segment_rule(f.a, f.b, order);
-    eval_basis(m.bbox[K], p, r.pts, vk, &gxk, &gyk);
-    eval_basis(m.bbox[L], p, r.pts, vl, &gxl, &gyl);
-    Vec kk(nloc * nloc, 0.0), ll(nloc * nloc, 0.0), kl(nloc * nloc, 0.0), ak(nloc), al(nloc);
-    const Tensor &sk = sig[K], &sl = sig[L];
-    for (std::size_t q = 0; q < r.w.size(); ++q) {
-      const double w = r.w[q];
-      const double *VK = &vk[q * nloc], *VL = &vl[q * nloc];
-      for (int mm = 0; mm < nloc; ++mm) {
-        const double xk = gxk[q * nloc + mm], yk = gyk[q * nloc + mm];
-        const double xl = gxl[q * nloc + mm], yl = gyl[q * nloc + mm];
-        ak[mm] = (sk.a00 * xk + sk.a01 * yk) * f.n.x + (sk.a10 * xk + sk.a11 * yk) * f.n.y;
-        al[mm] = (sl.a00 * xl + sl.a01 * yl) * f.n.x + (sl.a10 * xl + sl.a11 * yl) * f.n.y;
-      }
-      for (int i = 0; i < nloc; ++i) {
-        for (int j = i; j < nloc; ++j) {
-          kk[i * nloc + j] += w * (-0.5 * (ak[j] * VK[i] + ak[i] * VK[j]) + eta * VK[j] * VK[i]);
-          ll[i * nloc + j] += w * (0.5 * (al[j] * VL[i] + al[i] * VL[j]) + eta * VL[j] * VL[i]);
-        }
-        for (int j = 0; j < nloc; ++j)
-          kl[i * nloc + j] += w * (-0.5 * al[j] * VK[i] + 0.5 * ak[i] * VL[j] - eta * VL[j] * VK[i]);
+    nbr[f.in].push_back(f.out);
+    nbr[f.out].push_back(f.in);
+  }
+  for (auto& v : nbr) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  auto block_pattern = [&](bool diag_only) {
+    return build_rows(n, n, [&](int64_t r) { return static_cast<int64_t>(diag_only ? 1 : nbr[r / nl].size()) * nl; },
+                      [&](int64_t r, int64_t* idx, double* val) {
+                        const int e = static_cast<int>(r / nl);
+                        int w = 0;
+                        for (int cb : nbr[e]) {
+                          if (diag_only && cb != e) continue;
+                          for (int j = 0; j < nl; ++j, ++w) {
+                            idx[w] = static_cast<int64_t>(cb) * nl + j;
+                            val[w] = 0.0;
+                          }
+                        }
+                      });
+  };
+  M = block_pattern(true);
+  A = block_pattern(false);
+  auto slot = [&](int e, int cb) {  // block position of column block cb in row block e
+    return static_cast<int64_t>(std::lower_bound(nbr[e].begin(), nbr[e].end(), cb) - nbr[e].begin()) * nl;
+  };
+  auto add_diag = [&](Csr& X, int e, int64_t pos, const double* Lu) {  // upper triangle mirrored
+    const int64_t r0 = static_cast<int64_t>(e) * nl;
+    for (int i = 0; i < nl; ++i) {
+      X.val[X.ptr[r0 + i] + pos + i] += Lu[i * nl + i];
+      for (int j = i + 1; j < nl; ++j) {
+        X.val[X.ptr[r0 + i] + pos + j] += Lu[i * nl + j];
+        X.val[X.ptr[r0 + j] + pos + i] += Lu[i * nl + j];
       }
     }
-    push_diag(ta, static_cast<int64_t>(K) * nloc, kk, nloc);
-    push_diag(ta, static_cast<int64_t>(L) * nloc, ll, nloc);
-    for (int i = 0; i < nloc; ++i)
-      for (int j = 0; j < nloc; ++j) {
-        ta.push_back({static_cast<int64_t>(K) * nloc + i, static_cast<int64_t>(L) * nloc + j, kl[i * nloc + j]});
-        ta.push_back({static_cast<int64_t>(L) * nloc + j, static_cast<int64_t>(K) * nloc + i, kl[i * nloc + j]});
+  };
+  Mchol.assign(nc, Vec());
+  parallel_rows(nc, [&](int64_t e0, int64_t e1) {
+    Vec val, gx, gy, lm(nl2), la(nl2), full(nl2);
+    for (int64_t ee = e0; ee < e1; ++ee) {
+      const int e = static_cast<int>(ee);
+      const Rule r = polygon_rule(m.cell(e), order);
+      eval_basis(m.bbox[e], p, r.pts, val, &gx, &gy);
+      std::fill(lm.begin(), lm.end(), 0.0);
+      std::fill(la.begin(), la.end(), 0.0);
+      for (std::size_t q = 0; q < r.w.size(); ++q) {
+        const double* v = &val[q * nloc];
+        for (int i = 0; i < nloc; ++i)
+          for (int j = i; j < nloc; ++j) lm[i * nloc + j] += r.w[q] * v[i] * v[j];
       }
+      const Tensor& s = sig[e];
+      for (std::size_t q = 0; q < r.w.size(); ++q) {
+        const double* X = &gx[q * nloc];
+        const double* Y = &gy[q * nloc];
+        for (int j = 0; j < nloc; ++j) {
+          const double sx = s.a00 * X[j] + s.a01 * Y[j], sy = s.a10 * X[j] + s.a11 * Y[j];
+          for (int i = 0; i <= j; ++i) la[i * nloc + j] += r.w[q] * (X[i] * sx + Y[i] * sy);
+        }
+      }
+      // volume blocks are the first contribution to their entries and touch
+      // only this cell's rows: safe to add from any thread
+      add_diag(M, e, 0, lm.data());
+      add_diag(A, e, slot(e, e), la.data());
+      for (int i = 0; i < nloc; ++i)
+        for (int j = 0; j < nloc; ++j) full[i * nloc + j] = lm[std::min(i, j) * nloc + std::max(i, j)];
+      Mchol[e].resize(nl2);
+      dense_llt(nloc, full.data(), Mchol[e].data());
+    }
+  });
+  const int64_t nf = static_cast<int64_t>(m.faces.size());
+  const int64_t chunk = 1 << 17;
+  Vec buf(static_cast<std::size_t>(std::min(nf, chunk)) * 3 * nl2);
+  for (int64_t f0 = 0; f0 < nf; f0 += chunk) {
+    const int64_t f1 = std::min(nf, f0 + chunk);
+    parallel_rows(f1 - f0, [&](int64_t b0, int64_t b1) {
+      Vec vk, vl, gxk, gyk, gxl, gyl, ak(nl), al(nl);
+      for (int64_t fi = f0 + b0; fi < f0 + b1; ++fi) {
+        const Face& f = m.faces[fi];
+        const int K = f.in, L = f.out;
+        const double hk = m.diam[K], hl = m.diam[L];
+        const double eta = c.eta0 * (0.5 * (snorm[K] + snorm[L])) * p * p / (2.0 * hk * hl / (hk + hl));
+        const Rule r = segment_rule(f.a, f.b, order);
+        eval_basis(m.bbox[K], p, r.pts, vk, &gxk, &gyk);
+        eval_basis(m.bbox[L], p, r.pts, vl, &gxl, &gyl);
+        double* kk = &buf[static_cast<std::size_t>(fi - f0) * 3 * nl2];
+        double* ll = kk + nl2;
+        double* kl = ll + nl2;
+        std::fill(kk, kk + 3 * nl2, 0.0);
+        const Tensor &sk = sig[K], &sl = sig[L];
+        for (std::size_t q = 0; q < r.w.size(); ++q) {
+          const double w = r.w[q];
+          const double *VK = &vk[q * nloc], *VL = &vl[q * nloc];
+          for (int mm = 0; mm < nloc; ++mm) {
+            const double xk = gxk[q * nloc + mm], yk = gyk[q * nloc + mm];
+            const double xl = gxl[q * nloc + mm], yl = gyl[q * nloc + mm];
+            ak[mm] = (sk.a00 * xk + sk.a01 * yk) * f.n.x + (sk.a10 * xk + sk.a11 * yk) * f.n.y;
+            al[mm] = (sl.a00 * xl + sl.a01 * yl) * f.n.x + (sl.a10 * xl + sl.a11 * yl) * f.n.y;
+          }
+          for (int i = 0; i < nloc; ++i) {
+            for (int j = i; j < nloc; ++j) {
+              kk[i * nloc + j] += w * (-0.5 * (ak[j] * VK[i] + ak[i] * VK[j]) + eta * VK[j] * VK[i]);
+              ll[i * nloc + j] += w * (0.5 * (al[j] * VL[i] + al[i] * VL[j]) + eta * VL[j] * VL[i]);
+            }
+            for (int j = 0; j < nloc; ++j)
+              kl[i * nloc + j] += w * (-0.5 * al[j] * VK[i] + 0.5 * ak[i] * VL[j] - eta * VL[j] * VK[i]);
+          }
+        }
+      }
+    });
+    // accumulate in stream order: every thread owns a range of row cells and
+    // walks the faces one after the other, adding only into its own rows, so
+    // each entry still receives its contributions in face order
+    const int parts = std::max(1, thread_count());
+    parallel_for(static_cast<std::size_t>(parts), [&](std::size_t w) {
+      const int lo = static_cast<int>(static_cast<int64_t>(nc) * w / parts);
+      const int hi = static_cast<int>(static_cast<int64_t>(nc) * (w + 1) / parts);
+      auto mine = [&](int e) { return e >= lo && e < hi; };
+      for (int64_t fi = f0; fi < f1; ++fi) {
+        const Face& f = m.faces[fi];
+        const int K = f.in, L = f.out;
+        if (!mine(K) && !mine(L)) continue;
+        const double* kk = &buf[static_cast<std::size_t>(fi - f0) * 3 * nl2];
+        const double* kl = kk + 2 * nl2;
+        if (mine(K)) {
+          add_diag(A, K, slot(K, K), kk);
+          const int64_t pKL = slot(K, L), rK = static_cast<int64_t>(K) * nl;
+          for (int i = 0; i < nl; ++i)
+            for (int j = 0; j < nl; ++j) A.val[A.ptr[rK + i] + pKL + j] += kl[i * nl + j];
+        }
+        if (mine(L)) {
+          add_diag(A, L, slot(L, L), kk + nl2);
+          const int64_t pLK = slot(L, K), rL = static_cast<int64_t>(L) * nl;
+          for (int i = 0; i < nl; ++i)
+            for (int j = 0; j < nl; ++j) A.val[A.ptr[rL + j] + pLK + i] += kl[i * nl + j];
+        }
+      }
+    });
   }
-  M = from_triplets(n, n, tm);
-  A = from_triplets(n, n, ta);
   K = combine(M, c.C_m * c.chi_m, A, 0.5 * c.dt);
-  Krhs = combine(M, c.chi_m * c.C_m, A, -0.5 * c.dt);
+  if (g_lean < 2) Krhs = combine(M, c.chi_m * c.C_m, A, -0.5 * c.dt);
+  if (g_lean >= 1) {  // large parity runs: only K (and K_rhs) are needed after setup
+    A = Csr();
+    M = Csr();
+  }
 }
 
 Vec Discretization::mass_solve(const Vec& rhs) const {

@@ -11,7 +11,7 @@
 //
 // Deliberately independent of the product code: its own quadrature, basis,
 // assembly (triplets summed in insertion order like Eigen's setFromTriplets),
-// exact local solvers (RCM + envelope Cholesky instead of the product's
+// exact local solvers (minimum-degree block Cholesky instead of the product's
 // nested-dissection supernodal factor), PCG loop and a QL tridiagonal
 // eigensolver for the Lanczos estimate (the product uses bisection).
 //
@@ -56,6 +56,13 @@ using Vec = std::vector<double>;
 // ---- threading: the reference's fork/join parallel_for (parallel.cpp:23-41) ----
 int thread_count();
 void parallel_for(std::size_t n, const std::function<void(std::size_t)>& fn);
+
+// ---- operator threading and memory (large parity runs) ----
+// set_parallel_ops(true): row-parallel Csr::apply (same bits; default off =
+// single-threaded like Eigen's SpMV). set_lean(1): Discretization drops M and
+// A after building K and K_rhs; set_lean(2): K only (one-solve workloads).
+void set_parallel_ops(bool on);
+void set_lean(int level);
 
 // ---- scalar CSR matrix ----
 struct Csr {
@@ -178,25 +185,26 @@ Vec pcg(const Operator& K, const Vec& b, const Operator* P, double tol, int maxi
         PcgReport& rep);
 bool condition_estimate(const Vec& alpha, const Vec& beta, double* kappa);
 
-// ---- exact local solver: RCM + envelope Cholesky ----
-struct Envelope {
-  int n = 0;
-  std::vector<int> perm;      // new -> old
-  std::vector<int> first;     // first column of row i (new numbering)
-  std::vector<int64_t> start; // offset of row i
-  Vec L;
-  void factor(const Csr& A);  // throws SolverError
-  void solve(Vec& x) const;   // in place, original numbering
+// ---- exact local / coarse solver: minimum-degree block Cholesky (blockchol.cpp) ----
+struct BlockChol {
+  int nb = 0, b = 1;
+  std::vector<int> perm;         // new -> old block
+  std::vector<int64_t> colptr;   // block column j: rows rowidx[colptr[j]..colptr[j+1]), first = j
+  std::vector<int> rowidx;
+  Vec L;                         // b x b row-major blocks, aligned with rowidx
+  void factor(const Csr& A, int block);  // throws SolverError
+  void solve(Vec& x) const;              // in place, original numbering
+  int64_t blocks() const { return colptr.empty() ? 0 : colptr.back(); }
 };
 
 // ---- Schwarz (schwarz.cpp) ----
 struct Schwarz {
   int64_t n = 0;
   std::vector<std::vector<int64_t>> dofs;
-  std::vector<Envelope> local;
+  std::vector<BlockChol> local;
   bool two_level = false;
   Csr E, Et, K0;
-  Envelope coarse;
+  BlockChol coarse;
   void build(const Csr& K, const Discretization& D, const std::vector<int>& sub_owner, int n_sub,
              const std::vector<int>& coarse_owner, int n_coarse, int q);
   void apply(const Vec& r, Vec& z) const;

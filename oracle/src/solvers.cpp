@@ -3,9 +3,10 @@
 // (coarse embedding, two-level additive Schwarz) and timestepper.cpp:36-200
 // (Simulation::step) of /root/reference/proj/src.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <numeric>
-#include <queue>
 
 #include "oracle.hpp"
 
@@ -135,102 +136,6 @@ bool condition_estimate(const Vec& alpha, const Vec& beta, double* kappa) {
   return true;
 }
 
-// ---------------- RCM + envelope Cholesky ----------------
-void Envelope::factor(const Csr& A) {
-  n = static_cast<int>(A.rows);
-  std::vector<int> deg(n);
-  for (int i = 0; i < n; ++i) deg[i] = static_cast<int>(A.ptr[i + 1] - A.ptr[i]);
-  std::vector<int> order;
-  order.reserve(n);
-  std::vector<char> seen(n, 0);
-  auto bfs = [&](int s, std::vector<int>& out) {
-    std::vector<int> lvl(n, -1);
-    std::queue<int> qu;
-    qu.push(s);
-    lvl[s] = 0;
-    out.clear();
-    while (!qu.empty()) {
-      const int v = qu.front();
-      qu.pop();
-      out.push_back(v);
-      std::vector<int> nb;
-      for (int64_t k = A.ptr[v]; k < A.ptr[v + 1]; ++k)
-        if (lvl[A.idx[k]] < 0 && !seen[A.idx[k]]) nb.push_back(static_cast<int>(A.idx[k]));
-      std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b] || (deg[a] == deg[b] && a < b); });
-      for (int u : nb)
-        if (lvl[u] < 0) {
-          lvl[u] = lvl[v] + 1;
-          qu.push(u);
-        }
-    }
-  };
-  std::vector<int> comp;
-  for (int s0 = 0; s0 < n; ++s0) {
-    if (seen[s0]) continue;
-    int s = s0;
-    for (int rep = 0; rep < 3; ++rep) {  // pseudo-peripheral start
-      bfs(s, comp);
-      s = comp.back();
-    }
-    bfs(s, comp);
-    for (int v : comp) seen[v] = 1;
-    order.insert(order.end(), comp.begin(), comp.end());
-  }
-  std::reverse(order.begin(), order.end());
-  perm = order;
-  std::vector<int> inv(n);
-  for (int i = 0; i < n; ++i) inv[perm[i]] = i;
-  first.assign(n, 0);
-  for (int i = 0; i < n; ++i) {
-    int f = i;
-    const int o = perm[i];
-    for (int64_t k = A.ptr[o]; k < A.ptr[o + 1]; ++k) f = std::min(f, inv[A.idx[k]]);
-    first[i] = f;
-  }
-  start.assign(n + 1, 0);
-  for (int i = 0; i < n; ++i) start[i + 1] = start[i] + (i - first[i] + 1);
-  L.assign(start[n], 0.0);
-  for (int i = 0; i < n; ++i) {
-    const int o = perm[i];
-    for (int64_t k = A.ptr[o]; k < A.ptr[o + 1]; ++k) {
-      const int j = inv[A.idx[k]];
-      if (j <= i) L[start[i] + (j - first[i])] = A.val[k];
-    }
-  }
-  for (int i = 0; i < n; ++i) {
-    double* Li = &L[start[i]];
-    for (int j = first[i]; j < i; ++j) {
-      const double* Lj = &L[start[j]];
-      const int k0 = std::max(first[i], first[j]);
-      double s = Li[j - first[i]];
-      for (int k = k0; k < j; ++k) s -= Li[k - first[i]] * Lj[k - first[j]];
-      Li[j - first[i]] = s / Lj[j - first[j]];
-    }
-    double d = Li[i - first[i]];
-    for (int k = first[i]; k < i; ++k) d -= Li[k - first[i]] * Li[k - first[i]];
-    if (!(d > 0.0) || !std::isfinite(d)) throw SolverError("factorization failed (not positive definite)");
-    Li[i - first[i]] = std::sqrt(d);
-  }
-}
-
-void Envelope::solve(Vec& x) const {
-  Vec y(n);
-  for (int i = 0; i < n; ++i) y[i] = x[perm[i]];
-  for (int i = 0; i < n; ++i) {
-    const double* Li = &L[start[i]];
-    double s = y[i];
-    for (int k = first[i]; k < i; ++k) s -= Li[k - first[i]] * y[k];
-    y[i] = s / Li[i - first[i]];
-  }
-  for (int i = n - 1; i >= 0; --i) {
-    const double* Li = &L[start[i]];
-    y[i] /= Li[i - first[i]];
-    const double yi = y[i];
-    for (int k = first[i]; k < i; ++k) y[k] -= Li[k - first[i]] * yi;
-  }
-  for (int i = 0; i < n; ++i) x[perm[i]] = y[i];
-}
-
 // ---------------- coarse embedding (schwarz.cpp:13-77) ----------------
 Csr coarse_embedding(const Discretization& D, const std::vector<int>& owner, int count, int q) {
   const int p = D.p;
@@ -252,9 +157,14 @@ Csr coarse_embedding(const Discretization& D, const std::vector<int>& owner, int
       box[a].y1 = std::max(box[a].y1, cb.y1);
     }
   }
-  std::vector<Triplet> t;
-  Vec fv, cv;
-  for (int c = 0; c < m.n_cells(); ++c) {
+  // one nl x nq coefficient block per cell, computed in parallel; E's rows
+  // (cell-major dofs) hold exactly that block at columns agg*nq.., so the CSR
+  // is written directly (no duplicates to sum)
+  const int nc = m.n_cells();
+  Vec coef(static_cast<std::size_t>(nc) * nl * nq);
+  parallel_for(static_cast<std::size_t>(nc), [&](std::size_t ci) {
+    const int c = static_cast<int>(ci);
+    Vec fv, cv;
     const int a = owner[c];
     const Rule r = polygon_rule(m.cell(c), 2 * p + 2);
     eval_basis(m.bbox[c], p, r.pts, fv, nullptr, nullptr);
@@ -277,6 +187,7 @@ Csr coarse_embedding(const Discretization& D, const std::vector<int>& owner, int
         Lm[i * nl + j] = s / Lm[j * nl + j];
       }
     }
+    double* out = &coef[ci * nl * nq];
     for (int mm = 0; mm < nq; ++mm) {
       Vec x(nl);
       for (int i = 0; i < nl; ++i) x[i] = rhs[i * nq + mm];
@@ -290,11 +201,19 @@ Csr coarse_embedding(const Discretization& D, const std::vector<int>& owner, int
         for (int k = i + 1; k < nl; ++k) s -= Lm[k * nl + i] * x[k];
         x[i] = s / Lm[i * nl + i];
       }
-      for (int i = 0; i < nl; ++i)
-        t.push_back({static_cast<int64_t>(c) * nl + i, static_cast<int64_t>(a) * nq + mm, x[i]});
+      for (int i = 0; i < nl; ++i) out[i * nq + mm] = x[i];
     }
-  }
-  return from_triplets(static_cast<int64_t>(m.n_cells()) * nl, static_cast<int64_t>(count) * nq, t);
+  });
+  Csr E;
+  E.rows = static_cast<int64_t>(nc) * nl;
+  E.cols = static_cast<int64_t>(count) * nq;
+  E.ptr.resize(E.rows + 1);
+  for (int64_t r = 0; r <= E.rows; ++r) E.ptr[r] = r * nq;
+  E.idx.resize(E.rows * nq);
+  E.val.assign(coef.begin(), coef.end());
+  for (int64_t r = 0; r < E.rows; ++r)
+    for (int mm = 0; mm < nq; ++mm) E.idx[r * nq + mm] = static_cast<int64_t>(owner[r / nl]) * nq + mm;
+  return E;
 }
 
 // ---------------- Schwarz (schwarz.cpp:79-169) ----------------
@@ -305,7 +224,7 @@ void Schwarz::build(const Csr& K, const Discretization& D, const std::vector<int
   dofs.assign(n_sub, {});
   for (int c = 0; c < D.mesh->n_cells(); ++c)
     for (int i = 0; i < nl; ++i) dofs[sub_owner[c]].push_back(static_cast<int64_t>(c) * nl + i);
-  local.assign(n_sub, Envelope());
+  local.assign(n_sub, BlockChol());
   std::vector<std::string> err(n_sub);
   parallel_for(n_sub, [&](std::size_t s) {
     const auto& d = dofs[s];
@@ -319,7 +238,7 @@ void Schwarz::build(const Csr& K, const Discretization& D, const std::vector<int
       }
     const Csr Ki = from_triplets(static_cast<int64_t>(d.size()), static_cast<int64_t>(d.size()), t);
     try {
-      local[s].factor(Ki);
+      local[s].factor(Ki, nl);
     } catch (const SolverError&) {
       err[s] = "schwarz: subdomain " + std::to_string(s) + " factorization failed (not positive definite)";
     }
@@ -327,12 +246,17 @@ void Schwarz::build(const Csr& K, const Discretization& D, const std::vector<int
   for (const auto& e : err)
     if (!e.empty()) throw SolverError(e);
   two_level = n_coarse > 0;
+  if (std::getenv("ORC_TIMES")) std::fprintf(stderr, "oracle setup: local factors done\n");
+  const auto tE = std::chrono::steady_clock::now();
   if (two_level) {
     E = coarse_embedding(D, coarse_owner, n_coarse, q);
     Et = transpose(E);
     K0 = multiply(Et, multiply(K, E));
+    if (std::getenv("ORC_TIMES"))
+      std::fprintf(stderr, "oracle setup: E, K0 %.2f s\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tE).count());
     try {
-      coarse.factor(K0);
+      coarse.factor(K0, n_modes(q));
     } catch (const SolverError&) {
       throw SolverError("schwarz: coarse operator factorization failed");
     }
@@ -379,13 +303,24 @@ void Simulation::build(const Config& c, MeshView m, const std::vector<int>& sub_
   cfg = c;
   if (!(c.dt > 0.0)) throw ConfigError("time.dt must be positive");
   if (!(c.tol > 0.0 && c.tol < 1.0)) throw ConfigError("solver.tol must lie in (0, 1)");
+  static const bool times = std::getenv("ORC_TIMES") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!times) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "oracle setup: %s %.2f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
+  };
   mesh = std::move(m);
   mesh.build();
+  lap("mesh topology");
   D.build(mesh, cfg);
+  lap("assembly");
   has_precond = cfg.precond != 0;
   if (has_precond) {
     const int q = cfg.q > 0 ? cfg.q : cfg.degree;
     S.build(D.K, D, sub_owner, n_sub, coarse_owner, cfg.precond == 2 ? n_coarse : 0, q);
+    lap("schwarz");
   }
   U = D.l2_project([this](P2 x) { return initial(x); });
   Up = U;

@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
             "pdg_problem_halo": (None, [vp, i32, P(i32), P(i32), P(i32)]),
             "pdg_problem_mesh": (i32, [vp, P(vp)]),
             "pdg_default_max_iterations": (i32, [i64]),
+            "pdg_uniform_rhs": (None, [C.c_uint64, i64, P(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -168,6 +169,15 @@ def iptr(a: np.ndarray):
 def lptr(a: np.ndarray):
     assert a.dtype == np.int64 and a.flags.c_contiguous
     return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def uniform_rhs(seed: int, n: int):
+    """BASELINE config-5 right-hand side: 2 (rng()>>11) 2^-53 - 1, mt19937_64(seed)
+    (proj/tests/acceptance.cpp:285-286)."""
+    import numpy as np
+    out = np.zeros(int(n))
+    lib().pdg_uniform_rhs(C.c_uint64(seed), int(n), out.ctypes.data_as(C.POINTER(C.c_double)))
+    return out
 
 
 def default_config(**kw) -> PdgConfig:

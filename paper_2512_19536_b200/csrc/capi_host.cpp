@@ -3,6 +3,7 @@
 // pdg_status codes (errors.hpp:13-35 -> PDG_ERR_*).
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <string>
 
 #include "../../include/polydg_b200.h"
@@ -91,6 +92,11 @@ pdg_status pdg_ionic_rest(const pdg_config* cfg, int* n_comp, double* u_rest, do
     if (y_rest)
       for (int l = 0; l < nc; ++l) y_rest[l] = y[l];
   });
+}
+
+void pdg_uniform_rhs(uint64_t seed, int64_t n, double* out) {
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
 }
 
 int pdg_default_max_iterations(int64_t n) {

@@ -108,6 +108,8 @@ void DeviceSim::attach_comm(const void* id128, int r, int w) {
   if (w != pr.cfg.world || r != pr.cfg.rank)
     throw ConfigError("attach_comm: rank/world differ from the configuration the problem was built for");
   if (w == 1) return;
+  // K0 below is all-reduced in place: a second attach would scale it by world
+  if (comm) throw ConfigError("attach_comm: a communicator is already attached");
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof id);
   ncclComm_t c = nullptr;

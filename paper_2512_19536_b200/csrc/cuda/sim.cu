@@ -949,19 +949,34 @@ StepResult DeviceSim::step() {
              c.warm_start, d_rhs, d_x, d_r, red_for(kFinDenom), st);
   after_reduce(kFinDenom, false);
   PDG_CUDA(cudaEventRecord(ev1, st));
+  // the ionic flags are read and cleared whatever the solve does, and a
+  // non-finite ionic state is reported in preference to the PCG breakdown it
+  // causes (the reference throws from the ionic assembly before solving,
+  // ionics.cpp:22-23, timestepper.cpp:156)
+  auto take_ionflags = [&]() {
+    int f = 0;
+    if (ionic) {
+      PDG_CUDA(cudaMemcpyAsync(&f, d_ionflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
+    }
+    PDG_CUDA(cudaStreamSynchronize(st));
+    return f;
+  };
+  auto ionic_error = [&]() {
+    return SolverError(c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN
+                           ? "barreto-cressman: non-finite state in current evaluation"
+                           : "fhn: non-finite state in current evaluation");
+  };
   PcgResult res;
-  run_solve(maxit, res);
-  PDG_CUDA(cudaEventRecord(ev2, st));
-  int ionflags = 0;
-  if (ionic) {
-    PDG_CUDA(cudaMemcpyAsync(&ionflags, d_ionflags, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
+  try {
+    run_solve(maxit, res);
+  } catch (const SolverError&) {
+    if (take_ionflags() & 2) throw ionic_error();
+    throw;
   }
-  PDG_CUDA(cudaStreamSynchronize(st));
-  if (ionflags & 2)
-    throw SolverError(c.ionic_model == PDG_IONIC_BARRETO_CRESSMAN
-                          ? "barreto-cressman: non-finite state in current evaluation"
-                          : "fhn: non-finite state in current evaluation");
+  PDG_CUDA(cudaEventRecord(ev2, st));
+  const int ionflags = take_ionflags();
+  if (ionflags & 2) throw ionic_error();
   if (ionflags & 1)
     std::fprintf(stderr,
                  "polydg: warning: membrane potential left the admissible range by more than 10x "

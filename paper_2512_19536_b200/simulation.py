@@ -79,10 +79,13 @@ class SimulationConfig:
     device: int = 0
 
     def n_steps(self) -> int:
-        return max(1, int(round(self.T / self.dt)))
+        # std::llround (timestepper.cpp:37): halves round away from zero
+        return max(1, int(math.floor(self.T / self.dt + 0.5)))
 
-    def to_c(self) -> _lib.PdgConfig:
-        c = _lib.default_config()
+    def to_c(self, base: Optional[_lib.PdgConfig] = None) -> _lib.PdgConfig:
+        """The C struct; `base` supplies the defaults of fields this dataclass
+        does not carry (default: pdg_config_default of the library)."""
+        c = base if base is not None else _lib.default_config()
         c.mesh_cells, c.mesh_seed, c.mesh_lloyd = self.cells, self.seed, self.lloyd
         for i, v in enumerate(self.domain):
             c.domain[i] = v
@@ -205,11 +208,20 @@ class Problem:
         self._read_info()
 
     @classmethod
-    def _view(cls, handle, config):
+    def _view(cls, handle, config, owner):
+        # non-owning view of the Problem held by `owner` (a Simulation): keep
+        # the owner alive as long as the view is reachable
         obj = cls.__new__(cls)
-        obj.config, obj._h, obj._owned = config, C.c_void_p(handle), False
+        obj.config, obj._h, obj._owned, obj._owner = config, C.c_void_p(handle), False, owner
         obj._read_info()
         return obj
+
+    def _handle(self):
+        if getattr(self, "_owner", None) is not None:
+            self._owner._handle()
+        if not self._h:
+            raise _lib.PdgError(2, "problem: handle is closed")
+        return self._h
 
     def _read_info(self):
         info = (C.c_int64 * 12)()
@@ -227,32 +239,32 @@ class Problem:
         """scipy.sparse.csr_matrix of K, M, A, E (n x coarse_dim) or K0 (reference order)."""
         import scipy.sparse as sp
         w = {"K": 0, "M": 1, "A": 2, "E": 3, "K0": 4}[which]
-        nnz = lib().pdg_problem_export(self._h, w, None, None, None)
+        nnz = lib().pdg_problem_export(self._handle(), w, None, None, None)
         if nnz < 0:
             raise ValueError(f"{which} not available")
         r = np.zeros(nnz, np.int64)
         c = np.zeros(nnz, np.int64)
         v = np.zeros(nnz)
-        lib().pdg_problem_export(self._h, w, _lib.lptr(r), _lib.lptr(c), dptr(v))
+        lib().pdg_problem_export(self._handle(), w, _lib.lptr(r), _lib.lptr(c), dptr(v))
         shape = {"E": (self.dimension, self.coarse_dim), "K0": (self.coarse_dim, self.coarse_dim)}.get(
             which, (self.dimension, self.dimension))
         return sp.csr_matrix((v, (r, c)), shape=shape)
 
     def owner(self, which: str = "subdomain") -> np.ndarray:
         o = np.zeros(self.n_cells, np.int32)
-        lib().pdg_problem_owner(self._h, 0 if which == "subdomain" else 1, _lib.iptr(o))
+        lib().pdg_problem_owner(self._handle(), 0 if which == "subdomain" else 1, _lib.iptr(o))
         return o
 
     def mesh(self):
         """The problem's mesh (reference cell order) as an owning mesh.Mesh."""
         from .mesh import Mesh
         h = C.c_void_p()
-        check(lib().pdg_problem_mesh(self._h, C.byref(h)))
+        check(lib().pdg_problem_mesh(self._handle(), C.byref(h)))
         return Mesh._adopt(h)
 
     def perm(self) -> np.ndarray:
         p = np.zeros(self.n_cells, np.int32)
-        lib().pdg_problem_perm(self._h, _lib.iptr(p))
+        lib().pdg_problem_perm(self._handle(), _lib.iptr(p))
         return p
 
 
@@ -264,7 +276,7 @@ class Simulation:
         self._cfg = config.to_c()
         self._h = C.c_void_p()
         check(lib().pdg_sim_create(C.byref(self._cfg), C.byref(self._h)))
-        self.problem = Problem._view(lib().pdg_sim_problem(self._h), config)
+        self.problem = Problem._view(lib().pdg_sim_problem(self._h), config, self)
         self.dimension = self.problem.dimension
         self.n_comp = self.problem.n_comp
 
@@ -273,13 +285,26 @@ class Simulation:
             lib().pdg_sim_free(self._h)
             self._h = None
 
+    def _handle(self):
+        if not getattr(self, "_h", None):
+            raise _lib.PdgError(2, "simulation: handle is closed")
+        return self._h
+
+    def _vec(self, a, what, rows=1):
+        """float64 contiguous copy of `a`, checked against the dimension the
+        C-ABI reads (krylov.cpp:22-23 throws SolverError on a mismatch)."""
+        a = np.ascontiguousarray(a, dtype=np.float64).ravel()
+        if a.size != rows * self.dimension:
+            raise _lib.PdgError(3, f"{what}: vector dimension mismatch")
+        return a
+
     def __del__(self):
         self.close()
 
     # --- timestepper.hpp:122-152 ---
     def step(self) -> StepStats:
         s = _StepStats()
-        check(lib().pdg_sim_step(self._h, C.byref(s)))
+        check(lib().pdg_sim_step(self._handle(), C.byref(s)))
         return StepStats(s.iterations, s.final_residual, bool(s.converged),
                          s.condition_estimate if s.has_condition else None, s.solve_ms, s.step_ms)
 
@@ -298,51 +323,53 @@ class Simulation:
         U, Up = np.zeros(n), np.zeros(n)
         Y, Yp = np.zeros(max(nc, 1) * n), np.zeros(max(nc, 1) * n)
         k, t = C.c_int(), C.c_double()
-        check(lib().pdg_sim_get_state(self._h, C.byref(k), C.byref(t), dptr(U), dptr(Up),
+        check(lib().pdg_sim_get_state(self._handle(), C.byref(k), C.byref(t), dptr(U), dptr(Up),
                                       dptr(Y), dptr(Yp)))
         return k.value, t.value, U, Up, Y[:nc * n].reshape(nc, n), Yp[:nc * n].reshape(nc, n)
 
     def set_state(self, k, U_curr, U_prev=None, Y_curr=None, Y_prev=None):
-        f = lambda a: None if a is None else dptr(np.ascontiguousarray(a, dtype=np.float64).ravel())
-        keep = [np.ascontiguousarray(a, dtype=np.float64).ravel() if a is not None else None
-                for a in (U_curr, U_prev, Y_curr, Y_prev)]
-        check(lib().pdg_sim_set_state(self._h, int(k), *[dptr(a) if a is not None else None for a in keep]))
+        nc = max(self.n_comp, 1)
+        keep = [None if a is None else self._vec(a, "set_state", rows)
+                for a, rows in ((U_curr, 1), (U_prev, 1), (Y_curr, nc), (Y_prev, nc))]
+        if keep[0] is None:
+            raise _lib.PdgError(3, "set_state: U_curr is required")
+        check(lib().pdg_sim_set_state(self._handle(), int(k), *[dptr(a) if a is not None else None for a in keep]))
 
     # --- snapshot.hpp:13-22 (means on the device, file written by the library) ---
     def cell_means(self) -> np.ndarray:
         """Per-cell means of U^k (snapshot.cpp:13-28), reference cell order."""
         m = np.zeros(self.problem.n_cells)
-        check(lib().pdg_sim_cell_means(self._h, dptr(m)))
+        check(lib().pdg_sim_cell_means(self._handle(), dptr(m)))
         return m
 
     def export_snapshot(self, path: str, fmt: str = "vtk-legacy") -> None:
         """export_snapshot (snapshot.cpp:30-75) of U^k at the current time."""
-        check(lib().pdg_sim_export_snapshot(self._h, str(path).encode(), fmt.encode()))
+        check(lib().pdg_sim_export_snapshot(self._handle(), str(path).encode(), fmt.encode()))
 
     # --- LinearOperator::apply (krylov.hpp:15-30, schwarz.hpp:47-72) ---
     def apply_K(self, x: np.ndarray) -> np.ndarray:
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        x = self._vec(x, "apply_K")
         y = np.zeros(self.dimension)
-        check(lib().pdg_sim_apply_K(self._h, dptr(x), dptr(y)))
+        check(lib().pdg_sim_apply_K(self._handle(), dptr(x), dptr(y)))
         return y
 
     def apply_precond(self, r: np.ndarray) -> np.ndarray:
-        r = np.ascontiguousarray(r, dtype=np.float64)
+        r = self._vec(r, "schwarz apply")
         z = np.zeros(self.dimension)
-        check(lib().pdg_sim_apply_precond(self._h, dptr(r), dptr(z)))
+        check(lib().pdg_sim_apply_precond(self._handle(), dptr(r), dptr(z)))
         return z
 
     # --- pcg_solve (krylov.hpp:49-57) ---
     def pcg_solve(self, b, tol, maxit: int = 0, x0=None, use_precond: bool = True):
-        b = np.ascontiguousarray(b, dtype=np.float64)
+        b = self._vec(b, "pcg")
         x = np.zeros(self.dimension)
-        x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        x0a = None if x0 is None else self._vec(x0, "pcg")
         cap = (maxit if maxit > 0 else default_max_iterations(self.dimension)) + 2
         hist = [np.zeros(cap) for _ in range(3)]
         rep = _PcgReport()
         rep.capacity = cap
         rep.residual_history, rep.alphas, rep.betas = (dptr(h) for h in hist)
-        check(lib().pdg_sim_pcg(self._h, dptr(b), dptr(x0a) if x0a is not None else None,
+        check(lib().pdg_sim_pcg(self._handle(), dptr(b), dptr(x0a) if x0a is not None else None,
                                 float(tol), int(maxit), int(use_precond), dptr(x), C.byref(rep)))
         it = rep.iterations
         nres = it if it > 0 else (1 if rep.converged else 0)

@@ -67,6 +67,11 @@ def lib():
             "orc_bc": (i32, [P(dbl), dbl, P(dbl), P(dbl), P(dbl)]),
             "orc_ionic_rest": (i32, [P(PdgConfig), P(i32), P(dbl), P(dbl)]),
             "orc_polygon_quadrature": (i32, [P(dbl), i32, i32, P(dbl), P(dbl), i32]),
+            "orc_set_parallel": (None, [i32]),
+            "orc_set_lean": (None, [i32]),
+            "orc_config_default": (None, [P(PdgConfig)]),
+            "orc_uniform_rhs": (None, [C.c_uint64, i64, P(dbl)]),
+            "orc_sim_factor_blocks": (i64, [vp, i32]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(L, k)
@@ -74,6 +79,30 @@ def lib():
         assert L.orc_config_size() == C.sizeof(PdgConfig), "oracle/product config layouts differ"
         _L = L
     return _L
+
+
+def oracle_config(config: SimulationConfig) -> PdgConfig:
+    """config.to_c() on the oracle's own defaults (does not load the product library)."""
+    base = PdgConfig()
+    lib().orc_config_default(C.byref(base))
+    return config.to_c(base)
+
+
+def set_parallel(on: bool) -> None:
+    """Row-parallel CSR products in the oracle (same bits; large parity runs only)."""
+    lib().orc_set_parallel(int(on))
+
+
+def set_lean(level: int) -> None:
+    """1: drop M, A after setup; 2: also skip K_rhs (single-solve workloads)."""
+    lib().orc_set_lean(int(level))
+
+
+def uniform_rhs(seed: int, n: int) -> np.ndarray:
+    """b_i = 2 (rng()>>11) 2^-53 - 1, mt19937_64(seed) (acceptance.cpp:285-286)."""
+    out = np.zeros(int(n))
+    lib().orc_uniform_rhs(C.c_uint64(seed), int(n), _d(out))
+    return out
 
 
 def _d(a):
@@ -159,7 +188,7 @@ class OracleSim:
 
     def __init__(self, config: SimulationConfig, mesh, sub_owner, n_sub, coarse_owner=None, n_coarse=0):
         self.config = config
-        cfg = config.to_c()
+        cfg = oracle_config(config)
         verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
         off = np.ascontiguousarray(mesh.cell_off, dtype=np.int32)
         idx = np.ascontiguousarray(mesh.cell_vtx, dtype=np.int32)
@@ -233,6 +262,10 @@ class OracleSim:
             shape = (self.dimension, self.dimension)
         return sp.csr_matrix((v, (r, c)), shape=shape)
 
+    def factor_blocks(self, coarse=False):
+        """Stored b x b blocks of the oracle's local (or coarse) factors."""
+        return lib().orc_sim_factor_blocks(self._h, int(coarse))
+
     def ionic_terms(self, U, Y):
         U = np.ascontiguousarray(U, dtype=np.float64)
         Y = np.ascontiguousarray(Y, dtype=np.float64)
@@ -248,15 +281,22 @@ class OracleSim:
         return m
 
 
-def oracle_for(config: SimulationConfig, mesh=None):
-    """Builds the oracle on the product's bit-exact mesh/partitions for `config`.
+def oracle_for(config: SimulationConfig, mesh=None, reference_mesh=False):
+    """Builds the oracle on the bit-exact mesh/partitions for `config`.
 
+    reference_mesh=False: the product's mesh code (bit-exact against the
+    reference, tests/test_mesh_golden.py); True: the reference's own mesh and
+    agglomeration sources compiled in oracle/_ref (no product library loaded).
     Partitions follow the reference recipe: identity subdomains unless
     config.subdomains > 0 (agglomerate), coarse = hierarchy / explicit count.
     """
-    from paper_2512_19536_b200.mesh import Mesh
-    m = Mesh(config.cells, config.domain, config.seed, config.lloyd,
-             config.split_y if config.domain[1] < config.split_y < config.domain[3] else None)
+    split = config.split_y if config.domain[1] < config.split_y < config.domain[3] else None
+    if reference_mesh:
+        from tests.refmesh import RefMesh
+        m = RefMesh(config.cells, config.domain, config.seed, config.lloyd, split)
+    else:
+        from paper_2512_19536_b200.mesh import Mesh
+        m = Mesh(config.cells, config.domain, config.seed, config.lloyd, split)
     data = m.data()
     nc = data.n_cells
     if config.subdomains > 0:

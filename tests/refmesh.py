@@ -61,6 +61,8 @@ class RefMesh:
             ref().ref_mesh_free(self._h)
 
     def data(self) -> MeshData:
+        if getattr(self, "_data", None) is not None:
+            return self._data
         L = ref()
         # the ref shim uses the same argument layout as the product's mesh readers
         class _Shim:
@@ -68,7 +70,8 @@ class RefMesh:
             mesh_arrays = L.ref_mesh_arrays
             mesh_faces = L.ref_mesh_faces
             mesh_cell_geometry = L.ref_mesh_cell_geometry
-        return _read_mesh(_Shim, self._h, "")
+        self._data = _read_mesh(_Shim, self._h, "")
+        return self._data
 
     def agglomerate(self, target):
         nc = self.data().n_cells
