@@ -4,20 +4,26 @@
 A "step" is one Crank-Nicolson step of the PolyDG monodomain system
 (Simulation::step, /root/reference/proj/src/timestepper.cpp:144-200): ionic
 terms at quadrature nodes, CN right-hand side, two-level-Schwarz PCG to rtol
-1e-8, explicit ionic-state update. Workload: BASELINE config 2 (16,384
-Voronoi cells, p = 3, 64 subdomains = 64 coarse agglomerates, grey/white
-anisotropy), synthetic seeded mesh and data.
+1e-8, explicit ionic-state update. Default workload: BASELINE config 4 (the
+config the metric's 1/2/4/8-GPU figures are quoted on): 1,048,576 seeded
+Voronoi cells, p = 3 (10.5 M dofs), 512 subdomains = 512 coarse agglomerates,
+grey/white anisotropy with per-element fibres, strip stimulus, FHN.
 
-    value  = PCG DOF-iterations/s = n_dofs * sum(PCG iterations) / device time,
-             whole job over all ranks (max-over-ranks device time)
+    value  = PCG DOF-iterations/s = n_dofs * sum(PCG iterations) / device time
+             of the timed steps (whole job, max over ranks)
     e2e    = the same metric through the public C-ABI with the state held on
              the host: every step set_state (H2D from pinned memory) -> step ->
              get_state (D2H)
-    --impl reference: the reference's CPU path (the Eigen-free restatement in
-             oracle/, since the reference itself cannot be built here) on the
-             same workload with all host threads.
+    roofline: the Schwarz sweep (dominant kernel) against the measured HBM
+             peak, bytes per SURVEY §8(d): 2 * 8 * nnz(L) (structural, local +
+             coarse factors) + r read / z write; stored panel bytes separately
+    --impl reference: the reference's CPU path (oracle/ restatement; the
+             reference's numeric sources need Eigen, which is absent) on the
+             same config, mesh and partitions from the reference's own
+             compiled mesh code (oracle/_ref), no product library loaded.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+       [--config config4|config2|...] [--scaling strong|weak]
 Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
 """
 from __future__ import annotations
@@ -38,22 +44,24 @@ sys.path.insert(0, str(ROOT))
 METRIC = "PCG DOF-iterations/s and solve time per CN step; % of HBM roofline, 1/2/4/8 GPU"
 UNIT = "DOF-iter/s"
 KERNELS = ["spmv", "update", "restrict", "sweep", "restrict_combine", "prolong_dot", "pupdate", "ionic", "rhs"]
-REF_BUDGET_S = 150.0
+L2_BYTES = 126 * 2**20
+REF_BUDGET_S = 75.0        # timed CPU work of the reference arm (bounded sample)
+REF_ITERS_PER_STEP = 2     # PCG iterations per reference-arm step
+CPU_BASELINE_S = 20.0
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload_config(name, rank=0, world=1, device=0, scaling="weak"):
-    """The BASELINE workload. Weak scaling (default) keeps the per-GPU problem
-    at the config's size: N GPUs solve one coupled mesh of N x cells with
-    N x subdomains (one halo exchange + all-reduces per PCG iteration);
-    strong scaling shards the config's own mesh over the N GPUs."""
+def workload_config(name, rank=0, world=1, device=0, scaling="strong"):
+    """The BASELINE workload. Strong scaling (default) shards the config's own
+    mesh over the N GPUs (whole subdomains per rank); weak scaling solves one
+    coupled mesh of N x cells with N x subdomains."""
     from paper_2512_19536_b200 import configs
     cfg = getattr(configs, name)()
     if scaling == "weak" and world > 1:
@@ -63,10 +71,27 @@ def workload_config(name, rank=0, world=1, device=0, scaling="weak"):
     return cfg
 
 
-def workload_desc(cfg):
-    return (f"{cfg.cells} seeded Voronoi cells (lloyd {cfg.lloyd}), p={cfg.degree}, "
-            f"{cfg.subdomains} subdomains = {cfg.subdomains} coarse agglomerates (q=p), grey/white "
-            f"anisotropy with per-element fibres, FHN ionics, dt={cfg.dt} ms, rtol {cfg.tol}")
+def config_json(name, cfg, world, scaling):
+    """The `config` object both arms print (computed without any library)."""
+    b = (cfg.degree + 1) * (cfg.degree + 2) // 2
+    q = cfg.q if cfg.q > 0 else cfg.degree
+    aniso = cfg.sigma_white_l != cfg.sigma_white_n or cfg.sigma_grey_l != cfg.sigma_grey_n
+    stim = "none"
+    if cfg.stimulus and cfg.stimulus[0] == "strip":
+        stim = f"strip x<{cfg.stimulus[2]} for t<{cfg.stimulus[3]} ms, {cfg.stimulus[1]:g} uA/cm^3"
+    return {
+        "workload": name,
+        "mesh": f"{cfg.cells} seeded Voronoi cells (seed {cfg.seed}, lloyd {cfg.lloyd}), unit square",
+        "degree": cfg.degree, "dofs": cfg.cells * b,
+        "subdomains": cfg.subdomains, "coarse_agglomerates": cfg.subdomains if cfg.coarse == -1 else cfg.coarse,
+        "coarse_degree": q,
+        "conductivity": ("grey/white anisotropic, per-element fibres" if aniso and cfg.fiber_random
+                         else "anisotropic" if aniso else "isotropic"),
+        "ionic": cfg.ionic_model, "stimulus": stim, "dt_ms": cfg.dt, "rtol": cfg.tol,
+        "l2": f"no flush needed: the operands streamed by one PCG iteration (K ~{8 * cfg.cells * 7 * b * b / 1e9:.2f} GB "
+              f"plus Schwarz factors > {2 * 8 * cfg.cells * 10 * b * b / 1e9:.2f} GB) exceed the {L2_BYTES >> 20} MB L2",
+        "parallelism": f"{world} GPU(s), whole subdomains per rank, {scaling} scaling",
+    }
 
 
 class ClockSampler:
@@ -106,69 +131,101 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(cfg, budget_s=20.0, min_steps=1):
-    """Times the oracle port (reference algorithm, reference threading) on the workload."""
-    from tests.oracle_binding import lib as orc_lib, oracle_for
+def time_oracle_iterations(orc, budget_s, iters_per_sample, max_samples=None, warmup=1):
+    """Times bounded samples of PCG iterations on the oracle: each sample is
+    `iters_per_sample` iterations (SpMV, Schwarz local + coarse apply, vector
+    updates; tol 1e-300 so the sample never stops early) from the warm start
+    U^k on a seeded right-hand side. Returns (samples, iterations, seconds)."""
+    from tests import oracle_binding as ob
+    n = orc.dimension
+    b = ob.uniform_rhs(42, n)
+    x0 = orc.state()[2]
+    for _ in range(warmup):
+        orc.pcg_solve(b, 1e-300, maxit=iters_per_sample, x0=x0)
+    samples, its, t0 = 0, 0, time.perf_counter()
+    while True:
+        _, rep = orc.pcg_solve(b, 1e-300, maxit=iters_per_sample, x0=x0)
+        its += rep["iterations"]
+        samples += 1
+        el = time.perf_counter() - t0
+        if max_samples is not None and samples >= max_samples:
+            break
+        if el >= budget_s or el + el / samples > 1.5 * budget_s:
+            break
+    return samples, its, time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, budget_s=CPU_BASELINE_S):
+    """The oracle port (reference algorithm and threading) on the workload."""
+    from tests import oracle_binding as ob
+    ob.set_parallel(False)   # the reference's single-threaded SpMV / vector ops
+    ob.set_lean(1)
     t0 = time.perf_counter()
-    orc, _ = oracle_for(cfg)
+    orc, _ = ob.oracle_for(cfg)
     setup = time.perf_counter() - t0
     n = orc.dimension
-    its, steps, t0 = 0, 0, time.perf_counter()
-    while True:
-        its += orc.step()["iterations"]
-        steps += 1
-        el = time.perf_counter() - t0
-        if steps >= min_steps and el >= budget_s:
-            break
-        if el + el / steps > budget_s * 1.5 and steps >= min_steps:
-            break
-    return {"value": n * its / el, "unit": UNIT, "cores": orc_lib().orc_threads(), "kind": "port",
-            "sample": f"{steps} CN steps of the workload ({its} PCG iterations, {el:.1f} s) after {setup:.1f} s "
-                      f"untimed setup; oracle/ restatement (reference cannot be built: Eigen3 absent)"}
+    samples, its, el = time_oracle_iterations(orc, budget_s, REF_ITERS_PER_STEP)
+    return {"value": n * its / el, "unit": UNIT, "cores": ob.lib().orc_threads(), "kind": "port",
+            "sample": f"{its} PCG iterations ({samples} x {REF_ITERS_PER_STEP}) of the workload's system in "
+                      f"{el:.1f} s after {setup:.0f} s untimed setup; oracle/ restatement with the reference's "
+                      f"threading (parallel_for local solves, serial SpMV/vector ops); the reference's numeric "
+                      f"sources need Eigen3, which is absent"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # the arm's own workload (weak scaling: N x the config's mesh), solved by
-    # the single-process CPU oracle
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    cfg = workload_config(args.config, 0, world, 0, args.scaling)
-    cfg.rank, cfg.world = 0, 1
-    from tests.oracle_binding import lib as orc_lib, oracle_for
-    orc, _ = oracle_for(cfg)
+    from paper_2512_19536_b200 import configs  # dataclasses only; no library is loaded
+    cfg = getattr(configs, args.config)()
+    if args.scaling == "weak" and world > 1:
+        cfg.cells *= world
+        cfg.subdomains *= world
+    from tests import oracle_binding as ob
+    ob.set_parallel(False)
+    ob.set_lean(1)
+    t0 = time.perf_counter()
+    orc, _ = ob.oracle_for(cfg, reference_mesh=True)
+    setup = time.perf_counter() - t0
     n = orc.dimension
-    for _ in range(args.warmup):
-        orc.step()
-    its, done, t0 = 0, 0, time.perf_counter()
-    for _ in range(args.steps):
-        its += orc.step()["iterations"]
-        done += 1
-        if time.perf_counter() - t0 > REF_BUDGET_S:
-            break
-    el = time.perf_counter() - t0
+    for _ in range(min(args.warmup, 1)):
+        orc.pcg_solve(ob.uniform_rhs(42, n), 1e-300, maxit=REF_ITERS_PER_STEP, x0=orc.state()[2])
+    samples, its, el = time_oracle_iterations(orc, REF_BUDGET_S, REF_ITERS_PER_STEP, max_samples=args.steps,
+                                              warmup=0)
     value = n * its / el
+    loaded = sorted({p for p in _loaded_libs() if str(ROOT) in p})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / samples, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc_lib().orc_threads(), "kind": "port",
-                             "sample": f"{done} of {args.steps} requested CN steps timed "
-                                       f"(budget {REF_BUDGET_S:.0f} s), {its} PCG iterations"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": config_json(args.config, cfg, world, args.scaling),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": ob.lib().orc_threads(), "kind": "port",
+                             "sample": f"{samples} of {args.steps} requested steps timed, each step = "
+                                       f"{REF_ITERS_PER_STEP} PCG iterations of the workload's CN system "
+                                       f"({its} iterations, {el:.1f} s, budget {REF_BUDGET_S:.0f} s) after "
+                                       f"{setup:.0f} s untimed setup (mesh and partitions by the reference's own "
+                                       f"compiled mesh code, oracle/_ref); ms_per_step is per sampled step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_libs": loaded}
     print(json.dumps(line), flush=True)
+
+
+def _loaded_libs():
+    try:
+        return [l.split()[-1] for l in open("/proc/self/maps") if l.rstrip().endswith(".so")]
+    except OSError:
+        return []
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config2")
+    ap.add_argument("--config", default="config4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -189,6 +246,7 @@ def main():
     from paper_2512_19536_b200.simulation import Simulation
     L = _lib.lib()
     cfg = workload_config(args.config, rank, world, local, args.scaling)
+    t_setup = time.perf_counter()
     sim = Simulation(cfg)
     if world > 1:
         nb = L.pdg_nccl_unique_id_bytes()
@@ -199,6 +257,7 @@ def main():
         dist.broadcast(t, 0)
         uid = (C.c_char * nb).from_buffer_copy(bytes(t.tolist()))
         _lib.check(L.pdg_sim_attach_comm(sim._h, uid, rank, world))
+    setup_s = time.perf_counter() - t_setup
     n_global = sim.dimension
 
     def barrier():
@@ -206,19 +265,15 @@ def main():
         if dist:
             dist.barrier()
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         if not dist:
             return x
         t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x):
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t)
-        return float(t.item())
+    max_over_ranks = lambda x: reduce(x, dist.ReduceOp.MAX if dist else None)
+    sum_over_ranks = lambda x: reduce(x, dist.ReduceOp.SUM if dist else None)
 
     for _ in range(args.warmup):
         sim.step()
@@ -231,10 +286,11 @@ def main():
     ms = C.c_double()
     barrier()
     _lib.check(L.pdg_sim_timer(sim._h, 0, None))
-    its, solve_ms = 0, 0.0
+    its, solve_ms, per_step_its = 0, 0.0, []
     for _ in range(args.steps):
         s = sim.step()
         its += s.iterations
+        per_step_its.append(s.iterations)
         solve_ms += s.solve_ms
     _lib.check(L.pdg_sim_timer(sim._h, 1, C.byref(ms)))
     barrier()
@@ -244,8 +300,8 @@ def main():
     _lib.check(L.pdg_sim_sweep_live(sim._h, C.byref(live_n1), C.byref(live_ms1)))
     # the sweep's average launch duration inside the timed region (device
     # globaltimer, first CTA start -> last CTA end), max over ranks
-    sweep_live_ms = max_over_ranks((live_ms1.value - live_ms0.value) / max(1, live_n1.value - live_n0.value))
     sweep_live_launches = live_n1.value - live_n0.value
+    sweep_live_ms = max_over_ranks((live_ms1.value - live_ms0.value) / max(1, sweep_live_launches))
     elapsed_ms = max_over_ranks(ms.value)
     value = n_global * its / (elapsed_ms * 1e-3)
 
@@ -257,10 +313,9 @@ def main():
     hU[:], hUp[:] = U, Up
     hY[:nc * n], hYp[:nc * n] = Y.ravel(), Yp.ravel()
     d = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
-    kk = C.c_int()
-    t_ = C.c_double()
+    kk, t_ = C.c_int(), C.c_double()
     e2e_its = 0
-    e2e_steps = max(1, min(args.steps, 50))
+    e2e_steps = max(1, min(args.steps, 5))
     barrier()
     _lib.check(L.pdg_sim_timer(sim._h, 0, None))
     st = _lib.StepStats()
@@ -280,37 +335,41 @@ def main():
     h2d = (2 + 2 * nc) * n * 8
     d2h = (1 + nc) * n * 8
 
-    # ---- per-kernel device times for the roofline ----
+    # ---- per-kernel device times; the sweep's live time replaces its cold one ----
     kms = (C.c_double * 9)()
     kby = (C.c_int64 * 9)()
-    _lib.check(L.pdg_sim_profile(sim._h, 20, kms, kby))
+    _lib.check(L.pdg_sim_profile(sim._h, 10, kms, kby))
+    stats = sim.problem.factor_stats()
     per_step = {"spmv": its / args.steps, "update": its / args.steps}
     for k in ("restrict", "sweep", "restrict_combine", "prolong_dot", "pupdate"):
         per_step[k] = its / args.steps + 1
-    per_step["rhs"] = 1
-    per_step["ionic"] = 1
-    # the sweep's duration as measured live inside the timed region replaces
-    # its isolated (cold-L2) profile time
+    per_step["rhs"] = per_step["ionic"] = 1
     iso_sweep_ms = kms[KERNELS.index("sweep")]
     if sweep_live_launches > 0:
         kms[KERNELS.index("sweep")] = sweep_live_ms
-    shares = {k: kms[i] * per_step.get(k, 0) / (elapsed_ms / args.steps) for i, k in enumerate(KERNELS)}
-    dom = max(shares, key=shares.get)
+    step_ms = elapsed_ms / args.steps
+    shares = {k: kms[i] * per_step.get(k, 0) / step_ms for i, k in enumerate(KERNELS)}
+    dom = "sweep"
     di = KERNELS.index(dom)
     peak, peak_kind = peaks()
-    achieved = kby[di] / (kms[di] * 1e-3) / 1e9
-    timing = ("live: device globaltimer per launch inside the timed region, "
-              f"{sweep_live_launches} launches" if dom == "sweep" and sweep_live_launches > 0
-              else "isolated launches, L2 flushed before each")
+    # SURVEY §8(d) algorithmic bytes of one Schwarz apply (this rank): forward +
+    # backward over the structural local factors and the coarse factor, r in, z out
+    N_local = sim.problem.cell_end - sim.problem.cell_begin
+    n_local = N_local * sim.problem.n_local
+    sweep_alg = 2 * 8 * (stats["l_struct"] + stats["l0_struct"]) + 16 * n_local
+    sweep_stored = int(kby[di])
+    achieved = sweep_alg / (kms[di] * 1e-3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
-    # bytes of one whole PCG iteration vs its device time (all kernels of the body)
-    iter_bytes = sum(kby[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep", "restrict_combine",
-                                                      "prolong_dot", "pupdate"))
-    iter_ms = sum(kms[KERNELS.index(k)] for k in ("spmv", "update", "restrict", "sweep", "restrict_combine",
-                                                   "prolong_dot", "pupdate"))
+    # whole PCG iteration by §8(d): K + row structure, factors, E^T and E, 12 vectors
+    qd = cfg.q if cfg.q > 0 else cfg.degree
+    b, bq = sim.problem.n_local, (qd + 1) * (qd + 2) // 2
+    iter_alg = (8 * stats["k_blocks"] * b * b + 4 * stats["k_blocks"] + 4 * (N_local + 1)
+                + 2 * 8 * (stats["l_struct"] + stats["l0_struct"]) + 2 * 8 * N_local * b * bq + 12 * 8 * n_local)
+    iter_ms = solve_ms / its if its else None
+    iter_frac = max_over_ranks(iter_alg / (iter_ms * 1e-3) / 1e9) / peak if iter_ms else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -322,25 +381,26 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": f"{args.config}: " + workload_desc(cfg), "dofs": n_global,
-                       "steps_timed": args.steps, "pcg_iterations": its,
-                       "avg_iterations_per_step": its / args.steps,
-                       "solve_ms_per_step": solve_ms / args.steps,
-                       "l2": "operands (K 91 MB + Schwarz panels 408 MB) exceed the 126 MB L2; "
-                             "per-kernel profile times flush L2 before each launch",
-                       "parallelism": f"subdomains sharded over {world} GPU(s)" + (
-                           f" ({args.config} per GPU: {cfg.cells} cells, {cfg.subdomains} subdomains in total)"
-                           if args.scaling == "weak" and world > 1 else "")},
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(args.config, cfg, world, args.scaling),
+            "stats": {"pcg_iterations": its, "iterations_per_step": per_step_its,
+                      "solve_ms_per_step": solve_ms / args.steps, "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "algorithmic_bytes_per_launch": int(kby[di]),
-                         "launch_ms": kms[di], "launch_timing": timing, "share_of_step": shares[dom],
-                         "sweep_isolated_ms": iso_sweep_ms,
-                         "pcg_iteration": {"bytes": int(iter_bytes), "kernel_ms": iter_ms,
-                                           "GB/s": iter_bytes / (iter_ms * 1e-3) / 1e9 if iter_ms else None},
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": sweep_alg,
+                         "algorithmic_bytes": "SURVEY 8(d): 2*8*(nnz(L_loc)+nnz(L_0)) structural (this "
+                                              "implementation's ordering) + 16 n (r in, z out)",
+                         "nnz_L_loc": stats["l_struct"], "nnz_L0": stats["l0_struct"],
+                         "stored_panel_bytes_per_launch": sweep_stored,
+                         "stored_GB/s": sweep_stored / (kms[di] * 1e-3) / 1e9,
+                         "launch_ms": kms[di],
+                         "launch_timing": f"live: device globaltimer per launch inside the timed region, "
+                                          f"{sweep_live_launches} launches",
+                         "share_of_step": shares[dom], "sweep_isolated_ms": iso_sweep_ms,
+                         "pcg_iteration": {"algorithmic_bytes": iter_alg, "ms": iter_ms, "frac": iter_frac,
+                                           "note": "SpMV + Schwarz apply + E/E^T + 12 vectors per SURVEY 8(d) "
+                                                   "over the device time of the solves / iterations"},
                          "kernels": {k: {"ms": kms[i], "bytes": int(kby[i]),
                                          "GB/s": (kby[i] / (kms[i] * 1e-3) / 1e9) if kms[i] else None,
                                          "share": shares[k]} for i, k in enumerate(KERNELS)}},

@@ -140,6 +140,12 @@ void pdg_problem_info(const pdg_problem* p, int64_t info[12]);
  * rows == NULL. which: 0 = K, 1 = M, 2 = A, 3 = E (n x coarse_dim), 4 = K0 */
 int64_t pdg_problem_export(const pdg_problem* p, int which, int64_t* rows, int64_t* cols,
                            double* vals);
+/* factor / operator sizes of this rank for the SURVEY §8(d) byte model:
+ * stats[0] structural nnz(L) of the local Schwarz factors (scalar, lower incl.
+ * diagonal, this implementation's ordering), [1] the same for the coarse
+ * factor, [2] / [3] stored forward / backward sweep panel doubles (explicit
+ * zeros and padding included), [4] local K blocks, [5] E doubles held */
+void pdg_problem_factor_stats(const pdg_problem* p, int64_t stats[6]);
 /* partition maps: which 0 = subdomain owner, 1 = coarse owner; per reference cell */
 void pdg_problem_owner(const pdg_problem* p, int which, int* owner);
 /* internal order: perm[i] = reference cell of internal position i */

@@ -215,6 +215,18 @@ void pdg_problem_owner(const pdg_problem* h, int which, int* owner) {
   for (std::size_t c = 0; c < src.size(); ++c) owner[c] = src[c];
 }
 
+void pdg_problem_factor_stats(const pdg_problem* h, int64_t stats[6]) {
+  const auto& pr = *h->p;
+  int64_t nnzb_local = 0;
+  for (std::size_t i = 0; i + 1 < pr.K.ptr.size(); ++i) nnzb_local += pr.K.ptr[i + 1] - pr.K.ptr[i];
+  stats[0] = pr.l_struct;
+  stats[1] = pr.l0_struct;
+  stats[2] = pr.fmat_len;
+  stats[3] = pr.hmat_len;
+  stats[4] = nnzb_local;
+  stats[5] = static_cast<int64_t>(pr.E.size());
+}
+
 void pdg_problem_perm(const pdg_problem* h, int* perm) {
   std::memcpy(perm, h->p->perm.data(), sizeof(int) * h->p->perm.size());
 }

@@ -403,4 +403,42 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
   return F;
 }
 
+FillCount structural_fill(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
+                          const std::vector<int>& order) {
+  std::vector<int> pos(m);
+  for (int i = 0; i < m; ++i) pos[order[i]] = i;
+  std::vector<int> parent(m, -1), anc(m, -1), mark(m, -1);
+  // elimination tree with path-compressed ancestors
+  for (int i = 0; i < m; ++i) {
+    const int node = order[i];
+    for (int k = adj_ptr[node]; k < adj_ptr[node + 1]; ++k) {
+      int r = pos[adj[k]];
+      if (r >= i) continue;
+      while (anc[r] != -1 && anc[r] != i) {
+        const int t = anc[r];
+        anc[r] = i;
+        r = t;
+      }
+      if (anc[r] == -1) {
+        anc[r] = i;
+        parent[r] = i;
+      }
+    }
+  }
+  FillCount f;
+  f.diag = m;
+  // row i of L: the union of the etree paths from its lower neighbours up to i
+  for (int i = 0; i < m; ++i) {
+    mark[i] = i;
+    const int node = order[i];
+    for (int k = adj_ptr[node]; k < adj_ptr[node + 1]; ++k) {
+      for (int j = pos[adj[k]]; j < i && mark[j] != i; j = parent[j]) {
+        mark[j] = i;
+        ++f.offdiag;
+      }
+    }
+  }
+  return f;
+}
+
 }  // namespace pdg

@@ -65,6 +65,19 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd);
 // No values (A.val may be empty); Linv and B stay empty.
 SupernodalFactor symbolic_factor(const BlockMatrix& A, const NdTree& nd, std::vector<std::vector<int>>& upd);
 
+// Structural blocks of the Cholesky factor of a graph (adjacency without
+// self loops) eliminated in `order` (position -> node): diagonal blocks plus
+// the strictly lower nonzero blocks, by elimination tree + row subtrees
+// (Liu). The SURVEY §8(d) byte count uses nnz(L) = offdiag*bs^2 + m*bs(bs+1)/2.
+struct FillCount {
+  std::int64_t diag = 0, offdiag = 0;
+  std::int64_t scalar(int bs) const {
+    return offdiag * bs * bs + diag * static_cast<std::int64_t>(bs) * (bs + 1) / 2;
+  }
+};
+FillCount structural_fill(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj,
+                          const std::vector<int>& order);
+
 // Permutes a block matrix: out node i = in node order[i].
 BlockMatrix permute(const BlockMatrix& A, const std::vector<int>& order);
 

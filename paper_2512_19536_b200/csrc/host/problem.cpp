@@ -426,6 +426,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
+  std::vector<std::int64_t> unit_fill(n_units, 0);
   parallel_for(n_units, [&](int u) {
     const auto& cells = units[u];
     const int m = static_cast<int>(cells.size());
@@ -446,6 +447,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       pos[i] = mesh.centroid(cells[i]);
     }
     nd[u] = nested_dissection(m, ap, aj, pos, leaf, nd_merge, nd_top);
+    unit_fill[u] = structural_fill(m, ap, aj, nd[u].order).scalar(b);
     unit_cells[u].resize(m);
     for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
   });
@@ -461,6 +463,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
   }
   pr.rank_cell_start[cfg.world] = N;
+  for (int u = 0; u < n_units; ++u)
+    if (unit_rank[u] == cfg.rank)
+      pr.l_struct += multi_sub ? unit_fill[u] : static_cast<std::int64_t>(b) * (b + 1) / 2 * units[u].size();
   pr.iperm.assign(N, -1);
   for (int i = 0; i < N; ++i) pr.iperm[pr.perm[i]] = i;
   pr.cell_begin = pr.rank_cell_start[cfg.rank];
@@ -867,6 +872,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       apos[a] = {0.5 * (abox[a].xmin + abox[a].xmax), 0.5 * (abox[a].ymin + abox[a].ymax)};
     }
     const NdTree cnd = nested_dissection(na, ap, aj, apos, std::clamp(64 / pr.bq, 4, 16));
+    pr.l0_struct = structural_fill(na, ap, aj, cnd.order).scalar(pr.bq);
     pr.n_agg = na;
     pr.agg_order = cnd.order;  // position -> label
     pr.coarse_nd = cnd;

@@ -121,6 +121,9 @@ struct Problem {
   NdTree coarse_nd;                     // coarse supernode tree (positions)
   Bsr K0;                               // coarse matrix in coarse internal order
   std::int64_t factor_values = 0;
+  // structural nnz(L) (scalar, lower incl. diagonal) of this rank's local
+  // factors and of the coarse factor, for the SURVEY §8(d) byte count
+  std::int64_t l_struct = 0, l0_struct = 0;
 
   // ionic geometry per local cell: bbox (4) and fan triangles
   std::vector<double> bbox;

@@ -250,6 +250,13 @@ class Problem:
             which, (self.dimension, self.dimension))
         return sp.csr_matrix((v, (r, c)), shape=shape)
 
+    def factor_stats(self) -> dict:
+        """Sizes for the SURVEY §8(d) byte model (pdg_problem_factor_stats)."""
+        st = (C.c_int64 * 6)()
+        lib().pdg_problem_factor_stats(self._handle(), st)
+        keys = ["l_struct", "l0_struct", "fwd_panel_doubles", "bwd_panel_doubles", "k_blocks", "e_doubles"]
+        return dict(zip(keys, list(st)))
+
     def owner(self, which: str = "subdomain") -> np.ndarray:
         o = np.zeros(self.n_cells, np.int32)
         lib().pdg_problem_owner(self._handle(), 0 if which == "subdomain" else 1, _lib.iptr(o))
