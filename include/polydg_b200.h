@@ -248,6 +248,14 @@ int pdg_condition_estimate(const double* alphas, const double* betas, int m, dou
 int pdg_nccl_unique_id_bytes(void);
 pdg_status pdg_nccl_get_unique_id(void* id128);
 pdg_status pdg_sim_attach_comm(pdg_sim* s, const void* id128, int rank, int world);
+/* In-process loopback transport: `world` simulations of one process (e.g. on
+ * one GPU), each driven by its own host thread, exchange halos and all-reduces
+ * through host staging. A test transport for the multi-rank data path where
+ * NCCL cannot run (NCCL rejects two ranks on one device); not a fast path. */
+typedef struct pdg_loopback pdg_loopback;
+pdg_status pdg_loopback_create(int world, pdg_loopback** out);
+void pdg_loopback_free(pdg_loopback* g);
+pdg_status pdg_sim_attach_loopback(pdg_sim* s, pdg_loopback* g, int rank, int world);
 
 #ifdef __cplusplus
 }

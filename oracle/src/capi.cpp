@@ -328,6 +328,18 @@ int orc_sim_cell_means(void* h, const double* U, double* means) {
   });
 }
 
+// l2_error against c0 cos(pi x) cos(pi y) e^{-c1 t} (acceptance.cpp:147-150)
+int orc_l2_error_cosine(void* h, const double* U, double c0, double c1, double t, double* err) {
+  return guarded([&] {
+    auto& s = *static_cast<orc::Simulation*>(h);
+    *err = orc::l2_error(s.D, orc::Vec(U, U + s.U.size()), [=](orc::P2 p) {
+      return c0 * std::cos(M_PI * p.x) * std::cos(M_PI * p.y) * std::exp(-c1 * t);
+    });
+  });
+}
+
+double orc_mesh_size(void* h) { return static_cast<orc::Simulation*>(h)->mesh.mesh_size(); }
+
 int orc_pcg_dense(int n, const double* A, const double* b, const double* Pm, double tol, int maxit,
                   const double* x0, double* x, orc_report* rep) {
   return guarded([&] {

@@ -698,6 +698,26 @@ Vec cell_means(const Discretization& D, const Vec& U) {
   return means;
 }
 
+// l2_error (dg_space.cpp:94-115): sqrt(sum_K sum_q w_q (u_h - g)^2) at order 2p+2
+double l2_error(const Discretization& D, const Vec& U, const std::function<double(P2)>& g) {
+  const int nl = D.nloc, nc = D.mesh->n_cells();
+  double acc = 0.0;
+  Vec val;
+  for (int e = 0; e < nc; ++e) {
+    const Rule r = polygon_rule(D.mesh->cell(e), 2 * D.p + 2);
+    eval_basis(D.mesh->bbox[e], D.p, r.pts, val, nullptr, nullptr);
+    for (std::size_t q = 0; q < r.w.size(); ++q) {
+      double u = 0.0;
+      for (int i = 0; i < nl; ++i) u += val[q * nl + i] * U[static_cast<int64_t>(e) * nl + i];
+      const double diff = u - g(r.pts[q]);
+      acc += r.w[q] * diff * diff;
+    }
+  }
+  return std::sqrt(acc);
+}
+
+double MeshView::mesh_size() const { return *std::max_element(diam.begin(), diam.end()); }
+
 // ---------------- ionics ----------------
 double fhn_current(const double* P, double u, double w) {
   if (!std::isfinite(u) || !std::isfinite(w)) throw SolverError("fhn: non-finite state in current evaluation");

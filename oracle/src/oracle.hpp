@@ -108,6 +108,7 @@ struct MeshView {
   std::vector<double> diam;
   std::vector<Box> bbox;
   int n_cells() const { return static_cast<int>(region.size()); }
+  double mesh_size() const;  // max cell diameter (mesh.cpp:40-47)
   std::vector<P2> cell(int c) const;
   void build();
 };
@@ -150,6 +151,8 @@ struct Discretization {
 
 // ---- snapshot.cpp:13-28 ----
 Vec cell_means(const Discretization& D, const Vec& U);
+// ---- dg_space.cpp:94-115 ----
+double l2_error(const Discretization& D, const Vec& U, const std::function<double(P2)>& g);
 
 // ---- ionics (ionics.cpp:20-113) ----
 double fhn_current(const double* prm, double u, double w);

@@ -137,6 +137,9 @@ def _bind_device(L):
         "pdg_nccl_unique_id_bytes": (i32, []),
         "pdg_nccl_get_unique_id": (i32, [vp]),
         "pdg_sim_attach_comm": (i32, [vp, vp, i32, i32]),
+        "pdg_loopback_create": (i32, [i32, P(vp)]),
+        "pdg_loopback_free": (None, [vp]),
+        "pdg_sim_attach_loopback": (i32, [vp, vp, i32, i32]),
         "pdg_sim_timer": (i32, [vp, i32, P(dbl)]),
         "pdg_sim_kernel_launches": (i64, [vp]),
         "pdg_sim_profile": (i32, [vp, i32, P(dbl), P(i64)]),

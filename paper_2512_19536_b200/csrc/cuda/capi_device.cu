@@ -241,6 +241,12 @@ pdg_status pdg_sim_attach_comm(pdg_sim* s, const void* id128, int rank, int worl
   return pdg::guarded([&] { S(s).attach_comm(id128, rank, world); });
 }
 
+pdg_status pdg_sim_attach_loopback(pdg_sim* s, pdg_loopback* g, int rank, int world) {
+  return pdg::guarded([&] {
+    S(s).attach_loopback(*reinterpret_cast<std::shared_ptr<pdg::LoopbackGroup>*>(g), rank, world);
+  });
+}
+
 pdg_status pdg_sim_pcg_device(pdg_sim* s, const double* d_b, const double* d_x0, double tol, int maxit,
                               double* d_x, pdg_pcg_report* rep) {
   return pdg::guarded([&] {

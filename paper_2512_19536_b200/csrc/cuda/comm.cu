@@ -11,6 +11,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstring>
 #include <string>
 
@@ -74,34 +77,126 @@ T* dmalloc(std::size_t n) {
 
 }  // namespace
 
+// ---- transports ----
+// NCCL: one communicator per rank (one process per GPU), stream-ordered.
+class NcclTransport final : public Transport {
+ public:
+  explicit NcclTransport(ncclComm_t c) : comm_(c) {}
+  ~NcclTransport() override { nccl().CommDestroy(comm_); }
+  void allreduce(const double* src, double* dst, long long count, cudaStream_t st) override {
+    nccl_check(nccl().AllReduce(src, dst, static_cast<size_t>(count), ncclFloat64, ncclSum, comm_, st),
+               "ncclAllReduce");
+  }
+  void exchange(DeviceSim& s, double* v) override {
+    auto& api = nccl();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (const auto& h : s.halo_peers) {
+      if (h.send_count)
+        nccl_check(api.Send(s.d_sendbuf + static_cast<long long>(h.send_off) * s.b,
+                            static_cast<size_t>(h.send_count) * s.b, ncclFloat64, h.peer, comm_, s.st),
+                   "ncclSend");
+      if (h.recv_count)
+        nccl_check(api.Recv(v + (static_cast<long long>(s.ncells) + h.recv_off) * s.b,
+                            static_cast<size_t>(h.recv_count) * s.b, ncclFloat64, h.peer, comm_, s.st),
+                   "ncclRecv");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+  const char* name() const override { return "nccl"; }
+
+ private:
+  ncclComm_t comm_;
+};
+
+// Loopback: `world` DeviceSims in ONE process (any devices, typically one
+// GPU), each driven by its own host thread. Every exchange goes through host
+// staging between two barriers: a test transport that runs the complete
+// multi-rank data path (halo pack, halo tail layout, combined coarse/dot
+// all-reduce, finish kernels, redundant coarse solve, host-driven loop) where
+// NCCL cannot (it rejects two ranks on one device). Sums run in rank order.
+struct LoopbackGroup {
+  explicit LoopbackGroup(int w) : world(w), buf(w), peers(w, nullptr), sims(w, nullptr) {}
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<std::vector<double>> buf;           // per rank staging
+  std::vector<const std::vector<DeviceSim::HaloPeer>*> peers;
+  std::vector<DeviceSim*> sims;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return generation != gen; }))
+      throw CudaError("loopback transport: a peer rank did not arrive (timeout)");
+  }
+};
+
+class LoopbackTransport final : public Transport {
+ public:
+  LoopbackTransport(std::shared_ptr<LoopbackGroup> g, int rank) : g_(std::move(g)), rank_(rank) {}
+  void allreduce(const double* src, double* dst, long long count, cudaStream_t st) override {
+    auto& mine = g_->buf[rank_];
+    mine.resize(static_cast<std::size_t>(count));
+    PDG_CUDA(cudaMemcpyAsync(mine.data(), src, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    g_->barrier();
+    sum_.assign(static_cast<std::size_t>(count), 0.0);
+    for (int r = 0; r < g_->world; ++r) {
+      if (static_cast<long long>(g_->buf[r].size()) != count)
+        throw CudaError("loopback transport: all-reduce sizes differ between ranks");
+      for (long long i = 0; i < count; ++i) sum_[i] += g_->buf[r][i];
+    }
+    g_->barrier();  // every rank has read every buffer
+    PDG_CUDA(cudaMemcpyAsync(dst, sum_.data(), count * sizeof(double), cudaMemcpyHostToDevice, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+  }
+  void exchange(DeviceSim& s, double* v) override {
+    long long nsend = 0;
+    for (const auto& h : s.halo_peers) nsend = std::max<long long>(nsend, h.send_off + h.send_count);
+    auto& mine = g_->buf[rank_];
+    mine.resize(static_cast<std::size_t>(nsend * s.b));
+    if (nsend)
+      PDG_CUDA(cudaMemcpyAsync(mine.data(), s.d_sendbuf, nsend * s.b * sizeof(double), cudaMemcpyDeviceToHost, s.st));
+    PDG_CUDA(cudaStreamSynchronize(s.st));
+    g_->peers[rank_] = &s.halo_peers;
+    g_->barrier();
+    for (const auto& h : s.halo_peers) {
+      if (!h.recv_count) continue;
+      const DeviceSim::HaloPeer* src = nullptr;
+      for (const auto& o : *g_->peers[h.peer])
+        if (o.peer == rank_) src = &o;
+      if (!src || src->send_count != h.recv_count)
+        throw CudaError("loopback transport: halo plans of the two ranks disagree");
+      PDG_CUDA(cudaMemcpyAsync(v + (static_cast<long long>(s.ncells) + h.recv_off) * s.b,
+                               g_->buf[h.peer].data() + static_cast<long long>(src->send_off) * s.b,
+                               static_cast<std::size_t>(h.recv_count) * s.b * sizeof(double), cudaMemcpyHostToDevice,
+                               s.st));
+    }
+    PDG_CUDA(cudaStreamSynchronize(s.st));
+    g_->barrier();
+  }
+  const char* name() const override { return "loopback"; }
+
+ private:
+  std::shared_ptr<LoopbackGroup> g_;
+  int rank_;
+  std::vector<double> sum_;
+};
+
 void DeviceSim::comm_allreduce(const double* src, double* dst, long long count) {
-  nccl_check(nccl().AllReduce(src, dst, static_cast<size_t>(count), ncclFloat64, ncclSum,
-                              static_cast<ncclComm_t>(comm), st),
-             "ncclAllReduce");
+  transport->allreduce(src, dst, count, st);
 }
 
-void DeviceSim::comm_exchange(double* v) {
-  auto& api = nccl();
-  nccl_check(api.GroupStart(), "ncclGroupStart");
-  for (const HaloPeer& h : halo_peers) {
-    if (h.send_count)
-      nccl_check(api.Send(d_sendbuf + static_cast<long long>(h.send_off) * b, static_cast<size_t>(h.send_count) * b,
-                          ncclFloat64, h.peer, static_cast<ncclComm_t>(comm), st),
-                 "ncclSend");
-    if (h.recv_count)
-      nccl_check(api.Recv(v + (static_cast<long long>(ncells) + h.recv_off) * b, static_cast<size_t>(h.recv_count) * b,
-                          ncclFloat64, h.peer, static_cast<ncclComm_t>(comm), st),
-                 "ncclRecv");
-  }
-  nccl_check(api.GroupEnd(), "ncclGroupEnd");
-}
+void DeviceSim::comm_exchange(double* v) { transport->exchange(*this, v); }
 
-void DeviceSim::comm_destroy() {
-  if (comm) {
-    nccl().CommDestroy(static_cast<ncclComm_t>(comm));
-    comm = nullptr;
-  }
-}
+void DeviceSim::comm_destroy() { transport.reset(); }
 
 void DeviceSim::attach_comm(const void* id128, int r, int w) {
   Problem& pr = *P;
@@ -109,13 +204,30 @@ void DeviceSim::attach_comm(const void* id128, int r, int w) {
     throw ConfigError("attach_comm: rank/world differ from the configuration the problem was built for");
   if (w == 1) return;
   // K0 below is all-reduced in place: a second attach would scale it by world
-  if (comm) throw ConfigError("attach_comm: a communicator is already attached");
+  if (transport) throw ConfigError("attach_comm: a communicator is already attached");
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof id);
   ncclComm_t c = nullptr;
   PDG_CUDA(cudaSetDevice(pr.cfg.device));
   nccl_check(nccl().CommInitRank(&c, w, id, r), "ncclCommInitRank");
-  comm = c;
+  connect(std::make_unique<NcclTransport>(c));
+}
+
+void DeviceSim::attach_loopback(const std::shared_ptr<LoopbackGroup>& g, int r, int w) {
+  Problem& pr = *P;
+  if (w != pr.cfg.world || r != pr.cfg.rank || w != g->world)
+    throw ConfigError("attach_loopback: rank/world differ from the configuration the problem was built for");
+  if (w == 1) return;
+  if (transport) throw ConfigError("attach_comm: a communicator is already attached");
+  PDG_CUDA(cudaSetDevice(pr.cfg.device));
+  connect(std::make_unique<LoopbackTransport>(g, r));
+}
+
+// halo plan, reduction scratch, K0 summed over ranks, coarse factor
+void DeviceSim::connect(std::unique_ptr<Transport> t) {
+  Problem& pr = *P;
+  const int r = pr.cfg.rank, w = pr.cfg.world;
+  transport = std::move(t);
   d_dot_local = dmalloc<double>(1);
   d_dot_global = dmalloc<double>(1);
 
@@ -126,9 +238,9 @@ void DeviceSim::attach_comm(const void* id128, int r, int w) {
   halo_peers.clear();
   for (int peer = 0; peer < w; ++peer) {
     if (peer == r) continue;
-    const auto& s = send[peer];
-    HaloPeer h{peer, static_cast<int>(send_cells.size()), static_cast<int>(s.size()), 0, 0};
-    send_cells.insert(send_cells.end(), s.begin(), s.end());
+    const auto& sc = send[peer];
+    HaloPeer h{peer, static_cast<int>(send_cells.size()), static_cast<int>(sc.size()), 0, 0};
+    send_cells.insert(send_cells.end(), sc.begin(), sc.end());
     const auto lo = std::lower_bound(halo_cells.begin(), halo_cells.end(), pr.rank_cell_start[peer]);
     const auto hi = std::lower_bound(halo_cells.begin(), halo_cells.end(), pr.rank_cell_start[peer + 1]);
     h.recv_off = static_cast<int>(lo - halo_cells.begin());
@@ -171,5 +283,15 @@ pdg_status pdg_nccl_get_unique_id(void* id128) {
     std::memcpy(id128, &id, sizeof id);
   });
 }
+
+pdg_status pdg_loopback_create(int world, pdg_loopback** out) {
+  return pdg::guarded([&] {
+    if (world < 1) throw pdg::ConfigError("loopback: world must be >= 1");
+    *out = reinterpret_cast<pdg_loopback*>(new std::shared_ptr<pdg::LoopbackGroup>(
+        std::make_shared<pdg::LoopbackGroup>(world)));
+  });
+}
+
+void pdg_loopback_free(pdg_loopback* g) { delete reinterpret_cast<std::shared_ptr<pdg::LoopbackGroup>*>(g); }
 
 }  // extern "C"

@@ -125,7 +125,8 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     d_cell_agg = dupload(pr.cell_agg, st);
     d_agg_ptr = dupload(pr.agg_cell_ptr, st);
     d_agg_cells = dupload(pr.agg_cells, st);
-    d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
+    // + 1: the multi-rank loop all-reduces [r0 ; ||r||^2 partial] in one call
+    d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq + 1);
     d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
     // restriction chunks: <= kChunk (<= 64) cells of one agglomerate per CTA;
     // small chunks keep the fused update + restriction spread over all SMs
@@ -651,9 +652,10 @@ void DeviceSim::precond_apply(const double* r, double* z, int finish, bool honor
     after_reduce(finish, honor);
     return;
   }
-  if (pr.two_level) {
-    // restricted: the chunk partials came from the fused update (record_iteration)
-    if (!restricted) launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, r, d_r0part, Sh, st);
+  if (pr.two_level && !restricted) {
+    // restricted: r0 is already in place (single rank: the chunk partials of
+    // the fused update; several ranks: combined and all-reduced with ||r||^2)
+    launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, r, d_r0part, Sh, st);
     if (world > 1) {
       launch_restrict_combine(bq, pr.n_agg, d_node_chunk_ptr, d_r0part, d_r0, Sh, st);
       coarse_reduce_hook();
@@ -713,6 +715,28 @@ void DeviceSim::record_iteration(int parity) {
     launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
   }
   after_reduce(kFinPq, true);
+  if (world > 1) {
+    // Several ranks: the update stores this rank's ||r||^2 partial behind r0,
+    // the restriction runs speculatively (gated kernels, before the
+    // convergence test), and ONE all-reduce carries [r0 ; ||r||^2]. Per
+    // iteration: the p halo + three all-reduces (p.q, [r0 ; r.r], r.z).
+    const bool coarse = use_pc() && P->two_level;
+    const long long nr0 = coarse ? static_cast<long long>(P->n_agg) * P->bq : 0;
+    double* rr = coarse ? d_r0 + nr0 : d_dot_local;
+    launch_update(n, d_x, d_r, p, d_q, rctx(kFinStore, rr), st);
+    if (coarse) {
+      launch_restrict(b, bq, n_chunks, d_chunk_ptr, d_agg_cells, d_E, d_r, d_r0part, d_S, st);
+      launch_restrict_combine(bq, P->n_agg, d_node_chunk_ptr, d_r0part, d_r0, d_S, st);
+      comm_allreduce(d_r0, d_r0, nr0 + 1);
+      launch_finish(rctx(kFinRr), rr, true, st);
+    } else {
+      comm_allreduce(d_dot_local, d_dot_global, 1);
+      launch_finish(rctx(kFinRr), d_dot_global, true, st);
+    }
+    precond_apply(d_r, z_of(d_r), kFinRz, true, coarse);
+    if (!pfuse) launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
+    return;
+  }
   const bool fuse = use_pc() && P->two_level && world == 1;
   if (fuse && chunks_contiguous)
     launch_update_restrict_tma(b, bq, n_chunks, max_chunk_cells, d_chunk_ptr, d_agg_cells, d_E, d_x, d_r, p, d_q,
@@ -795,7 +819,7 @@ void DeviceSim::run_solve(int maxit, PcgResult& res) {
     // multi-rank: host-driven loop (NCCL calls stay outside conditional
     // graphs); every rank sees the same all-reduced scalars, so all ranks
     // stop after the same iteration and issue the same collectives.
-    if (world > 1 && !comm) throw SolverError("multi-rank simulation: call pdg_sim_attach_comm first");
+    if (world > 1 && !transport) throw SolverError("multi-rank simulation: call pdg_sim_attach_comm first");
     record_solve_tail();
     constexpr int kPoll = 4;
     for (int it = 0; it < maxit;) {
@@ -1031,7 +1055,7 @@ int DeviceSim::body_launches() const {
   const int fused = (use_pc() && P->two_level && world == 1) ? 1 : 0;
   // spmv, update, preconditioner, pupdate (folded into the spmv with pfuse), set_condition
   int k = 1 + 1 + precond_launches() - fused + (pfuse ? 0 : 1) + (world == 1 && !pfuse ? 1 : 0);
-  if (world > 1) k += 3 + static_cast<int>(halo_peers.size());
+  if (world > 1) k += 3 + static_cast<int>(halo_peers.size());  // finish kernels + halo packs
   return k;
 }
 

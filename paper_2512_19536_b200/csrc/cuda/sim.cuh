@@ -30,6 +30,20 @@ int sweep_ctas_per_sm(int smem);  // occupancy of the sweep kernel
 // Extreme-eigenvalue ratio of the Lanczos tridiagonal (krylov.cpp:85-103).
 bool lanczos_condition(const double* alpha, const double* beta, int m, double* kappa);
 
+class DeviceSim;
+struct LoopbackGroup;
+
+// Exchanges of the multi-rank data path (comm.cu): NCCL between processes, or
+// an in-process loopback group (test transport for several ranks on one GPU).
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual void allreduce(const double* src, double* dst, long long count, cudaStream_t st) = 0;
+  // halo tail of v from the peers' packed d_sendbuf
+  virtual void exchange(DeviceSim& s, double* v) = 0;
+  virtual const char* name() const = 0;
+};
+
 class DeviceSim {
  public:
   explicit DeviceSim(std::unique_ptr<Problem> prob);
@@ -113,7 +127,7 @@ class DeviceSim {
 
   // ---- multi-rank state (comm.cu) ----
   int rank = 0, world = 1;
-  void* comm = nullptr;  // ncclComm_t
+  std::unique_ptr<Transport> transport;
   struct HaloPeer {
     int peer;
     int send_off, send_count;  // cells in d_send_cells / d_sendbuf
@@ -124,6 +138,8 @@ class DeviceSim {
   double* d_sendbuf = nullptr;
   double *d_dot_local = nullptr, *d_dot_global = nullptr;
   void attach_comm(const void* id128, int rank, int world);
+  void attach_loopback(const std::shared_ptr<LoopbackGroup>& g, int rank, int world);
+  void connect(std::unique_ptr<Transport> t);
   void comm_allreduce(const double* src, double* dst, long long count);
   void comm_exchange(double* v);
   void release_tasks();

@@ -387,5 +387,26 @@ class Simulation:
         return x, out
 
 
+class LoopbackGroup:
+    """In-process transport for `world` ranks (pdg_loopback_create): every
+    rank's Simulation lives in this process, typically on one GPU, and is
+    driven from its own thread. Exercises the whole multi-rank data path where
+    NCCL cannot run (two ranks on one device). Not a fast path."""
+
+    def __init__(self, world: int):
+        self._h = C.c_void_p()
+        check(lib().pdg_loopback_create(int(world), C.byref(self._h)))
+        self.world = world
+
+    def attach(self, sim: "Simulation") -> None:
+        check(lib().pdg_sim_attach_loopback(sim._handle(), self._h, sim.config.rank, self.world))
+        sim._group = self  # the group outlives its members
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().pdg_loopback_free(self._h)
+            self._h = None
+
+
 def run_simulation(config: SimulationConfig) -> SimulationResult:
     return Simulation(config).run()

@@ -72,6 +72,8 @@ def lib():
             "orc_config_default": (None, [P(PdgConfig)]),
             "orc_uniform_rhs": (None, [C.c_uint64, i64, P(dbl)]),
             "orc_sim_factor_blocks": (i64, [vp, i32]),
+            "orc_l2_error_cosine": (i32, [vp, P(dbl), dbl, dbl, dbl, P(dbl)]),
+            "orc_mesh_size": (dbl, [vp]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(L, k)
@@ -261,6 +263,16 @@ class OracleSim:
         if which in ("K", "M", "A", "Krhs"):
             shape = (self.dimension, self.dimension)
         return sp.csr_matrix((v, (r, c)), shape=shape)
+
+    def l2_error_cosine(self, U, c0, c1, t):
+        """l2_error (dg_space.cpp:94-115) of U against c0 cos(pi x) cos(pi y) e^{-c1 t}."""
+        e = C.c_double()
+        _check(lib().orc_l2_error_cosine(self._h, _d(np.ascontiguousarray(U, dtype=np.float64)), c0, c1, t,
+                                         C.byref(e)))
+        return e.value
+
+    def mesh_size(self):
+        return lib().orc_mesh_size(self._h)
 
     def factor_blocks(self, coarse=False):
         """Stored b x b blocks of the oracle's local (or coarse) factors."""

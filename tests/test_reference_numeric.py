@@ -1,0 +1,150 @@
+"""The oracle against the REFERENCE's own numeric code (CPU, no GPU).
+
+oracle/_ref/libpolydg_refnum.so is the reference's proj/src numeric path
+(assembly, ionics, krylov, schwarz, timestepper, ...) compiled where it lies
+with the Eigen API stand-in oracle/eigen_shim (tests/refnum.py). Where it is
+present (this container) the restated oracle (oracle/src) is compared with it
+directly; everywhere, the oracle is compared with the committed golden outputs
+of that reference build (tests/golden/reference_numeric.json, written by
+scripts/make_reference_golden.py): acceptance criteria 2, 3, 7, 8, 9
+(proj/tests/acceptance.cpp:138-203,339-400), BASELINE config 1 over all 100
+steps, and the reference's default Simulation.
+"""
+import json
+import math
+import pathlib
+
+import numpy as np
+import pytest
+
+from tests import refnum
+from tests.oracle_binding import OracleError, oracle_for, uniform_rhs
+from tests.reference_configs import config1, default_sim, manufactured, paper
+
+GOLD = json.loads((pathlib.Path(__file__).parent / "golden" / "reference_numeric.json").read_text())
+need_ref = pytest.mark.skipif(not refnum.available(), reason="reference numeric build absent (oracle/_ref)")
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def _steps(sim, n):
+    return [sim.step()["iterations"] for _ in range(n)]
+
+
+@need_ref
+def test_reference_build_matches_oracle_operators():
+    R = refnum.RefSim(config1())
+    O, _ = oracle_for(config1())
+    for w in ("M", "A", "K", "E"):  # same triplet streams summed in the same order: bitwise
+        a, b = R.export(w), O.export(w)
+        assert a.nnz == b.nnz and abs(a - b).max() == 0.0, w
+    K0r, K0o = R.export("K0"), O.export("K0")  # E^T K E: product orders differ
+    assert abs(K0r - K0o).max() <= 1e-12 * abs(K0o).max()
+    b = uniform_rhs(42, O.dimension)
+    assert _rel(R.apply_K(b), O.apply_K(b)) <= 1e-15
+    assert _rel(R.apply_precond(b), O.apply_precond(b)) <= 1e-13
+
+
+@need_ref
+@pytest.mark.parametrize("use_precond", [True, False])
+def test_reference_build_pcg_semantics_match_oracle(use_precond):
+    R = refnum.RefSim(config1())
+    O, _ = oracle_for(config1())
+    b = uniform_rhs(7, O.dimension)
+    xr, rr = R.pcg_solve(b, 1e-10, use_precond=use_precond)
+    xo, ro = O.pcg_solve(b, 1e-10, use_precond=use_precond)
+    assert rr["iterations"] == ro["iterations"] and rr["converged"] and ro["converged"]
+    assert _rel(xr, xo) <= 1e-12
+    assert _rel(rr["alphas"], ro["alphas"]) <= 1e-10 and _rel(rr["betas"], ro["betas"]) <= 1e-10
+    assert _rel(rr["residual_history"], ro["residual_history"]) <= 1e-10
+    assert abs(rr["condition_estimate"] - ro["condition_estimate"]) <= 1e-8 * ro["condition_estimate"]
+    # krylov.cpp:22-24 / 30-35: the same failures and the zero right-hand side
+    for sim, err in ((R, refnum.RefError), (O, OracleError)):
+        with pytest.raises(err, match="tol must lie"):
+            sim.pcg_solve(b, 1.5)
+        x0, rep = sim.pcg_solve(np.zeros_like(b), 1e-10)
+        assert rep["converged"] and rep["iterations"] == 0 and list(rep["residual_history"]) == [0.0]
+
+
+def test_oracle_matches_reference_config1_full_run():
+    cfg = config1()
+    O, _ = oracle_for(cfg)
+    its = _steps(O, cfg.n_steps())
+    g = GOLD["config1"]
+    assert max(abs(a - b) for a, b in zip(its, g["iterations"])) <= 1
+    _, _, U, _, Y, _ = O.state()
+    assert _rel(U, g["U"]) <= 1e-12 and _rel(Y[0], g["Y"]) <= 1e-12
+
+
+def test_oracle_matches_reference_default_simulation():
+    cfg = default_sim()
+    O, _ = oracle_for(cfg)
+    its = _steps(O, cfg.n_steps())
+    g = GOLD["default_sim"]
+    assert max(abs(a - b) for a, b in zip(its, g["iterations"])) <= 1
+    _, _, U, _, Y, _ = O.state()
+    assert _rel(U, g["U"]) <= 1e-12 and _rel(Y[0], g["Y"]) <= 1e-12
+
+
+def check_iteration_criteria(run):
+    """Acceptance criteria 7-9 (acceptance.cpp:339-400) on `run(cfg) -> per-step
+    iterations`, with every step within +-1 of the reference build's."""
+    g = GOLD["iterations"]
+    got = {}
+    for key, cfg in {"c7_two_level": paper(512, 1, 2, "two-level"), "c7_cg": paper(512, 1, 2, "none"),
+                     "c8_128": paper(128, 1, 2, "two-level"), "c8_2048": paper(2048, 1, 2, "two-level"),
+                     "c9_4": paper(512, 1, 4, "two-level"), "c9_8": paper(512, 1, 8, "two-level")}.items():
+        got[key] = run(cfg)
+        assert max(abs(a - b) for a, b in zip(got[key], g[key])) <= 1, key
+    avg = {k: float(np.mean(v)) for k, v in got.items()}
+    assert avg["c7_two_level"] <= 0.25 * avg["c7_cg"]                      # criterion 7
+    spread = [avg["c8_128"], avg["c7_two_level"], avg["c8_2048"]]
+    assert max(spread) / min(spread) <= 1.35                                 # criterion 8
+    assert avg["c7_two_level"] < avg["c9_4"] < avg["c9_8"]                  # criterion 9
+    return avg
+
+
+def test_oracle_acceptance_iteration_criteria():
+    check_iteration_criteria(lambda cfg: _steps(oracle_for(cfg)[0], cfg.n_steps()))
+
+
+def check_convergence_criteria(final_state, l2_error_of):
+    """Acceptance criteria 2 and 3 (acceptance.cpp:138-203): observed spatial
+    order >= p + 0.8 and temporal order 2 +- 0.2, errors equal to the
+    reference build's to 1e-6 relative. final_state(cfg) -> (U, sim-like);
+    l2_error_of(cfg, U) -> l2_error against the manufactured solution."""
+    g2 = GOLD["criterion2"]
+    for p in (1, 2):
+        errs = [l2_error_of(manufactured(c, p, 1e-4, 0.02), final_state(manufactured(c, p, 1e-4, 0.02))[0])
+                for c in (128, 512, 2048)]
+        ref = g2[str(p)]
+        for e, r in zip(errs, ref["errors"]):
+            assert abs(e - r) <= 1e-6 * r
+        slope = float(np.polyfit(np.log(ref["h"]), np.log(errs), 1)[0])
+        assert slope >= p + 0.8
+    g3 = GOLD["criterion3"]
+    uref, M = final_state(manufactured(64, 1, 1.25e-4, 0.4), want_mass=True)
+    assert _rel(uref, g3["u_fine"]) <= 1e-10
+    errs = []
+    for dt in g3["dts"]:
+        d = final_state(manufactured(64, 1, dt, 0.4))[0] - uref
+        errs.append(math.sqrt(d @ (M @ d)))
+    for e, r in zip(errs, g3["errors"]):
+        assert abs(e - r) <= 1e-6 * r
+    slope = float(np.polyfit(np.log(g3["dts"]), np.log(errs), 1)[0])
+    assert abs(slope - 2.0) <= 0.2
+
+
+@pytest.mark.slow
+def test_oracle_acceptance_convergence_criteria():
+    def final_state(cfg, want_mass=False):
+        O, _ = oracle_for(cfg)
+        _steps(O, cfg.n_steps())
+        return O.state()[2], (O.export("M") if want_mass else None)
+
+    def l2(cfg, U):
+        return oracle_for(cfg)[0].l2_error_cosine(U, 1.0, 1.0, cfg.T)
+
+    check_convergence_criteria(final_state, l2)
