@@ -21,6 +21,7 @@
 #include <random>
 #include <string>
 
+#include "ordering.hpp"
 #include "parallel.hpp"
 #include "quadrature.hpp"
 
@@ -424,6 +425,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
   int nd_top = nd_merge;
   if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
+  // PDG_ORDER=md: minimum degree + fundamental supernodes (relaxed by PDG_MD_RELAX cells)
+  const bool md_order = std::getenv("PDG_ORDER") && std::string(std::getenv("PDG_ORDER")) == "md";
+  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::atoi(std::getenv("PDG_MD_RELAX")) : 1;
   std::vector<NdTree> nd(n_units);
   std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
   std::vector<std::int64_t> unit_fill(n_units, 0);
@@ -446,7 +450,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       ap.push_back(static_cast<int>(aj.size()));
       pos[i] = mesh.centroid(cells[i]);
     }
-    nd[u] = nested_dissection(m, ap, aj, pos, leaf, nd_merge, nd_top);
+    nd[u] = md_order ? md_supernodes(m, ap, aj, md_relax) : nested_dissection(m, ap, aj, pos, leaf, nd_merge, nd_top);
     unit_fill[u] = structural_fill(m, ap, aj, nd[u].order).scalar(b);
     unit_cells[u].resize(m);
     for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];

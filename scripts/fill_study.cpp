@@ -1,0 +1,82 @@
+// Fill study for the Schwarz local factors (development tool, not product):
+// structural nnz(L) and stored supernodal bytes of several orderings on a
+// sample of the subdomains of a seeded mesh.
+//   g++ -O2 -std=c++20 -I paper_2512_19536_b200/csrc/host scripts/fill_study.cpp build/csrc/host/*.o -lpthread
+//   ./a.out N S sample_every
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <numeric>
+
+#include "factor.hpp"
+#include "mesh.hpp"
+#include "ordering.hpp"
+
+using namespace pdg;
+
+int main(int argc, char** argv) {
+  const int N = argc > 1 ? atoi(argv[1]) : 1048576;
+  const int S = argc > 2 ? atoi(argv[2]) : 512;
+  const int every = argc > 3 ? atoi(argv[3]) : 16;
+  const int bs = argc > 4 ? atoi(argv[4]) : 10;
+  auto t0 = std::chrono::steady_clock::now();
+  Mesh mesh = assign_regions(generate_mesh(N, Box{0, 0, 1, 1}, 42, 5), 0.5);
+  Partition part = agglomerate(mesh, S);
+  auto t1 = std::chrono::steady_clock::now();
+  fprintf(stderr, "mesh+partition %.1f s\n", std::chrono::duration<double>(t1 - t0).count());
+  std::vector<std::vector<int>> nbr(mesh.n_cells());
+  for (const Face& f : mesh.interior_faces()) {
+    nbr[f.cell_in].push_back(f.cell_out);
+    nbr[f.cell_out].push_back(f.cell_in);
+  }
+  auto members = part.members();
+  struct Acc {
+    double cells = 0, structural = 0, stored = 0, nsn = 0, height = 0, n = 0;
+  };
+  std::map<std::string, Acc> acc;
+  for (int u = 0; u < part.count; u += every) {
+    const auto& cells = members[u];
+    const int m = static_cast<int>(cells.size());
+    std::map<int, int> loc;
+    for (int i = 0; i < m; ++i) loc[cells[i]] = i;
+    std::vector<int> ap{0}, aj;
+    std::vector<Pt> pos(m);
+    for (int i = 0; i < m; ++i) {
+      for (int nb : nbr[cells[i]]) {
+        auto it = loc.find(nb);
+        if (it != loc.end()) aj.push_back(it->second);
+      }
+      ap.push_back(static_cast<int>(aj.size()));
+      pos[i] = mesh.centroid(cells[i]);
+    }
+    auto add = [&](const std::string& name, const NdTree& t) {
+      FillCount f = structural_fill(m, ap, aj, t.order);
+      auto st = supernode_storage(m, ap, aj, t);
+      Acc& a = acc[name];
+      a.cells += m;
+      a.structural += f.offdiag + f.diag;
+      a.stored += st.blocks;
+      a.nsn += st.supernodes;
+      std::vector<int> h(t.parent.size(), 1);
+      int hmax = 0;
+      for (size_t s = 0; s < t.parent.size(); ++s) {
+        hmax = std::max(hmax, h[s]);
+        if (t.parent[s] >= 0) h[t.parent[s]] = std::max(h[t.parent[s]], h[s] + 1);
+      }
+      a.height += hmax;
+      a.n += 1;
+    };
+    add("nd_leaf6", nested_dissection(m, ap, aj, pos, 6, 1, 1));
+    for (int leaf : {32, 64, 128}) {
+      NdTree nd = nested_dissection(m, ap, aj, pos, leaf, 1, 1);
+      for (int relax : {4, 6, 8}) add("nd" + std::to_string(leaf) + "+md relax" + std::to_string(relax),
+                                      hybrid_md_supernodes(m, ap, aj, nd, relax));
+    }
+    for (int relax : {1, 4, 6, 8, 12}) add("md relax" + std::to_string(relax), md_supernodes(m, ap, aj, relax));
+  }
+  for (auto& [k, a] : acc)
+    printf("%-28s structural %.2f blocks/cell  stored %.2f blocks/cell (x%.3f)  cells/supernode %.1f height %.0f\n", k.c_str(),
+           a.structural / a.cells, a.stored / a.cells, a.stored / a.structural, a.cells / a.nsn, a.height / a.n);
+}
