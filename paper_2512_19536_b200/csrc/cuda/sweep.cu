@@ -79,14 +79,26 @@ __device__ __forceinline__ long long gtimer() {
 // A count that never arrives is a schedule bug: fail the launch instead of
 // hanging the device.
 __device__ __forceinline__ void wait_count(const int* flag, int need) {
-  if (ld_relaxed_s(flag) < need) {
-    const long long t0 = clock64();
-    do {
-      __nanosleep(PDG_SPIN_NS);
-      if (clock64() - t0 > (1LL << 33)) __trap();
-    } while (ld_relaxed_s(flag) < need);
-  }
+  // common case (the list schedule releases units after their dependencies):
+  // one acquire load and done
+  if (ld_acquire_s(flag) >= need) return;
+  const long long t0 = clock64();
+  do {
+    __nanosleep(PDG_SPIN_NS);
+    if (clock64() - t0 > (1LL << 33)) __trap();
+  } while (ld_relaxed_s(flag) < need);
   (void)ld_acquire_s(flag);
+}
+// panel loads: read-only path; EF marks the lines evict-first in L2 once read,
+// so consumed panel lines give way before prefetched, not-yet-read ones
+template <bool EF>
+__device__ __forceinline__ double2 ld_panel(const double2* p, unsigned long long pol) {
+  if (!EF) return __ldg(p);
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
 }
 // named barrier for the staging warps (1..kWarps-1) only
 __device__ __forceinline__ void staging_sync() {
@@ -129,14 +141,23 @@ __device__ __forceinline__ void fetch_ahead(const SweepArgs& a, Ahead& q) {
 // L2 bulk prefetch of the running unit's panel (issued when the unit starts:
 // prefetching the lookahead units as well overcommits the L2)
 __device__ __forceinline__ void prefetch_panel(const SweepArgs& a, const DevUnit& u) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((u.dir == 0 ? a.fmat : a.hmat) + u.src_off),
-               "r"(u.bytes)
-               : "memory");
+  const double* src = (u.dir == 0 ? a.fmat : a.hmat) + u.src_off;
+  if (a.prefetch & 4) {  // prefetched lines evict-last until read (evict-first) by the unit
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(u.bytes), "l"(pol)
+                 : "memory");
+    return;
+  }
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(u.bytes) : "memory");
 }
 
 // one warp: rows of tile `tl` restricted to input columns [j0, j1) of the
 // panel `m` (tile base, global, L2-prefetched); (row 2*l2, row 2*l2+1) sums in half 0
+template <bool EF>
 __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, const double* x, int j0, int j1) {
+  unsigned long long pol = 0;
+  if (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const int lane = threadIdx.x & 31, half = lane >> 4, l2 = lane & 15;
   double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
   if (2 * l2 < tl.rows) {
@@ -147,7 +168,7 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
     for (; j + 2 * D - 2 < j1; j += 2 * D) {
       double2 v[D];
 #pragma unroll
-      for (int u = 0; u < D; ++u) v[u] = __ldg(mm + (j + 2 * u) * cs);
+      for (int u = 0; u < D; ++u) v[u] = ld_panel<EF>(mm + (j + 2 * u) * cs, pol);
 #pragma unroll
       for (int u = 0; u < D; u += 4) {
         acc0.x = fma(v[u].x, x[j + 2 * u], acc0.x);
@@ -161,7 +182,7 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
       }
     }
     for (; j < j1; j += 2) {
-      const double2 v0 = __ldg(mm + j * cs);
+      const double2 v0 = ld_panel<EF>(mm + j * cs, pol);
       acc0.x = fma(v0.x, x[j], acc0.x);
       acc0.y = fma(v0.y, x[j], acc0.y);
     }
@@ -189,7 +210,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   const int nst = kSweepThreads - 32;
   const DevUnit& U = s.u;
   const DevTask& T = s.t;
-  if (t == 0 && a.prefetch) prefetch_panel(a, U);
+  if (t == 0 && (a.prefetch & 1)) prefetch_panel(a, U);
   // every load below depends only on the (host-precomputed) descriptor, so
   // the whole staging is one round of independent loads
   const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
@@ -248,7 +269,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   }
 }
 
-template <bool FWD>
+template <bool FWD, bool EF>
 __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* xin, double* part, int tk) {
   long long* tr = a.trace ? a.trace + 8LL * tk : nullptr;
   const int ep = s.ep;
@@ -322,7 +343,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     const int nc = U.c1 - U.c0;
     const int per = (((nc + kWarps - 1) / kWarps) + 1) & ~1;
     const int j0 = warp * per, j1 = min(nc, j0 + per);
-    const double2 v = tile_dot((FWD ? a.fmat : a.hmat) + U.src_off, tl, xin, j0, j1);
+    const double2 v = tile_dot<EF>((FWD ? a.fmat : a.hmat) + U.src_off, tl, xin, j0, j1);
     if (lane < 16) {
       part[warp * 32 + 2 * l2] = v.x;
       part[warp * 32 + 2 * l2 + 1] = v.y;
@@ -363,7 +384,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     const double* m = (FWD ? a.fmat : a.hmat) + tl.off;
     const int chunk = (((tl.ncol + split - 1) / split) + 1) & ~1;
     const int j0 = c * chunk, j1 = min(tl.ncol, j0 + chunk);
-    const double2 v = tile_dot(m, tl, xin + (tl.col0 - col_lo), j0, j1);
+    const double2 v = tile_dot<EF>(m, tl, xin + (tl.col0 - col_lo), j0, j1);
     if (lane < 16 && 2 * l2 < tl.rows) {
       if (split == 1) {
         const int o = (U.tile_begin + R) * 32 + 2 * l2;
@@ -391,6 +412,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
+template <bool EF>
 __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
   pdl_wait();
   if (a.S && a.S->stop) return;
@@ -431,8 +453,8 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
     __syncthreads();
     const int tk = s.tk;
     if (tk >= a.n_units) break;
-    if (s.u.dir == 0) run_unit<true>(a, s, xin, part, tk);
-    else run_unit<false>(a, s, xin, part, tk);
+    if (s.u.dir == 0) run_unit<true, EF>(a, s, xin, part, tk);
+    else run_unit<false, EF>(a, s, xin, part, tk);
     __syncthreads();
   }
   // the last CTA of this sweep resets the tickets and advances the epoch
@@ -459,22 +481,24 @@ void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
     int per_sm = 0, sms = 0, dev = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel, kSweepThreads, smem));
+    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
     resident = (per_sm > 0 ? per_sm : 1) * sms;
     cached_smem = smem;
   }
   const int grid = a.n_units < resident ? a.n_units : resident;
-  launch_pdl(sweep_kernel, grid, kSweepThreads, smem, st, a);
+  if (a.prefetch & 2) launch_pdl(sweep_kernel<true>, grid, kSweepThreads, smem, st, a);
+  else launch_pdl(sweep_kernel<false>, grid, kSweepThreads, smem, st, a);
 }
 
 int sweep_ctas_per_sm(int smem) {
   int per_sm = 0;
-  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel, kSweepThreads, smem));
+  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
   return per_sm > 0 ? per_sm : 1;
 }
 
 void set_sweep_smem(int bytes) {
-  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 }  // namespace pdg
