@@ -184,6 +184,42 @@ typedef struct pdg_pcg_report { /* PCGReport (krylov.hpp:32-39) */
 } pdg_pcg_report;
 
 pdg_status pdg_sim_create(const pdg_config* cfg, pdg_sim** out);
+
+/* ---- solver from caller-supplied operator data ----
+ * SparseOperator(K) (krylov.hpp:22-30) + SchwarzPreconditioner(K, space,
+ * partition_S, coarse) (schwarz.hpp:51-53) + pcg_solve (krylov.hpp:49-51)
+ * without the mesh / time stepper: the caller hands over K and the partitions
+ * the reference's constructor takes, and gets a pdg_sim whose apply_K,
+ * apply_precond and pcg (host or device vectors) work; pdg_sim_step returns
+ * PDG_ERR_CONFIG. The context copies everything; vectors are in the caller's
+ * (reference) dof order, element-major blocks of `block` dofs. */
+typedef struct pdg_operator_desc {
+  int n_cells;              /* elements (DGSpace::n_elements); dimension = n_cells * block */
+  int block;                /* dofs per element (DGSpace::n_local, assembly.hpp:44-50 block_dim) */
+  const int64_t* row_ptr;   /* K as scalar CSR (symmetric, both triangles, Eigen's SparseMatrix */
+  const int* col;           /*   arrays; for a symmetric matrix CSR == CSC): n+1 / nnz / nnz */
+  const double* val;
+  int precond_kind;         /* PDG_PRECOND_NONE / _BLOCK_JACOBI / _TWO_LEVEL */
+  const int* sub_owner;     /* partition_S.owner: element -> subdomain (NULL: one element each) */
+  int n_sub;                /* partition_S.count */
+  /* CoarseEmbedding (schwarz.hpp:29-36), two-level only: E as scalar CSR of
+   * n rows x n_coarse*coarse_block columns, one block per element row (the
+   * element's agglomerate columns), as build_coarse_embedding forms it */
+  int n_coarse;
+  int coarse_block;         /* b_q */
+  const int64_t* e_row_ptr;
+  const int* e_col;
+  const double* e_val;
+  int maxit;                /* default maxit for pcg (0: min(20 sqrt(n), n)) */
+  int device;
+} pdg_operator_desc;
+pdg_status pdg_sim_create_from_operator(const pdg_operator_desc* desc, pdg_sim** out);
+/* build_coarse_embedding(space, partition, q) (schwarz.hpp:38-39) on a
+ * generated mesh with degree-p elements: E as the per-element blocks
+ * (n_cells x block x coarse_block doubles, column-major blocks) for
+ * agglomerate owner[] (count agglomerates). ConfigError if q not in [1, p]. */
+pdg_status pdg_mesh_coarse_embedding(const pdg_mesh* m, int p, const int* owner, int count, int q,
+                                     double* E_blocks);
 void pdg_sim_free(pdg_sim* s);
 const pdg_problem* pdg_sim_problem(const pdg_sim* s);
 int64_t pdg_sim_dimension(const pdg_sim* s);

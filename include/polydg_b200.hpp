@@ -4,8 +4,10 @@
 // timestepper,errors}.hpp so a caller of the reference's per-step path can
 // switch by changing includes and namespace:
 //   polydg::LinearOperator          -> polydg_b200::LinearOperator    (krylov.hpp:15-20)
-//   polydg::SparseOperator          -> polydg_b200::SystemOperator    (krylov.hpp:22-30)
-//   polydg::SchwarzPreconditioner   -> polydg_b200::SchwarzPreconditioner (schwarz.hpp:47-72)
+//   polydg::SparseOperator          -> polydg_b200::SparseOperator(K) / SystemOperator (krylov.hpp:22-30)
+//   polydg::SchwarzPreconditioner   -> polydg_b200::SchwarzPreconditioner (schwarz.hpp:47-72):
+//                                      (K, partition_S, coarse) from caller data, or a Simulation's
+//   polydg::build_coarse_embedding  -> polydg_b200::build_coarse_embedding (schwarz.hpp:38-39)
 //   polydg::pcg_solve / PCGReport   -> polydg_b200::pcg_solve / PCGReport (krylov.hpp:32-57)
 //   polydg::condition_estimate      -> polydg_b200::condition_estimate (krylov.hpp:59-63)
 //   polydg::Simulation / StepStats  -> polydg_b200::Simulation / StepStats (timestepper.hpp:94-155)
@@ -13,8 +15,10 @@
 // Differences: Eigen::VectorXd becomes std::vector<double> (Eigen is not a
 // dependency), SimulationConfig is the C struct pdg_config (closed forms
 // instead of std::function hooks), and pcg_solve runs on the device, so its
-// operators must be the ones of a Simulation (dimension mismatch, tol outside
-// (0, 1) and breakdown throw SolverError exactly as krylov.cpp:22-24,46-68).
+// operators must be device operators: a Simulation's, or SparseOperator(K) with
+// SchwarzPreconditioner(K, partition_S, coarse) built from the same caller
+// matrix (dimension mismatch, tol outside (0, 1) and breakdown throw
+// SolverError exactly as krylov.cpp:22-24,46-68).
 #pragma once
 
 #include <algorithm>
@@ -111,36 +115,129 @@ inline std::optional<double> condition_estimate(const PCGReport& r) {
 
 class Simulation;
 
+// Eigen::SparseMatrix<double> stand-in: scalar CSR arrays (for the symmetric
+// matrices of this path CSR == CSC). SparseSymMatrix adds the element block
+// size (assembly.hpp:44-50 block_dim).
+struct SparseMatrix {
+  std::int64_t rows = 0, cols = 0;
+  std::vector<std::int64_t> row_ptr{0};
+  std::vector<int> col;
+  std::vector<double> val;
+};
+struct SparseSymMatrix : SparseMatrix {
+  int block_dim = 0;
+};
+// AgglomeratedPartition (mesh.hpp): element -> agglomerate
+struct AgglomeratedPartition {
+  std::vector<int> owner;
+  int count = 0;
+};
+// CoarseEmbedding (schwarz.hpp:29-36): E (n x count*n_local), degree q, n_local = b_q
+struct CoarseEmbedding {
+  SparseMatrix E;
+  int q = 0;
+  int n_local = 0;
+  int count = 0;
+};
+
+namespace detail {
+struct SimFree {
+  void operator()(pdg_sim* s) const { pdg_sim_free(s); }
+};
+using Context = std::shared_ptr<pdg_sim>;
+inline Context make_operator_context(const SparseSymMatrix& K, int kind, const AgglomeratedPartition* S,
+                                     const CoarseEmbedding* coarse) {
+  if (K.block_dim <= 0 || K.rows != K.cols || K.rows % K.block_dim != 0)
+    throw ConfigError("operator: K must be square with block_dim > 0 dividing its size");
+  pdg_operator_desc d{};
+  d.n_cells = static_cast<int>(K.rows / K.block_dim);
+  d.block = K.block_dim;
+  d.row_ptr = K.row_ptr.data();
+  d.col = K.col.data();
+  d.val = K.val.data();
+  d.precond_kind = kind;
+  if (S) {
+    d.sub_owner = S->owner.data();
+    d.n_sub = S->count;
+  }
+  if (coarse) {
+    d.n_coarse = coarse->count;
+    d.coarse_block = coarse->n_local;
+    d.e_row_ptr = coarse->E.row_ptr.data();
+    d.e_col = coarse->E.col.data();
+    d.e_val = coarse->E.val.data();
+  }
+  pdg_sim* h = nullptr;
+  check(pdg_sim_create_from_operator(&d, &h));
+  return Context(h, SimFree{});
+}
+}  // namespace detail
+
 class LinearOperator {
  public:
   virtual ~LinearOperator() = default;
   virtual std::int64_t dimension() const = 0;
   virtual void apply(const Vector& x, Vector& y) const = 0;
-  virtual const Simulation* device_owner() const { return nullptr; }
+  // the device context that holds this operator, and the caller matrix it was
+  // built from (pcg_solve pairs a SparseOperator with a SchwarzPreconditioner
+  // built from the same matrix)
+  virtual pdg_sim* device_context() const { return nullptr; }
+  virtual const void* source_matrix() const { return nullptr; }
 };
 
-// y = K x with the device system matrix
+// y = K x with the device system matrix of a Simulation (SparseOperator role)
 class SystemOperator final : public LinearOperator {
  public:
   explicit SystemOperator(const Simulation* s) : sim_(s) {}
   std::int64_t dimension() const override;
   void apply(const Vector& x, Vector& y) const override;
-  const Simulation* device_owner() const override { return sim_; }
+  pdg_sim* device_context() const override;
 
  private:
   const Simulation* sim_;
 };
 
-// z = B r with the device two-level Schwarz preconditioner
+// SparseOperator(K) (krylov.hpp:22-30) over a caller matrix: K lives on the device
+class SparseOperator final : public LinearOperator {
+ public:
+  explicit SparseOperator(const SparseSymMatrix& K)
+      : K_(&K), ctx_(detail::make_operator_context(K, PDG_PRECOND_NONE, nullptr, nullptr)) {}
+  std::int64_t dimension() const override { return pdg_sim_dimension(ctx_.get()); }
+  void apply(const Vector& x, Vector& y) const override {
+    if (static_cast<std::int64_t>(x.size()) != dimension()) throw SolverError("apply: vector dimension mismatch");
+    y.resize(x.size());
+    check(pdg_sim_apply_K(ctx_.get(), x.data(), y.data()));
+  }
+  pdg_sim* device_context() const override { return ctx_.get(); }
+  const void* source_matrix() const override { return K_; }
+
+ private:
+  const SparseSymMatrix* K_;
+  detail::Context ctx_;
+};
+
+// z = B r with the device Schwarz preconditioner: a Simulation's, or built like
+// the reference's SchwarzPreconditioner(K, space, partition_S, coarse)
+// (schwarz.hpp:51-53; the block size comes from K.block_dim, coarse may be
+// null for the one-level method). Immutable after construction.
 class SchwarzPreconditioner final : public LinearOperator {
  public:
   explicit SchwarzPreconditioner(const Simulation* s) : sim_(s) {}
+  SchwarzPreconditioner(const SparseSymMatrix& K, const AgglomeratedPartition& partition_S,
+                        const CoarseEmbedding* coarse)
+      : sim_(nullptr),
+        K_(&K),
+        ctx_(detail::make_operator_context(K, coarse ? PDG_PRECOND_TWO_LEVEL : PDG_PRECOND_BLOCK_JACOBI,
+                                           &partition_S, coarse)) {}
   std::int64_t dimension() const override;
   void apply(const Vector& r, Vector& z) const override;
-  const Simulation* device_owner() const override { return sim_; }
+  pdg_sim* device_context() const override;
+  const void* source_matrix() const override { return K_; }
 
  private:
   const Simulation* sim_;
+  const SparseSymMatrix* K_ = nullptr;
+  detail::Context ctx_;
 };
 
 class Simulation {
@@ -213,23 +310,57 @@ class Simulation {
 };
 
 inline std::int64_t SystemOperator::dimension() const { return sim_->dimension(); }
+inline pdg_sim* SystemOperator::device_context() const { return sim_->handle(); }
 inline void SystemOperator::apply(const Vector& x, Vector& y) const {
+  if (static_cast<std::int64_t>(x.size()) != dimension()) throw SolverError("apply: vector dimension mismatch");
   y.resize(x.size());
   check(pdg_sim_apply_K(sim_->handle(), x.data(), y.data()));
 }
-inline std::int64_t SchwarzPreconditioner::dimension() const { return sim_->dimension(); }
+inline pdg_sim* SchwarzPreconditioner::device_context() const { return sim_ ? sim_->handle() : ctx_.get(); }
+inline std::int64_t SchwarzPreconditioner::dimension() const { return pdg_sim_dimension(device_context()); }
 inline void SchwarzPreconditioner::apply(const Vector& r, Vector& z) const {
+  if (static_cast<std::int64_t>(r.size()) != dimension()) throw SolverError("apply: vector dimension mismatch");
   z.resize(r.size());
-  check(pdg_sim_apply_precond(sim_->handle(), r.data(), z.data()));
+  check(pdg_sim_apply_precond(device_context(), r.data(), z.data()));
+}
+
+// build_coarse_embedding(space, partition, q) (schwarz.hpp:38-39) on a
+// generated mesh with degree-p elements; ConfigError if q is not in [1, p]
+inline CoarseEmbedding build_coarse_embedding(const pdg_mesh* mesh, int p, const AgglomeratedPartition& part, int q) {
+  const int b = (p + 1) * (p + 2) / 2, bq = (q + 1) * (q + 2) / 2;
+  const std::int64_t nc = static_cast<std::int64_t>(part.owner.size());
+  std::vector<double> blocks(static_cast<std::size_t>(nc) * b * bq);
+  check(pdg_mesh_coarse_embedding(mesh, p, part.owner.data(), part.count, q, blocks.data()));
+  CoarseEmbedding ce;
+  ce.q = q;
+  ce.n_local = bq;
+  ce.count = part.count;
+  ce.E.rows = nc * b;
+  ce.E.cols = static_cast<std::int64_t>(part.count) * bq;
+  ce.E.row_ptr.assign(1, 0);
+  for (std::int64_t c = 0; c < nc; ++c)
+    for (int r = 0; r < b; ++r) {
+      for (int m = 0; m < bq; ++m) {
+        ce.E.col.push_back(part.owner[c] * bq + m);
+        ce.E.val.push_back(blocks[static_cast<std::size_t>(c) * b * bq + static_cast<std::size_t>(m) * b + r]);
+      }
+      ce.E.row_ptr.push_back(static_cast<std::int64_t>(ce.E.col.size()));
+    }
+  return ce;
 }
 
 // pcg_solve(K, b, precond, tol, maxit, x0) (krylov.hpp:49-51), device-resident loop
 inline std::pair<Vector, PCGReport> pcg_solve(const LinearOperator& K, const Vector& b,
                                               const LinearOperator* precond, double tol, int maxit,
                                               const Vector& x0) {
-  const Simulation* sim = K.device_owner();
-  if (!sim || (precond && precond->device_owner() != sim))
-    throw ConfigError("pcg_solve: operators must belong to the same device Simulation");
+  // the device context that holds both operators: a Simulation's K and B, or
+  // a SparseOperator and a SchwarzPreconditioner built from the same matrix
+  pdg_sim* ctx = K.device_context();
+  if (precond && precond->device_context() != ctx) {
+    if (precond->source_matrix() && precond->source_matrix() == K.source_matrix()) ctx = precond->device_context();
+    else ctx = nullptr;
+  }
+  if (!ctx) throw ConfigError("pcg_solve: K and the preconditioner must be device operators of the same matrix");
   if (static_cast<std::int64_t>(b.size()) != K.dimension() || x0.size() != b.size())
     throw SolverError("pcg: vector dimension mismatch");
   const int cap = (maxit > 0 ? maxit : default_max_iterations(K.dimension())) + 2;
@@ -243,7 +374,7 @@ inline std::pair<Vector, PCGReport> pcg_solve(const LinearOperator& K, const Vec
   c.alphas = rep.alphas.data();
   c.betas = rep.betas.data();
   Vector x(b.size());
-  check(pdg_sim_pcg(sim->handle(), b.data(), x0.data(), tol, maxit, precond != nullptr, x.data(), &c));
+  check(pdg_sim_pcg(ctx, b.data(), x0.data(), tol, maxit, precond != nullptr, x.data(), &c));
   rep.iterations = c.iterations;
   rep.converged = c.converged != 0;
   rep.residual_history.resize(c.iterations > 0 ? c.iterations : (c.converged ? 1 : 0));

@@ -60,6 +60,16 @@ class PcgReport(C.Structure):
                 ("betas", C.POINTER(C.c_double))]
 
 
+class OperatorDesc(C.Structure):
+    """pdg_operator_desc: K, partition_S and the coarse embedding from the caller."""
+    _fields_ = [("n_cells", C.c_int), ("block", C.c_int),
+                ("row_ptr", C.POINTER(C.c_int64)), ("col", C.POINTER(C.c_int)), ("val", C.POINTER(C.c_double)),
+                ("precond_kind", C.c_int), ("sub_owner", C.POINTER(C.c_int)), ("n_sub", C.c_int),
+                ("n_coarse", C.c_int), ("coarse_block", C.c_int),
+                ("e_row_ptr", C.POINTER(C.c_int64)), ("e_col", C.POINTER(C.c_int)), ("e_val", C.POINTER(C.c_double)),
+                ("maxit", C.c_int), ("device", C.c_int)]
+
+
 class PdgError(RuntimeError):
     """Raised for a non-OK pdg_status; ``kind`` is the reference exception name."""
 
@@ -93,6 +103,7 @@ def lib() -> C.CDLL:
             "pdg_mesh_cell_geometry": (None, [vp, P(dbl)]),
             "pdg_mesh_agglomerate": (i32, [vp, i32, P(i32), P(dbl)]),
             "pdg_mesh_agglomerate_hierarchy": (i32, [vp, i32, P(i32)]),
+            "pdg_mesh_coarse_embedding": (i32, [vp, i32, P(i32), i32, i32, P(dbl)]),
             "pdg_polygon_quadrature": (i32, [P(dbl), i32, i32, P(dbl), P(dbl), i32]),
             "pdg_problem_create": (i32, [P(PdgConfig), P(vp)]),
             "pdg_problem_free": (None, [vp]),
@@ -121,6 +132,7 @@ def _bind_device(L):
     P = C.POINTER
     sig = {
         "pdg_sim_create": (i32, [P(PdgConfig), P(vp)]),
+        "pdg_sim_create_from_operator": (i32, [P(OperatorDesc), P(vp)]),
         "pdg_sim_free": (None, [vp]),
         "pdg_sim_problem": (vp, [vp]),
         "pdg_sim_dimension": (i64, [vp]),

@@ -157,6 +157,16 @@ void pdg_mesh_cell_geometry(const pdg_mesh* h, double* out) {
   }
 }
 
+pdg_status pdg_mesh_coarse_embedding(const pdg_mesh* h, int p, const int* owner, int count, int q,
+                                     double* E_blocks) {
+  return pdg::guarded([&] {
+    if (p < 1) throw pdg::ConfigError("build_coarse_embedding: degree must be >= 1");
+    const std::vector<int> own(owner, owner + h->m.n_cells());
+    const std::vector<double> E = pdg::coarse_embedding(h->m, p, own, count, q);
+    std::memcpy(E_blocks, E.data(), sizeof(double) * E.size());
+  });
+}
+
 int pdg_mesh_agglomerate(const pdg_mesh* h, int target, int* owner, double* H) {
   int count = -1;
   const pdg_status st = pdg::guarded([&] {
@@ -236,7 +246,7 @@ void pdg_problem_perm(const pdg_problem* h, int* perm) {
 namespace pdg {
 
 void problem_info(const Problem& pr, int64_t info[12]) {
-  info[0] = pr.mesh.n_cells();
+  info[0] = pr.n_cells_global;
   info[1] = pr.b;
   info[2] = pr.n_global_dofs();
   info[3] = pr.sub.count;

@@ -70,9 +70,10 @@ void fill_report(const pdg::PcgResult& r, pdg_pcg_report* rep) {
 // device cell means scattered to reference cell order (other ranks' cells 0)
 void cell_means_ref(pdg::DeviceSim& d, double* means) {
   const pdg::Problem& pr = *d.P;
+  if (pr.from_operator) throw pdg::ConfigError("cell_means: this solver was built from an operator (no mesh)");
   std::vector<double> local;
   d.cell_means(local);
-  std::fill(means, means + pr.mesh.n_cells(), 0.0);
+  std::fill(means, means + pr.n_cells_global, 0.0);
   for (int i = 0; i < d.ncells; ++i) means[pr.perm[pr.cell_begin + i]] = local[i];
 }
 
@@ -86,6 +87,24 @@ pdg_status pdg_sim_create(const pdg_config* cfg, pdg_sim** out) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw pdg::CudaError("no CUDA device available (the solver has no CPU fallback)");
     auto prob = pdg::build_problem(*cfg);
+    auto* s = new pdg_sim;
+    try {
+      s->d = std::make_unique<pdg::DeviceSim>(std::move(prob));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+pdg_status pdg_sim_create_from_operator(const pdg_operator_desc* desc, pdg_sim** out) {
+  return pdg::guarded([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw pdg::CudaError("no CUDA device available (the solver has no CPU fallback)");
+    if (!desc) throw pdg::ConfigError("operator: null descriptor");
+    auto prob = pdg::build_problem_from_operator(*desc);
     auto* s = new pdg_sim;
     try {
       s->d = std::make_unique<pdg::DeviceSim>(std::move(prob));
@@ -140,7 +159,7 @@ pdg_status pdg_sim_export_snapshot(pdg_sim* s, const char* path, const char* for
     const pdg::Problem& pr = *d.P;
     if (std::string(format) != "vtk-legacy" && std::string(format) != "csv-cellmeans")
       throw pdg::ConfigError("unknown snapshot format '" + std::string(format) + "'");
-    std::vector<double> means(pr.mesh.n_cells());
+    std::vector<double> means(pr.n_cells_global);
     cell_means_ref(d, means.data());
     pdg::write_snapshot(pr.mesh, means, d.t, path, format);
   });

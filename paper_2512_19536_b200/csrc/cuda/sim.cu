@@ -157,7 +157,7 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   d_bbox = dupload(pr.bbox, st);
   d_tri_ptr = dupload(pr.tri_ptr, st);
   d_tri = dupload(pr.tri, st);
-  set_gauss_nodes(pr.gl_x.data(), pr.gl_w.data(), static_cast<int>(pr.gl_x.size()));
+  if (!pr.gl_x.empty()) set_gauss_nodes(pr.gl_x.data(), pr.gl_w.data(), static_cast<int>(pr.gl_x.size()));
   d_ionflags = dalloc<int>(1);
   PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
 
@@ -956,6 +956,7 @@ void DeviceSim::cell_means(std::vector<double>& out) {
 
 StepResult DeviceSim::step() {
   const Problem& pr = *P;
+  if (pr.from_operator) throw ConfigError("step: this solver was built from an operator (no time stepper)");
   const pdg_config& c = pr.cfg;
   const bool has_prev = k > 0;
   StepResult out;

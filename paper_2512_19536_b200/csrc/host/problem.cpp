@@ -307,6 +307,398 @@ static void add_factor_plan(Problem& pr, const SupernodalFactor& F, const std::v
   (void)bs;
 }
 
+
+struct Placement {
+  std::vector<std::vector<int>> units;  // reference cells per unit (subdomain)
+  std::vector<int> unit_order;          // placement order of the units
+  std::vector<int> unit_rank, unit_start;
+  std::vector<NdTree> nd;               // per unit: supernode tree of its local factor
+  std::vector<std::vector<int>> unit_cells;  // per unit: cells in internal order
+  std::vector<int> my_units;            // this rank's units in placement order
+  bool multi_sub = false;
+};
+
+// Internal order (problem.hpp): units (subdomains) in `unit_order`, split over
+// ranks as contiguous cell-balanced ranges; inside each multi-cell unit a
+// fill-reducing order of its exact local factor (host/ordering.hpp). `pos`
+// (cell centroids) enables geometric nested dissection; without it (an
+// operator given by the caller) the order is graph-only minimum degree.
+static void place_units(Problem& pr, Placement& pl, const std::vector<std::vector<int>>& nbr,
+                        const std::vector<Pt>* pos) {
+  const pdg_config& cfg = pr.cfg;
+  const int N = static_cast<int>(nbr.size());
+  const int b = pr.b;
+  const int n_units = static_cast<int>(pl.units.size());
+  const auto& units = pl.units;
+  const auto& unit_order = pl.unit_order;
+  const bool multi_sub = pl.multi_sub;
+  // contiguous split of the ordered units over ranks, balanced by cells
+  pl.unit_rank.assign(n_units, 0);
+  auto& unit_rank = pl.unit_rank;
+  pr.rank_cell_start.assign(cfg.world + 1, 0);
+  {
+    std::int64_t acc = 0;
+    int r = 0;
+    for (int k = 0; k < n_units; ++k) {
+      const int u = unit_order[k];
+      while (r < cfg.world - 1 && acc >= static_cast<std::int64_t>(N) * (r + 1) / cfg.world) ++r;
+      unit_rank[u] = r;
+      acc += static_cast<std::int64_t>(units[u].size());
+    }
+  }
+  // ND inside each multi-cell subdomain
+  // Nested-dissection shape. Merging two separator levels per supernode
+  // halves the elimination-tree depth (the sweep's critical path) at ~20%
+  // more panel bytes; it pays while the sweep is latency bound (config2,
+  // config3 p=3: +2-9%) and costs once it streams with wide blocks (config3
+  // p=4: -9%, config4: -11%, config5 p=4: -35%). With p <= 2 the unmerged
+  // tree of small blocks is latency bound even on the 1M-cell mesh (config5
+  // p=2: -9%). Leaf size: dense leaves of ~64 dofs.
+  // PDG_ND_MERGE / PDG_ND_LEAF override.
+  const bool big = static_cast<std::int64_t>(N) * b > 800000 && b >= 10;
+  int nd_merge = big ? 1 : 2;
+  if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
+  int leaf = std::clamp(64 / b, 4, 16);  // config4: 6-cell leaves +3.8% over 4
+  if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
+  // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
+  int nd_top = nd_merge;
+  if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
+  // PDG_ORDER=md: minimum degree + fundamental supernodes (relaxed by PDG_MD_RELAX cells)
+  const bool md_order = !pos || (std::getenv("PDG_ORDER") && std::string(std::getenv("PDG_ORDER")) == "md");
+  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::atoi(std::getenv("PDG_MD_RELAX")) : 1;
+  pl.nd.assign(n_units, NdTree{});
+  auto& nd = pl.nd;
+  pl.unit_cells.assign(n_units, {});
+  auto& unit_cells = pl.unit_cells;  // cells in internal order
+  std::vector<std::int64_t> unit_fill(n_units, 0);
+  parallel_for(n_units, [&](int u) {
+    const auto& cells = units[u];
+    const int m = static_cast<int>(cells.size());
+    if (!multi_sub) {
+      unit_cells[u] = cells;
+      return;
+    }
+    std::map<int, int> loc;
+    for (int i = 0; i < m; ++i) loc[cells[i]] = i;
+    std::vector<int> ap{0}, aj;
+    std::vector<Pt> lpos(m);
+    for (int i = 0; i < m; ++i) {
+      for (int nb : nbr[cells[i]]) {
+        auto it = loc.find(nb);
+        if (it != loc.end()) aj.push_back(it->second);
+      }
+      ap.push_back(static_cast<int>(aj.size()));
+      if (pos) lpos[i] = (*pos)[cells[i]];
+    }
+    nd[u] = md_order ? md_supernodes(m, ap, aj, md_relax) : nested_dissection(m, ap, aj, lpos, leaf, nd_merge, nd_top);
+    unit_fill[u] = structural_fill(m, ap, aj, nd[u].order).scalar(b);
+    unit_cells[u].resize(m);
+    for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
+  });
+  pr.perm.clear();
+  pl.unit_start.assign(n_units, 0);
+  auto& unit_start = pl.unit_start;
+  for (int r = 0; r < cfg.world; ++r) {
+    pr.rank_cell_start[r] = static_cast<int>(pr.perm.size());
+    for (int k = 0; k < n_units; ++k) {
+      const int u = unit_order[k];
+      if (unit_rank[u] != r) continue;
+      unit_start[u] = static_cast<int>(pr.perm.size());
+      pr.perm.insert(pr.perm.end(), unit_cells[u].begin(), unit_cells[u].end());
+    }
+  }
+  pr.rank_cell_start[cfg.world] = N;
+  for (int u = 0; u < n_units; ++u)
+    if (unit_rank[u] == cfg.rank)
+      pr.l_struct += multi_sub ? unit_fill[u] : static_cast<std::int64_t>(b) * (b + 1) / 2 * units[u].size();
+  pr.iperm.assign(N, -1);
+  for (int i = 0; i < N; ++i) pr.iperm[pr.perm[i]] = i;
+  pr.cell_begin = pr.rank_cell_start[cfg.rank];
+  pr.cell_end = pr.rank_cell_start[cfg.rank + 1];
+  for (int k = 0; k < n_units; ++k)
+    if (unit_rank[unit_order[k]] == cfg.rank) pl.my_units.push_back(unit_order[k]);
+}
+
+
+// Exact local factors of this rank's subdomains (schwarz.cpp:99-136): the
+// symbolic plan (device factorisation) or the host supernodal Cholesky, packed
+// into sweep tasks (host/pack.cpp). pr.K must be in internal order.
+static void factor_units(Problem& pr, const Placement& pl) {
+  const pdg_config& cfg = pr.cfg;
+  const int b = pr.b, b2 = b * b;
+  const int nloc = pr.cell_end - pr.cell_begin;
+  const bool multi_sub = pl.multi_sub;
+  const auto& unit_cells = pl.unit_cells;
+  const auto& unit_start = pl.unit_start;
+  const auto& nd = pl.nd;
+  // ---- Schwarz local factors (schwarz.cpp:99-136) ----
+  struct UnitFactor {
+    int unit;
+    SupernodalFactor F;
+    std::vector<std::vector<int>> upd;  // device factorisation: left-looking updaters
+  };
+  // one rank, multi-cell subdomains: the GPU computes the numeric factor
+  // (cuda/factor.cu) from a host symbolic plan; PDG_HOST_FACTOR=1 keeps the
+  // host supernodal Cholesky
+  pr.device_factor = multi_sub && cfg.world == 1 && pr.has_precond &&
+                     !(std::getenv("PDG_HOST_FACTOR") && std::getenv("PDG_HOST_FACTOR")[0] == '1');
+  const std::vector<int>& my_units = pl.my_units;
+  std::vector<UnitFactor> factors;
+  pr.in_ptr = {0};
+  bool packed = false;
+  if (pr.has_precond) {
+    if (multi_sub) {
+      // factor a batch of subdomains in parallel, pack it (in subdomain
+      // order) and free it: only one batch of unpacked factors is alive, so
+      // the host peak is the packed panels plus a batch (config 4: ~40 GB of
+      // panels instead of twice that)
+      const int n_my = static_cast<int>(my_units.size());
+      const int batch = std::max(1, 4 * setup_threads());
+      for (int b0 = 0; b0 < n_my; b0 += batch) {
+      const int b1 = std::min(n_my, b0 + batch);
+      factors.assign(b1 - b0, UnitFactor{});
+      parallel_for(b1 - b0, [&](int kb) {
+        const int k = kb;
+        const int u = my_units[b0 + kb];
+        const int m = static_cast<int>(unit_cells[u].size());
+        const int s0 = unit_start[u];
+        BlockMatrix Bm;
+        Bm.m = m;
+        Bm.bs = b;
+        Bm.ptr.assign(m + 1, 0);
+        for (int i = 0; i < m; ++i) {
+          const int li = s0 + i - pr.cell_begin;
+          for (int kk = pr.K.ptr[li]; kk < pr.K.ptr[li + 1]; ++kk) {
+            const int j = pr.K.col[kk];
+            if (j < s0 || j >= s0 + m) continue;
+            Bm.col.push_back(j - s0);
+            if (!pr.device_factor)
+              Bm.val.insert(Bm.val.end(), pr.K.val.begin() + static_cast<std::size_t>(kk) * b2,
+                            pr.K.val.begin() + static_cast<std::size_t>(kk + 1) * b2);
+          }
+          Bm.ptr[i + 1] = static_cast<int>(Bm.col.size());
+        }
+        NdTree t;
+        t.order.resize(m);
+        std::iota(t.order.begin(), t.order.end(), 0);
+        t.sn_start = nd[u].sn_start;
+        t.parent = nd[u].parent;
+        factors[k].unit = u;
+        if (pr.device_factor) {
+          factors[k].F = symbolic_factor(Bm, t, factors[k].upd);
+          return;
+        }
+        try {
+          factors[k].F = supernodal_cholesky(Bm, t);
+        } catch (const SolverError&) {
+          throw SolverError("schwarz: subdomain " + std::to_string(u) +
+                            " factorization failed (not positive definite)");
+        }
+      });
+      for (const UnitFactor& uf : factors) {
+        const int base = static_cast<int>(pr.tasks.size());
+        pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b);
+        if (pr.device_factor) add_factor_plan(pr, uf.F, uf.upd, base, unit_start[uf.unit] - pr.cell_begin);
+      }
+      factors.clear();
+      }
+      packed = true;
+    } else {
+      // one element per subdomain: dense b x b Cholesky (schwarz.cpp:103-112)
+      factors.resize(nloc);
+      parallel_for(nloc, [&](int i) {
+        BlockMatrix Bm;
+        Bm.m = 1;
+        Bm.bs = b;
+        Bm.ptr = {0, 1};
+        Bm.col = {0};
+        const int k = pr.K.ptr[i] + static_cast<int>(std::lower_bound(pr.K.col.begin() + pr.K.ptr[i],
+                                                                 pr.K.col.begin() + pr.K.ptr[i + 1],
+                                                                 pr.cell_begin + i) -
+                                                  (pr.K.col.begin() + pr.K.ptr[i]));
+        Bm.val.assign(pr.K.val.begin() + static_cast<std::size_t>(k) * b2,
+                      pr.K.val.begin() + static_cast<std::size_t>(k + 1) * b2);
+        NdTree t;
+        t.order = {0};
+        t.sn_start = {0, 1};
+        t.parent = {-1};
+        factors[i].unit = pr.sub.owner[pr.perm[pr.cell_begin + i]];
+        try {
+          factors[i].F = supernodal_cholesky(Bm, t);
+        } catch (const SolverError&) {
+          throw SolverError("schwarz: subdomain " + std::to_string(factors[i].unit) +
+                            " block is not positive definite");
+        }
+      }, 256);
+    }
+  }
+  // pack fine tasks (host/pack.cpp); the multi-cell subdomains were packed
+  // batch by batch above
+  if (!packed)
+    for (const UnitFactor& uf : factors)
+      pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(&uf - factors.data()) * b);
+  pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
+  factors.clear();
+
+}
+
+
+// Coarse space from E (one b x bq block per cell, schwarz.cpp:49-75): coarse
+// internal order over the agglomerate graph (geometric ND with centres `apos`,
+// else minimum degree), per local cell E block and coarse node, coarse node ->
+// cells lists, and this rank's partial K0 = E^T K E (schwarz.cpp:141) in the
+// coarse internal order. Eall[e_slot[g]] = E block of global internal cell g
+// (local cells and the halo cells their rows touch).
+static void coarse_space(Problem& pr, std::vector<std::vector<int>>& anbr, const std::vector<Pt>* apos,
+                         const std::vector<double>& Eall, const std::vector<int>& e_slot) {
+  const int na = pr.coarse.count;
+  const int b = pr.b, b2 = b * b, bq = pr.bq;
+  const int nloc = pr.cell_end - pr.cell_begin;
+  std::vector<int> ap{0}, aj;
+  for (int a = 0; a < na; ++a) {
+    auto& v = anbr[a];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    aj.insert(aj.end(), v.begin(), v.end());
+    ap.push_back(static_cast<int>(aj.size()));
+  }
+  const NdTree cnd = apos ? nested_dissection(na, ap, aj, *apos, std::clamp(64 / pr.bq, 4, 16))
+                          : md_supernodes(na, ap, aj, 8);
+  pr.l0_struct = structural_fill(na, ap, aj, cnd.order).scalar(pr.bq);
+  pr.n_agg = na;
+  pr.agg_order = cnd.order;  // position -> label
+  pr.coarse_nd = cnd;
+  std::vector<int> apos_of(na);
+  for (int i = 0; i < na; ++i) apos_of[cnd.order[i]] = i;
+  pr.E.resize(static_cast<std::size_t>(nloc) * b * bq);
+  pr.cell_agg.resize(nloc);
+  for (int i = 0; i < nloc; ++i) {
+    const int g = pr.cell_begin + i;
+    std::copy(Eall.begin() + static_cast<std::size_t>(e_slot[g]) * b * bq,
+              Eall.begin() + static_cast<std::size_t>(e_slot[g] + 1) * b * bq,
+              pr.E.begin() + static_cast<std::size_t>(i) * b * bq);
+    pr.cell_agg[i] = apos_of[pr.coarse.owner[pr.perm[g]]];
+  }
+  // agglomerate -> local cells
+  pr.agg_cell_ptr.assign(na + 1, 0);
+  for (int i = 0; i < nloc; ++i) ++pr.agg_cell_ptr[pr.cell_agg[i] + 1];
+  for (int a = 0; a < na; ++a) pr.agg_cell_ptr[a + 1] += pr.agg_cell_ptr[a];
+  pr.agg_cells.resize(nloc);
+  {
+    std::vector<int> fill(pr.agg_cell_ptr.begin(), pr.agg_cell_ptr.end() - 1);
+    for (int i = 0; i < nloc; ++i) pr.agg_cells[fill[pr.cell_agg[i]]++] = i;
+  }
+  // K0 partial over local rows: K0[a,a'] += E_i^T K_ij E_j, coarse internal order
+  Bsr& K0 = pr.K0;
+  K0.rows = na;
+  K0.b = bq;
+  K0.ptr.assign(na + 1, 0);
+  for (int i = 0; i < na; ++i) {
+    const int a = cnd.order[i];
+    std::vector<int> cols{i};
+    for (int nb : anbr[a]) cols.push_back(apos_of[nb]);
+    std::sort(cols.begin(), cols.end());
+    K0.col.insert(K0.col.end(), cols.begin(), cols.end());
+    K0.ptr[i + 1] = static_cast<int>(K0.col.size());
+  }
+  const int bq2 = bq * bq;
+  K0.val.assign(static_cast<std::size_t>(K0.col.size()) * bq2, 0.0);
+  // one coarse row per task: its cells in increasing local index, which is
+  // the order a serial sweep over all local rows would add them (same bits)
+  parallel_for(na, [&](int ai) {
+  std::vector<double> KE(static_cast<std::size_t>(b) * bq);
+  for (int ci = pr.agg_cell_ptr[ai]; ci < pr.agg_cell_ptr[ai + 1]; ++ci) {
+    const int i = pr.agg_cells[ci];
+    const double* Ei = &pr.E[static_cast<std::size_t>(i) * b * bq];
+    for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1]; ++k) {
+      const int j = pr.K.col[k];
+      const int aj2 = apos_of[pr.coarse.owner[pr.perm[j]]];
+      const double* Ej = &Eall[static_cast<std::size_t>(e_slot[j]) * b * bq];
+      const double* Kb = &pr.K.val[static_cast<std::size_t>(k) * b2];
+      // KE = K_ij E_j  (b x bq)
+      for (int m = 0; m < bq; ++m)
+        for (int r = 0; r < b; ++r) {
+          double s = 0.0;
+          for (int c = 0; c < b; ++c) s += Kb[c * b + r] * Ej[m * b + c];
+          KE[m * b + r] = s;
+        }
+      const int* c0 = K0.col.data() + K0.ptr[ai];
+      const int* c1 = K0.col.data() + K0.ptr[ai + 1];
+      const int blk = static_cast<int>(std::lower_bound(c0, c1, aj2) - K0.col.data());
+      double* out = &K0.val[static_cast<std::size_t>(blk) * bq2];
+      for (int m2 = 0; m2 < bq; ++m2)
+        for (int m1 = 0; m1 < bq; ++m1) {
+          double s = 0.0;
+          for (int r = 0; r < b; ++r) s += Ei[m1 * b + r] * KE[m2 * b + r];
+          out[m2 * bq + m1] += s;
+        }
+    }
+  }
+  }, 1);
+}
+
+
+// Bounding box of every agglomerate: union of its cells' boxes (schwarz.cpp:26-36).
+static std::vector<Box> agglomerate_boxes(const Mesh& mesh, const std::vector<int>& owner, int na) {
+  std::vector<Box> abox(na);
+  std::vector<bool> seen(na, false);
+  for (int c = 0; c < mesh.n_cells(); ++c) {
+    const int a = owner[c];
+    const std::vector<Pt> pts = mesh.cell_points(c);
+    const Box cb = bbox_of(pts.data(), static_cast<int>(pts.size()));
+    if (!seen[a]) {
+      abox[a] = cb;
+      seen[a] = true;
+    } else {
+      abox[a].xmin = std::min(abox[a].xmin, cb.xmin);
+      abox[a].xmax = std::max(abox[a].xmax, cb.xmax);
+      abox[a].ymin = std::min(abox[a].ymin, cb.ymin);
+      abox[a].ymax = std::max(abox[a].ymax, cb.ymax);
+    }
+  }
+  return abox;
+}
+
+// E_K = M_K^{-1} int_K phi psi^T for the listed cells (schwarz.cpp:49-75):
+// fine modes on the cell's bbox, degree-q coarse modes on its agglomerate's
+// bbox, quadrature order 2p+2 (exact). One b x bq column-major block per cell.
+static std::vector<double> coarse_embedding_cells(const Mesh& mesh, int p, const std::vector<int>& owner,
+                                                  const std::vector<Box>& abox, int q, const std::vector<int>& cells) {
+  const int b = n_modes(p), bq = n_modes(q), order = 2 * p + 2;
+  std::vector<double> Eall(cells.size() * static_cast<std::size_t>(b) * bq);
+  parallel_for(static_cast<int>(cells.size()), [&](int k) {
+    const int c = cells[k];
+    const int a = owner[c];
+    const std::vector<Pt> poly = mesh.cell_points(c);
+    const Box cb = bbox_of(poly.data(), static_cast<int>(poly.size()));
+    const Rule rule = polygon_rule(poly, order);
+    std::vector<double> mass(static_cast<std::size_t>(b) * b, 0.0), rhs(static_cast<std::size_t>(b) * bq, 0.0);
+    std::vector<double> fv(b), cv(bq);
+    for (std::size_t qp = 0; qp < rule.size(); ++qp) {
+      const double w = rule.w[qp];
+      basis_at(cb, p, rule.pts[qp], fv.data());
+      basis_at(abox[a], q, rule.pts[qp], cv.data());
+      for (int jj = 0; jj < b; ++jj)
+        for (int ii = 0; ii < b; ++ii) mass[jj * b + ii] += w * fv[ii] * fv[jj];
+      for (int m = 0; m < bq; ++m)
+        for (int ii = 0; ii < b; ++ii) rhs[m * b + ii] += w * fv[ii] * cv[m];
+    }
+    spd_solve(b, bq, mass.data(), rhs.data());
+    std::copy(rhs.begin(), rhs.end(), Eall.begin() + static_cast<std::size_t>(k) * b * bq);
+  }, 64);
+  return Eall;
+}
+
+std::vector<double> coarse_embedding(const Mesh& mesh, int p, const std::vector<int>& owner, int count, int q) {
+  if (q < 1 || q > p) throw ConfigError("build_coarse_embedding: q must lie in [1, p]");
+  if (static_cast<int>(owner.size()) != mesh.n_cells()) throw ConfigError("build_coarse_embedding: owner size");
+  for (int o : owner)
+    if (o < 0 || o >= count) throw ConfigError("build_coarse_embedding: owner out of range");
+  std::vector<int> cells(mesh.n_cells());
+  std::iota(cells.begin(), cells.end(), 0);
+  return coarse_embedding_cells(mesh, p, owner, agglomerate_boxes(mesh, owner, count), q, cells);
+}
+
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   validate_config(cfg);
   auto P = std::make_unique<Problem>();
@@ -329,6 +721,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   phase("mesh");
   const Mesh& mesh = pr.mesh;
   const int N = mesh.n_cells();
+  pr.n_cells_global = N;
   pr.p = cfg.degree;
   pr.b = n_modes(pr.p);
   pr.q = cfg.q > 0 ? cfg.q : cfg.degree;
@@ -365,12 +758,12 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   }
 
   // ---- placement units and internal order ----
-  std::vector<std::vector<int>> units;
+  std::vector<std::vector<int>> units_in;
   const bool multi_sub = cfg.subdomains > 0;
   if (multi_sub) {
-    units = pr.sub.members();
+    units_in = pr.sub.members();
   } else if (pr.two_level) {
-    units = pr.coarse.members();
+    units_in = pr.coarse.members();
   } else {
     std::vector<int> cells(N);
     std::iota(cells.begin(), cells.end(), 0);
@@ -378,12 +771,13 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     for (int c = 0; c < N; ++c) code[c] = morton(mesh.centroid(c).x, mesh.centroid(c).y, dom);
     std::stable_sort(cells.begin(), cells.end(), [&](int a, int b2_) { return code[a] < code[b2_]; });
     for (int s = 0; s < N; s += 256)
-      units.emplace_back(cells.begin() + s, cells.begin() + std::min(N, s + 256));
+      units_in.emplace_back(cells.begin() + s, cells.begin() + std::min(N, s + 256));
   }
-  const int n_units = static_cast<int>(units.size());
-  std::vector<int> unit_order(n_units);
-  std::iota(unit_order.begin(), unit_order.end(), 0);
+  std::vector<int> unit_order_in(units_in.size());
+  std::iota(unit_order_in.begin(), unit_order_in.end(), 0);
   {
+    const int n_units = static_cast<int>(units_in.size());
+    const auto& units = units_in;
     std::vector<std::uint32_t> code(n_units);
     for (int u = 0; u < n_units; ++u) {
       double sx = 0, sy = 0;
@@ -393,85 +787,17 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       }
       code[u] = morton(sx / units[u].size(), sy / units[u].size(), dom);
     }
-    std::stable_sort(unit_order.begin(), unit_order.end(), [&](int a, int c) { return code[a] < code[c]; });
+    std::stable_sort(unit_order_in.begin(), unit_order_in.end(), [&](int a, int c) { return code[a] < code[c]; });
   }
-  // contiguous split of the ordered units over ranks, balanced by cells
-  std::vector<int> unit_rank(n_units, 0);
-  pr.rank_cell_start.assign(cfg.world + 1, 0);
+  Placement pl;
+  pl.units = std::move(units_in);
+  pl.unit_order = std::move(unit_order_in);
+  pl.multi_sub = multi_sub;
   {
-    std::int64_t acc = 0;
-    int r = 0;
-    for (int k = 0; k < n_units; ++k) {
-      const int u = unit_order[k];
-      while (r < cfg.world - 1 && acc >= static_cast<std::int64_t>(N) * (r + 1) / cfg.world) ++r;
-      unit_rank[u] = r;
-      acc += static_cast<std::int64_t>(units[u].size());
-    }
+    std::vector<Pt> cpos(N);
+    for (int c = 0; c < N; ++c) cpos[c] = mesh.centroid(c);
+    place_units(pr, pl, nbr, &cpos);
   }
-  // ND inside each multi-cell subdomain
-  // Nested-dissection shape. Merging two separator levels per supernode
-  // halves the elimination-tree depth (the sweep's critical path) at ~20%
-  // more panel bytes; it pays while the sweep is latency bound (config2,
-  // config3 p=3: +2-9%) and costs once it streams with wide blocks (config3
-  // p=4: -9%, config4: -11%, config5 p=4: -35%). With p <= 2 the unmerged
-  // tree of small blocks is latency bound even on the 1M-cell mesh (config5
-  // p=2: -9%). Leaf size: dense leaves of ~64 dofs.
-  // PDG_ND_MERGE / PDG_ND_LEAF override.
-  const bool big = static_cast<std::int64_t>(N) * b > 800000 && b >= 10;
-  int nd_merge = big ? 1 : 2;
-  if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
-  int leaf = std::clamp(64 / b, 4, 16);  // config4: 6-cell leaves +3.8% over 4
-  if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
-  // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
-  int nd_top = nd_merge;
-  if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
-  // PDG_ORDER=md: minimum degree + fundamental supernodes (relaxed by PDG_MD_RELAX cells)
-  const bool md_order = std::getenv("PDG_ORDER") && std::string(std::getenv("PDG_ORDER")) == "md";
-  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::atoi(std::getenv("PDG_MD_RELAX")) : 1;
-  std::vector<NdTree> nd(n_units);
-  std::vector<std::vector<int>> unit_cells(n_units);  // cells in internal order
-  std::vector<std::int64_t> unit_fill(n_units, 0);
-  parallel_for(n_units, [&](int u) {
-    const auto& cells = units[u];
-    const int m = static_cast<int>(cells.size());
-    if (!multi_sub) {
-      unit_cells[u] = cells;
-      return;
-    }
-    std::map<int, int> loc;
-    for (int i = 0; i < m; ++i) loc[cells[i]] = i;
-    std::vector<int> ap{0}, aj;
-    std::vector<Pt> pos(m);
-    for (int i = 0; i < m; ++i) {
-      for (int nb : nbr[cells[i]]) {
-        auto it = loc.find(nb);
-        if (it != loc.end()) aj.push_back(it->second);
-      }
-      ap.push_back(static_cast<int>(aj.size()));
-      pos[i] = mesh.centroid(cells[i]);
-    }
-    nd[u] = md_order ? md_supernodes(m, ap, aj, md_relax) : nested_dissection(m, ap, aj, pos, leaf, nd_merge, nd_top);
-    unit_fill[u] = structural_fill(m, ap, aj, nd[u].order).scalar(b);
-    unit_cells[u].resize(m);
-    for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
-  });
-  pr.perm.clear();
-  std::vector<int> unit_start(n_units, 0);
-  for (int r = 0; r < cfg.world; ++r) {
-    pr.rank_cell_start[r] = static_cast<int>(pr.perm.size());
-    for (int k = 0; k < n_units; ++k) {
-      const int u = unit_order[k];
-      if (unit_rank[u] != r) continue;
-      unit_start[u] = static_cast<int>(pr.perm.size());
-      pr.perm.insert(pr.perm.end(), unit_cells[u].begin(), unit_cells[u].end());
-    }
-  }
-  pr.rank_cell_start[cfg.world] = N;
-  for (int u = 0; u < n_units; ++u)
-    if (unit_rank[u] == cfg.rank)
-      pr.l_struct += multi_sub ? unit_fill[u] : static_cast<std::int64_t>(b) * (b + 1) / 2 * units[u].size();
-  pr.iperm.assign(N, -1);
-  for (int i = 0; i < N; ++i) pr.iperm[pr.perm[i]] = i;
   pr.cell_begin = pr.rank_cell_start[cfg.rank];
   pr.cell_end = pr.rank_cell_start[cfg.rank + 1];
   const int nloc = pr.cell_end - pr.cell_begin;
@@ -725,137 +1051,12 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   }
 
   phase("assembly");
-  // ---- Schwarz local factors (schwarz.cpp:99-136) ----
-  struct UnitFactor {
-    int unit;
-    SupernodalFactor F;
-    std::vector<std::vector<int>> upd;  // device factorisation: left-looking updaters
-  };
-  // one rank, multi-cell subdomains: the GPU computes the numeric factor
-  // (cuda/factor.cu) from a host symbolic plan; PDG_HOST_FACTOR=1 keeps the
-  // host supernodal Cholesky
-  pr.device_factor = multi_sub && cfg.world == 1 && pr.has_precond &&
-                     !(std::getenv("PDG_HOST_FACTOR") && std::getenv("PDG_HOST_FACTOR")[0] == '1');
-  std::vector<int> my_units;
-  for (int k = 0; k < n_units; ++k)
-    if (unit_rank[unit_order[k]] == cfg.rank) my_units.push_back(unit_order[k]);
-  std::vector<UnitFactor> factors;
-  pr.in_ptr = {0};
-  bool packed = false;
-  if (pr.has_precond) {
-    if (multi_sub) {
-      // factor a batch of subdomains in parallel, pack it (in subdomain
-      // order) and free it: only one batch of unpacked factors is alive, so
-      // the host peak is the packed panels plus a batch (config 4: ~40 GB of
-      // panels instead of twice that)
-      const int n_my = static_cast<int>(my_units.size());
-      const int batch = std::max(1, 4 * setup_threads());
-      for (int b0 = 0; b0 < n_my; b0 += batch) {
-      const int b1 = std::min(n_my, b0 + batch);
-      factors.assign(b1 - b0, UnitFactor{});
-      parallel_for(b1 - b0, [&](int kb) {
-        const int k = kb;
-        const int u = my_units[b0 + kb];
-        const int m = static_cast<int>(unit_cells[u].size());
-        const int s0 = unit_start[u];
-        BlockMatrix Bm;
-        Bm.m = m;
-        Bm.bs = b;
-        Bm.ptr.assign(m + 1, 0);
-        for (int i = 0; i < m; ++i) {
-          const int li = s0 + i - pr.cell_begin;
-          for (int kk = pr.K.ptr[li]; kk < pr.K.ptr[li + 1]; ++kk) {
-            const int j = pr.K.col[kk];
-            if (j < s0 || j >= s0 + m) continue;
-            Bm.col.push_back(j - s0);
-            if (!pr.device_factor)
-              Bm.val.insert(Bm.val.end(), pr.K.val.begin() + static_cast<std::size_t>(kk) * b2,
-                            pr.K.val.begin() + static_cast<std::size_t>(kk + 1) * b2);
-          }
-          Bm.ptr[i + 1] = static_cast<int>(Bm.col.size());
-        }
-        NdTree t;
-        t.order.resize(m);
-        std::iota(t.order.begin(), t.order.end(), 0);
-        t.sn_start = nd[u].sn_start;
-        t.parent = nd[u].parent;
-        factors[k].unit = u;
-        if (pr.device_factor) {
-          factors[k].F = symbolic_factor(Bm, t, factors[k].upd);
-          return;
-        }
-        try {
-          factors[k].F = supernodal_cholesky(Bm, t);
-        } catch (const SolverError&) {
-          throw SolverError("schwarz: subdomain " + std::to_string(u) +
-                            " factorization failed (not positive definite)");
-        }
-      });
-      for (const UnitFactor& uf : factors) {
-        const int base = static_cast<int>(pr.tasks.size());
-        pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(unit_start[uf.unit] - pr.cell_begin) * b);
-        if (pr.device_factor) add_factor_plan(pr, uf.F, uf.upd, base, unit_start[uf.unit] - pr.cell_begin);
-      }
-      factors.clear();
-      }
-      packed = true;
-    } else {
-      // one element per subdomain: dense b x b Cholesky (schwarz.cpp:103-112)
-      factors.resize(nloc);
-      parallel_for(nloc, [&](int i) {
-        BlockMatrix Bm;
-        Bm.m = 1;
-        Bm.bs = b;
-        Bm.ptr = {0, 1};
-        Bm.col = {0};
-        const int k = A.ptr[i] + static_cast<int>(std::lower_bound(pr.K.col.begin() + pr.K.ptr[i],
-                                                                 pr.K.col.begin() + pr.K.ptr[i + 1],
-                                                                 pr.cell_begin + i) -
-                                                  (pr.K.col.begin() + pr.K.ptr[i]));
-        Bm.val.assign(pr.K.val.begin() + static_cast<std::size_t>(k) * b2,
-                      pr.K.val.begin() + static_cast<std::size_t>(k + 1) * b2);
-        NdTree t;
-        t.order = {0};
-        t.sn_start = {0, 1};
-        t.parent = {-1};
-        factors[i].unit = pr.sub.owner[pr.perm[pr.cell_begin + i]];
-        try {
-          factors[i].F = supernodal_cholesky(Bm, t);
-        } catch (const SolverError&) {
-          throw SolverError("schwarz: subdomain " + std::to_string(factors[i].unit) +
-                            " block is not positive definite");
-        }
-      }, 256);
-    }
-  }
-  // pack fine tasks (host/pack.cpp); the multi-cell subdomains were packed
-  // batch by batch above
-  if (!packed)
-    for (const UnitFactor& uf : factors)
-      pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(&uf - factors.data()) * b);
-  pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
-  factors.clear();
-
+  factor_units(pr, pl);
   phase("factor+pack");
   // ---- coarse embedding E (schwarz.cpp:13-77) and local K0 contribution ----
   if (pr.two_level) {
     const int na = pr.coarse.count;
-    std::vector<Box> abox(na);
-    std::vector<bool> seen(na, false);
-    for (int c = 0; c < N; ++c) {
-      const int a = pr.coarse.owner[c];
-      const std::vector<Pt> pts = mesh.cell_points(c);
-      const Box cb = bbox_of(pts.data(), static_cast<int>(pts.size()));
-      if (!seen[a]) {
-        abox[a] = cb;
-        seen[a] = true;
-      } else {
-        abox[a].xmin = std::min(abox[a].xmin, cb.xmin);
-        abox[a].xmax = std::max(abox[a].xmax, cb.xmax);
-        abox[a].ymin = std::min(abox[a].ymin, cb.ymin);
-        abox[a].ymax = std::max(abox[a].ymax, cb.ymax);
-      }
-    }
+    const std::vector<Box> abox = agglomerate_boxes(mesh, pr.coarse.owner, na);
     // coarse internal order: ND over the agglomerate graph
     std::vector<std::vector<int>> anbr(na);
     for (const Face& f : mesh.interior_faces()) {
@@ -865,25 +1066,9 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
         anbr[c2].push_back(a);
       }
     }
-    std::vector<int> ap{0}, aj;
     std::vector<Pt> apos(na);
-    for (int a = 0; a < na; ++a) {
-      auto& v = anbr[a];
-      std::sort(v.begin(), v.end());
-      v.erase(std::unique(v.begin(), v.end()), v.end());
-      aj.insert(aj.end(), v.begin(), v.end());
-      ap.push_back(static_cast<int>(aj.size()));
-      apos[a] = {0.5 * (abox[a].xmin + abox[a].xmax), 0.5 * (abox[a].ymin + abox[a].ymax)};
-    }
-    const NdTree cnd = nested_dissection(na, ap, aj, apos, std::clamp(64 / pr.bq, 4, 16));
-    pr.l0_struct = structural_fill(na, ap, aj, cnd.order).scalar(pr.bq);
-    pr.n_agg = na;
-    pr.agg_order = cnd.order;  // position -> label
-    pr.coarse_nd = cnd;
-    std::vector<int> apos_of(na);
-    for (int i = 0; i < na; ++i) apos_of[cnd.order[i]] = i;
+    for (int a = 0; a < na; ++a) apos[a] = {0.5 * (abox[a].xmin + abox[a].xmax), 0.5 * (abox[a].ymin + abox[a].ymax)};
     // E for local cells and for the halo cells their rows touch
-    const int bq = pr.bq;
     std::vector<int> need;  // global internal cells needing E
     {
       std::vector<char> mark(N, 0);
@@ -894,95 +1079,164 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     }
     std::vector<int> e_slot(N, -1);
     for (std::size_t k = 0; k < need.size(); ++k) e_slot[need[k]] = static_cast<int>(k);
-    std::vector<double> Eall(need.size() * static_cast<std::size_t>(b) * bq);
-    parallel_for(static_cast<int>(need.size()), [&](int k) {
-      const int c = pr.perm[need[k]];
-      const int a = pr.coarse.owner[c];
-      const std::vector<Pt> poly = mesh.cell_points(c);
-      const Box cb = bbox_of(poly.data(), static_cast<int>(poly.size()));
-      const Rule rule = polygon_rule(poly, order);
-      std::vector<double> mass(static_cast<std::size_t>(b) * b, 0.0), rhs(static_cast<std::size_t>(b) * bq, 0.0);
-      std::vector<double> fv(b), cv(bq);
-      for (std::size_t qp = 0; qp < rule.size(); ++qp) {
-        const double w = rule.w[qp];
-        basis_at(cb, pr.p, rule.pts[qp], fv.data());
-        basis_at(abox[a], pr.q, rule.pts[qp], cv.data());
-        for (int jj = 0; jj < b; ++jj)
-          for (int ii = 0; ii < b; ++ii) mass[jj * b + ii] += w * fv[ii] * fv[jj];
-        for (int m = 0; m < bq; ++m)
-          for (int ii = 0; ii < b; ++ii) rhs[m * b + ii] += w * fv[ii] * cv[m];
-      }
-      spd_solve(b, bq, mass.data(), rhs.data());
-      std::copy(rhs.begin(), rhs.end(), Eall.begin() + static_cast<std::size_t>(k) * b * bq);
-    }, 64);
-    pr.E.resize(static_cast<std::size_t>(nloc) * b * bq);
-    pr.cell_agg.resize(nloc);
-    for (int i = 0; i < nloc; ++i) {
-      const int g = pr.cell_begin + i;
-      std::copy(Eall.begin() + static_cast<std::size_t>(e_slot[g]) * b * bq,
-                Eall.begin() + static_cast<std::size_t>(e_slot[g] + 1) * b * bq,
-                pr.E.begin() + static_cast<std::size_t>(i) * b * bq);
-      pr.cell_agg[i] = apos_of[pr.coarse.owner[pr.perm[g]]];
-    }
-    // agglomerate -> local cells
-    pr.agg_cell_ptr.assign(na + 1, 0);
-    for (int i = 0; i < nloc; ++i) ++pr.agg_cell_ptr[pr.cell_agg[i] + 1];
-    for (int a = 0; a < na; ++a) pr.agg_cell_ptr[a + 1] += pr.agg_cell_ptr[a];
-    pr.agg_cells.resize(nloc);
-    {
-      std::vector<int> fill(pr.agg_cell_ptr.begin(), pr.agg_cell_ptr.end() - 1);
-      for (int i = 0; i < nloc; ++i) pr.agg_cells[fill[pr.cell_agg[i]]++] = i;
-    }
-    // K0 partial over local rows: K0[a,a'] += E_i^T K_ij E_j, coarse internal order
-    Bsr& K0 = pr.K0;
-    K0.rows = na;
-    K0.b = bq;
-    K0.ptr.assign(na + 1, 0);
-    for (int i = 0; i < na; ++i) {
-      const int a = cnd.order[i];
-      std::vector<int> cols{i};
-      for (int nb : anbr[a]) cols.push_back(apos_of[nb]);
-      std::sort(cols.begin(), cols.end());
-      K0.col.insert(K0.col.end(), cols.begin(), cols.end());
-      K0.ptr[i + 1] = static_cast<int>(K0.col.size());
-    }
-    const int bq2 = bq * bq;
-    K0.val.assign(static_cast<std::size_t>(K0.col.size()) * bq2, 0.0);
-    // one coarse row per task: its cells in increasing local index, which is
-    // the order a serial sweep over all local rows would add them (same bits)
-    parallel_for(na, [&](int ai) {
-    std::vector<double> KE(static_cast<std::size_t>(b) * bq);
-    for (int ci = pr.agg_cell_ptr[ai]; ci < pr.agg_cell_ptr[ai + 1]; ++ci) {
-      const int i = pr.agg_cells[ci];
-      const double* Ei = &pr.E[static_cast<std::size_t>(i) * b * bq];
-      for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1]; ++k) {
-        const int j = pr.K.col[k];
-        const int aj2 = apos_of[pr.coarse.owner[pr.perm[j]]];
-        const double* Ej = &Eall[static_cast<std::size_t>(e_slot[j]) * b * bq];
-        const double* Kb = &pr.K.val[static_cast<std::size_t>(k) * b2];
-        // KE = K_ij E_j  (b x bq)
-        for (int m = 0; m < bq; ++m)
-          for (int r = 0; r < b; ++r) {
-            double s = 0.0;
-            for (int c = 0; c < b; ++c) s += Kb[c * b + r] * Ej[m * b + c];
-            KE[m * b + r] = s;
-          }
-        const int* c0 = K0.col.data() + K0.ptr[ai];
-        const int* c1 = K0.col.data() + K0.ptr[ai + 1];
-        const int blk = static_cast<int>(std::lower_bound(c0, c1, aj2) - K0.col.data());
-        double* out = &K0.val[static_cast<std::size_t>(blk) * bq2];
-        for (int m2 = 0; m2 < bq; ++m2)
-          for (int m1 = 0; m1 < bq; ++m1) {
-            double s = 0.0;
-            for (int r = 0; r < b; ++r) s += Ei[m1 * b + r] * KE[m2 * b + r];
-            out[m2 * bq + m1] += s;
-          }
-      }
-    }
-    }, 1);
+    std::vector<int> need_ref(need.size());
+    for (std::size_t k = 0; k < need.size(); ++k) need_ref[k] = pr.perm[need[k]];
+    const std::vector<double> Eall = coarse_embedding_cells(mesh, pr.p, pr.coarse.owner, abox, pr.q, need_ref);
+    coarse_space(pr, anbr, &apos, Eall, e_slot);
     phase("coarse E,K0");
     if (cfg.world == 1) finish_coarse(pr);
     phase("coarse factor");
+  }
+  return P;
+}
+
+
+std::unique_ptr<Problem> build_problem_from_operator(const pdg_operator_desc& d) {
+  const int N = d.n_cells, b = d.block;
+  if (N <= 0 || b <= 0) throw ConfigError("operator: n_cells and block must be positive");
+  if (!d.row_ptr || !d.col || !d.val) throw ConfigError("operator: K arrays are required");
+  if (d.precond_kind != PDG_PRECOND_NONE && d.precond_kind != PDG_PRECOND_BLOCK_JACOBI &&
+      d.precond_kind != PDG_PRECOND_TWO_LEVEL)
+    throw ConfigError("operator: unknown preconditioner kind");
+  auto P = std::make_unique<Problem>();
+  Problem& pr = *P;
+  pdg_config_default(&pr.cfg);
+  pr.cfg.device = d.device;
+  pr.cfg.maxit = d.maxit;
+  pr.cfg.precond_kind = d.precond_kind;
+  pr.cfg.subdomains = d.sub_owner ? d.n_sub : 0;
+  pr.cfg.ionic_model = PDG_IONIC_NONE;
+  pr.cfg.rank = 0;
+  pr.cfg.world = 1;
+  pr.from_operator = true;
+  pr.n_cells_global = N;
+  pr.b = b;
+  pr.p = 0;
+  while (n_modes(pr.p + 1) <= b) ++pr.p;  // P^p with (p+1)(p+2)/2 = b when b is triangular
+  pr.has_precond = d.precond_kind != PDG_PRECOND_NONE;
+  pr.two_level = d.precond_kind == PDG_PRECOND_TWO_LEVEL;
+  pr.n_comp = 0;
+  const std::int64_t n = static_cast<std::int64_t>(N) * b;
+  const int b2 = b * b;
+  // ---- K: scalar CSR -> element blocks (cell adjacency = nonzero blocks) ----
+  std::vector<std::vector<int>> nbr(N);
+  for (std::int64_t i = 0; i < n; ++i) {
+    if (d.row_ptr[i + 1] < d.row_ptr[i]) throw ConfigError("operator: row_ptr must be non-decreasing");
+    for (std::int64_t k = d.row_ptr[i]; k < d.row_ptr[i + 1]; ++k) {
+      const int j = d.col[k];
+      if (j < 0 || j >= n) throw ConfigError("operator: column index out of range");
+      const int ci = static_cast<int>(i / b), cj = j / b;
+      if (ci != cj) {
+        nbr[ci].push_back(cj);
+        nbr[cj].push_back(ci);  // symmetric pattern even if an entry is missing
+      }
+    }
+  }
+  parallel_for(N, [&](int c) {
+    auto& v = nbr[c];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }, 1024);
+  // ---- partitions ----
+  auto check_owner = [&](const int* o, int count, const char* what) {
+    if (count <= 0) throw ConfigError(std::string("operator: ") + what + " count must be positive");
+    for (int c = 0; c < N; ++c)
+      if (o[c] < 0 || o[c] >= count) throw ConfigError(std::string("operator: ") + what + " owner out of range");
+  };
+  if (d.sub_owner) {
+    check_owner(d.sub_owner, d.n_sub, "subdomain");
+    pr.sub.owner.assign(d.sub_owner, d.sub_owner + N);
+    pr.sub.count = d.n_sub;
+  } else {
+    pr.sub.owner.resize(N);
+    std::iota(pr.sub.owner.begin(), pr.sub.owner.end(), 0);
+    pr.sub.count = N;
+  }
+  // coarse embedding: agglomerate of each element row block from E's columns
+  std::vector<double> Eblk;
+  if (pr.two_level) {
+    if (!d.e_row_ptr || !d.e_col || !d.e_val || d.n_coarse <= 0 || d.coarse_block <= 0)
+      throw ConfigError("operator: two-level preconditioner needs the coarse embedding E");
+    const int bq = d.coarse_block;
+    pr.bq = bq;
+    pr.q = 0;
+    while (n_modes(pr.q + 1) <= bq) ++pr.q;
+    pr.coarse.owner.assign(N, -1);
+    pr.coarse.count = d.n_coarse;
+    Eblk.assign(static_cast<std::size_t>(N) * b * bq, 0.0);
+    for (std::int64_t i = 0; i < n; ++i)
+      for (std::int64_t k = d.e_row_ptr[i]; k < d.e_row_ptr[i + 1]; ++k) {
+        const int j = d.e_col[k];
+        if (j < 0 || j >= d.n_coarse * bq) throw ConfigError("operator: E column out of range");
+        const int c = static_cast<int>(i / b), a = j / bq;
+        if (pr.coarse.owner[c] < 0) pr.coarse.owner[c] = a;
+        if (pr.coarse.owner[c] != a) throw ConfigError("operator: E must hold one agglomerate block per element");
+        Eblk[static_cast<std::size_t>(c) * b * bq + static_cast<std::size_t>(j % bq) * b + i % b] = d.e_val[k];
+      }
+    for (int c = 0; c < N; ++c)
+      if (pr.coarse.owner[c] < 0) throw ConfigError("operator: E has an empty element row block");
+  }
+  // ---- placement units: subdomains (label order), else 256-cell runs ----
+  Placement pl;
+  pl.multi_sub = d.sub_owner != nullptr;
+  if (pl.multi_sub) {
+    pl.units = pr.sub.members();
+  } else if (pr.two_level) {
+    pl.units = pr.coarse.members();
+  } else {
+    for (int s = 0; s < N; s += 256) {
+      pl.units.emplace_back();
+      for (int c = s; c < std::min(N, s + 256); ++c) pl.units.back().push_back(c);
+    }
+  }
+  pl.unit_order.resize(pl.units.size());
+  std::iota(pl.unit_order.begin(), pl.unit_order.end(), 0);
+  place_units(pr, pl, nbr, nullptr);
+  // ---- K in internal order ----
+  Bsr& K = pr.K;
+  K.rows = N;
+  K.b = b;
+  K.ptr.assign(N + 1, 0);
+  for (int i = 0; i < N; ++i) K.ptr[i + 1] = K.ptr[i] + 1 + static_cast<int>(nbr[pr.perm[i]].size());
+  K.col.resize(K.ptr[N]);
+  K.val.assign(static_cast<std::size_t>(K.ptr[N]) * b2, 0.0);
+  parallel_for(N, [&](int i) {
+    const int c = pr.perm[i];
+    std::vector<int> cols{i};
+    for (int nb : nbr[c]) cols.push_back(pr.iperm[nb]);
+    std::sort(cols.begin(), cols.end());
+    std::copy(cols.begin(), cols.end(), K.col.begin() + K.ptr[i]);
+    for (int r = 0; r < b; ++r) {
+      const std::int64_t row = static_cast<std::int64_t>(c) * b + r;
+      for (std::int64_t k = d.row_ptr[row]; k < d.row_ptr[row + 1]; ++k) {
+        const int j = d.col[k], gj = pr.iperm[j / b];
+        const int blk = static_cast<int>(std::lower_bound(cols.begin(), cols.end(), gj) - cols.begin());
+        K.val[static_cast<std::size_t>(K.ptr[i] + blk) * b2 + static_cast<std::size_t>(j % b) * b + r] += d.val[k];
+      }
+    }
+  }, 256);
+  pr.keep_matrices = false;
+  pr.U0.assign(static_cast<std::size_t>(n), 0.0);
+  factor_units(pr, pl);
+  // ---- coarse space from the caller's E ----
+  if (pr.two_level) {
+    const int na = pr.coarse.count, bq = pr.bq;
+    std::vector<std::vector<int>> anbr(na);
+    for (int c = 0; c < N; ++c)
+      for (int nb : nbr[c]) {
+        const int a = pr.coarse.owner[c], a2 = pr.coarse.owner[nb];
+        if (a != a2) anbr[a].push_back(a2);
+      }
+    std::vector<double> Eall(static_cast<std::size_t>(N) * b * bq);
+    std::vector<int> e_slot(N);
+    for (int g = 0; g < N; ++g) {
+      e_slot[g] = g;
+      std::copy(Eblk.begin() + static_cast<std::size_t>(pr.perm[g]) * b * bq,
+                Eblk.begin() + static_cast<std::size_t>(pr.perm[g] + 1) * b * bq,
+                Eall.begin() + static_cast<std::size_t>(g) * b * bq);
+    }
+    coarse_space(pr, anbr, nullptr, Eall, e_slot);
+    finish_coarse(pr);
   }
   return P;
 }

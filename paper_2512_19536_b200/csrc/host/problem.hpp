@@ -136,8 +136,11 @@ struct Problem {
   std::vector<double> Y0;    // n_comp fields
   int n_comp = 0;
 
+  int n_cells_global = 0;
+  bool from_operator = false;  // built from caller data (no mesh, no time stepper)
+
   std::int64_t n_local_dofs() const { return static_cast<std::int64_t>(cell_end - cell_begin) * b; }
-  std::int64_t n_global_dofs() const { return static_cast<std::int64_t>(mesh.n_cells()) * b; }
+  std::int64_t n_global_dofs() const { return static_cast<std::int64_t>(n_cells_global) * b; }
 };
 
 // Appends the supernodes of one exact local factor (fine subdomain, coarse=0,
@@ -154,6 +157,12 @@ void validate_config(const pdg_config& cfg);
 // IonicModel::state_dim / resting_potential / resting_state (ionics.hpp:25-31)
 int ionic_rest(const pdg_config& cfg, double& u_rest, double* y_rest);
 std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
+// Solver setup from a caller's K, subdomain partition and coarse embedding
+// (pdg_sim_create_from_operator): one rank, graph-only orderings.
+std::unique_ptr<Problem> build_problem_from_operator(const pdg_operator_desc& d);
+// build_coarse_embedding (schwarz.cpp:13-77): per cell b x bq blocks of E for
+// agglomerates `owner` (count) with degree-q bbox-Legendre coarse modes.
+std::vector<double> coarse_embedding(const Mesh& mesh, int p, const std::vector<int>& owner, int count, int q);
 // coarse factorisation + task packing; split out so a multi-rank run can sum
 // K0 partials before factorising.
 void finish_coarse(Problem& P);

@@ -69,6 +69,20 @@ class Mesh:
             check(3 if b"target" not in lib().pdg_last_error() else 2)
         return owner, cnt, H[:cnt]
 
+    def coarse_embedding(self, p: int, owner: np.ndarray, count: int, q: int):
+        """build_coarse_embedding(space, partition, q) (schwarz.hpp:38-39): E as a
+        scipy CSR matrix (n_cells*b x count*bq), one b x bq block per element."""
+        import scipy.sparse as sp
+        nc = self.data().n_cells
+        b, bq = (p + 1) * (p + 2) // 2, (q + 1) * (q + 2) // 2
+        own = np.ascontiguousarray(owner, np.int32)
+        blocks = np.zeros(nc * b * bq)
+        check(lib().pdg_mesh_coarse_embedding(self._h, int(p), iptr(own), int(count), int(q), dptr(blocks)))
+        blocks = blocks.reshape(nc, bq, b)  # column-major b x bq per element
+        rows = (np.arange(nc)[:, None, None] * b + np.arange(b)[None, None, :]).repeat(bq, 1)
+        cols = (own[:, None, None] * bq + np.arange(bq)[None, :, None]).repeat(b, 2)
+        return sp.csr_matrix((blocks.ravel(), (rows.ravel(), cols.ravel())), shape=(nc * b, count * bq))
+
     def agglomerate_hierarchy(self, levels: int) -> tuple[np.ndarray, int]:
         nc = self.data().n_cells
         owner = np.zeros(nc, np.int32)

@@ -287,6 +287,55 @@ class Simulation:
         self.dimension = self.problem.dimension
         self.n_comp = self.problem.n_comp
 
+    @classmethod
+    def from_operator(cls, K, block: int, precond: str = "two-level", partition=None, coarse=None,
+                      maxit: int = 0, device: int = 0) -> "Simulation":
+        """SparseOperator(K) + SchwarzPreconditioner(K, space, partition_S, coarse)
+        (schwarz.hpp:51-53) from caller data, for apply_K / apply_precond /
+        pcg_solve (no time stepper). K: scipy sparse (n x n, symmetric, element-major
+        blocks of `block` dofs). partition: (owner, count) or None (one element
+        per subdomain). coarse: (E, n_coarse, coarse_block) with E scipy sparse
+        n x n_coarse*coarse_block, one block per element row (CoarseEmbedding::E),
+        required for "two-level"."""
+        import scipy.sparse as sp
+        kind = {"none": _lib.PRECOND_NONE, "block-jacobi": _lib.PRECOND_BLOCK_JACOBI,
+                "two-level": _lib.PRECOND_TWO_LEVEL}[precond]
+        Kc = sp.csr_matrix(K)
+        n = Kc.shape[0]
+        if Kc.shape != (n, n) or n % block:
+            raise _lib.PdgError(2, "operator: K must be square with a multiple of block rows")
+        keep = []  # arrays referenced by the descriptor until the call returns
+        d = _lib.OperatorDesc()
+        d.n_cells, d.block = n // block, block
+        rp = np.ascontiguousarray(Kc.indptr, np.int64)
+        ci = np.ascontiguousarray(Kc.indices, np.int32)
+        va = np.ascontiguousarray(Kc.data, np.float64)
+        keep += [rp, ci, va]
+        d.row_ptr, d.col, d.val = _lib.lptr(rp), _lib.iptr(ci), dptr(va)
+        d.precond_kind = kind
+        if partition is not None:
+            own = np.ascontiguousarray(partition[0], np.int32)
+            keep.append(own)
+            d.sub_owner, d.n_sub = _lib.iptr(own), int(partition[1])
+        if coarse is not None:
+            E, nco, bq = coarse
+            Ec = sp.csr_matrix(E)
+            erp = np.ascontiguousarray(Ec.indptr, np.int64)
+            eci = np.ascontiguousarray(Ec.indices, np.int32)
+            eva = np.ascontiguousarray(Ec.data, np.float64)
+            keep += [erp, eci, eva]
+            d.n_coarse, d.coarse_block = int(nco), int(bq)
+            d.e_row_ptr, d.e_col, d.e_val = _lib.lptr(erp), _lib.iptr(eci), dptr(eva)
+        d.maxit, d.device = maxit, device
+        obj = cls.__new__(cls)
+        obj.config = None
+        obj._h = C.c_void_p()
+        check(lib().pdg_sim_create_from_operator(C.byref(d), C.byref(obj._h)))
+        obj.problem = Problem._view(lib().pdg_sim_problem(obj._h), None, obj)
+        obj.dimension = obj.problem.dimension
+        obj.n_comp = 0
+        return obj
+
     def close(self):
         if getattr(self, "_h", None):
             lib().pdg_sim_free(self._h)
