@@ -604,7 +604,7 @@ ReduceCtx DeviceSim::rctx(int finish, double* out) {
 SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScalars* S) {
   SweepArgs a;
   static const char* pf = std::getenv("PDG_SWEEP_PREFETCH");
-  a.prefetch = pf ? std::atoi(pf) : 1;  // bit 0: L2 bulk prefetch, bit 1: evict-first panel loads
+  a.prefetch = pf ? std::atoi(pf) : 3;  // bit 0: L2 bulk prefetch, bit 1: evict-first panel loads
   a.tasks = d_tasks;
   a.units = d_fwd_units;
   a.n_units_f = n_units_f;

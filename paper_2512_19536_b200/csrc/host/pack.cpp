@@ -20,7 +20,9 @@ namespace pdg {
 
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {
   constexpr int kTile = 32;
-  constexpr int kRowAlign = 8;      // doubles per 64-byte burst
+  // rows per column segment are padded to a multiple of kRowAlign doubles
+  // (PDG_ROW_ALIGN overrides; 8 = one 64-byte burst)
+  static const int kRowAlign = std::getenv("PDG_ROW_ALIGN") ? std::max(2, std::atoi(std::getenv("PDG_ROW_ALIGN"))) : 8;
   constexpr int kTileAlign = 16;    // 128 bytes
   const int bs = F.bs;
   const int base = static_cast<int>(pr.tasks.size());
@@ -69,7 +71,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     // covers whole bursts. (16-byte alignment over-fetched 27% of the panel
     // bytes from DRAM at config 4, profiles/r01u.) Each lane streams double2
     // pairs of rows.
-    auto seg = [](int rows) { return (rows + kRowAlign - 1) / kRowAlign * kRowAlign; };
+    auto seg = [&](int rows) { return (rows + kRowAlign - 1) / kRowAlign * kRowAlign; };
     auto align = [](std::int64_t off) { return (off + kTileAlign - 1) / kTileAlign * kTileAlign; };
     t.f_tile0 = static_cast<int>(pr.ftiles.size());
     for (int r0 = 0; r0 < h; r0 += kTile) {
