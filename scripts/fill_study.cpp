@@ -34,6 +34,7 @@ int main(int argc, char** argv) {
   auto members = part.members();
   struct Acc {
     double cells = 0, structural = 0, stored = 0, nsn = 0, height = 0, n = 0;
+    double panel[4] = {0, 0, 0, 0};  // panel doubles (fwd + bwd): align 8 / align 2 / tri16+align8 / tri16+align2
   };
   std::map<std::string, Acc> acc;
   for (int u = 0; u < part.count; u += every) {
@@ -59,6 +60,34 @@ int main(int argc, char** argv) {
       a.structural += f.offdiag + f.diag;
       a.stored += st.blocks;
       a.nsn += st.supernodes;
+      // panel layout of host/pack.cpp: 32-row tiles, staircase triangle, rows padded
+      {
+        std::vector<int> pos(m);
+        for (int i = 0; i < m; ++i) pos[t.order[i]] = i;
+        const int ns = static_cast<int>(t.parent.size());
+        std::vector<std::vector<int>> rows(ns), kids(ns);
+        for (int q = 0; q < ns; ++q)
+          if (t.parent[q] >= 0) kids[t.parent[q]].push_back(q);
+        std::vector<int> mark(m, -1);
+        for (int q = 0; q < ns; ++q) {
+          const int a0 = t.sn_start[q], e = t.sn_start[q + 1];
+          auto addr = [&](int r) { if (r >= e && mark[r] != q) { mark[r] = q; rows[q].push_back(r); } };
+          for (int pp = a0; pp < e; ++pp) { const int v = t.order[pp]; for (int k = ap[v]; k < ap[v + 1]; ++k) addr(pos[aj[k]]); }
+          for (int c : kids[q]) for (int r : rows[c]) addr(r);
+          const long w = (long)(e - a0) * bs, h = w + (long)rows[q].size() * bs;
+          for (int var = 0; var < 4; ++var) {
+            const int al = (var & 1) ? 2 : 8, trit = (var & 2) ? 16 : 32;
+            auto seg = [&](long r) { return (r + al - 1) / al * al; };
+            double tot = 0;
+            // forward: triangle rows [0, w) in trit-row tiles, below rows in 32-row tiles
+            for (long r0 = 0; r0 < w; r0 += trit) { long rr = std::min<long>(trit, w - r0); tot += (double)std::min(w, r0 + rr) * seg(rr); }
+            for (long r0 = w; r0 < h; r0 += 32) { long rr = std::min<long>(32, h - r0); tot += (double)w * seg(rr); }
+            // backward: rows of H = columns of F, inputs i >= r0
+            for (long r0 = 0; r0 < w; r0 += trit) { long rr = std::min<long>(trit, w - r0); tot += (double)(h - r0) * seg(rr); }
+            a.panel[var] += tot;
+          }
+        }
+      }
       std::vector<int> h(t.parent.size(), 1);
       int hmax = 0;
       for (size_t s = 0; s < t.parent.size(); ++s) {
@@ -69,13 +98,12 @@ int main(int argc, char** argv) {
       a.n += 1;
     };
     add("nd_leaf6", nested_dissection(m, ap, aj, pos, 6, 1, 1));
-    for (int leaf : {32, 64, 128}) {
-      NdTree nd = nested_dissection(m, ap, aj, pos, leaf, 1, 1);
-      for (int relax : {4, 6, 8}) add("nd" + std::to_string(leaf) + "+md relax" + std::to_string(relax),
-                                      hybrid_md_supernodes(m, ap, aj, nd, relax));
-    }
     for (int relax : {1, 4, 6, 8, 12}) add("md relax" + std::to_string(relax), md_supernodes(m, ap, aj, relax));
   }
+  for (auto& [k, a] : acc)
+    printf("%-28s panel/cell (fwd+bwd doubles): a8 %.0f a2 %.0f tri16a8 %.0f tri16a2 %.0f | 2x structural %.0f\n", k.c_str(),
+           a.panel[0] / a.cells, a.panel[1] / a.cells, a.panel[2] / a.cells, a.panel[3] / a.cells,
+           2 * (a.structural * bs * bs - a.cells * bs * (bs - 1) / 2.0) / a.cells);
   for (auto& [k, a] : acc)
     printf("%-28s structural %.2f blocks/cell  stored %.2f blocks/cell (x%.3f)  cells/supernode %.1f height %.0f\n", k.c_str(),
            a.structural / a.cells, a.stored / a.cells, a.stored / a.structural, a.cells / a.nsn, a.height / a.n);
