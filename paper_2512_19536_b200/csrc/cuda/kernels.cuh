@@ -120,11 +120,6 @@ struct SweepArgs {
   int prefetch;      // 1: L2 bulk prefetch of each unit's panel when it starts (PDG_SWEEP_PREFETCH)
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
-// warp-worker variant (sweep_warp.cu), PDG_SWEEP=warp
-void launch_sweep_warp(const SweepArgs& a, int smem_bytes, cudaStream_t st);
-int sweep_warp_workers_per_sm(int smem);
-void set_sweep_warp_smem(int bytes);
-bool sweep_warp_mode();
 
 // Ionic model + stimulus at quadrature nodes (one warp per cell).
 struct IonicArgs {

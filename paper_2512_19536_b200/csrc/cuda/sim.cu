@@ -369,7 +369,7 @@ void DeviceSim::upload_tasks() {
     const char* e = std::getenv(k);
     return 1024LL * (e ? std::max(2, std::atoi(e)) : d);
   };
-  // Default: ~20 units per resident CTA per sweep, clamped to [44, 88] KB.
+  // Default: ~20 units per resident CTA per sweep, clamped to [44, 128] KB.
   // Small problems (config2: 351 KB of panel per CTA) are critical-path
   // bound and want small units (44 KB was the best of a 16-96 KB scan);
   // large ones (config3 p=3: 1.9 MB per CTA) are bandwidth bound and want
@@ -380,10 +380,10 @@ void DeviceSim::upload_tasks() {
   int sms_u = 148, dev_u = 0;
   PDG_CUDA(cudaGetDevice(&dev_u));
   PDG_CUDA(cudaDeviceGetAttribute(&sms_u, cudaDevAttrMultiProcessorCount, dev_u));
-  const int max_kb = std::getenv("PDG_UNIT_MAX_KB") ? std::max(44, std::atoi(std::getenv("PDG_UNIT_MAX_KB"))) : 88;
+  // up to 128 KB: config4 sweep 6.33 ms vs 6.51 ms at 88 KB (profiles/r02e)
+  const int max_kb = std::getenv("PDG_UNIT_MAX_KB") ? std::max(44, std::atoi(std::getenv("PDG_UNIT_MAX_KB"))) : 128;
   const int auto_kb = static_cast<int>(std::clamp<long long>(panel_bytes / (20LL * sms_u * 8) / 1024, 44, max_kb));
-  // warp workers (PDG_SWEEP=warp): one warp streams a unit, so units are small
-  const long long kUnitBytes = env_kb("PDG_UNIT_KB", sweep_warp_mode() ? 16 : auto_kb);
+  const long long kUnitBytes = env_kb("PDG_UNIT_KB", auto_kb);
   const long long kLeafBytes = env_kb("PDG_LEAF_KB", static_cast<int>(kUnitBytes / 1024));
   int n_parts = 0, n_tile_ctr = 0;
   long long max_panel = 0, max_in = 0;
@@ -508,20 +508,15 @@ void DeviceSim::upload_tasks() {
   // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
   // partial sums + the unit's input buffer (sweep.cu)
   sweep_xcap = static_cast<int>(max_in) + 2;
-  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) *
-                        (sweep_warp_mode() ? (kSweepThreads / 32) * sweep_xcap : kSweepThreads + sweep_xcap);
-  if (smem_fwd > 200 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
-  if (smem_fwd > 48 * 1024) {
-    if (sweep_warp_mode()) set_sweep_warp_smem(smem_fwd);
-    else set_sweep_smem(smem_fwd);
-  }
+  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
+  if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
+  if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   const char* ord_env = std::getenv("PDG_SWEEP_ORDER");
   if (!(ord_env && std::strcmp(ord_env, "level") == 0)) {
     int sms = 148, dev = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int slots = sms * (sweep_warp_mode() ? sweep_warp_workers_per_sm(smem_fwd) : sweep_ctas_per_sm(smem_fwd));
-    const std::vector<int> perm = list_schedule(pr, fu, slots);
+    const std::vector<int> perm = list_schedule(pr, fu, sms * sweep_ctas_per_sm(smem_fwd));
     std::vector<DevUnit> o(fu.size());
     for (std::size_t i = 0; i < perm.size(); ++i) o[i] = fu[perm[i]];
     fu.swap(o);

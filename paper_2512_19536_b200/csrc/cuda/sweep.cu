@@ -28,8 +28,6 @@
 // one red.release.gpu. Counters are monotone across launches (sweep number
 // `epoch`), so no memsets are needed between sweeps.
 #include <cstdint>
-#include <cstdlib>
-#include <string>
 
 #include "kernels.cuh"
 
@@ -476,17 +474,8 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
 
 }  // namespace
 
-bool sweep_warp_mode() {
-  static const bool on = [] {
-    const char* e = std::getenv("PDG_SWEEP");
-    return e && std::string(e) == "warp";
-  }();
-  return on;
-}
-
 void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
   if (a.n_units == 0) return;
-  if (sweep_warp_mode()) return launch_sweep_warp(a, smem, st);
   static int cached_smem = -1, resident = 0;
   if (cached_smem != smem) {
     int per_sm = 0, sms = 0, dev = 0;

@@ -39,7 +39,7 @@ std::vector<int> etree(int m, const std::vector<std::vector<int>>& padj) {
 }
 
 double relax_z() {
-  static const double z = std::getenv("PDG_RELAX_Z") ? std::atof(std::getenv("PDG_RELAX_Z")) : 0.3;
+  static const double z = std::getenv("PDG_RELAX_Z") ? std::atof(std::getenv("PDG_RELAX_Z")) : 0.5;
   return z;
 }
 

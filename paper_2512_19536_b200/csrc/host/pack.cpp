@@ -20,9 +20,11 @@ namespace pdg {
 
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {
   constexpr int kTile = 32;
-  // rows per column segment are padded to a multiple of kRowAlign doubles
-  // (PDG_ROW_ALIGN overrides; 8 = one 64-byte burst)
-  static const int kRowAlign = std::getenv("PDG_ROW_ALIGN") ? std::max(2, std::atoi(std::getenv("PDG_ROW_ALIGN"))) : 8;
+  // Rows per column segment are padded to an even count (each lane streams
+  // double2 row pairs); PDG_ROW_ALIGN=8 pads to whole 64-byte bursts, which
+  // only added bytes once the L2 re-reads were fixed (config4 sweep 6.40 ms
+  // at 2 vs 6.51 ms at 8, profiles/r02e).
+  static const int kRowAlign = std::getenv("PDG_ROW_ALIGN") ? std::max(2, std::atoi(std::getenv("PDG_ROW_ALIGN"))) : 2;
   constexpr int kTileAlign = 16;    // 128 bytes
   const int bs = F.bs;
   const int base = static_cast<int>(pr.tasks.size());
@@ -65,12 +67,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     static const bool dense_roots = !(std::getenv("PDG_DENSE_ROOT") && std::getenv("PDG_DENSE_ROOT")[0] == '0');
     t.root_dense = dense_roots && S.parent < 0 && nr == 0 ? 1 : 0;
     // forward tiles: output rows of F
-    // Tiles start 128-byte aligned and every column segment is a whole number
-    // of 64-byte DRAM bursts (zero rows pad the tail): a warp's column reads
-    // then touch exactly the sectors they use, and the tile's L2 bulk prefetch
-    // covers whole bursts. (16-byte alignment over-fetched 27% of the panel
-    // bytes from DRAM at config 4, profiles/r01u.) Each lane streams double2
-    // pairs of rows.
+    // Tiles start 128-byte aligned; each lane streams double2 pairs of rows.
     auto seg = [&](int rows) { return (rows + kRowAlign - 1) / kRowAlign * kRowAlign; };
     auto align = [](std::int64_t off) { return (off + kTileAlign - 1) / kTileAlign * kTileAlign; };
     t.f_tile0 = static_cast<int>(pr.ftiles.size());

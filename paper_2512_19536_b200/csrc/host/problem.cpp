@@ -363,9 +363,19 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
   int nd_top = nd_merge;
   if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
-  // PDG_ORDER=md: minimum degree + fundamental supernodes (relaxed by PDG_MD_RELAX cells)
-  const bool md_order = !pos || (std::getenv("PDG_ORDER") && std::string(std::getenv("PDG_ORDER")) == "md");
-  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::atoi(std::getenv("PDG_MD_RELAX")) : 1;
+  // Ordering family (profiles/r02c-r02e, B200). Minimum degree with relaxed
+  // supernodes (host/ordering.hpp: <= 8 cells merged while the merge adds
+  // < 50% explicit zeros) stores fewer panel bytes than the ND above on the
+  // large meshes and its supernodes are as wide: config4 6.4 vs 7.5 ms per
+  // sweep, config5 p=2 2.8 vs 3.2 ms, p=4 12.2 vs 13.3 ms. Below ~2M dofs the
+  // sweep is latency bound and the shallower ND tree wins (config2 0.10 vs
+  // 0.22 ms, config3 p=3 0.43 vs 0.56 ms). Without cell positions (an
+  // operator handed over by the caller) the order is graph-only MD.
+  // PDG_ORDER=nd|md and PDG_MD_RELAX override.
+  const bool md_default = static_cast<std::int64_t>(N) * b >= 2000000;
+  const char* ord_env = std::getenv("PDG_ORDER");
+  const bool md_order = !pos || (ord_env ? std::string(ord_env) == "md" : md_default);
+  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : 8;
   pl.nd.assign(n_units, NdTree{});
   auto& nd = pl.nd;
   pl.unit_cells.assign(n_units, {});
