@@ -197,29 +197,17 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
 // double2 never straddles a column, so lane l always accumulates the fixed
 // row pair r = (2l + 64t) % B of column (2j)/B; lanes l = k (mod B/2) share a
 // pair and are summed by a shuffle tree in a fixed order (deterministic).
-//
-// FUSE: the CG direction update p' = z + beta p (krylov.cpp:70-72) is folded
-// in: every gathered operand is formed as fma(beta, p, z), the row's own p' is
-// written to `pnew` and weighs the fused p'.q. x = p (previous direction) and
-// pnew are distinct buffers (alternated by the caller), so no CTA reads a
-// value another CTA overwrites. Same bits as pupdate_kernel + plain SpMV.
-template <int B, bool FUSE = false>
+
+template <int B>
 __global__ void __launch_bounds__(256)
     spmv_warp_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                      const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop,
-                     const double* __restrict__ zv = nullptr, double* __restrict__ pnew = nullptr) {
+                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
   static_assert(B % 2 == 0, "even block size");
   constexpr int H = B * B / 2, NT = (H + 31) / 32, S = B / 2;
   pdl_wait();
   if (honor_stop && rc.S->stop) return;
-  const double beta = FUSE ? rc.S->beta : 0.0;
-  auto operand = [&](long long idx) {
-    if constexpr (FUSE)
-      return fma(beta, __ldg(x + idx), __ldg(zv + idx));
-    else
-      return __ldg(x + idx);
-  };
+  auto operand = [&](long long idx) { return __ldg(x + idx); };
   __shared__ double ys[8][B];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int row = blockIdx.x * 8 + wl;
@@ -305,13 +293,7 @@ __global__ void __launch_bounds__(256)
       const double yv = ys[wl][lane];
       const long long i = static_cast<long long>(row) * B + lane;
       y[i] = yv;
-      if constexpr (FUSE) {
-        const double pv = operand(i);
-        pnew[i] = pv;
-        contrib = pv * yv;
-      } else if (dotw) {
-        contrib = dotw[i] * yv;
-      }
+      if (dotw) contrib = dotw[i] * yv;
     }
   }
   if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
@@ -973,11 +955,9 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
   if (rows > 0 && warp_rows && (b == 6 || b == 10)) {
     const int g = (rows + 7) / 8;
     if (b == 6)
-      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
-                 nullptr, nullptr);
+      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
     else
-      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
-                 nullptr, nullptr);
+      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
     return;
   }
 #define L(B)                                                                                  \
@@ -988,27 +968,6 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
   }
   if (rows > 0) PDG_B_DISPATCH(b, L)
 #undef L
-}
-
-bool spmv_fuses_pupdate(int b, int rows) {
-  static const char* wenv = std::getenv("PDG_SPMV_WARP");
-  static const char* fenv = std::getenv("PDG_FUSE_P");
-  const bool warp_rows = wenv ? wenv[0] == '1' : rows <= 32768;
-  // opt-in: measured 1.7 % slower at config2 on B200 (the doubled operand gathers
-  // cost more than the pupdate launch they save, tried and reverted)
-  return (fenv ? fenv[0] == '1' : false) && rows > 0 && warp_rows && (b == 6 || b == 10);
-}
-
-void launch_spmv_pfused(int b, int rows, const int* ptr, const int* col, const double* val, const double* pold,
-                        const double* z, double* pnew, double* q, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
-  const int hs = honor_stop ? 1 : 0;
-  const int g = (rows + 7) / 8;
-  if (b == 6)
-    launch_pdl(spmv_warp_kernel<6, true>, g, 256, 0, st, rows, ptr, col, val, pold, q, nullptr, rc, hs, z, pnew);
-  else if (b == 10)
-    launch_pdl(spmv_warp_kernel<10, true>, g, 256, 0, st, rows, ptr, col, val, pold, q, nullptr, rc, hs, z, pnew);
-  else
-    throw CudaError("direction-fused SpMV needs the warp-row kernel (b = 6 or 10)");
 }
 
 void launch_residual(int b, int rows, const int* ptr, const int* col, const double* val,

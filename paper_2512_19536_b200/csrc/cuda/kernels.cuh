@@ -35,10 +35,6 @@ struct ReduceCtx {
 // y = K x (+ grid dot with `dotw`), BSR rows [0, rows). Early-exits when S->stop.
 // q = K p' with the direction update p' = z + beta p folded into the gather
 // (single rank, warp-row SpMV); p' goes to pnew (!= pold), p'.q is reduced
-bool spmv_fuses_pupdate(int b, int rows);
-void launch_spmv_pfused(int b, int rows, const int* ptr, const int* col, const double* val, const double* pold,
-                        const double* z, double* pnew, double* q, ReduceCtx rc, bool honor_stop,
-                        cudaStream_t st);
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val,
                  const double* x, double* y, const double* dotw, ReduceCtx rc, bool honor_stop,
                  cudaStream_t st);

@@ -101,11 +101,6 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   for (auto& v : d_U) v = dalloc<double>(n_ext);
   d_x = dalloc<double>(n_ext);
   d_p = dalloc<double>(n_ext);
-  pfuse = world == 1 && spmv_fuses_pupdate(b, ncells);
-  if (pfuse) {
-    d_p2 = dalloc<double>(n_ext);
-    PDG_CUDA(cudaMemsetAsync(d_p2, 0, n_ext * sizeof(double), st));
-  }
   d_r = dalloc<double>(n);
   d_z = dalloc<double>(n);
   d_q = dalloc<double>(n);
@@ -130,7 +125,7 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
     // restriction chunks: <= kChunk (<= 64) cells of one agglomerate per CTA;
     // small chunks keep the fused update + restriction spread over all SMs
-    const int kChunk = std::getenv("PDG_CHUNK_CELLS") ? std::clamp(std::atoi(std::getenv("PDG_CHUNK_CELLS")), 1, 64) : 32;
+    constexpr int kChunk = 32;
     std::vector<int> cptr{0}, nptr{0};
     for (int a = 0; a < pr.n_agg; ++a) {
       for (int k = pr.agg_cell_ptr[a]; k < pr.agg_cell_ptr[a + 1]; k += kChunk)
@@ -146,7 +141,6 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
       for (int k = cptr[c]; k < cptr[c + 1]; ++k)
         if (pr.agg_cells[k] != pr.agg_cells[cptr[c]] + (k - cptr[c])) chunks_contiguous = false;
     }
-    if (std::getenv("PDG_COARSE_TMA") && std::atoi(std::getenv("PDG_COARSE_TMA")) == 0) chunks_contiguous = false;
     d_chunk_ptr = dupload(cptr, st);
     d_node_chunk_ptr = dupload(nptr, st);
     d_r0part = dalloc<double>(static_cast<std::size_t>(std::max(n_chunks, 1)) * pr.bq);
@@ -500,8 +494,7 @@ void DeviceSim::upload_tasks() {
   make_units(fo, true, fu);
   make_units(bo, false, bu);
   // one ticket space (sweep.cu): forward and backward units in the order of a
-  // simulated list schedule (critical path first), or PDG_SWEEP_ORDER=level:
-  // all forward units by height, then all backward units by depth
+  // simulated list schedule (critical path first)
   n_units_f = static_cast<int>(fu.size());
   n_units_b = static_cast<int>(bu.size());
   fu.insert(fu.end(), bu.begin(), bu.end());
@@ -511,8 +504,7 @@ void DeviceSim::upload_tasks() {
   smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
-  const char* ord_env = std::getenv("PDG_SWEEP_ORDER");
-  if (!(ord_env && std::strcmp(ord_env, "level") == 0)) {
+  {
     int sms = 148, dev = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -578,7 +570,7 @@ DeviceSim::~DeviceSim() {
                   d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
                   d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage, d_chunk_ptr, d_node_chunk_ptr, d_r0part,
-                  d_live, d_area, d_means, d_p2};
+                  d_live, d_area, d_means};
   cudaEventDestroy(ev_t0);
   cudaEventDestroy(ev_t1);
   comm_destroy();
@@ -703,18 +695,10 @@ void DeviceSim::coarse_reduce_hook() {
 void DeviceSim::dot_reduce_hook(int) {}
 
 // The body of one PCG iteration (krylov.cpp:49-73), every kernel gated on S->stop.
-// With pfuse the SpMV also forms this iteration's direction p = z + beta p
-// from the previous one; the two direction buffers alternate with `parity`.
-void DeviceSim::record_iteration(int parity) {
+void DeviceSim::record_iteration() {
   double* p = d_p;
-  if (pfuse) {
-    const double* pold = parity ? d_p2 : d_p;
-    p = parity ? d_p : d_p2;
-    launch_spmv_pfused(b, ncells, d_ptr, d_col, d_kval, pold, z_of(d_r), p, d_q, red_for(kFinPq), true, st);
-  } else {
-    halo_exchange(d_p);
-    launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
-  }
+  halo_exchange(d_p);
+  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
   after_reduce(kFinPq, true);
   if (world > 1) {
     // Several ranks: the update stores this rank's ||r||^2 partial behind r0,
@@ -735,7 +719,7 @@ void DeviceSim::record_iteration(int parity) {
       launch_finish(rctx(kFinRr), d_dot_global, true, st);
     }
     precond_apply(d_r, z_of(d_r), kFinRz, true, coarse);
-    if (!pfuse) launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
+    launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
     return;
   }
   const bool fuse = use_pc() && P->two_level && world == 1;
@@ -749,7 +733,7 @@ void DeviceSim::record_iteration(int parity) {
     launch_update(n, d_x, d_r, p, d_q, red_for(kFinRr), st);
   after_reduce(kFinRr, true);
   precond_apply(d_r, z_of(d_r), kFinRz, true, fuse);
-  if (!pfuse) launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
+  launch_pupdate(n, d_p, z_of(d_r), d_S, false, st);
 }
 
 // PCG after r = b - K x0 and denom are in place: z = B r, rho, p = z, then
@@ -790,8 +774,7 @@ void DeviceSim::build_solve_graph(Graph& g) {
   PDG_CUDA(cudaGraphAddNode(&cond_node, g.graph, &tail_node, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   PDG_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  record_iteration(0);
-  if (pfuse) record_iteration(1);  // the direction buffers alternate: two iterations per body
+  record_iteration();
   launch_pdl(set_condition_kernel, 1, 1, 0, st, handle, d_S);
   PDG_CUDA(cudaStreamEndCapture(st, &body));
   PDG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
@@ -824,7 +807,7 @@ void DeviceSim::run_solve(int maxit, PcgResult& res) {
     record_solve_tail();
     constexpr int kPoll = 4;
     for (int it = 0; it < maxit;) {
-      for (int j = 0; j < kPoll && it < maxit; ++j, ++it) record_iteration(it & 1);
+      for (int j = 0; j < kPoll && it < maxit; ++j, ++it) record_iteration();
       PDG_CUDA(cudaMemcpyAsync(h_S, d_S, sizeof(PcgScalars), cudaMemcpyDeviceToHost, st));
       PDG_CUDA(cudaStreamSynchronize(st));
       if (h_S->stop) break;
@@ -1024,8 +1007,7 @@ StepResult DeviceSim::step() {
   }
   k += 1;
   t = k * c.dt;
-  launches += (ionic ? 1 : 0) + 1 + precond_launches() + 1 + body_launches() * static_cast<long long>(res.iterations) +
-              (pfuse ? (res.iterations + 1) / 2 : 0);  // one set_condition per two-iteration body
+  launches += (ionic ? 1 : 0) + 1 + precond_launches() + 1 + body_launches() * static_cast<long long>(res.iterations);
   float ms_all = 0.f, ms_solve = 0.f;
   cudaEventElapsedTime(&ms_all, ev0, ev2);
   cudaEventElapsedTime(&ms_solve, ev1, ev2);
@@ -1055,8 +1037,8 @@ int DeviceSim::precond_launches() const {
 // restriction is fused into the update
 int DeviceSim::body_launches() const {
   const int fused = (use_pc() && P->two_level && world == 1) ? 1 : 0;
-  // spmv, update, preconditioner, pupdate (folded into the spmv with pfuse), set_condition
-  int k = 1 + 1 + precond_launches() - fused + (pfuse ? 0 : 1) + (world == 1 && !pfuse ? 1 : 0);
+  // spmv, update, preconditioner, pupdate, set_condition
+  int k = 1 + 1 + precond_launches() - fused + 1 + (world == 1 ? 1 : 0);
   if (world > 1) k += 3 + static_cast<int>(halo_peers.size());  // finish kernels + halo packs
   return k;
 }
@@ -1131,12 +1113,8 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
     ms[i] = 0.0;
     bytes[i] = 0;
   }
-  if (pfuse)  // slot 0 = the SpMV with the direction update folded in (slot 6 stays 0)
-    timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 32 * n,
-           [&] { launch_spmv_pfused(b, ncells, d_ptr, d_col, d_kval, d_p, d_z, d_p2, d_q, rs, false, st); });
-  else
-    timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 24 * n,
-           [&] { launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rs, false, st); });
+  timeit(0, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 24 * n,
+         [&] { launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, rs, false, st); });
   const bool fused = use_pc() && pr.two_level && world == 1;
   if (fused)  // slot 1 = the update fused with the restriction (slots 2, 4 stay 0)
     timeit(1, 48 * n + 8 * N * b * bq + 4 * N + 8LL * n_chunks * bq, [&] {
@@ -1171,7 +1149,7 @@ void DeviceSim::profile(int reps, double* ms, long long* bytes) {
                launch_prolong_dot(b, bq, ncells, d_E, d_cell_agg, d_y0, d_r, d_z, rs, st);
            });
   }
-  if (!pfuse) timeit(6, 24 * n, [&] { launch_pupdate(n, d_tmp, d_z, d_S, false, st); });
+  timeit(6, 24 * n, [&] { launch_pupdate(n, d_tmp, d_z, d_S, false, st); });
   timeit(8, 8 * nnzb * b * b + 4 * nnzb + 4 * (N + 1) + 8 * N * b * b + 56 * n, [&] {
     launch_rhs(b, ncells, d_ptr, d_col, d_kval, d_M, 2.0, d_U[0], nullptr, 1, d_tmp, d_tmp2, d_q, rs, st);
   });

@@ -65,8 +65,6 @@ class DeviceSim {
   // state and work vectors (internal order)
   double* d_U[2] = {nullptr, nullptr};  // curr, prev
   double* d_Y[3] = {nullptr, nullptr, nullptr};  // curr, prev, next
-  double* d_p2 = nullptr;  // second direction buffer of the direction-fused SpMV
-  bool pfuse = false;       // p = z + beta p folded into the SpMV (spmv_fuses_pupdate)
   double *d_x = nullptr, *d_p = nullptr, *d_r = nullptr, *d_z = nullptr, *d_q = nullptr;
   double *d_rhs = nullptr, *d_ion = nullptr, *d_tmp = nullptr, *d_tmp2 = nullptr, *d_scratch = nullptr;
   // coarse
@@ -173,7 +171,7 @@ class DeviceSim {
   void precond_apply(const double* r, double* z, int finish, bool honor, bool restricted = false);
   IonicArgs ionic_args(bool has_prev) const;
   double* z_of(double* r);
-  void record_iteration(int parity = 0);
+  void record_iteration();
   void record_solve_tail();
   void build_solve_graph(Graph& g);
   void reset_scalars(double tol, int maxit);

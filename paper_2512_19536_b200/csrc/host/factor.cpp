@@ -18,14 +18,6 @@ std::int64_t SupernodalFactor::values() const {
 
 namespace {
 
-bool separator_cover() {
-  static const bool on = [] {
-    const char* e = std::getenv("PDG_ND_COVER");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // Minimum vertex cover of the bipartite graph of edges between side 0 and
 // side 1 (nodes of `ord`, side[] in {0,1}): maximum matching by augmenting
 // paths (Kuhn, sides scanned in `ord` order, so deterministic), then Koenig's
@@ -119,7 +111,6 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
   t.sn_start.push_back(0);
   std::vector<int> side(m, -1), mate(m, -1), seen(m, -1), par(m, -1);
   constexpr int n_dirs = 4;
-  const bool mvc = separator_cover();
   auto emit = [&](const std::vector<int>& nodes) {
     for (int v : nodes) t.order.push_back(v);
     t.sn_start.push_back(static_cast<int>(t.order.size()));
@@ -166,7 +157,7 @@ NdTree nested_dissection(int m, const std::vector<int>& adj_ptr, const std::vect
               }
             }
           }
-          if (mvc) {
+          {
             // minimum vertex cover of the cut edges (Koenig): the smallest
             // separator whose removal disconnects the two halves
             std::vector<int> cover = min_cut_cover(ord, side, adj_ptr, adj, mate, seen, par);
@@ -367,15 +358,6 @@ SupernodalFactor supernodal_cholesky(const BlockMatrix& A, const NdTree& nd) {
         double* ck = P.data() + static_cast<std::size_t>(k) * H;
         for (int i = k; i < H; ++i) ck[i] -= cj[i] * lkj;
       }
-    }
-    if (std::getenv("PDG_FILL_STATS")) {
-      static std::atomic<long long> dense{0}, lnz{0}, sky{0}, diag{0};
-      static std::atomic<int> cnt{0};
-      long long d = (long long)w * (w + 1) / 2 + (long long)r * bs * w, l = 0, sk = 0;
-      for (int j = 0; j < w; ++j) for (int i = j; i < H; ++i) if (P[(size_t)j * H + i] != 0.0) ++l;
-      for (int i = w; i < H; ++i) { int f = w; for (int j = 0; j < w; ++j) if (P[(size_t)j * H + i] != 0.0) { f = j; break; } sk += w - f; }
-      dense += d; lnz += l; sky += sk; diag += (long long)w * (w + 1) / 2;
-      if (++cnt % 500 == 0) fprintf(stderr, "fill: dense %lld lnz %lld diag+skyline %lld diag %lld\n", dense.load(), lnz.load(), diag.load() + sky.load(), diag.load());
     }
     // inv(L_SS), packed column-major lower
     S.Linv.assign(static_cast<std::size_t>(w) * (w + 1) / 2, 0.0);

@@ -63,9 +63,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
       pr.lval.insert(pr.lval.end(), S.B.begin(), S.B.end());
     }
     // a root with no below rows takes one dense symmetric panel
-    // (PDG_DENSE_ROOT=0 keeps the forward/backward pair)
-    static const bool dense_roots = !(std::getenv("PDG_DENSE_ROOT") && std::getenv("PDG_DENSE_ROOT")[0] == '0');
-    t.root_dense = dense_roots && S.parent < 0 && nr == 0 ? 1 : 0;
+    t.root_dense = S.parent < 0 && nr == 0 ? 1 : 0;
     // forward tiles: output rows of F
     // Tiles start 128-byte aligned; each lane streams double2 pairs of rows.
     auto seg = [&](int rows) { return (rows + kRowAlign - 1) / kRowAlign * kRowAlign; };

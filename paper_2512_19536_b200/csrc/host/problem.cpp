@@ -360,9 +360,6 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   if (const char* env = std::getenv("PDG_ND_MERGE")) nd_merge = std::max(1, std::atoi(env));
   int leaf = std::clamp(64 / b, 4, 16);  // config4: 6-cell leaves +3.8% over 4
   if (const char* env = std::getenv("PDG_ND_LEAF")) leaf = std::max(1, std::atoi(env));
-  // separator levels in the root supernode (applied densely, pack.cpp); PDG_ND_TOP overrides
-  int nd_top = nd_merge;
-  if (const char* env = std::getenv("PDG_ND_TOP")) nd_top = std::max(1, std::atoi(env));
   // Ordering family (profiles/r02c-r02e, B200). Minimum degree with relaxed
   // supernodes (host/ordering.hpp: <= 8 cells merged while the merge adds
   // < 50% explicit zeros) stores fewer panel bytes than the ND above on the
@@ -400,7 +397,7 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
       ap.push_back(static_cast<int>(aj.size()));
       if (pos) lpos[i] = (*pos)[cells[i]];
     }
-    nd[u] = md_order ? md_supernodes(m, ap, aj, md_relax) : nested_dissection(m, ap, aj, lpos, leaf, nd_merge, nd_top);
+    nd[u] = md_order ? md_supernodes(m, ap, aj, md_relax) : nested_dissection(m, ap, aj, lpos, leaf, nd_merge);
     unit_fill[u] = structural_fill(m, ap, aj, nd[u].order).scalar(b);
     unit_cells[u].resize(m);
     for (int i = 0; i < m; ++i) unit_cells[u][i] = cells[nd[u].order[i]];
