@@ -2,17 +2,21 @@
 //
 // An Eigen-free restatement of the reference's numeric path
 // (/root/reference/proj/src/{dg_space,quadrature,assembly,ionics,krylov,
-// schwarz,timestepper}.cpp). The reference itself cannot be built here
-// (Eigen3 is absent, proj/CMakeLists.txt:12), so parity of the GPU path is
-// anchored on this restatement, which is in turn pinned by the reference's own
-// unit/acceptance assertions (tests/test_oracle_*.py) and, for the mesh half,
-// by the compiled reference sources (oracle/_ref). Only tests/, smoke() and
-// bench.py's cpu_baseline leg load it; the product never links it.
+// schwarz,timestepper}.cpp). Pinned two ways: by the reference's own unit and
+// acceptance assertions (tests/test_oracle_pins.py), and by the reference's
+// numeric sources themselves, compiled in oracle/_ref against a small Eigen
+// API stand-in (oracle/eigen_shim; Eigen3 is absent here): M/A/K/E agree
+// bitwise, and acceptance criteria 2/3/7/8/9, config 1 and the default
+// Simulation match the goldens that build produced (tests/golden/
+// reference_numeric.json, tests/test_reference_numeric.py). The mesh half is
+// pinned by the reference's compiled mesh sources (oracle/_ref). Only tests/,
+// smoke() and bench.py's cpu_baseline / reference legs load it; the product
+// never links it.
 //
 // Deliberately independent of the product code: its own quadrature, basis,
 // assembly (triplets summed in insertion order like Eigen's setFromTriplets),
-// exact local solvers (minimum-degree block Cholesky instead of the product's
-// nested-dissection supernodal factor), PCG loop and a QL tridiagonal
+// exact local solvers (its own minimum-degree block Cholesky; the product
+// packs supernodal factors for the GPU sweep), PCG loop and a QL tridiagonal
 // eigensolver for the Lanczos estimate (the product uses bisection).
 //
 // Barreto-Cressman (ionic == 2): PARITY UNPINNED against the reference, which

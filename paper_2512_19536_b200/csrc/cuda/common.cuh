@@ -84,7 +84,10 @@ struct Reducer {
   unsigned int* counter;
 };
 
-constexpr int kSweepThreads = 128;
+#ifndef PDG_SWEEP_THREADS
+#define PDG_SWEEP_THREADS 128
+#endif
+constexpr int kSweepThreads = PDG_SWEEP_THREADS;  // build knob (-DPDG_SWEEP_THREADS=64/128/256)
 constexpr int kVecThreads = 256;
 
 // Programmatic dependent launch: the PCG body kernels are launched so that a

@@ -107,11 +107,12 @@ def test_config1_full_run():
 
 
 def test_config2_mesh_partial_run():
-    """BASELINE config 2 (16,384 cells, p = 3, 64 subdomains): 3 steps against the oracle."""
+    """BASELINE config 2 (16,384 cells, p = 3, 64 subdomains): the first 20 CN
+    steps against the oracle (all 200 steps: scripts/parity_full.py, profiles/)."""
     cfg = configs.config2()
     sim = Simulation(cfg)
     orc, _ = oracle_for(cfg)
-    for _ in range(3):
+    for _ in range(20):
         s, so = sim.step(), orc.step()
         assert abs(s.iterations - so["iterations"]) <= 1
     assert rel(sim.state()[2], orc.state()[2]) <= STATE_TOL
@@ -189,12 +190,21 @@ def test_equilibrium_fixed_point():
 
 @pytest.mark.parametrize("p,S", [(1, 256), (2, 64)])
 def test_config3_solve_property(p, S):
-    """Full-size config-3 operator: one rtol-1e-10 solve, residual checked through apply_K."""
+    """Full-size config-3 operator: B r and one rtol-1e-10 solve against the
+    CPU oracle on the same seeded right-hand side (mt19937_64, acceptance.cpp:
+    285-286), plus the residual through apply_K and the symmetry of B."""
+    from paper_2512_19536_b200 import _lib
+    from tests import oracle_binding as ob
     cfg = configs.config3(p, S)
     sim = Simulation(cfg)
-    b = np.random.default_rng(42).uniform(-1, 1, sim.dimension)
+    b = _lib.uniform_rhs(42, sim.dimension)
+    orc, _ = oracle_for(cfg)
+    assert np.array_equal(b, ob.uniform_rhs(42, sim.dimension))
+    assert rel(sim.apply_precond(b), orc.apply_precond(b)) <= 1e-10
     x, rep = sim.pcg_solve(b, 1e-10)
-    assert rep.converged
+    xo, ro = orc.pcg_solve(b, 1e-10)
+    assert rep.converged and abs(rep.iterations - ro["iterations"]) <= 1 and rel(x, xo) <= 1e-10
+    del orc
     r = b - sim.apply_K(x)
     assert np.linalg.norm(r) <= 1.5e-10 * np.linalg.norm(b)
     # z = B r is linear and symmetric: <u, B v> == <v, B u>
