@@ -15,3 +15,10 @@ for T in 64 128 256; do
   run $D t${T}_c2 config2
   run $D t${T}_c5p2 config5:2
 done
+# lookahead-unit L2 prefetch (bit 8) on top of the default (3), and instead of it (10)
+run $R pf11_c2 config2 PDG_SWEEP_PREFETCH=11
+run $R pf10_c2 config2 PDG_SWEEP_PREFETCH=10
+run $R pf11_c4 config4 PDG_SWEEP_PREFETCH=11
+run $R pf10_c4 config4 PDG_SWEEP_PREFETCH=10
+run $R pf11_c3p3 config3:3:64 PDG_SWEEP_PREFETCH=11
+run $R pf3_c3p3 config3:3:64
