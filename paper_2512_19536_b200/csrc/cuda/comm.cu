@@ -87,17 +87,17 @@ class NcclTransport final : public Transport {
     nccl_check(nccl().AllReduce(src, dst, static_cast<size_t>(count), ncclFloat64, ncclSum, comm_, st),
                "ncclAllReduce");
   }
-  void exchange(DeviceSim& s, double* v) override {
+  void exchange(DeviceSim& s, double* v, cudaStream_t st) override {
     auto& api = nccl();
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (const auto& h : s.halo_peers) {
       if (h.send_count)
         nccl_check(api.Send(s.d_sendbuf + static_cast<long long>(h.send_off) * s.b,
-                            static_cast<size_t>(h.send_count) * s.b, ncclFloat64, h.peer, comm_, s.st),
+                            static_cast<size_t>(h.send_count) * s.b, ncclFloat64, h.peer, comm_, st),
                    "ncclSend");
       if (h.recv_count)
         nccl_check(api.Recv(v + (static_cast<long long>(s.ncells) + h.recv_off) * s.b,
-                            static_cast<size_t>(h.recv_count) * s.b, ncclFloat64, h.peer, comm_, s.st),
+                            static_cast<size_t>(h.recv_count) * s.b, ncclFloat64, h.peer, comm_, st),
                    "ncclRecv");
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
@@ -157,14 +157,14 @@ class LoopbackTransport final : public Transport {
     PDG_CUDA(cudaMemcpyAsync(dst, sum_.data(), count * sizeof(double), cudaMemcpyHostToDevice, st));
     PDG_CUDA(cudaStreamSynchronize(st));
   }
-  void exchange(DeviceSim& s, double* v) override {
+  void exchange(DeviceSim& s, double* v, cudaStream_t st) override {
     long long nsend = 0;
     for (const auto& h : s.halo_peers) nsend = std::max<long long>(nsend, h.send_off + h.send_count);
     auto& mine = g_->buf[rank_];
     mine.resize(static_cast<std::size_t>(nsend * s.b));
     if (nsend)
-      PDG_CUDA(cudaMemcpyAsync(mine.data(), s.d_sendbuf, nsend * s.b * sizeof(double), cudaMemcpyDeviceToHost, s.st));
-    PDG_CUDA(cudaStreamSynchronize(s.st));
+      PDG_CUDA(cudaMemcpyAsync(mine.data(), s.d_sendbuf, nsend * s.b * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
     g_->peers[rank_] = &s.halo_peers;
     g_->barrier();
     for (const auto& h : s.halo_peers) {
@@ -177,9 +177,9 @@ class LoopbackTransport final : public Transport {
       PDG_CUDA(cudaMemcpyAsync(v + (static_cast<long long>(s.ncells) + h.recv_off) * s.b,
                                g_->buf[h.peer].data() + static_cast<long long>(src->send_off) * s.b,
                                static_cast<std::size_t>(h.recv_count) * s.b * sizeof(double), cudaMemcpyHostToDevice,
-                               s.st));
+                               st));
     }
-    PDG_CUDA(cudaStreamSynchronize(s.st));
+    PDG_CUDA(cudaStreamSynchronize(st));
     g_->barrier();
   }
   const char* name() const override { return "loopback"; }
@@ -194,7 +194,21 @@ void DeviceSim::comm_allreduce(const double* src, double* dst, long long count) 
   transport->allreduce(src, dst, count, st);
 }
 
-void DeviceSim::comm_exchange(double* v) { transport->exchange(*this, v); }
+void DeviceSim::comm_exchange(double* v, cudaStream_t on) { transport->exchange(*this, v, on); }
+
+void DeviceSim::spmv_overlapped(double* v, double* y) {
+  for (const HaloPeer& h : halo_peers)
+    launch_pack(v, d_send_cells + h.send_off, h.send_count, b, d_sendbuf + static_cast<long long>(h.send_off) * b, st);
+  PDG_CUDA(cudaEventRecord(ev_pack, st));
+  // p.q partial: interior rows store it, the halo rows add theirs (fixed order)
+  launch_spmv(b, n_rows_int, d_ptr, d_col, d_kval, v, y, v, rctx(kFinStore, d_dot_local), true, st, d_rows_int);
+  PDG_CUDA(cudaStreamWaitEvent(st_comm, ev_pack, 0));
+  comm_exchange(v, st_comm);
+  PDG_CUDA(cudaEventRecord(ev_halo, st_comm));
+  PDG_CUDA(cudaStreamWaitEvent(st, ev_halo, 0));
+  launch_spmv(b, n_rows_bnd, d_ptr, d_col, d_kval, v, y, v, rctx(n_rows_int > 0 ? kFinAccum : kFinStore, d_dot_local),
+              true, st, d_rows_bnd);
+}
 
 void DeviceSim::comm_destroy() { transport.reset(); }
 
@@ -254,6 +268,25 @@ void DeviceSim::connect(std::unique_ptr<Transport> t) {
   if (!send_cells.empty())
     PDG_CUDA(cudaMemcpy(d_send_cells, send_cells.data(), send_cells.size() * sizeof(int), cudaMemcpyHostToDevice));
   d_sendbuf = dmalloc<double>(send_cells.size() * static_cast<std::size_t>(b));
+  // rows that read no halo cell run while the halo is in flight (spmv_overlapped)
+  {
+    std::vector<int> ri, rb;
+    for (int i = 0; i < ncells; ++i) {
+      bool halo = false;
+      for (int k = pr.K.ptr[i]; k < pr.K.ptr[i + 1] && !halo; ++k)
+        halo = pr.K.col[k] < pr.cell_begin || pr.K.col[k] >= pr.cell_end;
+      (halo ? rb : ri).push_back(i);
+    }
+    n_rows_int = static_cast<int>(ri.size());
+    n_rows_bnd = static_cast<int>(rb.size());
+    d_rows_int = dmalloc<int>(ri.size());
+    d_rows_bnd = dmalloc<int>(rb.size());
+    if (!ri.empty()) PDG_CUDA(cudaMemcpy(d_rows_int, ri.data(), ri.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!rb.empty()) PDG_CUDA(cudaMemcpy(d_rows_bnd, rb.data(), rb.size() * sizeof(int), cudaMemcpyHostToDevice));
+    PDG_CUDA(cudaStreamCreateWithFlags(&st_comm, cudaStreamNonBlocking));
+    PDG_CUDA(cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming));
+    PDG_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
+  }
 
   // K0 = sum over ranks of the local-row Galerkin products, then the
   // replicated coarse factorisation and the full task list

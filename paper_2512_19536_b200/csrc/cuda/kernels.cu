@@ -108,6 +108,9 @@ __device__ void apply_finish(const ReduceCtx& rc, double s) {
     case kFinStore:
       *rc.out = s;
       break;
+    case kFinAccum:
+      *rc.out += s;
+      break;
     default:
       break;
   }
@@ -176,13 +179,15 @@ template <int B>
 __global__ void __launch_bounds__(RowGeom<B>::kThreads)
     spmv_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+                const double* __restrict__ dotw, ReduceCtx rc, int honor_stop,
+                const int* __restrict__ rowlist) {
   pdl_wait();
   if (honor_stop && rc.S->stop) return;
   const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
-  const int row = blockIdx.x * RowGeom<B>::kRows + lr;
+  const int slot = blockIdx.x * RowGeom<B>::kRows + lr;
   double contrib = 0.0;
-  if (lr < RowGeom<B>::kRows && row < rows) {
+  if (lr < RowGeom<B>::kRows && slot < rows) {
+    const int row = rowlist ? __ldg(rowlist + slot) : slot;
     const double acc = bsr_row_dot<B>(row, r, ptr, col, val, x);
     const long long i = static_cast<long long>(row) * B + r;
     y[i] = acc;
@@ -202,7 +207,8 @@ template <int B>
 __global__ void __launch_bounds__(256)
     spmv_warp_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                      const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop) {
+                     const double* __restrict__ dotw, ReduceCtx rc, int honor_stop,
+                     const int* __restrict__ rowlist) {
   static_assert(B % 2 == 0, "even block size");
   constexpr int H = B * B / 2, NT = (H + 31) / 32, S = B / 2;
   pdl_wait();
@@ -210,9 +216,10 @@ __global__ void __launch_bounds__(256)
   auto operand = [&](long long idx) { return __ldg(x + idx); };
   __shared__ double ys[8][B];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int row = blockIdx.x * 8 + wl;
+  const int slot = blockIdx.x * 8 + wl;
   double contrib = 0.0;
-  if (row < rows) {
+  if (slot < rows) {
+    const int row = rowlist ? __ldg(rowlist + slot) : slot;
     const double2* __restrict__ v2 = reinterpret_cast<const double2*>(val);
     double2 acc[NT];
     int cj[NT];
@@ -945,7 +952,8 @@ int vec_grid(long long n) {
   }
 
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val, const double* x,
-                 double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st) {
+                 double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st,
+                 const int* rowlist) {
   // even B (p = 2, 3) on small row counts: warp per block row. The
   // thread-per-row kernel fills only ~half the GPU below ~30K block rows
   // (config2: 656 CTAs) but streams better once every SM holds several of its
@@ -955,16 +963,18 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
   if (rows > 0 && warp_rows && (b == 6 || b == 10)) {
     const int g = (rows + 7) / 8;
     if (b == 6)
-      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+      launch_pdl(spmv_warp_kernel<6>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
+                 rowlist);
     else
-      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0);
+      launch_pdl(spmv_warp_kernel<10>, g, 256, 0, st, rows, ptr, col, val, x, y, dotw, rc, honor_stop ? 1 : 0,
+                 rowlist);
     return;
   }
 #define L(B)                                                                                  \
   {                                                                                           \
     const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \
     launch_pdl(spmv_kernel<B>, g, RowGeom<B>::kThreads, 0, st, rows, ptr, col, val, x, y, dotw, rc, \
-               honor_stop ? 1 : 0);                                                           \
+               honor_stop ? 1 : 0, rowlist);                                                  \
   }
   if (rows > 0) PDG_B_DISPATCH(b, L)
 #undef L

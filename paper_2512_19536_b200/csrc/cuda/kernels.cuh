@@ -22,6 +22,7 @@ enum Finish : int {
   kFinRzInit = 4,  // first rho with breakdown checks
   kFinRz = 5,      // rho_next, beta, maxit
   kFinStore = 6,   // *out = sum
+  kFinAccum = 7,   // *out += sum (a second partial added in a fixed order)
 };
 
 struct ReduceCtx {
@@ -32,12 +33,12 @@ struct ReduceCtx {
   int finish;
 };
 
-// y = K x (+ grid dot with `dotw`), BSR rows [0, rows). Early-exits when S->stop.
-// q = K p' with the direction update p' = z + beta p folded into the gather
-// (single rank, warp-row SpMV); p' goes to pnew (!= pold), p'.q is reduced
+// y = K x (+ grid dot with `dotw`), BSR rows [0, rows), or the `rows` block
+// rows listed in `rowlist` (multi-rank: interior rows while the halo is in
+// flight, then the rows that read it). Early-exits when S->stop.
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val,
                  const double* x, double* y, const double* dotw, ReduceCtx rc, bool honor_stop,
-                 cudaStream_t st);
+                 cudaStream_t st, const int* rowlist = nullptr);
 // r = bvec - K x ; x untouched ; sum r.r -> kFinDenom
 void launch_residual(int b, int rows, const int* ptr, const int* col, const double* val,
                      const double* x, const double* bvec, double* r, ReduceCtx rc, cudaStream_t st);

@@ -570,7 +570,7 @@ DeviceSim::~DeviceSim() {
                   d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
                   d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage, d_chunk_ptr, d_node_chunk_ptr, d_r0part,
-                  d_live, d_area, d_means};
+                  d_live, d_area, d_means, d_rows_int, d_rows_bnd};
   cudaEventDestroy(ev_t0);
   cudaEventDestroy(ev_t1);
   comm_destroy();
@@ -578,6 +578,9 @@ DeviceSim::~DeviceSim() {
     if (p) cudaFree(p);
   if (h_S) cudaFreeHost(h_S);
   if (st) cudaStreamDestroy(st);
+  if (st_comm) cudaStreamDestroy(st_comm);
+  if (ev_pack) cudaEventDestroy(ev_pack);
+  if (ev_halo) cudaEventDestroy(ev_halo);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   cudaEventDestroy(ev2);
@@ -684,7 +687,7 @@ void DeviceSim::halo_exchange(double* v) {
   if (world == 1 || halo_peers.empty()) return;
   for (const HaloPeer& h : halo_peers)
     launch_pack(v, d_send_cells + h.send_off, h.send_count, b, d_sendbuf + static_cast<long long>(h.send_off) * b, st);
-  comm_exchange(v);
+  comm_exchange(v, st);
 }
 
 // every rank solves the coarse problem redundantly on the summed r0 (C3)
@@ -697,8 +700,12 @@ void DeviceSim::dot_reduce_hook(int) {}
 // The body of one PCG iteration (krylov.cpp:49-73), every kernel gated on S->stop.
 void DeviceSim::record_iteration() {
   double* p = d_p;
-  halo_exchange(d_p);
-  launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
+  if (world > 1 && !halo_peers.empty()) {
+    spmv_overlapped(d_p, d_q);  // p.q partial -> d_dot_local, all-reduced below
+  } else {
+    halo_exchange(d_p);
+    launch_spmv(b, ncells, d_ptr, d_col, d_kval, d_p, d_q, d_p, red_for(kFinPq), true, st);
+  }
   after_reduce(kFinPq, true);
   if (world > 1) {
     // Several ranks: the update stores this rank's ||r||^2 partial behind r0,

@@ -40,7 +40,7 @@ class Transport {
   virtual ~Transport() = default;
   virtual void allreduce(const double* src, double* dst, long long count, cudaStream_t st) = 0;
   // halo tail of v from the peers' packed d_sendbuf
-  virtual void exchange(DeviceSim& s, double* v) = 0;
+  virtual void exchange(DeviceSim& s, double* v, cudaStream_t st) = 0;
   virtual const char* name() const = 0;
 };
 
@@ -139,7 +139,14 @@ class DeviceSim {
   void attach_loopback(const std::shared_ptr<LoopbackGroup>& g, int rank, int world);
   void connect(std::unique_ptr<Transport> t);
   void comm_allreduce(const double* src, double* dst, long long count);
-  void comm_exchange(double* v);
+  void comm_exchange(double* v, cudaStream_t on);
+  // multi-rank SpMV with the halo in flight: interior rows, then the rows
+  // that read the halo (row lists built at connect)
+  void spmv_overlapped(double* v, double* y);
+  cudaStream_t st_comm = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+  int *d_rows_int = nullptr, *d_rows_bnd = nullptr;
+  int n_rows_int = 0, n_rows_bnd = 0;
   void release_tasks();
   void comm_destroy();
 
