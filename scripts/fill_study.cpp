@@ -35,6 +35,7 @@ int main(int argc, char** argv) {
   struct Acc {
     double cells = 0, structural = 0, stored = 0, nsn = 0, height = 0, n = 0;
     double panel[4] = {0, 0, 0, 0};  // panel doubles (fwd + bwd): align 8 / align 2 / tri16+align8 / tri16+align2
+    double bundled_tasks = 0, bundles = 0, free_tasks = 0;
   };
   std::map<std::string, Acc> acc;
   for (int u = 0; u < part.count; u += every) {
@@ -69,6 +70,7 @@ int main(int argc, char** argv) {
         for (int q = 0; q < ns; ++q)
           if (t.parent[q] >= 0) kids[t.parent[q]].push_back(q);
         std::vector<int> mark(m, -1);
+        std::vector<double> fbytes_of(ns, 0.0);
         for (int q = 0; q < ns; ++q) {
           const int a0 = t.sn_start[q], e = t.sn_start[q + 1];
           auto addr = [&](int r) { if (r >= e && mark[r] != q) { mark[r] = q; rows[q].push_back(r); } };
@@ -85,8 +87,38 @@ int main(int argc, char** argv) {
             // backward: rows of H = columns of F, inputs i >= r0
             for (long r0 = 0; r0 < w; r0 += trit) { long rr = std::min<long>(trit, w - r0); tot += (double)(h - r0) * seg(rr); }
             a.panel[var] += tot;
+            if (var == 1) fbytes_of[q] = tot * 8 / 2;  // ~forward half
           }
         }
+        // bundles: maximal complete subtrees (non-root) with <= 64 KB of forward
+        // panel, siblings grouped while the group stays <= 64 KB
+        std::vector<double> sub(ns, 0.0);
+        for (int q = 0; q < ns; ++q) {
+          sub[q] += fbytes_of[q];
+          if (t.parent[q] >= 0) sub[t.parent[q]] += sub[q];
+        }
+        const double Bmax = 65536;
+        std::vector<char> in_bundle(ns, 0);
+        for (int q = 0; q < ns; ++q) {
+          // children of q that are small complete subtrees, grouped greedily
+          double acc = 0; int cnt = 0;
+          for (int c : kids[q]) {
+            if (sub[c] > Bmax) continue;
+            if (acc + sub[c] > Bmax && cnt > 0) { a.bundles += 1; acc = 0; cnt = 0; }
+            acc += sub[c]; ++cnt;
+          }
+          if (cnt > 0) a.bundles += 1;
+        }
+        for (int q = 0; q < ns; ++q) {
+          const int pp = t.parent[q];
+          if (pp >= 0 && sub[q] <= Bmax) in_bundle[q] = 1;
+        }
+        // a task is bundled if it or an ancestor (below a big node) is a small subtree root
+        for (int q = ns - 1; q >= 0; --q) {
+          const int pp = t.parent[q];
+          if (pp >= 0 && in_bundle[pp]) in_bundle[q] = 1;
+        }
+        for (int q = 0; q < ns; ++q) (in_bundle[q] ? a.bundled_tasks : a.free_tasks) += 1;
       }
       std::vector<int> h(t.parent.size(), 1);
       int hmax = 0;
@@ -98,8 +130,12 @@ int main(int argc, char** argv) {
       a.n += 1;
     };
     add("nd_leaf6", nested_dissection(m, ap, aj, pos, 6, 1, 1));
-    for (int relax : {1, 4, 6, 8, 12}) add("md relax" + std::to_string(relax), md_supernodes(m, ap, aj, relax));
+    for (int relax : {1, 2, 4, 8}) add("md relax" + std::to_string(relax), md_supernodes(m, ap, aj, relax));
   }
+  for (auto& [k, a] : acc)
+    printf("%-28s tasks %.0f (bundled %.0f in %.0f bundles, free %.0f) -> units ~%.0f per subdomain\n", k.c_str(),
+           (a.bundled_tasks + a.free_tasks) / a.n, a.bundled_tasks / a.n, a.bundles / a.n, a.free_tasks / a.n,
+           (a.bundles + a.free_tasks) / a.n);
   for (auto& [k, a] : acc)
     printf("%-28s panel/cell (fwd+bwd doubles): a8 %.0f a2 %.0f tri16a8 %.0f tri16a2 %.0f | 2x structural %.0f\n", k.c_str(),
            a.panel[0] / a.cells, a.panel[1] / a.cells, a.panel[2] / a.cells, a.panel[3] / a.cells,

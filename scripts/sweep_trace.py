@@ -21,7 +21,7 @@ for _ in range(2):
 L = _lib.lib()
 L.pdg_sim_trace_sweep.restype = C.c_int
 L.pdg_sim_trace_sweep.argtypes = [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]
-cap = 400000
+cap = 3000000
 F = 12
 buf = np.zeros(cap * F, np.int64)
 for rep in range(3):
@@ -51,7 +51,7 @@ for e, a_, w_ in zip(edges, active, waiting):
     print(f"    {e / 1e3:7.1f} {a_:6d} {w_:6d}")
 print(f"  bytes {nbytes.sum() / 1e6:.1f} MB -> {nbytes.sum() / span:.0f} GB/s over the span")
 kb = nbytes / 1024
-for lo, hi in ((0, 2), (2, 4), (4, 8), (8, 12), (12, 16.1)):
+for lo, hi in ((0, 4), (4, 16), (16, 44), (44, 88), (88, 129)):
     m = (kb >= lo) & (kb < hi)
     print(f"  unit {lo:4.0f}-{hi:4.0f} KB: {int(m.sum()):6d} units, {nbytes[m].sum() / 1e6:6.1f} MB, "
           f"mean time {((done - st)[m].mean() if m.any() else 0) / 1e3:5.2f} us")
