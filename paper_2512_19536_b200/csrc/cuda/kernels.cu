@@ -674,20 +674,34 @@ __global__ void __launch_bounds__(256) prolong_dot_tma_kernel(const int* __restr
   const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
   const double* Es = reinterpret_cast<const double*>(dyn + off);
   if (threadIdx.x < BQ) ys[threadIdx.x] = y0[static_cast<long long>(cell_agg[cell0]) * BQ + threadIdx.x];
+  // r and z of the chunk are loaded while the E copy is in flight (chunks
+  // hold <= 32 cells: at most kPer elements per thread)
+  constexpr int kPer = (32 * B + 255) / 256;
+  const long long d0 = cell0 * B;
+  double rv[kPer], zv[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * 256;
+    if (e < nc * B) {
+      rv[j] = r[d0 + e];
+      zv[j] = z[d0 + e];
+    }
+  }
   __syncthreads();
   wait_bytes(&bar);
   double contrib = 0.0;
-  const long long d0 = cell0 * B;
-  for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * 256;
+    if (e >= nc * B) continue;
     const int k = e / B, i = e - k * B;
-    const long long d = d0 + e;
     const double* ek = Es + k * (B * BQ) + i;
     double acc = 0.0;
 #pragma unroll
     for (int m = 0; m < BQ; ++m) acc = fma(ek[m * B], ys[m], acc);
-    const double zi = z[d] + acc;
-    z[d] = zi;
-    contrib += r[d] * zi;
+    const double zi = zv[j] + acc;
+    z[d0 + e] = zi;
+    contrib += rv[j] * zi;
   }
   grid_finish(block_sum(contrib), rc);
 }

@@ -123,7 +123,7 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     // + 1: the multi-rank loop all-reduces [r0 ; ||r||^2 partial] in one call
     d_r0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq + 1);
     d_y0 = dalloc<double>(static_cast<std::size_t>(pr.n_agg) * pr.bq);
-    // restriction chunks: <= kChunk (<= 64) cells of one agglomerate per CTA;
+    // restriction chunks: <= kChunk cells of one agglomerate per CTA;
     // small chunks keep the fused update + restriction spread over all SMs
     constexpr int kChunk = 32;
     std::vector<int> cptr{0}, nptr{0};
