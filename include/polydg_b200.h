@@ -147,6 +147,9 @@ int64_t pdg_problem_export(const pdg_problem* p, int which, int64_t* rows, int64
  * zeros and padding included), [4] local K blocks, [5] E doubles held */
 void pdg_problem_factor_stats(const pdg_problem* p, int64_t stats[6]);
 /* partition maps: which 0 = subdomain owner, 1 = coarse owner; per reference cell */
+/* where setup ran: bit 0 = operator assembled on the device (cuda/assemble.cu),
+ * bit 1 = local factors computed on the device (cuda/factor.cu) */
+int pdg_problem_flags(const pdg_problem* p);
 void pdg_problem_owner(const pdg_problem* p, int which, int* owner);
 /* internal order: perm[i] = reference cell of internal position i */
 void pdg_problem_perm(const pdg_problem* p, int* perm);

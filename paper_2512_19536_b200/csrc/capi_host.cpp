@@ -214,6 +214,10 @@ void pdg_problem_info(const pdg_problem* h, int64_t info[12]) {
   pdg::problem_info(*h->p, info);
 }
 
+int pdg_problem_flags(const pdg_problem* h) {
+  return (h->p->device_assembly ? 1 : 0) | (h->p->device_factor ? 2 : 0);
+}
+
 int64_t pdg_problem_export(const pdg_problem* h, int which, int64_t* rows, int64_t* cols,
                            double* vals) {
   return pdg::problem_export(*h->p, which, rows, cols, vals);

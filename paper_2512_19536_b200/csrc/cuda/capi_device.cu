@@ -86,7 +86,7 @@ pdg_status pdg_sim_create(const pdg_config* cfg, pdg_sim** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw pdg::CudaError("no CUDA device available (the solver has no CPU fallback)");
-    auto prob = pdg::build_problem(*cfg);
+    auto prob = pdg::build_problem(*cfg, true);
     auto* s = new pdg_sim;
     try {
       s->d = std::make_unique<pdg::DeviceSim>(std::move(prob));

@@ -118,6 +118,35 @@ struct SweepArgs {
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
 
+// Device assembly (assemble.cu): volume terms, faces, K, M^-1, U0/Y0, E, K0.
+struct AsmArgs {
+  int ncells, cell0, b, p, q, bq, n_comp, ngl, ngs, init_kind, two_level;
+  const double* bbox;     // 4 per cell (internal order; world 1: all cells)
+  const int* tri_ptr;
+  const double* tri;      // fan triangles, 6 doubles each
+  const double *glx, *glw, *gsx, *gsw;  // triangle-rule / segment-rule Gauss nodes
+  const double* sigma;    // 4 per cell (t00 t01 t10 t11)
+  const int* fptr;        // per local cell: its faces in face order
+  const int* fent;        // 2 f + side
+  const int* fcell;       // (K, L) per face, internal cell ids
+  const double* fgeo;     // mid.x mid.y dir.x dir.y half n.x n.y eta per face
+  const int *kptr, *kcol;
+  double* kval;
+  double *M, *Minv, *U0, *Y0;
+  double am, hb;          // K = am M + hb A
+  double u_rest, u_patch, omega0[2], omega0_r2, ip[4], y_rest[4];
+  const double* abox;     // coarse label -> bbox
+  const int* cell_label;  // local cell -> coarse label
+  const int* cell_agg;    // local cell -> coarse internal node
+  const int *agg_ptr, *agg_cells;
+  double* E;
+  const int *k0ptr, *k0col;
+  double* k0val;
+  int* err;               // bit 0: mass block not SPD, bit 1: E mass not SPD
+};
+void launch_assembly(const AsmArgs& a, cudaStream_t st);
+void launch_k0(const AsmArgs& a, int n_agg, cudaStream_t st);
+
 // Ionic model + stimulus at quadrature nodes (one warp per cell).
 struct IonicArgs {
   int b, p, ncells, n_comp, ngl, has_prev, model, stim;

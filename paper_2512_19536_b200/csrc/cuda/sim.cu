@@ -94,9 +94,17 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   n_ext = n + static_cast<long long>(halo_cells.size()) * b;
   d_ptr = dupload(pr.K.ptr, st);
   d_col = dupload(col, st);
-  d_kval = dupload(pr.K.val, st);
-  d_M = dupload(pr.M, st);
-  d_Minv = dupload(pr.Minv, st);
+  if (pr.device_assembly) {  // values formed by cuda/assemble.cu below
+    const std::size_t nkv = static_cast<std::size_t>(pr.K.ptr[ncells]) * b * b;
+    d_kval = dalloc<double>(nkv);
+    PDG_CUDA(cudaMemsetAsync(d_kval, 0, nkv * sizeof(double), st));
+    d_M = dalloc<double>(static_cast<std::size_t>(ncells) * b * b);
+    d_Minv = dalloc<double>(static_cast<std::size_t>(ncells) * b * b);
+  } else {
+    d_kval = dupload(pr.K.val, st);
+    d_M = dupload(pr.M, st);
+    d_Minv = dupload(pr.Minv, st);
+  }
 
   for (auto& v : d_U) v = dalloc<double>(n_ext);
   d_x = dalloc<double>(n_ext);
@@ -116,7 +124,7 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
 
   // ---- coarse space ----
   if (pr.two_level) {
-    d_E = dupload(pr.E, st);
+    d_E = pr.device_assembly ? dalloc<double>(static_cast<std::size_t>(ncells) * b * pr.bq) : dupload(pr.E, st);
     d_cell_agg = dupload(pr.cell_agg, st);
     d_agg_ptr = dupload(pr.agg_cell_ptr, st);
     d_agg_cells = dupload(pr.agg_cells, st);
@@ -145,12 +153,13 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
     d_node_chunk_ptr = dupload(nptr, st);
     d_r0part = dalloc<double>(static_cast<std::size_t>(std::max(n_chunks, 1)) * pr.bq);
   }
-  upload_tasks();
-
-  // ---- ionic geometry ----
+  // ---- ionic geometry (also the device assembly's) ----
   d_bbox = dupload(pr.bbox, st);
   d_tri_ptr = dupload(pr.tri_ptr, st);
   d_tri = dupload(pr.tri, st);
+  if (pr.device_assembly) assemble_on_device();
+  upload_tasks();
+
   if (!pr.gl_x.empty()) set_gauss_nodes(pr.gl_x.data(), pr.gl_w.data(), static_cast<int>(pr.gl_x.size()));
   d_ionflags = dalloc<int>(1);
   PDG_CUDA(cudaMemsetAsync(d_ionflags, 0, sizeof(int), st));
@@ -167,13 +176,116 @@ DeviceSim::DeviceSim(std::unique_ptr<Problem> prob) : P(std::move(prob)) {
   d_perm = dupload(std::vector<int>(pr.perm.begin() + pr.cell_begin, pr.perm.begin() + pr.cell_end), st);
 
   // ---- state ----
-  PDG_CUDA(cudaMemcpyAsync(d_U[0], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
-  PDG_CUDA(cudaMemcpyAsync(d_U[1], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (n_comp > 0) {
-    PDG_CUDA(cudaMemcpyAsync(d_Y[0], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
-    PDG_CUDA(cudaMemcpyAsync(d_Y[1], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (pr.device_assembly) {  // U0 / Y0 were projected into slot 0 on the device
+    PDG_CUDA(cudaMemcpyAsync(d_U[1], d_U[0], n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (n_comp > 0)
+      PDG_CUDA(cudaMemcpyAsync(d_Y[1], d_Y[0], n * n_comp * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    PDG_CUDA(cudaMemcpyAsync(d_U[0], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    PDG_CUDA(cudaMemcpyAsync(d_U[1], pr.U0.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (n_comp > 0) {
+      PDG_CUDA(cudaMemcpyAsync(d_Y[0], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
+      PDG_CUDA(cudaMemcpyAsync(d_Y[1], pr.Y0.data(), n * n_comp * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
   }
   PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+// M, A, K, M^-1, U0/Y0, E and this rank's K0 on the device (cuda/assemble.cu,
+// same bits as the host assembly), then the coarse factorisation on the host
+// (K0 is small) and the host copies the exports read (M, E; K when kept).
+void DeviceSim::assemble_on_device() {
+  Problem& pr = *P;
+  const pdg_config& c = pr.cfg;
+  std::vector<void*> tmp;
+  auto up = [&](const auto& v) {
+    auto* d = dupload(v, st);
+    tmp.push_back(d);
+    return d;
+  };
+  AsmArgs a{};
+  a.ncells = ncells;
+  a.cell0 = pr.cell_begin;
+  a.b = b;
+  a.p = pr.p;
+  a.q = pr.q;
+  a.bq = pr.two_level ? pr.bq : 0;
+  a.n_comp = n_comp;
+  a.ngl = static_cast<int>(pr.gl_x.size());
+  a.ngs = static_cast<int>(pr.gs_x.size());
+  a.init_kind = c.init_kind;
+  a.two_level = pr.two_level ? 1 : 0;
+  a.bbox = d_bbox;
+  a.tri_ptr = d_tri_ptr;
+  a.tri = d_tri;
+  a.glx = up(pr.gl_x);
+  a.glw = up(pr.gl_w);
+  a.gsx = up(pr.gs_x);
+  a.gsw = up(pr.gs_w);
+  a.sigma = up(pr.sigma);
+  a.fptr = up(pr.fptr);
+  a.fent = up(pr.fent);
+  a.fcell = up(pr.fcell);
+  a.fgeo = up(pr.fgeo);
+  a.kptr = d_ptr;
+  a.kcol = d_col;
+  a.kval = d_kval;
+  a.M = d_M;
+  a.Minv = d_Minv;
+  a.U0 = d_U[0];
+  a.Y0 = d_Y[0];
+  a.am = c.C_m * c.chi_m;
+  a.hb = 0.5 * c.dt;
+  a.u_rest = c.u_rest;
+  a.u_patch = c.u_patch;
+  a.omega0[0] = c.omega0[0];
+  a.omega0[1] = c.omega0[1];
+  a.omega0_r2 = c.omega0_r2;
+  for (int k = 0; k < 4; ++k) {
+    a.ip[k] = c.init_params[k];
+    a.y_rest[k] = pr.y_rest[k];
+  }
+  int* d_err = dalloc<int>(1);
+  tmp.push_back(d_err);
+  PDG_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+  a.err = d_err;
+  double* d_k0 = nullptr;
+  if (pr.two_level) {
+    a.abox = up(pr.abox);
+    a.cell_label = up(pr.cell_label);
+    a.cell_agg = d_cell_agg;
+    a.agg_ptr = d_agg_ptr;
+    a.agg_cells = d_agg_cells;
+    a.E = d_E;
+    a.k0ptr = up(pr.K0.ptr);
+    a.k0col = up(pr.K0.col);
+    d_k0 = dalloc<double>(pr.K0.val.size());
+    tmp.push_back(d_k0);
+    PDG_CUDA(cudaMemsetAsync(d_k0, 0, pr.K0.val.size() * sizeof(double), st));
+    a.k0val = d_k0;
+  }
+  launch_assembly(a, st);
+  int err = 0;
+  PDG_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PDG_CUDA(cudaStreamSynchronize(st));
+  if (err & 1) throw SolverError("mass block is not positive definite");
+  if (err & 2) throw SolverError("coarse embedding: cell mass not positive definite");
+  const std::size_t b2 = static_cast<std::size_t>(b) * b;
+  pr.M.resize(static_cast<std::size_t>(ncells) * b2);
+  PDG_CUDA(cudaMemcpyAsync(pr.M.data(), d_M, pr.M.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (pr.keep_matrices) {
+    pr.K.val.resize(static_cast<std::size_t>(pr.K.ptr[ncells]) * b2);
+    PDG_CUDA(cudaMemcpyAsync(pr.K.val.data(), d_kval, pr.K.val.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  if (pr.two_level) {
+    launch_k0(a, pr.n_agg, st);
+    pr.E.resize(static_cast<std::size_t>(ncells) * b * pr.bq);
+    PDG_CUDA(cudaMemcpyAsync(pr.E.data(), d_E, pr.E.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(pr.K0.val.data(), d_k0, pr.K0.val.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  PDG_CUDA(cudaStreamSynchronize(st));
+  for (void* p : tmp) cudaFree(p);
+  if (pr.two_level && world == 1) finish_coarse(pr);
 }
 
 void DeviceSim::alloc_history(int cap) {

@@ -173,6 +173,7 @@ class DeviceSim {
   void build_panels();  // panels.cu
   void device_factor(double* d_lval);  // factor.cu: numeric subdomain factors into d_lval
   void alloc_history(int cap);
+  void assemble_on_device();
   ReduceCtx rctx(int finish, double* out = nullptr);
   SweepArgs sweep_args(bool fwd, const double* r, double* z, const PcgScalars* S);
   void precond_apply(const double* r, double* z, int finish, bool honor, bool restricted = false);

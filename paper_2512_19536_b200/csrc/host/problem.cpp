@@ -577,13 +577,15 @@ static void coarse_space(Problem& pr, std::vector<std::vector<int>>& anbr, const
   pr.coarse_nd = cnd;
   std::vector<int> apos_of(na);
   for (int i = 0; i < na; ++i) apos_of[cnd.order[i]] = i;
-  pr.E.resize(static_cast<std::size_t>(nloc) * b * bq);
+  const bool values = !Eall.empty();  // false: E and K0 are formed on the device
+  if (values) pr.E.resize(static_cast<std::size_t>(nloc) * b * bq);
   pr.cell_agg.resize(nloc);
   for (int i = 0; i < nloc; ++i) {
     const int g = pr.cell_begin + i;
-    std::copy(Eall.begin() + static_cast<std::size_t>(e_slot[g]) * b * bq,
-              Eall.begin() + static_cast<std::size_t>(e_slot[g] + 1) * b * bq,
-              pr.E.begin() + static_cast<std::size_t>(i) * b * bq);
+    if (values)
+      std::copy(Eall.begin() + static_cast<std::size_t>(e_slot[g]) * b * bq,
+                Eall.begin() + static_cast<std::size_t>(e_slot[g] + 1) * b * bq,
+                pr.E.begin() + static_cast<std::size_t>(i) * b * bq);
     pr.cell_agg[i] = apos_of[pr.coarse.owner[pr.perm[g]]];
   }
   // agglomerate -> local cells
@@ -610,6 +612,7 @@ static void coarse_space(Problem& pr, std::vector<std::vector<int>>& anbr, const
   }
   const int bq2 = bq * bq;
   K0.val.assign(static_cast<std::size_t>(K0.col.size()) * bq2, 0.0);
+  if (!values) return;
   // one coarse row per task: its cells in increasing local index, which is
   // the order a serial sweep over all local rows would add them (same bits)
   parallel_for(na, [&](int ai) {
@@ -706,7 +709,7 @@ std::vector<double> coarse_embedding(const Mesh& mesh, int p, const std::vector<
   return coarse_embedding_cells(mesh, p, owner, agglomerate_boxes(mesh, owner, count), q, cells);
 }
 
-std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
+std::unique_ptr<Problem> build_problem(const pdg_config& cfg, bool device) {
   validate_config(cfg);
   auto P = std::make_unique<Problem>();
   Problem& pr = *P;
@@ -729,6 +732,11 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   const Mesh& mesh = pr.mesh;
   const int N = mesh.n_cells();
   pr.n_cells_global = N;
+  // one rank on the device: M, A, K, M^-1, U0/Y0, E and K0 are assembled by
+  // cuda/assemble.cu (same bits); PDG_HOST_ASSEMBLY=1 keeps the host assembly
+  pr.device_assembly = device && cfg.world == 1 &&
+                       !(std::getenv("PDG_HOST_ASSEMBLY") && std::getenv("PDG_HOST_ASSEMBLY")[0] == '1');
+  const bool dev_asm = pr.device_assembly;
   pr.p = cfg.degree;
   pr.b = n_modes(pr.p);
   pr.q = cfg.q > 0 ? cfg.q : cfg.degree;
@@ -825,7 +833,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     std::sort(cols.begin(), cols.end());
     std::copy(cols.begin(), cols.end(), A.col.begin() + A.ptr[i]);
   }
-  A.val.assign(static_cast<std::size_t>(A.ptr[nloc]) * b2, 0.0);
+  if (!dev_asm) A.val.assign(static_cast<std::size_t>(A.ptr[nloc]) * b2, 0.0);
   auto find_block = [&](int i_loc, int j_glob) {
     const int* b0 = A.col.data() + A.ptr[i_loc];
     const int* e0 = A.col.data() + A.ptr[i_loc + 1];
@@ -856,11 +864,24 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       sig_norm[c] = std::max(sl, sn);
     }
   }
+  if (dev_asm) {
+    pr.sigma.resize(static_cast<std::size_t>(N) * 4);
+    for (int g = 0; g < N; ++g) {
+      const Tensor& t = sig[pr.perm[g]];
+      pr.sigma[4 * g] = t.t00;
+      pr.sigma[4 * g + 1] = t.t01;
+      pr.sigma[4 * g + 2] = t.t10;
+      pr.sigma[4 * g + 3] = t.t11;
+    }
+  }
   const int order = 2 * pr.p + 2;
-  pr.M.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
-  pr.Minv.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
-  pr.U0.assign(static_cast<std::size_t>(nloc) * b, 0.0);
-  pr.Y0.assign(static_cast<std::size_t>(nloc) * b * pr.n_comp, 0.0);
+  if (!dev_asm) {
+    pr.M.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
+    pr.Minv.assign(static_cast<std::size_t>(nloc) * b2, 0.0);
+    pr.U0.assign(static_cast<std::size_t>(nloc) * b, 0.0);
+    pr.Y0.assign(static_cast<std::size_t>(nloc) * b * pr.n_comp, 0.0);
+  }
+  for (int l = 0; l < pr.n_comp; ++l) pr.y_rest[l] = y_rest[l];
   pr.bbox.resize(static_cast<std::size_t>(nloc) * 4);
   pr.tri_ptr.assign(nloc + 1, 0);
   std::vector<std::vector<double>> tri_loc(nloc);
@@ -879,6 +900,7 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
         tri_loc[i].push_back(v.x);
         tri_loc[i].push_back(v.y);
       }
+    if (dev_asm) return;  // the quadrature runs on the device (cuda/assemble.cu)
     const Rule rule = polygon_rule(poly, order);
     const int nq = static_cast<int>(rule.size());
     std::vector<double> val(static_cast<std::size_t>(nq) * b), gx(val.size()), gy(val.size());
@@ -938,7 +960,45 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
   pr.tri.reserve(static_cast<std::size_t>(pr.tri_ptr[nloc]) * 6);
   for (auto& t : tri_loc) pr.tri.insert(pr.tri.end(), t.begin(), t.end());
   gauss_legendre((order + 3) / 2, pr.gl_x, pr.gl_w);
+  gauss_legendre((order + 2) / 2, pr.gs_x, pr.gs_w);
 
+  if (dev_asm) {
+    // face records for the device: cells, midpoint, half direction, half
+    // length, normal, penalty (host/quadrature.cpp segment_rule, assembly.cpp:40-46)
+    const auto& faces = mesh.interior_faces();
+    const int nf = static_cast<int>(faces.size());
+    pr.fcell.resize(2 * static_cast<std::size_t>(nf));
+    pr.fgeo.resize(8 * static_cast<std::size_t>(nf));
+    pr.fptr.assign(nloc + 1, 0);
+    parallel_for(nf, [&](int f) {
+      const Face& fc = faces[f];
+      const int K = fc.cell_in, L = fc.cell_out;
+      pr.fcell[2 * f] = pr.iperm[K];
+      pr.fcell[2 * f + 1] = pr.iperm[L];
+      const double hk = mesh.diameter(K), hl = mesh.diameter(L);
+      const Pt mid = (fc.a + fc.b) * 0.5, dir = (fc.b - fc.a) * 0.5;
+      double* g = &pr.fgeo[8 * static_cast<std::size_t>(f)];
+      g[0] = mid.x;
+      g[1] = mid.y;
+      g[2] = dir.x;
+      g[3] = dir.y;
+      g[4] = 0.5 * dist(fc.a, fc.b);
+      g[5] = fc.normal.x;
+      g[6] = fc.normal.y;
+      g[7] = cfg.eta0 * (0.5 * (sig_norm[K] + sig_norm[L])) * pr.p * pr.p / (2.0 * hk * hl / (hk + hl));
+    }, 4096);
+    for (int f = 0; f < nf; ++f) {
+      ++pr.fptr[pr.fcell[2 * f] + 1];
+      ++pr.fptr[pr.fcell[2 * f + 1] + 1];
+    }
+    for (int i = 0; i < nloc; ++i) pr.fptr[i + 1] += pr.fptr[i];
+    pr.fent.resize(pr.fptr[nloc]);
+    std::vector<int> fill(pr.fptr.begin(), pr.fptr.end() - 1);
+    for (int f = 0; f < nf; ++f) {  // entry = 2 f + side, faces in face order per cell
+      pr.fent[fill[pr.fcell[2 * f]]++] = 2 * f;
+      pr.fent[fill[pr.fcell[2 * f + 1]]++] = 2 * f + 1;
+    }
+  } else {
   // interior faces (sequential in face order so the diagonal sums keep the reference order)
   {
     const auto& faces = mesh.interior_faces();
@@ -1034,13 +1094,14 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
       }
     }, 256);
   }
+  }  // host faces
   // K = C_m chi_m M + dt/2 A (assembly.cpp:197-202)
-  {
+  pr.K.rows = nloc;
+  pr.K.b = b;
+  pr.K.ptr = A.ptr;
+  pr.K.col = A.col;
+  if (!dev_asm) {
     const double a = cfg.C_m * cfg.chi_m, hb = 0.5 * cfg.dt;
-    pr.K.rows = nloc;
-    pr.K.b = b;
-    pr.K.ptr = A.ptr;
-    pr.K.col = A.col;
     pr.K.val.resize(A.val.size());
     parallel_for(nloc, [&](int i) {
       for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
@@ -1088,10 +1149,23 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg) {
     for (std::size_t k = 0; k < need.size(); ++k) e_slot[need[k]] = static_cast<int>(k);
     std::vector<int> need_ref(need.size());
     for (std::size_t k = 0; k < need.size(); ++k) need_ref[k] = pr.perm[need[k]];
-    const std::vector<double> Eall = coarse_embedding_cells(mesh, pr.p, pr.coarse.owner, abox, pr.q, need_ref);
+    std::vector<double> Eall;
+    if (dev_asm) {  // E and K0 on the device: coarse boxes and labels only
+      pr.abox.resize(4 * static_cast<std::size_t>(na));
+      for (int a = 0; a < na; ++a) {
+        pr.abox[4 * a] = abox[a].xmin;
+        pr.abox[4 * a + 1] = abox[a].ymin;
+        pr.abox[4 * a + 2] = abox[a].xmax;
+        pr.abox[4 * a + 3] = abox[a].ymax;
+      }
+      pr.cell_label.resize(nloc);
+      for (int i = 0; i < nloc; ++i) pr.cell_label[i] = pr.coarse.owner[pr.perm[pr.cell_begin + i]];
+    } else {
+      Eall = coarse_embedding_cells(mesh, pr.p, pr.coarse.owner, abox, pr.q, need_ref);
+    }
     coarse_space(pr, anbr, &apos, Eall, e_slot);
     phase("coarse E,K0");
-    if (cfg.world == 1) finish_coarse(pr);
+    if (cfg.world == 1 && !dev_asm) finish_coarse(pr);
     phase("coarse factor");
   }
   return P;

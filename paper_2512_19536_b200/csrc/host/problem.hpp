@@ -139,6 +139,16 @@ struct Problem {
   int n_cells_global = 0;
   bool from_operator = false;  // built from caller data (no mesh, no time stepper)
 
+  // device assembly (cuda/assemble.cu): the host keeps the geometry only
+  bool device_assembly = false;
+  std::vector<double> sigma;             // 4 per internal cell: conductivity tensor
+  std::vector<int> fptr, fent, fcell;    // per local cell its faces (2 f + side); per face (K, L)
+  std::vector<double> fgeo;              // per face: mid, half direction, half length, normal, penalty
+  std::vector<double> gs_x, gs_w;        // segment-rule Gauss nodes
+  std::vector<double> abox;              // 4 per coarse label: agglomerate bounding box
+  std::vector<int> cell_label;           // local cell -> coarse label
+  double y_rest[4] = {0.0, 0.0, 0.0, 0.0};
+
   std::int64_t n_local_dofs() const { return static_cast<std::int64_t>(cell_end - cell_begin) * b; }
   std::int64_t n_global_dofs() const { return static_cast<std::int64_t>(n_cells_global) * b; }
 };
@@ -156,7 +166,7 @@ void halo_plan(const Problem& pr, std::vector<std::vector<int>>& send, std::vect
 void validate_config(const pdg_config& cfg);
 // IonicModel::state_dim / resting_potential / resting_state (ionics.hpp:25-31)
 int ionic_rest(const pdg_config& cfg, double& u_rest, double* y_rest);
-std::unique_ptr<Problem> build_problem(const pdg_config& cfg);
+std::unique_ptr<Problem> build_problem(const pdg_config& cfg, bool device = false);
 // Solver setup from a caller's K, subdomain partition and coarse embedding
 // (pdg_sim_create_from_operator): one rank, graph-only orderings.
 std::unique_ptr<Problem> build_problem_from_operator(const pdg_operator_desc& d);

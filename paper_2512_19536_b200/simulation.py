@@ -257,6 +257,11 @@ class Problem:
         keys = ["l_struct", "l0_struct", "fwd_panel_doubles", "bwd_panel_doubles", "k_blocks", "e_doubles"]
         return dict(zip(keys, list(st)))
 
+    def flags(self) -> dict:
+        """Where setup ran (pdg_problem_flags)."""
+        f = lib().pdg_problem_flags(self._handle())
+        return {"device_assembly": bool(f & 1), "device_factor": bool(f & 2)}
+
     def owner(self, which: str = "subdomain") -> np.ndarray:
         o = np.zeros(self.n_cells, np.int32)
         lib().pdg_problem_owner(self._handle(), 0 if which == "subdomain" else 1, _lib.iptr(o))
