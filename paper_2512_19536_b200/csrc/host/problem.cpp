@@ -732,17 +732,21 @@ std::unique_ptr<Problem> build_problem(const pdg_config& cfg, bool device) {
   const Mesh& mesh = pr.mesh;
   const int N = mesh.n_cells();
   pr.n_cells_global = N;
-  // one rank on the device: M, A, K, M^-1, U0/Y0, E and K0 are assembled by
-  // cuda/assemble.cu (same bits); PDG_HOST_ASSEMBLY=1 keeps the host assembly
-  pr.device_assembly = device && cfg.world == 1 &&
-                       !(std::getenv("PDG_HOST_ASSEMBLY") && std::getenv("PDG_HOST_ASSEMBLY")[0] == '1');
-  const bool dev_asm = pr.device_assembly;
   pr.p = cfg.degree;
   pr.b = n_modes(pr.p);
   pr.q = cfg.q > 0 ? cfg.q : cfg.degree;
   pr.bq = n_modes(pr.q);
   pr.has_precond = cfg.precond_kind != PDG_PRECOND_NONE;
   pr.two_level = cfg.precond_kind == PDG_PRECOND_TWO_LEVEL;
+  // one rank on the device: M, A, K, M^-1, U0/Y0, E and K0 are assembled by
+  // cuda/assemble.cu (same bits) when no host step needs K's values, i.e.
+  // the local factors are computed on the device too (multi-cell subdomains,
+  // factor_units) or there is no preconditioner; PDG_HOST_ASSEMBLY=1 keeps
+  // the host assembly
+  auto env_on = [](const char* k) { return std::getenv(k) && std::getenv(k)[0] == '1'; };
+  pr.device_assembly = device && cfg.world == 1 && !env_on("PDG_HOST_ASSEMBLY") &&
+                       (!pr.has_precond || (cfg.subdomains > 0 && !env_on("PDG_HOST_FACTOR")));
+  const bool dev_asm = pr.device_assembly;
   double u_model_rest = 0.0, y_rest[4] = {0.0, 0.0, 0.0, 0.0};
   pr.n_comp = ionic_rest(cfg, u_model_rest, y_rest);
   const int b = pr.b, b2 = b * b;
