@@ -24,3 +24,5 @@ run $R pf11_c3p3 config3:3:64 PDG_SWEEP_PREFETCH=11
 run $R pf3_c3p3 config3:3:64
 # per-unit phase trace of one config4 sweep (HEAD defaults)
 (cd $R && timeout 900 python scripts/sweep_trace.py config4 > $R/$O/trace_c4.txt 2>&1)
+# SpMV kernel choice at config4 (warp-per-row forced)
+run $R spmvwarp_c4 config4 PDG_SPMV_WARP=1
