@@ -136,12 +136,6 @@ __device__ __forceinline__ void fetch_ahead(const SweepArgs& a, Ahead& q) {
   if (tk < a.n_units) {
     q.u = a.units[tk];
     q.t = a.tasks[q.u.task];
-    // bit 8: the lookahead unit's panel is prefetched into L2 now (one unit
-    // earlier than bit 1 does it)
-    if (a.prefetch & 8)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((q.u.dir == 0 ? a.fmat : a.hmat) + q.u.src_off),
-                   "r"(q.u.bytes)
-                   : "memory");
   }
 }
 // L2 bulk prefetch of the running unit's panel (issued when the unit starts:
