@@ -1,0 +1,18 @@
+#!/bin/bash
+# r02 batch L: sweep CTA size (build knob PDG_SWEEP_THREADS=64) x MD amalgamation (config4, config2, config5 p=2)
+O=gpurun_out/r02l; mkdir -p $O
+R=$(pwd)
+T=64
+rm -rf /tmp/v$T; mkdir -p /tmp/v$T; cp -r paper_2512_19536_b200 scripts tests include /tmp/v$T/
+(cd /tmp/v$T && make -C paper_2512_19536_b200/csrc -j16 BUILD=/tmp/v$T/build/csrc EXTRA_NVFLAGS=-DPDG_SWEEP_THREADS=$T > $R/$O/build_$T.log 2>&1; echo "build rc=$?" >> $R/$O/build_$T.log)
+grep -A2 sweep_kernel /tmp/v$T/build/csrc/sweep.ptxas.log >> $R/$O/build_$T.log
+run() { local dir=$1 name=$2 cfg=$3; shift 3; (cd $dir && env "$@" timeout 600 python scripts/c4_probe.py 2 $cfg > $R/$O/$name.txt 2>&1); }
+for v in "$R 128" "/tmp/v64 64"; do
+  set -- $v; D=$1; T=$2
+  run $D t${T}_c4 config4
+  run $D t${T}_c4_md4z4 config4 PDG_MD_RELAX=4 PDG_RELAX_Z=0.4
+  run $D t${T}_c4_md2z3 config4 PDG_MD_RELAX=2 PDG_RELAX_Z=0.3
+  run $D t${T}_c4_md4z4_u64 config4 PDG_MD_RELAX=4 PDG_RELAX_Z=0.4 PDG_UNIT_KB=64
+  run $D t${T}_c2 config2
+  run $D t${T}_c5p2 config5:2
+done
