@@ -304,15 +304,48 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   const bool meta = s.meta;
   double* outv = T.coarse ? a.y0 : a.z;
   // the one dependent gather level
-  if (FWD) {
+  if (FWD && meta) {
+    // two columns per pass, their update loads issued four at a time before
+    // any is consumed; each column subtracts its updates in list order (same
+    // sums as one load per step, fewer dependent round trips)
+    const int e0 = s.iptr[0];
+    for (int i0 = col_lo + threadIdx.x; i0 < col_hi; i0 += 2 * blockDim.x) {
+      int kk[2], ke[2], rr[2];
+      double v[2];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int i = i0 + g * blockDim.x;
+        const bool on = i < col_hi;
+        const int cell = on ? i / bs : cell_lo;
+        rr[g] = on ? i - cell * bs : 0;
+        kk[g] = on ? s.iptr[cell - cell_lo] : 0;
+        ke[g] = on ? s.iptr[cell - cell_lo + 1] : 0;
+        v[g] = on ? xin[i - col_lo] : 0.0;
+      }
+      while (kk[0] < ke[0] || kk[1] < ke[1]) {
+        double t[2][4];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            t[g][u] = kk[g] + u < ke[g] ? __ldcg(a.ubuf + s.idx[kk[g] + u - e0] + rr[g]) : 0.0;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (kk[g] + u < ke[g]) v[g] -= t[g][u];
+          kk[g] = min(kk[g] + 4, ke[g]);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+        if (i0 + g * static_cast<int>(blockDim.x) < col_hi) xin[i0 + g * blockDim.x - col_lo] = v[g];
+    }
+  } else if (FWD) {
     for (int i = col_lo + threadIdx.x; i < col_hi; i += blockDim.x) {
       const int cell = i / bs, rr = i - cell * bs;
       double v = xin[i - col_lo];
-      if (meta) {
-        const int e0 = s.iptr[0];
-        for (int k = s.iptr[cell - cell_lo]; k < s.iptr[cell - cell_lo + 1]; ++k)
-          v -= __ldcg(a.ubuf + s.idx[k - e0] + rr);
-      } else {
+      {
         const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
         for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
       }

@@ -16,3 +16,5 @@ for v in "$R 128" "/tmp/v64 64"; do
   run $D t${T}_c2 config2
   run $D t${T}_c5p2 config5:2
 done
+# per-unit trace with the batched forward gather (compare trace_c4 of r02j: gather|ready 3.16 us)
+(cd $R && timeout 900 python scripts/sweep_trace.py config4 > $R/$O/trace_c4.txt 2>&1)
