@@ -18,3 +18,8 @@ for v in "$R 128" "/tmp/v64 64"; do
 done
 # per-unit trace with the batched forward gather (compare trace_c4 of r02j: gather|ready 3.16 us)
 (cd $R && timeout 900 python scripts/sweep_trace.py config4 > $R/$O/trace_c4.txt 2>&1)
+# list-schedule cost model calibrated to the traced unit times (fixed ~7 us, ~10 GB/s per CTA, publish ~1.3 us)
+run $R sched_c4_a config4 PDG_SCHED_COST=7000,10,1300
+run $R sched_c4_b config4 PDG_SCHED_COST=4000,15,1000
+run $R sched_c2_a config2 PDG_SCHED_COST=7000,10,1300
+run $R sched_c2_b config2 PDG_SCHED_COST=4000,15,1000
