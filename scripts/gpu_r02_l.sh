@@ -23,3 +23,4 @@ run $R sched_c4_a config4 PDG_SCHED_COST=7000,10,1300
 run $R sched_c4_b config4 PDG_SCHED_COST=4000,15,1000
 run $R sched_c2_a config2 PDG_SCHED_COST=7000,10,1300
 run $R sched_c2_b config2 PDG_SCHED_COST=4000,15,1000
+(cd $R && timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $R/$O/smoke.log 2>&1; echo "smoke rc=$?" >> $R/$O/smoke.log)
