@@ -621,7 +621,7 @@ void DeviceSim::upload_tasks() {
   // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
   // partial sums + the unit's input buffer (sweep.cu)
   sweep_xcap = static_cast<int>(max_in) + 2;
-  smem_fwd = smem_bwd = static_cast<int>(sizeof(double)) * (kSweepThreads + sweep_xcap);
+  smem_fwd = smem_bwd = sweep_smem_bytes(sweep_xcap);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   {
