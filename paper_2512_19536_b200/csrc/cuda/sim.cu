@@ -323,15 +323,10 @@ namespace {
 // dependencies start strictly earlier, so the ticket order stays topological
 // (the persistent sweep's deadlock-freedom argument, sweep.cu).
 std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& units, int slots) {
-  double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;  // ns
-  if (const char* e = std::getenv("PDG_SCHED_COST")) {  // A/B: "fixed_ns,GB/s,publish_ns"
-    double f = 0, g = 0, pb = 0;
-    if (std::sscanf(e, "%lf,%lf,%lf", &f, &g, &pb) == 3 && g > 0) {
-      kFixed = f;
-      kPerByte = 1.0 / g;
-      kPublish = pb;
-    }
-  }
+  // cost model of the simulated schedule (ns); calibrating it to the traced
+  // unit times (7 us fixed, 10 GB/s per CTA) changed nothing measurable
+  // (profiles/r02l sched_*)
+  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;
   const int nt = static_cast<int>(pr.tasks.size()), nu = static_cast<int>(units.size());
   auto cost = [&](const DevUnit& u) { return kFixed + kPerByte * u.bytes; };
   std::vector<double> cmax_f(nt, 0.0), cmax_b(nt, 0.0);

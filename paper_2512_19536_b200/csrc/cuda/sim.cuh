@@ -28,7 +28,6 @@ struct StepResult {
 void set_sweep_smem(int bytes);
 int sweep_ctas_per_sm(int smem);  // occupancy of the sweep kernel
 int sweep_smem_bytes(int xcap);   // dynamic shared memory of the sweep (mode dependent)
-bool sweep_pipe_mode();
 // Extreme-eigenvalue ratio of the Lanczos tridiagonal (krylov.cpp:85-103).
 bool lanczos_condition(const double* alpha, const double* beta, int m, double* kappa);
 

@@ -28,8 +28,6 @@
 // one red.release.gpu. Counters are monotone across launches (sweep number
 // `epoch`), so no memsets are needed between sweeps.
 #include <cstdint>
-#include <cstdlib>
-#include <string>
 
 #include "kernels.cuh"
 
@@ -508,320 +506,12 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
 }
 
 
-// ---------------------------------------------------------------------------
-// Pipelined variant (PDG_SWEEP=pipe): warp specialisation inside the CTA.
-// Warps 0-1 (front) take the tickets and prepare unit i+1 — descriptor, L2
-// prefetch of its panel, staging, dependency wait, dependent gather — into
-// one of two shared-memory slots while warps 2-3 (mat-vec) stream unit i from
-// the other slot, store its rows and publish it. The per-unit latency chain
-// then overlaps the previous unit's streaming, so smaller units (smaller
-// supernodes, fewer stored bytes) cost less. Hand-off through named barriers:
-// FULL[k] (front arrives, mat-vec syncs) and EMPTY[k] (mat-vec arrives, front
-// syncs before refilling slot k). Tickets are taken and run in order per CTA,
-// so the deadlock-freedom argument of the sweep above holds (the lowest
-// unfinished ticket is in some CTA's front or mat-vec stage, and neither
-// stage waits on a larger ticket).
-constexpr int kPipeThreads = 128, kFront = 64, kMv = 64, kMvWarps = kMv / 32;
-
-struct PipeSlot {
-  DevUnit u;
-  DevTask t;
-  int tk, col_lo, col_hi, cell_lo, meta;
-  DevTile tiles[kMaxSmemTiles];
-};
-struct PipeSmem {
-  PipeSlot slot[2];
-  int iptr[kMetaCells];
-  long long idx[kMetaIdx];
-  int ep, last, tkn;
-};
-
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-constexpr int kBarFront = 1, kBarMv = 2, kBarFull = 3, kBarEmpty = 5;
-
-// front (threads 0..63): fill slot k with ticket tk's unit, inputs gathered
-template <bool FWD>
-__device__ void pipe_front_unit(const SweepArgs& a, PipeSmem& s, PipeSlot& S, double* xin) {
-  const int t = threadIdx.x;
-  const DevUnit& U = S.u;
-  const DevTask& T = S.t;
-  const int ep = s.ep;
-  if (t == 0 && (a.prefetch & 1)) prefetch_panel(a, U);
-  const int tile0 = (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
-  const int ntile = U.tile_end - U.tile_begin;
-  const DevTile* tiles = FWD ? a.ftiles : a.htiles;
-  for (int i = t; i < ntile && i < kMaxSmemTiles; i += kFront) S.tiles[i] = tiles[tile0 + i];
-  const int bs = T.bs, w = T.w;
-  const int col_lo = U.col_lo, col_hi = U.col_hi;
-  const int cell_lo = col_lo / bs, cell_hi = (col_hi + bs - 1) / bs;
-  int meta = 0;
-  if (FWD) {
-    if (T.coarse && a.r0part) {
-      for (int i = col_lo + t; i < col_hi; i += kFront) {
-        const int d = static_cast<int>(T.dof0) + i, node = d / bs, m = d - node * bs;
-        double v = 0.0;
-        for (int c = a.node_chunk_ptr[node]; c < a.node_chunk_ptr[node + 1]; ++c) v += a.r0part[c * bs + m];
-        xin[i - col_lo] = v;
-      }
-    } else {
-      const double* in = T.coarse ? a.r0 : a.r;
-      for (int i = col_lo + t; i < col_hi; i += kFront) xin[i - col_lo] = in[T.dof0 + i];
-    }
-    const int nc = cell_hi - cell_lo;
-    if (nc + 1 <= kMetaCells && U.in_n <= kMetaIdx) {
-      for (int c = t; c <= nc; c += kFront) s.iptr[c] = a.in_ptr[T.in_off + cell_lo + c];
-      for (int k = t; k < U.in_n; k += kFront) s.idx[k] = a.in_idx[U.in_e0 + k];
-      meta = 1;
-    }
-  } else {
-    const int r_lo = max(col_lo, w);
-    const int rc0 = (r_lo - w) / bs;
-    const int nr_cells = col_hi > w ? (col_hi - w + bs - 1) / bs - rc0 : 0;
-    if (nr_cells <= kMetaIdx) {
-      for (int k = t; k < nr_cells; k += kFront) s.idx[k] = a.row_dof[T.rows_off + rc0 + k];
-      meta = 1;
-    }
-  }
-  // dependencies (and, backward, the own forward result)
-  if (t == 0) {
-    if (U.n_dep <= 2) {
-      for (int d = 0; d < U.n_dep; ++d) wait_count(a.flags + U.dep[d], (ep + 1) * U.need[d]);
-    } else {
-      for (int k = 0; k < T.n_child; ++k) {
-        const int c = a.task_child[T.child_off + k];
-        wait_count(a.flags + c, (ep + 1) * a.tasks[c].f_ntile);
-      }
-    }
-    if (!FWD && U.own_fwd >= 0 && col_lo < w) wait_count(a.flags + U.own_fwd, (ep + 1) * U.own_need);
-  }
-  bar_sync_n(kBarFront, kFront);
-  double* outv = T.coarse ? a.y0 : a.z;
-  if (FWD) {
-    for (int i = col_lo + t; i < col_hi; i += kFront) {
-      const int cell = i / bs, rr = i - cell * bs;
-      double v = xin[i - col_lo];
-      if (meta) {
-        const int e0 = s.iptr[0];
-        int k = s.iptr[cell - cell_lo];
-        const int k1 = s.iptr[cell - cell_lo + 1];
-        for (; k < k1; k += 4) {
-          double tt[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) tt[u] = k + u < k1 ? __ldcg(a.ubuf + s.idx[k + u - e0] + rr) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (k + u < k1) v -= tt[u];
-        }
-      } else {
-        const int k0 = a.in_ptr[T.in_off + cell], k1 = a.in_ptr[T.in_off + cell + 1];
-        for (int k = k0; k < k1; ++k) v -= __ldcg(a.ubuf + a.in_idx[k] + rr);
-      }
-      xin[i - col_lo] = v;
-    }
-  } else {
-    const int rc0 = (max(col_lo, w) - w) / bs;
-    for (int i = col_lo + t; i < col_hi; i += kFront) {
-      double v;
-      if (i < w) {
-        v = __ldcg((T.coarse ? a.yc : a.yf) + T.dof0 + i);
-      } else {
-        const int k = i - w, cell = k / bs, rr = k - cell * bs;
-        const long long base = meta ? s.idx[cell - rc0] : a.row_dof[T.rows_off + cell];
-        v = -__ldcg(outv + base + rr);
-      }
-      xin[i - col_lo] = v;
-    }
-  }
-  if (t == 0) {
-    S.col_lo = col_lo;
-    S.col_hi = col_hi;
-    S.cell_lo = cell_lo;
-    S.meta = meta;
-  }
-}
-
-// mat-vec (threads 64..127): stream slot k's unit, store, publish
-template <bool FWD, bool EF>
-__device__ void pipe_mv_unit(const SweepArgs& a, PipeSmem& s, const PipeSlot& S, const double* xin, double* part) {
-  const int tm = threadIdx.x - kFront;
-  const int lane = tm & 31, warp = tm >> 5, l2 = lane & 15;
-  const DevUnit& U = S.u;
-  const DevTask& T = S.t;
-  const int ep = s.ep;
-  const int col_lo = S.col_lo;
-  double* outv = T.coarse ? a.y0 : a.z;
-  const int ntile = U.tile_end - U.tile_begin;
-  if (U.nchunk > 1) {
-    const DevTile tl = S.tiles[0];
-    const int nc = U.c1 - U.c0;
-    const int per = (((nc + kMvWarps - 1) / kMvWarps) + 1) & ~1;
-    const int j0 = warp * per, j1 = min(nc, j0 + per);
-    const double2 v = tile_dot<EF>((FWD ? a.fmat : a.hmat) + U.src_off, tl, xin, j0, j1);
-    if (lane < 16) {
-      part[warp * 32 + 2 * l2] = v.x;
-      part[warp * 32 + 2 * l2 + 1] = v.y;
-    }
-    bar_sync_n(kBarMv, kMv);
-    double* gp = a.part + static_cast<long long>(U.part_base + U.chunk) * 32;
-    if (tm < 32) {
-      double sum = 0.0;
-      for (int q = 0; q < kMvWarps; ++q) sum += part[q * 32 + tm];
-      __stcg(gp + tm, sum);
-    }
-    bar_sync_n(kBarMv, kMv);
-    if (tm == 0) s.last = atom_acq_rel_add(a.tile_ctr + U.tile_ctr, 1) + 1 == (ep + 1) * U.nchunk;
-    bar_sync_n(kBarMv, kMv);
-    if (!s.last) return;
-    if (tm < tl.rows) {
-      double sum = 0.0;
-      const double* base = a.part + static_cast<long long>(U.part_base) * 32 + tm;
-      for (int c = 0; c < U.nchunk; ++c) sum += __ldcg(base + c * 32);
-      store_row<FWD>(a, T, outv, U.tile_begin * 32 + tm, sum);
-    }
-    bar_sync_n(kBarMv, kMv);
-    if (tm == 0) red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, 1);
-    return;
-  }
-  const int split = ntile >= kMvWarps ? 1 : kMvWarps / ntile;
-  const int items = ntile * split;
-  const DevTile* gtiles = (FWD ? a.ftiles : a.htiles) + (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
-  for (int it = warp; it < items; it += kMvWarps) {
-    const int R = it / split, c = it - R * split;
-    const DevTile tl = R < kMaxSmemTiles ? S.tiles[R] : gtiles[R];
-    const double* m = (FWD ? a.fmat : a.hmat) + tl.off;
-    const int chunk = (((tl.ncol + split - 1) / split) + 1) & ~1;
-    const int j0 = c * chunk, j1 = min(tl.ncol, j0 + chunk);
-    const double2 v = tile_dot<EF>(m, tl, xin + (tl.col0 - col_lo), j0, j1);
-    if (lane < 16 && 2 * l2 < tl.rows) {
-      if (split == 1) {
-        const int o = (U.tile_begin + R) * 32 + 2 * l2;
-        store_row<FWD>(a, T, outv, o, v.x);
-        if (2 * l2 + 1 < tl.rows) store_row<FWD>(a, T, outv, o + 1, v.y);
-      } else {
-        part[it * 32 + 2 * l2] = v.x;
-        part[it * 32 + 2 * l2 + 1] = v.y;
-      }
-    }
-  }
-  if (split > 1) {
-    bar_sync_n(kBarMv, kMv);
-    for (int q = tm; q < ntile * 32; q += kMv) {
-      const int R = q >> 5, l = q & 31;
-      if (l >= S.tiles[R].rows) continue;
-      double v = 0.0;
-      for (int c = 0; c < split; ++c) v += part[(R * split + c) * 32 + l];
-      store_row<FWD>(a, T, outv, (U.tile_begin + R) * 32 + l, v);
-    }
-  }
-  bar_sync_n(kBarMv, kMv);
-  if (tm == 0) red_release_add(a.flags + (FWD ? 0 : a.n_tasks) + U.task, ntile);
-}
-
-template <bool EF>
-__global__ void __launch_bounds__(kPipeThreads) sweep_pipe_kernel(SweepArgs a) {
-  pdl_wait();
-  if (a.S && a.S->stop) return;
-  extern __shared__ __align__(128) double smp[];
-  __shared__ PipeSmem s;
-  double* part = smp;  // 2 warps x 32 (mat-vec)
-  double* xbuf = smp + kMvWarps * 32;
-  if (threadIdx.x == 0) {
-    if (blockIdx.x == 0 && a.live) a.live[0] = static_cast<unsigned long long>(gtimer());
-    s.ep = __ldcg(a.epoch);
-  }
-  __syncthreads();
-  if (threadIdx.x < kFront) {
-    // ---------------- front ----------------
-    const int t = threadIdx.x;
-    constexpr int nu = sizeof(DevUnit) / 4, nt = sizeof(DevTask) / 4;
-    int n = 0;
-    for (;; ++n) {
-      const int k = n & 1;
-      PipeSlot& S = s.slot[k];
-      if (n >= 2) bar_sync_n(kBarEmpty + k, kPipeThreads);  // mat-vec done with slot k
-      if (t == 0) s.tkn = static_cast<int>(atomicAdd(a.ticket, 1u));
-      bar_sync_n(kBarFront, kFront);
-      const int tk = s.tkn;
-      if (tk >= a.n_units) {
-        if (t == 0) S.tk = a.n_units;
-        bar_arrive_n(kBarFull + k, kPipeThreads);
-        break;
-      }
-      if (t < nu) reinterpret_cast<int*>(&S.u)[t] = reinterpret_cast<const int*>(a.units + tk)[t];
-      bar_sync_n(kBarFront, kFront);
-      if (t < nt) reinterpret_cast<int*>(&S.t)[t] = reinterpret_cast<const int*>(a.tasks + S.u.task)[t];
-      if (t == 0) S.tk = tk;
-      bar_sync_n(kBarFront, kFront);
-      double* xin = xbuf + static_cast<long long>(k) * a.xcap;
-      if (S.u.dir == 0) pipe_front_unit<true>(a, s, S, xin);
-      else pipe_front_unit<false>(a, s, S, xin);
-      bar_sync_n(kBarFront, kFront);  // gather complete (and the staging maps free for reuse)
-      bar_arrive_n(kBarFull + k, kPipeThreads);
-    }
-    // consume the mat-vec's EMPTY arrival for the last real unit (n - 1)
-    if (n >= 1) bar_sync_n(kBarEmpty + ((n - 1) & 1), kPipeThreads);
-  } else {
-    // ---------------- mat-vec ----------------
-    for (int n = 0;; ++n) {
-      const int k = n & 1;
-      bar_sync_n(kBarFull + k, kPipeThreads);
-      const PipeSlot& S = s.slot[k];
-      if (S.tk >= a.n_units) break;
-      const double* xin = xbuf + static_cast<long long>(k) * a.xcap;
-      if (S.u.dir == 0) pipe_mv_unit<true, EF>(a, s, S, xin, part);
-      else pipe_mv_unit<false, EF>(a, s, S, xin, part);
-      bar_arrive_n(kBarEmpty + k, kPipeThreads);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (atomicAdd(a.epoch + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-      a.epoch[1] = 0;
-      *a.ticket = 0u;
-      a.epoch[0] = s.ep + 1;
-      if (a.live) {
-        a.live[1] += static_cast<unsigned long long>(gtimer()) - __ldcg(a.live);
-        a.live[2] += 1;
-      }
-      __threadfence();
-    }
-  }
-}
-
 }  // namespace
 
-bool sweep_pipe_mode() {
-  static const bool on = [] {
-    const char* e = std::getenv("PDG_SWEEP");
-    return e && std::string(e) == "pipe";
-  }();
-  return on;
-}
-
-int sweep_smem_bytes(int xcap) {
-  return static_cast<int>(sizeof(double)) * (sweep_pipe_mode() ? kMvWarps * 32 + 2 * xcap : kSweepThreads + xcap);
-}
+int sweep_smem_bytes(int xcap) { return static_cast<int>(sizeof(double)) * (kSweepThreads + xcap); }
 
 void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
   if (a.n_units == 0) return;
-  if (sweep_pipe_mode()) {
-    static int cached = -1, resident_p = 0;
-    if (cached != smem) {
-      int per_sm = 0, sms = 0, dev = 0;
-      PDG_CUDA(cudaGetDevice(&dev));
-      PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<true>, kPipeThreads, smem));
-      resident_p = (per_sm > 0 ? per_sm : 1) * sms;
-      cached = smem;
-    }
-    const int grid = a.n_units < resident_p ? a.n_units : resident_p;
-    if (a.prefetch & 2) launch_pdl(sweep_pipe_kernel<true>, grid, kPipeThreads, smem, st, a);
-    else launch_pdl(sweep_pipe_kernel<false>, grid, kPipeThreads, smem, st, a);
-    return;
-  }
   static int cached_smem = -1, resident = 0;
   if (cached_smem != smem) {
     int per_sm = 0, sms = 0, dev = 0;
@@ -838,18 +528,13 @@ void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
 
 int sweep_ctas_per_sm(int smem) {
   int per_sm = 0;
-  if (sweep_pipe_mode())
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<true>, kPipeThreads, smem));
-  else
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
+  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
   return per_sm > 0 ? per_sm : 1;
 }
 
 void set_sweep_smem(int bytes) {
   PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  PDG_CUDA(cudaFuncSetAttribute(sweep_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  PDG_CUDA(cudaFuncSetAttribute(sweep_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 }  // namespace pdg
