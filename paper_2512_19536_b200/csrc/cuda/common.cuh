@@ -84,10 +84,7 @@ struct Reducer {
   unsigned int* counter;
 };
 
-#ifndef PDG_SWEEP_THREADS
-#define PDG_SWEEP_THREADS 128
-#endif
-constexpr int kSweepThreads = PDG_SWEEP_THREADS;  // build knob (-DPDG_SWEEP_THREADS=64/128/256)
+constexpr int kSweepThreads = 128;  // default sweep CTA size (sweep.cu also instantiates 64)
 constexpr int kVecThreads = 256;
 
 // Programmatic dependent launch: the PCG body kernels are launched so that a

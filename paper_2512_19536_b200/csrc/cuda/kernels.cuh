@@ -115,6 +115,7 @@ struct SweepArgs {
   unsigned long long* live;  // [0] start of this launch (CTA 0), [1] summed launch ns, [2] launches
   long long* trace;  // optional: 4 globaltimer stamps per unit (start, deps met, gathered, done)
   int prefetch;      // 1: L2 bulk prefetch of each unit's panel when it starts (PDG_SWEEP_PREFETCH)
+  int threads;       // CTA size: 128, or 64 for large problems with small blocks (sim.cu)
 };
 void launch_sweep(const SweepArgs& a, int smem_bytes, cudaStream_t st);
 

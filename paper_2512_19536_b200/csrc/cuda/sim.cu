@@ -616,14 +616,19 @@ void DeviceSim::upload_tasks() {
   // panels stream from L2 (bulk-prefetched); smem holds partial sums + inputs
   // partial sums + the unit's input buffer (sweep.cu)
   sweep_xcap = static_cast<int>(max_in) + 2;
-  smem_fwd = smem_bwd = sweep_smem_bytes(sweep_xcap);
+  // 64-thread CTAs (twice as many resident) for large problems with small
+  // blocks (b <= 6): config5 p=2 sweep 2.32 vs 2.64 ms; 128 everywhere else
+  // (config4 6.35 vs 7.16 ms, config2 0.098 vs 0.129 ms; profiles/r02l)
+  sweep_threads = (pr.b <= 6 && pr.n_global_dofs() >= 2000000) ? 64 : 128;
+  if (const char* e = std::getenv("PDG_SWEEP_THREADS")) sweep_threads = std::atoi(e) == 64 ? 64 : 128;
+  smem_fwd = smem_bwd = sweep_smem_bytes(sweep_xcap, sweep_threads);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");
   if (smem_fwd > 48 * 1024) set_sweep_smem(smem_fwd);
   {
     int sms = 148, dev = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const std::vector<int> perm = list_schedule(pr, fu, sms * sweep_ctas_per_sm(smem_fwd));
+    const std::vector<int> perm = list_schedule(pr, fu, sms * sweep_ctas_per_sm(smem_fwd, sweep_threads));
     std::vector<DevUnit> o(fu.size());
     for (std::size_t i = 0; i < perm.size(); ++i) o[i] = fu[perm[i]];
     fu.swap(o);
@@ -716,6 +721,7 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   SweepArgs a;
   static const char* pf = std::getenv("PDG_SWEEP_PREFETCH");
   a.prefetch = pf ? std::atoi(pf) : 3;  // bit 0: L2 bulk prefetch, bit 1: evict-first panel loads
+  a.threads = sweep_threads;
   a.tasks = d_tasks;
   a.units = d_fwd_units;
   a.n_units_f = n_units_f;

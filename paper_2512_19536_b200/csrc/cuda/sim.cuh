@@ -26,8 +26,8 @@ struct StepResult {
 };
 
 void set_sweep_smem(int bytes);
-int sweep_ctas_per_sm(int smem);  // occupancy of the sweep kernel
-int sweep_smem_bytes(int xcap);   // dynamic shared memory of the sweep (mode dependent)
+int sweep_ctas_per_sm(int smem, int threads);  // occupancy of the sweep kernel
+int sweep_smem_bytes(int xcap, int threads);   // dynamic shared memory of the sweep
 // Extreme-eigenvalue ratio of the Lanczos tridiagonal (krylov.cpp:85-103).
 bool lanczos_condition(const double* alpha, const double* beta, int m, double* kappa);
 
@@ -87,6 +87,7 @@ class DeviceSim {
   int* d_flags = nullptr;
   unsigned int* d_ticket = nullptr;
   int smem_fwd = 0, smem_bwd = 0, sweep_xcap = 0;
+  int sweep_threads = 128;  // sweep CTA size (64 or 128, chosen in upload_tasks)
   unsigned long long* d_live = nullptr;  // live sweep timing (sweep.cu)
   long long panel_values = 0;            // F + H doubles on the device
   // ionic

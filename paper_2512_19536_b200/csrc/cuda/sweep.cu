@@ -41,9 +41,9 @@
 // allocation must allow. Unset = the compiler's own choice (58 registers,
 // 8 CTAs/SM), which measured best; an explicit 1 lets it take 102.
 #ifdef PDG_SWEEP_MINB
-#define PDG_SWEEP_BOUNDS __launch_bounds__(kSweepThreads, PDG_SWEEP_MINB)
+#define PDG_SWEEP_BOUNDS __launch_bounds__(NT, PDG_SWEEP_MINB)
 #else
-#define PDG_SWEEP_BOUNDS __launch_bounds__(kSweepThreads)
+#define PDG_SWEEP_BOUNDS __launch_bounds__(NT)
 #endif
 static_assert(PDG_DOT_DEPTH % 4 == 0, "tile_dot consumes loads four at a time");
 
@@ -101,11 +101,11 @@ __device__ __forceinline__ double2 ld_panel(const double2* p, unsigned long long
   return v;
 }
 // named barrier for the staging warps (1..kWarps-1) only
+template <int NT>
 __device__ __forceinline__ void staging_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kSweepThreads - 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NT - 32) : "memory");
 }
 
-constexpr int kWarps = kSweepThreads / 32;
 constexpr int kMaxSmemTiles = 32;
 constexpr int kMetaCells = 160;  // staged in_ptr entries per unit
 constexpr int kMetaIdx = 768;    // staged update offsets / row dof starts per unit
@@ -204,10 +204,10 @@ __device__ __forceinline__ void store_row(const SweepArgs& a, const DevTask& T, 
 }
 
 // warps 1..3: everything that does not depend on the awaited units
-template <bool FWD>
+template <bool FWD, int NT>
 __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* xin) {
-  const int t = threadIdx.x - 32;  // 0 .. kSweepThreads-33
-  const int nst = kSweepThreads - 32;
+  const int t = threadIdx.x - 32;  // 0 .. NT-33
+  const int nst = NT - 32;
   const DevUnit& U = s.u;
   const DevTask& T = s.t;
   if (t == 0 && (a.prefetch & 1)) prefetch_panel(a, U);
@@ -258,7 +258,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
     // own y_S (this task's forward result) is independent of the awaited ancestors
     if (U.own_fwd >= 0 && col_lo < w) {
       if (t == 0) wait_count(a.flags + U.own_fwd, (s.ep + 1) * U.own_need);
-      staging_sync();
+      staging_sync<NT>();
       const double* ybuf = T.coarse ? a.yc : a.yf;
       for (int i = col_lo + t; i < min(col_hi, w); i += nst) xin[i - col_lo] = __ldcg(ybuf + T.dof0 + i);
     }
@@ -269,7 +269,7 @@ __device__ __forceinline__ void stage(const SweepArgs& a, UnitSmem& s, double* x
   }
 }
 
-template <bool FWD, bool EF>
+template <bool FWD, bool EF, int NT>
 __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double* xin, double* part, int tk) {
   long long* tr = a.trace ? a.trace + 8LL * tk : nullptr;
   const int ep = s.ep;
@@ -294,7 +294,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
     else q.tk = a.n_units;
   } else if (threadIdx.x >= 32) {
-    stage<FWD>(a, s, xin);
+    stage<FWD, NT>(a, s, xin);
   }
   __syncthreads();
   const DevUnit& U = s.u;
@@ -374,7 +374,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     // one tile, columns [c0, c1): warps split the columns, partials to global
     const DevTile tl = s.tiles[0];
     const int nc = U.c1 - U.c0;
-    const int per = (((nc + kWarps - 1) / kWarps) + 1) & ~1;
+    const int per = (((nc + (NT / 32) - 1) / (NT / 32)) + 1) & ~1;
     const int j0 = warp * per, j1 = min(nc, j0 + per);
     const double2 v = tile_dot<EF>((FWD ? a.fmat : a.hmat) + U.src_off, tl, xin, j0, j1);
     if (lane < 16) {
@@ -386,7 +386,7 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     double* gp = a.part + static_cast<long long>(U.part_base + U.chunk) * 32;
     if (threadIdx.x < 32) {
       double sum = 0.0;
-      for (int q = 0; q < kWarps; ++q) sum += part[q * 32 + threadIdx.x];
+      for (int q = 0; q < (NT / 32); ++q) sum += part[q * 32 + threadIdx.x];
       __stcg(gp + threadIdx.x, sum);
     }
     __syncthreads();
@@ -408,10 +408,10 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
     return;
   }
   // whole tiles: items = (tile, column split) over the warps
-  const int split = ntile >= kWarps ? 1 : kWarps / ntile;
+  const int split = ntile >= (NT / 32) ? 1 : (NT / 32) / ntile;
   const int items = ntile * split;
   const DevTile* gtiles = (FWD ? a.ftiles : a.htiles) + (FWD ? T.f_tile0 : T.h_tile0) + U.tile_begin;
-  for (int it = warp; it < items; it += kWarps) {
+  for (int it = warp; it < items; it += (NT / 32)) {
     const int R = it / split, c = it - R * split;
     const DevTile tl = R < kMaxSmemTiles ? s.tiles[R] : gtiles[R];
     const double* m = (FWD ? a.fmat : a.hmat) + tl.off;
@@ -445,14 +445,14 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
-template <bool EF>
+template <bool EF, int NT>
 __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
   pdl_wait();
   if (a.S && a.S->stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ UnitSmem s;
-  double* part = sm;  // kSweepThreads doubles
-  double* xin = part + kSweepThreads;
+  double* part = sm;  // NT doubles
+  double* xin = part + NT;
   if (threadIdx.x == 0) {
     // live duration of every launch (first CTA start -> last CTA end, read by
     // bench.py over its timed region)
@@ -486,8 +486,8 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
     __syncthreads();
     const int tk = s.tk;
     if (tk >= a.n_units) break;
-    if (s.u.dir == 0) run_unit<true, EF>(a, s, xin, part, tk);
-    else run_unit<false, EF>(a, s, xin, part, tk);
+    if (s.u.dir == 0) run_unit<true, EF, NT>(a, s, xin, part, tk);
+    else run_unit<false, EF, NT>(a, s, xin, part, tk);
     __syncthreads();
   }
   // the last CTA of this sweep resets the tickets and advances the epoch
@@ -508,33 +508,44 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
 
 }  // namespace
 
-int sweep_smem_bytes(int xcap) { return static_cast<int>(sizeof(double)) * (kSweepThreads + xcap); }
+int sweep_smem_bytes(int xcap, int threads) { return static_cast<int>(sizeof(double)) * (threads + xcap); }
 
-void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
-  if (a.n_units == 0) return;
-  static int cached_smem = -1, resident = 0;
-  if (cached_smem != smem) {
-    int per_sm = 0, sms = 0, dev = 0;
-    PDG_CUDA(cudaGetDevice(&dev));
-    PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
-    resident = (per_sm > 0 ? per_sm : 1) * sms;
-    cached_smem = smem;
-  }
-  const int grid = a.n_units < resident ? a.n_units : resident;
-  if (a.prefetch & 2) launch_pdl(sweep_kernel<true>, grid, kSweepThreads, smem, st, a);
-  else launch_pdl(sweep_kernel<false>, grid, kSweepThreads, smem, st, a);
-}
-
-int sweep_ctas_per_sm(int smem) {
+template <int NT>
+static int ctas_per_sm(int smem) {
   int per_sm = 0;
-  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false>, kSweepThreads, smem));
+  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<false, NT>, NT, smem));
   return per_sm > 0 ? per_sm : 1;
 }
 
+void launch_sweep(const SweepArgs& a, int smem, cudaStream_t st) {
+  if (a.n_units == 0) return;
+  static int cached_smem = -1, cached_threads = -1, resident = 0;
+  if (cached_smem != smem || cached_threads != a.threads) {
+    int sms = 0, dev = 0;
+    PDG_CUDA(cudaGetDevice(&dev));
+    PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    resident = (a.threads == 64 ? ctas_per_sm<64>(smem) : ctas_per_sm<128>(smem)) * sms;
+    cached_smem = smem;
+    cached_threads = a.threads;
+  }
+  const int grid = a.n_units < resident ? a.n_units : resident;
+  const bool ef = (a.prefetch & 2) != 0;
+  if (a.threads == 64) {
+    if (ef) launch_pdl(sweep_kernel<true, 64>, grid, 64, smem, st, a);
+    else launch_pdl(sweep_kernel<false, 64>, grid, 64, smem, st, a);
+  } else {
+    if (ef) launch_pdl(sweep_kernel<true, 128>, grid, 128, smem, st, a);
+    else launch_pdl(sweep_kernel<false, 128>, grid, 128, smem, st, a);
+  }
+}
+
+int sweep_ctas_per_sm(int smem, int threads) { return threads == 64 ? ctas_per_sm<64>(smem) : ctas_per_sm<128>(smem); }
+
 void set_sweep_smem(int bytes) {
-  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  PDG_CUDA(cudaFuncSetAttribute(sweep_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 }  // namespace pdg

@@ -26,6 +26,8 @@ CASES = {
     "spmv_warp_rows": {"PDG_SPMV_WARP": "1"},
     "host_loop": {"PDG_NO_GRAPH": "1"},
     "host_factor": {"PDG_HOST_FACTOR": "1"},
+    "host_assembly": {"PDG_HOST_ASSEMBLY": "1"},
+    "sweep_cta_64": {"PDG_SWEEP_THREADS": "64"},
 }
 
 
