@@ -169,7 +169,8 @@ def cpu_baseline(cfg, budget_s=CPU_BASELINE_S):
             "sample": f"{its} PCG iterations ({samples} x {REF_ITERS_PER_STEP}) of the workload's system in "
                       f"{el:.1f} s after {setup:.0f} s untimed setup; oracle/ restatement with the reference's "
                       f"threading (parallel_for local solves, serial SpMV/vector ops); the reference's numeric "
-                      f"sources need Eigen3, which is absent"}
+                      f"sources build here only against an Eigen API stand-in without Eigen's SIMD kernels "
+                      f"(oracle/eigen_shim, a parity oracle), so the restatement is the timed baseline"}
 
 
 def run_reference(args):

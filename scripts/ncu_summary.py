@@ -18,7 +18,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__maximum_warps_per_active_cycle_pct"]
 
 
-SETUP = {"factor_level_kernel", "assemble_kernel", "forward_panel_kernel", "backward_panel_kernel"}
+SETUP = {"factor_level_kernel", "assemble_kernel", "forward_panel_kernel", "backward_panel_kernel", "volume_kernel",
+         "face_kernel", "k0_kernel"}
 
 
 def rep(path):
