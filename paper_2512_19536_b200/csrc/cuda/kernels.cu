@@ -196,14 +196,17 @@ __global__ void __launch_bounds__(RowGeom<B>::kThreads)
   pdl_wait();
   if (honor_stop && rc.S->stop) return;
   const int lr = threadIdx.x / B, r = threadIdx.x - lr * B;
-  const int slot = blockIdx.x * RowGeom<B>::kRows + lr;
+  const int groups = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;
   double contrib = 0.0;
-  if (lr < RowGeom<B>::kRows && slot < rows) {
-    const int row = rowlist ? __ldg(rowlist + slot) : slot;
-    const double acc = bsr_row_dot<B>(row, r, ptr, col, val, x);
-    const long long i = static_cast<long long>(row) * B + r;
-    y[i] = acc;
-    if (dotw) contrib = dotw[i] * acc;
+  for (int gi = blockIdx.x; gi < groups; gi += gridDim.x) {  // persistent: groups blockIdx.x + k gridDim.x
+    const int slot = gi * RowGeom<B>::kRows + lr;
+    if (lr < RowGeom<B>::kRows && slot < rows) {
+      const int row = rowlist ? __ldg(rowlist + slot) : slot;
+      const double acc = bsr_row_dot<B>(row, r, ptr, col, val, x);
+      const long long i = static_cast<long long>(row) * B + r;
+      y[i] = acc;
+      if (dotw) contrib += dotw[i] * acc;
+    }
   }
   if (rc.finish != kFinNone) grid_finish(block_sum(contrib), rc);
 }
@@ -610,7 +613,8 @@ __global__ void __launch_bounds__(256) update_restrict_tma_kernel(const int* __r
                                                                   double* __restrict__ x, double* __restrict__ r,
                                                                   const double* __restrict__ p,
                                                                   const double* __restrict__ q,
-                                                                  double* __restrict__ r0part, ReduceCtx rc) {
+                                                                  double* __restrict__ r0part, ReduceCtx rc,
+                                                                  int n_chunks) {
   pdl_wait();
   PcgScalars* S = rc.S;
   if (S->stop) return;
@@ -632,36 +636,41 @@ __global__ void __launch_bounds__(256) update_restrict_tma_kernel(const int* __r
   __shared__ uint64_t bar;
   __shared__ double rs[64 * B];
   __shared__ double red[B * BQ];
-  const int c0 = chunk_ptr[blockIdx.x], nc = chunk_ptr[blockIdx.x + 1] - c0;
-  const long long cell0 = cells[c0];
-  const double* Eg = E + cell0 * (B * BQ);
-  const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
-  const double* Es = reinterpret_cast<const double*>(dyn + off);
-  // the x / r update overlaps the copy (consecutive dofs: coalesced)
+  // chunks blockIdx.x, + gridDim.x, ...: one grid reduction per CTA for all
+  // of its chunks (a grid of resident CTAs instead of one CTA per chunk)
   double contrib = 0.0;
-  const long long d0 = cell0 * B;
-  for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
-    const long long d = d0 + e;
-    x[d] += alpha * p[d];
-    const double rv = r[d] - alpha * q[d];
-    r[d] = rv;
-    rs[e] = rv;
-    contrib += rv * rv;
-  }
-  __syncthreads();
-  wait_bytes(&bar);
-  // r0part[m] = sum_i sum_k E_k(i, m) r_k(i): thread f = (m, i) sums over cells
-  for (int f = threadIdx.x; f < B * BQ; f += blockDim.x) {
-    const int i = f % B;
-    double acc = 0.0;
-    for (int k = 0; k < nc; ++k) acc = fma(Es[k * (B * BQ) + f], rs[k * B + i], acc);
-    red[f] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x < BQ) {
-    double s = 0.0;
-    for (int i = 0; i < B; ++i) s += red[threadIdx.x * B + i];
-    r0part[static_cast<long long>(blockIdx.x) * BQ + threadIdx.x] = s;
+  for (int ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    __syncthreads();  // smem and the barrier of the previous chunk are free
+    const int c0 = chunk_ptr[ch], nc = chunk_ptr[ch + 1] - c0;
+    const long long cell0 = cells[c0];
+    const double* Eg = E + cell0 * (B * BQ);
+    const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
+    const double* Es = reinterpret_cast<const double*>(dyn + off);
+    // the x / r update overlaps the copy (consecutive dofs: coalesced)
+    const long long d0 = cell0 * B;
+    for (int e = threadIdx.x; e < nc * B; e += blockDim.x) {
+      const long long d = d0 + e;
+      x[d] += alpha * p[d];
+      const double rv = r[d] - alpha * q[d];
+      r[d] = rv;
+      rs[e] = rv;
+      contrib += rv * rv;
+    }
+    __syncthreads();
+    wait_bytes(&bar);
+    // r0part[m] = sum_i sum_k E_k(i, m) r_k(i): thread f = (m, i) sums over cells
+    for (int f = threadIdx.x; f < B * BQ; f += blockDim.x) {
+      const int i = f % B;
+      double acc = 0.0;
+      for (int k = 0; k < nc; ++k) acc = fma(Es[k * (B * BQ) + f], rs[k * B + i], acc);
+      red[f] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < BQ) {
+      double s = 0.0;
+      for (int i = 0; i < B; ++i) s += red[threadIdx.x * B + i];
+      r0part[static_cast<long long>(ch) * BQ + threadIdx.x] = s;
+    }
   }
   grid_finish(block_sum(contrib), rc);
 }
@@ -674,13 +683,16 @@ __global__ void __launch_bounds__(256) prolong_dot_tma_kernel(const int* __restr
                                                               const double* __restrict__ E,
                                                               const double* __restrict__ y0,
                                                               const double* __restrict__ r, double* __restrict__ z,
-                                                              ReduceCtx rc) {
+                                                              ReduceCtx rc, int n_chunks) {
   pdl_wait();
   if (rc.S->stop) return;
   extern __shared__ __align__(128) unsigned char dyn[];
   __shared__ uint64_t bar;
   __shared__ double ys[BQ];
-  const int c0 = chunk_ptr[blockIdx.x], nc = chunk_ptr[blockIdx.x + 1] - c0;
+  double contrib = 0.0;
+  for (int ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+  __syncthreads();  // smem and the barrier of the previous chunk are free
+  const int c0 = chunk_ptr[ch], nc = chunk_ptr[ch + 1] - c0;
   const long long cell0 = cells[c0];
   const double* Eg = E + cell0 * (B * BQ);
   const int off = stage_bytes(Eg, Eg + static_cast<long long>(nc) * (B * BQ), dyn, &bar);
@@ -701,7 +713,6 @@ __global__ void __launch_bounds__(256) prolong_dot_tma_kernel(const int* __restr
   }
   __syncthreads();
   wait_bytes(&bar);
-  double contrib = 0.0;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int e = threadIdx.x + j * 256;
@@ -714,6 +725,7 @@ __global__ void __launch_bounds__(256) prolong_dot_tma_kernel(const int* __restr
     const double zi = zv[j] + acc;
     z[d0 + e] = zi;
     contrib += rv[j] * zi;
+  }
   }
   grid_finish(block_sum(contrib), rc);
 }
@@ -977,6 +989,25 @@ int vec_grid(long long n) {
     default: throw CudaError("unsupported block size"); \
   }
 
+// Persistent grids (default): the per-iteration vector kernels run one
+// resident grid that strides over their chunks / row groups, so the grid
+// reduction's per-CTA fence + atomic and the last CTA's sum happen once per
+// resident CTA instead of once per 32-cell chunk (30-40K CTAs at config 4).
+// PDG_PERSIST=0: one CTA per chunk / row group.
+bool persistent_grids() {
+  static const bool on = !(std::getenv("PDG_PERSIST") && std::getenv("PDG_PERSIST")[0] == '0');
+  return on;
+}
+
+template <class K>
+static int resident_ctas(K kernel, int threads, int smem) {
+  int per_sm = 0, sms = 0, dev = 0;
+  PDG_CUDA(cudaGetDevice(&dev));
+  PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  return std::max(1, per_sm) * sms;
+}
+
 void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* val, const double* x,
                  double* y, const double* dotw, ReduceCtx rc, bool honor_stop, cudaStream_t st,
                  const int* rowlist) {
@@ -999,8 +1030,9 @@ void launch_spmv(int b, int rows, const int* ptr, const int* col, const double* 
 #define L(B)                                                                                  \
   {                                                                                           \
     const int g = (rows + RowGeom<B>::kRows - 1) / RowGeom<B>::kRows;                         \
-    launch_pdl(spmv_kernel<B>, g, RowGeom<B>::kThreads, 0, st, rows, ptr, col, val, x, y, dotw, rc, \
-               honor_stop ? 1 : 0, rowlist);                                                  \
+    static const int res = resident_ctas(spmv_kernel<B>, RowGeom<B>::kThreads, 0);            \
+    launch_pdl(spmv_kernel<B>, persistent_grids() ? std::min(g, res) : g, RowGeom<B>::kThreads, 0, st, rows, ptr, \
+               col, val, x, y, dotw, rc, honor_stop ? 1 : 0, rowlist);                        \
   }
   if (rows > 0) PDG_B_DISPATCH(b, L)
 #undef L
@@ -1120,19 +1152,25 @@ static void coarse_tma_launch(bool update, int n_chunks, int max_nc, const int* 
                               const double* q, double* r0part, const double* y0, double* z, ReduceCtx rc,
                               cudaStream_t st) {
   const int smem = max_nc * B * BQ * 8 + 32;  // + widening of the range to 16-byte ends
-  static int set_u = 0, set_p = 0;
+  static int set_u = 0, set_p = 0, res_u = 0, res_p = 0;
   if (update) {
     if (smem > set_u) {
       PDG_CUDA(cudaFuncSetAttribute(update_restrict_tma_kernel<B, BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       set_u = smem;
+      res_u = resident_ctas(update_restrict_tma_kernel<B, BQ>, 256, smem);
     }
-    launch_pdl(update_restrict_tma_kernel<B, BQ>, n_chunks, 256, smem, st, chunk_ptr, cells, E, x, r, p, q, r0part, rc);
+    const int grid = persistent_grids() ? std::min(n_chunks, res_u) : n_chunks;
+    launch_pdl(update_restrict_tma_kernel<B, BQ>, grid, 256, smem, st, chunk_ptr, cells, E, x, r, p, q, r0part, rc,
+               n_chunks);
   } else {
     if (smem > set_p) {
       PDG_CUDA(cudaFuncSetAttribute(prolong_dot_tma_kernel<B, BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       set_p = smem;
+      res_p = resident_ctas(prolong_dot_tma_kernel<B, BQ>, 256, smem);
     }
-    launch_pdl(prolong_dot_tma_kernel<B, BQ>, n_chunks, 256, smem, st, chunk_ptr, cells, cell_agg, E, y0, r, z, rc);
+    const int grid = persistent_grids() ? std::min(n_chunks, res_p) : n_chunks;
+    launch_pdl(prolong_dot_tma_kernel<B, BQ>, grid, 256, smem, st, chunk_ptr, cells, cell_agg, E, y0, r, z, rc,
+               n_chunks);
   }
 }
 

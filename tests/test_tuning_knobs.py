@@ -28,6 +28,7 @@ CASES = {
     "host_factor": {"PDG_HOST_FACTOR": "1"},
     "host_assembly": {"PDG_HOST_ASSEMBLY": "1"},
     "sweep_cta_64": {"PDG_SWEEP_THREADS": "64"},
+    "one_cta_per_chunk": {"PDG_PERSIST": "0"},
 }
 
 
