@@ -11,3 +11,4 @@ run c5p4 config5:4
 run c5p4_np config5:4 PDG_PERSIST=0
 timeout 900 python bench.py --no-cpu-baseline > $O/bench.json 2> $O/bench.err
 PDG_PERSIST=0 timeout 900 python bench.py --no-cpu-baseline > $O/bench_np.json 2> $O/bench_np.err
+timeout 1200 python scripts/c3_study.py $O/c3 > $O/c3_study.log 2>&1
