@@ -35,7 +35,7 @@ int main(int argc, char** argv) {
   struct Acc {
     double cells = 0, structural = 0, stored = 0, nsn = 0, height = 0, n = 0;
     double panel[4] = {0, 0, 0, 0};  // panel doubles (fwd + bwd): align 8 / align 2 / tri16+align8 / tri16+align2
-    double bundled_tasks = 0, bundles = 0, free_tasks = 0, leaves = 0, leaf_bytes = 0, all_bytes = 0;
+    double bundled_bytes = 0, bundled_tasks = 0, bundles = 0, free_tasks = 0, leaves = 0, leaf_bytes = 0, all_bytes = 0;
   };
   std::map<std::string, Acc> acc;
   for (int u = 0; u < part.count; u += every) {
@@ -119,6 +119,7 @@ int main(int argc, char** argv) {
           if (pp >= 0 && in_bundle[pp]) in_bundle[q] = 1;
         }
         for (int q = 0; q < ns; ++q) (in_bundle[q] ? a.bundled_tasks : a.free_tasks) += 1;
+        for (int q = 0; q < ns; ++q) if (in_bundle[q]) a.bundled_bytes += fbytes_of[q];
         for (int q = 0; q < ns; ++q) {
           a.all_bytes += fbytes_of[q];
           if (kids[q].empty()) { a.leaves += 1; a.leaf_bytes += fbytes_of[q]; }
@@ -139,6 +140,9 @@ int main(int argc, char** argv) {
   for (auto& [k, a] : acc)
     printf("%-28s tasks %.0f leaves %.0f (%.0f%% of fwd bytes) per subdomain\n", k.c_str(),
            (a.bundled_tasks + a.free_tasks) / a.n, a.leaves / a.n, 100.0 * a.leaf_bytes / a.all_bytes);
+  for (auto& [k, a] : acc)
+    printf("%-28s bundles %.0f holding %.0f tasks (%.0f%% of fwd bytes), free tasks %.0f per subdomain\n", k.c_str(),
+           a.bundles / a.n, a.bundled_tasks / a.n, 100.0 * a.bundled_bytes / a.all_bytes, a.free_tasks / a.n);
   for (auto& [k, a] : acc)
     printf("%-28s panel/cell (fwd+bwd doubles): a8 %.0f a2 %.0f tri16a8 %.0f tri16a2 %.0f | 2x structural %.0f\n", k.c_str(),
            a.panel[0] / a.cells, a.panel[1] / a.cells, a.panel[2] / a.cells, a.panel[3] / a.cells,
