@@ -109,6 +109,11 @@ struct SweepArgs {
   double* yc;
   const double* r0part;   // non-null: the coarse forward sums r0 from the restriction chunks
   const int* node_chunk_ptr;
+  // subtree bundles (host/problem.hpp Bundle): records, forward publish list
+  // {root task, its forward tiles}, backward wait list {counter, count}
+  const int* bmeta;
+  const int2* broots;
+  const int2* bdeps;
   const PcgScalars* S;
   int* epoch;        // [0] sweep number (counters wait for (epoch+1) * count), [1] CTAs finished
   int xcap;          // doubles per unit input buffer

@@ -300,10 +300,12 @@ void DeviceSim::alloc_history(int cap) {
 
 void DeviceSim::release_tasks() {
   void* ptrs[] = {d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_part, d_task_child, d_fmat, d_hmat, d_ftiles, d_htiles,
-                  d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_yfwd};
+                  d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_yfwd, d_bmeta, d_broots, d_bdeps};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   d_yfwd = nullptr;
+  d_bmeta = nullptr;
+  d_broots = d_bdeps = nullptr;
   d_tasks = nullptr;
   d_nunit = d_task_child = d_in_ptr = d_flags = nullptr;
   d_fwd_units = d_bwd_units = nullptr;
@@ -326,79 +328,117 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   // cost model of the simulated schedule (ns); calibrating it to the traced
   // unit times (7 us fixed, 10 GB/s per CTA) changed nothing measurable
   // (profiles/r02l sched_*)
-  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;
-  const int nt = static_cast<int>(pr.tasks.size()), nu = static_cast<int>(units.size());
-  auto cost = [&](const DevUnit& u) { return kFixed + kPerByte * u.bytes; };
-  std::vector<double> cmax_f(nt, 0.0), cmax_b(nt, 0.0);
-  std::vector<int> left_f(nt, 0), left_b(nt, 0);
-  std::vector<std::vector<int>> units_f(nt), units_b(nt);
-  for (int i = 0; i < nu; ++i) {
-    const DevUnit& u = units[i];
-    if (u.dir == 0) {
-      cmax_f[u.task] = std::max(cmax_f[u.task], cost(u));
-      units_f[u.task].push_back(i);
-    } else {
-      cmax_b[u.task] = std::max(cmax_b[u.task], cost(u));
-      units_b[u.task].push_back(i);
+  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0, kLevel = 1500.0;
+  // schedule nodes: an unbundled task is its own node, a subtree bundle is
+  // one node whose parents are the distinct parents of its roots
+  const int nt = static_cast<int>(pr.tasks.size()), nb = static_cast<int>(pr.bundles.size());
+  const int nn = nt + nb, nu = static_cast<int>(units.size());
+  auto node_of_unit = [&](const DevUnit& u) { return u.nchunk == 0 ? nt + u.tile_begin : u.task; };
+  auto cost = [&](const DevUnit& u) {
+    return kFixed + kPerByte * u.bytes + (u.nchunk == 0 ? kLevel * pr.bundles[u.tile_begin].nlev : 0.0);
+  };
+  std::vector<std::vector<int>> pars(nn), kids(nn);
+  std::vector<char> dense_root(nn, 0);
+  for (int s = 0; s < nt; ++s) {
+    const TaskDesc& t = pr.tasks[s];
+    if (t.bundle >= 0) continue;
+    dense_root[s] = static_cast<char>(t.root_dense);
+    if (t.parent >= 0) {
+      pars[s].push_back(t.parent);
+      kids[t.parent].push_back(s);
     }
   }
-  // longest remaining path (bottom level) per task and direction; children
-  // precede parents in task order
-  std::vector<double> Lb(nt, 0.0), Lf(nt, 0.0), kid_b(nt, 0.0);
-  for (int s = 0; s < nt; ++s) {
-    Lb[s] = cmax_b[s] + kPublish + kid_b[s];
-    const int p = pr.tasks[s].parent;
-    if (p >= 0) kid_b[p] = std::max(kid_b[p], Lb[s]);
+  for (int b = 0; b < nb; ++b) {
+    const Bundle& B = pr.bundles[b];
+    for (int k = 0; k < B.n_par; ++k) {
+      const int p = pr.bundle_parents[B.par_off + k];
+      pars[nt + b].push_back(p);
+      kids[p].push_back(nt + b);
+    }
   }
-  for (int s = nt - 1; s >= 0; --s) {
-    const int p = pr.tasks[s].parent;
-    Lf[s] = cmax_f[s] + kPublish + std::max(p >= 0 ? Lf[p] : 0.0, Lb[s]);
+  std::vector<double> cmax_f(nn, 0.0), cmax_b(nn, 0.0);
+  std::vector<int> left_f(nn, 0), left_b(nn, 0);
+  std::vector<std::vector<int>> units_f(nn), units_b(nn);
+  for (int i = 0; i < nu; ++i) {
+    const DevUnit& u = units[i];
+    const int n = node_of_unit(u);
+    if (u.dir == 0) {
+      cmax_f[n] = std::max(cmax_f[n], cost(u));
+      units_f[n].push_back(i);
+    } else {
+      cmax_b[n] = std::max(cmax_b[n], cost(u));
+      units_b[n].push_back(i);
+    }
+  }
+  // longest remaining path (bottom level) per node and direction; bundles
+  // have no children, and children precede parents in task order
+  std::vector<int> topo;
+  topo.reserve(nn);
+  for (int b = 0; b < nb; ++b) topo.push_back(nt + b);
+  for (int s = 0; s < nt; ++s)
+    if (pr.tasks[s].bundle < 0) topo.push_back(s);
+  std::vector<double> Lb(nn, 0.0), Lf(nn, 0.0);
+  for (int n : topo) {
+    double kid = 0.0;
+    for (int c : kids[n]) kid = std::max(kid, Lb[c]);
+    Lb[n] = cmax_b[n] + kPublish + kid;
+  }
+  for (auto it = topo.rbegin(); it != topo.rend(); ++it) {
+    const int n = *it;
+    double up = Lb[n];
+    for (int p : pars[n]) up = std::max(up, Lf[p]);
+    Lf[n] = cmax_f[n] + kPublish + up;
   }
   std::vector<double> prio(nu);
   for (int i = 0; i < nu; ++i) {
     const DevUnit& u = units[i];
-    const int s = u.task;
-    prio[i] = u.dir == 0 ? Lf[s] - cmax_f[s] + cost(u) : Lb[s] - cmax_b[s] + cost(u);
+    const int n = node_of_unit(u);
+    prio[i] = u.dir == 0 ? Lf[n] - cmax_f[n] + cost(u) : Lb[n] - cmax_b[n] + cost(u);
   }
-  // pending dependency counts per task-direction
-  std::vector<int> dep_f(nt), dep_b(nt);
-  for (int s = 0; s < nt; ++s) {
-    dep_f[s] = pr.tasks[s].n_child;
-    dep_b[s] = 1 + (pr.tasks[s].parent >= 0 ? 1 : 0);
-    left_f[s] = static_cast<int>(units_f[s].size());
-    left_b[s] = static_cast<int>(units_b[s].size());
+  // pending dependency counts per node and direction
+  std::vector<int> dep_f(nn, 0), dep_b(nn, 0);
+  for (int n : topo) {
+    dep_f[n] = static_cast<int>(kids[n].size());
+    dep_b[n] = 1 + static_cast<int>(pars[n].size());
+    left_f[n] = static_cast<int>(units_f[n].size());
+    left_b[n] = static_cast<int>(units_b[n].size());
   }
   using TI = std::pair<double, int>;
   std::priority_queue<TI, std::vector<TI>, std::greater<TI>> release, finish, cta;
   std::priority_queue<TI> ready;  // by priority
-  std::vector<double> task_done_f(nt, 0.0), task_done_b(nt, 0.0), start(nu, 0.0);
-  auto release_dir = [&](int s, bool fwd, double t) {
-    for (int i : fwd ? units_f[s] : units_b[s]) release.push({t, i});
+  std::vector<double> done_f(nn, 0.0), done_b(nn, 0.0), start(nu, 0.0);
+  auto release_dir = [&](int n, bool fwd, double t) {
+    for (int i : fwd ? units_f[n] : units_b[n]) release.push({t, i});
   };
-  for (int s = 0; s < nt; ++s)
-    if (dep_f[s] == 0) release_dir(s, true, 0.0);
+  for (int n : topo)
+    if (dep_f[n] == 0) release_dir(n, true, 0.0);
   for (int c = 0; c < slots; ++c) cta.push({0.0, c});
-  auto release_children_bwd = [&](int s, double r) {
-    for (int k = 0; k < pr.tasks[s].n_child; ++k) {
-      const int c = pr.task_child[pr.tasks[s].child_off + k];
-      if (--dep_b[c] == 0) release_dir(c, false, r);
-    }
+  std::function<void(int, double)> release_children_bwd = [&](int n, double r) {
+    for (int c : kids[n])
+      if (--dep_b[c] == 0) {
+        release_dir(c, false, r);
+        // a node without backward units (nothing to do) passes the release on
+        if (units_b[c].empty()) release_children_bwd(c, r);
+      }
   };
   auto complete = [&](int i, double t) {
     const DevUnit& u = units[i];
-    const int s = u.task;
+    const int n = node_of_unit(u);
     if (u.dir == 0) {
-      task_done_f[s] = std::max(task_done_f[s], t);
-      if (--left_f[s] > 0) return;
-      const double r = task_done_f[s] + kPublish;
-      const int p = pr.tasks[s].parent;
-      if (p >= 0 && --dep_f[p] == 0) release_dir(p, true, r);
-      if (pr.tasks[s].root_dense) release_children_bwd(s, r);  // x_S is final after the forward
-      else if (--dep_b[s] == 0) release_dir(s, false, r);
+      done_f[n] = std::max(done_f[n], t);
+      if (--left_f[n] > 0) return;
+      const double r = done_f[n] + kPublish;
+      for (int p : pars[n])
+        if (--dep_f[p] == 0) release_dir(p, true, r);
+      if (dense_root[n]) release_children_bwd(n, r);  // x_S is final after the forward
+      else if (--dep_b[n] == 0) {
+        release_dir(n, false, r);
+        if (units_b[n].empty()) release_children_bwd(n, r);
+      }
     } else {
-      task_done_b[s] = std::max(task_done_b[s], t);
-      if (--left_b[s] > 0) return;
-      release_children_bwd(s, task_done_b[s] + kPublish);
+      done_b[n] = std::max(done_b[n], t);
+      if (--left_b[n] > 0) return;
+      release_children_bwd(n, done_b[n] + kPublish);
     }
   };
   int placed = 0;
@@ -527,6 +567,7 @@ void DeviceSim::upload_tasks() {
   auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units) {
     for (int tk : order) {
       const TaskDesc& s = pr.tasks[tk];
+      if (s.bundle >= 0) continue;  // solved inside its subtree bundle (below)
       const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
       auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };
@@ -608,6 +649,48 @@ void DeviceSim::upload_tasks() {
   std::vector<DevUnit> fu, bu;
   make_units(fo, true, fu);
   make_units(bo, false, bu);
+  // subtree bundles: one unit per direction (sweep.cu run_bundle). Forward
+  // publish list {root, its forward tiles}; backward wait list = the roots'
+  // distinct parents (their backward tiles, or a dense root's forward ones).
+  std::vector<int2> broots, bdeps;
+  for (std::size_t b = 0; b < pr.bundles.size(); ++b) {
+    const Bundle& B = pr.bundles[b];
+    const int root0 = pr.bundle_roots[B.root_off];
+    for (int dir = 0; dir < 2; ++dir) {
+      DevUnit u{};
+      u.task = root0;
+      u.tile_begin = static_cast<int>(b);
+      u.nchunk = 0;
+      u.dir = dir;
+      u.src_off = B.src_off[dir];
+      u.bytes = B.bytes[dir];
+      u.in_e0 = B.meta_off[dir];
+      u.in_n = B.meta_n[dir];
+      u.own_fwd = dir ? root0 : -1;
+      u.own_need = dir ? pr.tasks[root0].f_ntile : 0;
+      if (dir == 0) {
+        u.part_base = static_cast<int>(broots.size());
+        u.tile_ctr = B.n_root;
+        for (int k = 0; k < B.n_root; ++k) {
+          const int r = pr.bundle_roots[B.root_off + k];
+          broots.push_back(make_int2(r, pr.tasks[r].f_ntile));
+        }
+      } else {
+        u.c0 = static_cast<int>(bdeps.size());
+        u.c1 = B.n_par;
+        for (int k = 0; k < B.n_par; ++k) {
+          const int p = pr.bundle_parents[B.par_off + k];
+          const TaskDesc& ps = pr.tasks[p];
+          bdeps.push_back(ps.root_dense ? make_int2(p, ps.f_ntile) : make_int2(nt_flag + p, ps.h_ntile));
+        }
+      }
+      max_in = std::max<long long>(max_in, B.xneed);
+      (dir ? bu : fu).push_back(u);
+    }
+  }
+  d_bmeta = dupload(pr.bmeta, st);
+  d_broots = dupload(broots, st);
+  d_bdeps = dupload(bdeps, st);
   // one ticket space (sweep.cu): forward and backward units in the order of a
   // simulated list schedule (critical path first)
   n_units_f = static_cast<int>(fu.size());
@@ -687,7 +770,7 @@ DeviceSim::~DeviceSim() {
   void* ptrs[] = {d_ptr, d_col, d_kval, d_M, d_Minv, d_U[0], d_U[1], d_x, d_p, d_r, d_z, d_q,
                   d_rhs, d_ion, d_tmp, d_tmp2, d_Y[0], d_Y[1], d_E, d_cell_agg, d_agg_ptr,
                   d_agg_cells, d_r0, d_y0, d_tasks, d_fwd_units, d_bwd_units, d_nunit, d_task_child,
-                  d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bbox,
+                  d_fmat, d_hmat, d_ftiles, d_htiles, d_row_dof, d_in_ptr, d_in_idx, d_ubuf, d_flags, d_ticket, d_bmeta, d_broots, d_bdeps, d_bbox,
                   d_tri_ptr, d_tri, d_ionflags, red.partial, red.counter, d_S, d_hist, d_perm,
                   d_Y[2], d_scratch, d_send_cells, d_sendbuf, d_dot_local, d_dot_global, d_stage, d_chunk_ptr, d_node_chunk_ptr, d_r0part,
                   d_live, d_area, d_means, d_rows_int, d_rows_bnd};
@@ -732,6 +815,9 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.ticket = d_ticket;
   a.flags = d_flags;
   a.task_child = d_task_child;
+  a.bmeta = d_bmeta;
+  a.broots = d_broots;
+  a.bdeps = d_bdeps;
   a.fmat = d_fmat;
   a.hmat = d_hmat;
   a.ftiles = d_ftiles;

@@ -29,6 +29,7 @@
 // `epoch`), so no memsets are needed between sweeps.
 #include <cstdint>
 
+#include "../host/problem.hpp"
 #include "kernels.cuh"
 
 #ifndef PDG_SPIN_NS
@@ -121,9 +122,14 @@ struct UnitSmem {
   DevUnit u;  // running unit and its task
   DevTask t;
   int col_lo, col_hi, cell_lo, meta, last, ep, tk;
-  DevTile tiles[kMaxSmemTiles];
-  int iptr[kMetaCells];
-  long long idx[kMetaIdx];
+  union {
+    struct {
+      DevTile tiles[kMaxSmemTiles];
+      int iptr[kMetaCells];
+      long long idx[kMetaIdx];
+    };
+    alignas(16) int blob[kBundleMetaInts];  // a subtree bundle's record (host/problem.hpp Bundle)
+  };
   Ahead q[kAhead];
   int qh;
 };
@@ -136,6 +142,10 @@ __device__ __forceinline__ void fetch_ahead(const SweepArgs& a, Ahead& q) {
   if (tk < a.n_units) {
     q.u = a.units[tk];
     q.t = a.tasks[q.u.task];
+    // a bundle's record is the first thing its CTA needs: bring it to L2 now
+    if (q.u.nchunk == 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.bmeta + q.u.in_e0), "r"(q.u.in_n * 4)
+                   : "memory");
   }
 }
 // L2 bulk prefetch of the running unit's panel (issued when the unit starts:
@@ -190,6 +200,53 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
   double vx = (acc0.x + acc1.x) + (acc2.x + acc3.x), vy = (acc0.y + acc1.y) + (acc2.y + acc3.y);
   vx += __shfl_down_sync(0xffffffffu, vx, 16);
   vy += __shfl_down_sync(0xffffffffu, vy, 16);
+  return make_double2(vx, vy);
+}
+
+// one warp, narrow or short tiles of a subtree bundle: the lanes form G =
+// 32 / lg column groups of lg = 2..16 row pairs (lg = the power of two >= the
+// tile's row pairs), so a 10-row tile still keeps 20 lanes loading; group sums
+// are added in a fixed shuffle order. (row 2*l2, row 2*l2+1) sums in lanes < lg.
+template <bool EF>
+__device__ __forceinline__ double2 tile_dot_g(const double* m, int rows, int stride, int ncol, const double* x,
+                                              int lg) {
+  unsigned long long pol = 0;
+  if (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int lane = threadIdx.x & 31;
+  const int G = 32 / lg, l2 = lane & (lg - 1), grp = lane / lg;
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
+  if (2 * l2 < rows) {
+    const double2* mm = reinterpret_cast<const double2*>(m) + l2;
+    const long long cs = stride >> 1;
+    constexpr int D = PDG_DOT_DEPTH;
+    for (int j = grp; j < ncol; j += D * G) {
+      double2 v[D];
+      double xv[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        const int jj = j + u * G;
+        const bool on = jj < ncol;
+        v[u] = on ? ld_panel<EF>(mm + jj * cs, pol) : make_double2(0.0, 0.0);
+        xv[u] = on ? x[jj] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < D; u += 4) {
+        acc0.x = fma(v[u].x, xv[u], acc0.x);
+        acc0.y = fma(v[u].y, xv[u], acc0.y);
+        acc1.x = fma(v[u + 1].x, xv[u + 1], acc1.x);
+        acc1.y = fma(v[u + 1].y, xv[u + 1], acc1.y);
+        acc2.x = fma(v[u + 2].x, xv[u + 2], acc2.x);
+        acc2.y = fma(v[u + 2].y, xv[u + 2], acc2.y);
+        acc3.x = fma(v[u + 3].x, xv[u + 3], acc3.x);
+        acc3.y = fma(v[u + 3].y, xv[u + 3], acc3.y);
+      }
+    }
+  }
+  double vx = (acc0.x + acc1.x) + (acc2.x + acc3.x), vy = (acc0.y + acc1.y) + (acc2.y + acc3.y);
+  for (int off = 16; off >= lg; off >>= 1) {
+    vx += __shfl_down_sync(0xffffffffu, vx, off);
+    vy += __shfl_down_sync(0xffffffffu, vy, off);
+  }
   return make_double2(vx, vy);
 }
 
@@ -445,6 +502,133 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
+// A subtree bundle (host/problem.hpp Bundle): every supernode of a few whole
+// bottom subtrees, solved by this CTA alone level by level. No counters inside
+// the bundle and no global round trips between its levels: the bundle's vectors
+// live in shared memory. Forward: t_S = r_S for every member is loaded up
+// front; per level the members' incoming updates (shared u_D slices) are
+// subtracted, one barrier, one warp per 32-row tile (y_S to global, u_S to
+// global and shared), one barrier. Backward: y_S and the rows owned by outside
+// ancestors are loaded up front; per level the rows owned by members are copied
+// from their shared x_S. The forward pass has no dependencies and publishes the
+// subtree roots' counters at the end; the backward pass waits for the roots'
+// parents and for the bundle's own forward pass.
+template <bool FWD, bool EF, int NT>
+__device__ __forceinline__ void run_bundle(const SweepArgs& a, UnitSmem& s, double* xin, int tk) {
+  long long* tr = a.trace ? a.trace + 8LL * tk : nullptr;
+  const int ep = s.ep;
+  const DevUnit& U = s.u;
+  if (threadIdx.x == 0) {
+    if (tr) tr[0] = gtimer();
+    if (!FWD) {
+      for (int d = 0; d < U.c1; ++d) {
+        const int2 w = a.bdeps[U.c0 + d];
+        wait_count(a.flags + w.x, (ep + 1) * w.y);
+      }
+      wait_count(a.flags + U.own_fwd, (ep + 1) * U.own_need);
+    }
+    if (tr) tr[1] = gtimer();
+  } else if (threadIdx.x == 1) {
+    const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
+    Ahead& q = s.q[target];
+    if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
+    else q.tk = a.n_units;
+  } else if (threadIdx.x >= 32) {
+    const int t = threadIdx.x - 32;
+    if (t == 0 && (a.prefetch & 1)) prefetch_panel(a, U);
+    const int4* src = reinterpret_cast<const int4*>(a.bmeta + U.in_e0);
+    int4* dst = reinterpret_cast<int4*>(s.blob);
+    for (int i = t; i < (U.in_n >> 2); i += NT - 32) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[4] = gtimer();
+  const int nlev = s.blob[0], ncell = s.blob[1], naux = s.blob[3];
+  const int* lev = s.blob + 4;
+  const int* cells = lev + 2 * nlev;
+  const int* aux = cells + (FWD ? 4 : 2) * ncell;
+  const int* items = aux + (FWD ? naux : 2 * naux);
+  const int bs = s.t.bs;
+  const double* pan = (FWD ? a.fmat : a.hmat) + U.src_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // everything known at the start, in one round of independent loads
+  if (FWD) {
+    for (int q = threadIdx.x; q < ncell * bs; q += NT) {
+      const int c = q / bs, rr = q - c * bs;
+      xin[cells[4 * c + 1] + rr] = a.r[cells[4 * c] + rr];
+    }
+  } else {
+    for (int q = threadIdx.x; q < naux * bs; q += NT) {
+      const int c = q / bs, rr = q - c * bs;
+      const int src = aux[2 * c];
+      xin[aux[2 * c + 1] + rr] = src >= 0 ? __ldcg(a.yf + src + rr) : -__ldcg(a.z + (-1 - src) + rr);
+    }
+  }
+  int c0 = 0, i0 = 0;
+  for (int l = 0; l < nlev; ++l) {
+    const int c1 = lev[2 * l], i1 = lev[2 * l + 1];
+    if ((FWD && l == 0) || c1 > c0) {
+      if (FWD && l == 0) __syncthreads();  // leaves: inputs are r itself
+      else {
+        if (FWD) {
+          for (int q = c0 * bs + threadIdx.x; q < c1 * bs; q += NT) {
+            const int c = q / bs, rr = q - c * bs;
+            const int* ce = cells + 4 * c;
+            double v = xin[ce[1] + rr];
+            for (int k = ce[2]; k < ce[3]; ++k) v -= xin[aux[k] + rr];
+            xin[ce[1] + rr] = v;
+          }
+        } else {
+          for (int q = c0 * bs + threadIdx.x; q < c1 * bs; q += NT) {
+            const int c = q / bs, rr = q - c * bs;
+            xin[cells[2 * c + 1] + rr] = -xin[cells[2 * c] + rr];
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      __syncthreads();  // the up-front loads of the top level
+    }
+    for (int it = i0 + warp; it < i1; it += NT / 32) {
+      const int* e = items + 9 * it;
+      const int rows = e[2] & 63, dense = e[2] >> 30;
+      int lg = 2;
+      while (2 * lg < rows) lg <<= 1;
+      const double2 v = tile_dot_g<EF>(pan + e[0], rows, e[3], e[1], xin + e[4], lg);
+      const int l2 = lane & (lg - 1);
+      if (lane < lg && 2 * l2 < rows) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = 2 * l2 + h;
+          if (row >= rows) break;
+          const double val = h ? v.y : v.x;
+          if (!FWD) {
+            a.z[e[6] + row] = val;
+            xin[e[8] + row] = val;
+          } else if (row < e[5]) {
+            (dense ? a.z : a.yf)[e[6] + row] = val;
+          } else {
+            a.ubuf[e[7] + row] = val;
+            xin[e[8] + row] = val;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tr && l == 0 && threadIdx.x == 0) tr[5] = gtimer();
+    c0 = c1;
+    i0 = i1;
+  }
+  if (threadIdx.x == 0) {
+    if (tr) tr[2] = gtimer();
+    if (FWD)
+      for (int k = 0; k < U.tile_ctr; ++k) {
+        const int2 r = a.broots[U.part_base + k];
+        red_release_add(a.flags + r.x, r.y);
+      }
+    if (tr) tr[3] = gtimer();
+  }
+}
+
 template <bool EF, int NT>
 __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
   pdl_wait();
@@ -486,8 +670,14 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
     __syncthreads();
     const int tk = s.tk;
     if (tk >= a.n_units) break;
-    if (s.u.dir == 0) run_unit<true, EF, NT>(a, s, xin, part, tk);
-    else run_unit<false, EF, NT>(a, s, xin, part, tk);
+    if (s.u.nchunk == 0) {
+      if (s.u.dir == 0) run_bundle<true, EF, NT>(a, s, xin, tk);
+      else run_bundle<false, EF, NT>(a, s, xin, tk);
+    } else if (s.u.dir == 0) {
+      run_unit<true, EF, NT>(a, s, xin, part, tk);
+    } else {
+      run_unit<false, EF, NT>(a, s, xin, part, tk);
+    }
     __syncthreads();
   }
   // the last CTA of this sweep resets the tickets and advances the epoch

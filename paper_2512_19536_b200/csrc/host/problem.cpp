@@ -546,6 +546,30 @@ static void factor_units(Problem& pr, const Placement& pl) {
       pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(&uf - factors.data()) * b);
   pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
   factors.clear();
+  if (std::getenv("PDG_SETUP_TIMES")) {
+    std::int64_t bt = 0, bb = 0, mx = 0, lev = 0;
+    for (const Bundle& B : pr.bundles) {
+      bt += B.n_task;
+      bb += B.bytes[0] + B.bytes[1];
+      mx = std::max<std::int64_t>(mx, B.xneed);
+      lev += B.nlev;
+    }
+    int small16 = 0, small48 = 0, reg = 0;
+    for (const TaskDesc& t : pr.tasks) {
+      if (t.bundle >= 0) continue;
+      ++reg;
+      const std::int64_t fb = 8LL * t.w * (t.w + t.nr);
+      small16 += fb < 16384;
+      small48 += fb < 49152;
+    }
+    std::fprintf(stderr, "[pdg] unbundled tasks %d, of which %d under 16 KB and %d under 48 KB\n", reg, small16, small48);
+    std::fprintf(stderr,
+                 "[pdg] sweep tasks %zu, bundles %zu holding %lld tasks (%.2f GB of %.2f GB panels, "
+                 "%.1f levels each, x <= %lld)\n",
+                 pr.tasks.size(), pr.bundles.size(), static_cast<long long>(bt), bb / 1e9,
+                 8.0 * (pr.fmat_len + pr.hmat_len) / 1e9, pr.bundles.empty() ? 0.0 : double(lev) / pr.bundles.size(),
+                 static_cast<long long>(mx));
+  }
 
 }
 

@@ -47,6 +47,33 @@ struct TaskDesc {
   // forward and backward solves collapse into one level of the sweep
   int root_dense = 0;
   std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
+  int bundle = -1;     // >= 0: solved inside subtree bundle Problem::bundles[bundle] (host/pack.cpp)
+};
+
+// A descendant-closed set of small supernodes of one subdomain (whole subtrees
+// of the elimination tree) that ONE CTA solves as one sweep unit per
+// direction, level by level with CTA barriers only (cuda/sweep.cu run_bundle).
+// Its panels are contiguous (forward: leaves first; backward: top level
+// first). The CTA keeps the bundle's vectors in shared memory (xneed doubles;
+// forward [t_S of every member][u_S of every member], backward [[y_S ; -x_R]
+// of every member][x_S of every member]) and everything it needs to know is
+// one block of ints in bmeta (16-byte aligned):
+//   [nlev, ncell, nitem, naux] , nlev x {cell_end, item_end} ,
+//   cells, forward {dof, xoff, in0, in1}: t = r[dof..] minus aux[in0..in1) (shared u_D slices),
+//          backward {src, xoff}: x_R rows owned by members, copied from their x_S ,
+//   aux, forward: the incoming-update lists; backward {src, xoff} pairs known at
+//        the start: y_S (src >= 0) and -x_R rows from outside (z at -1-src) ,
+//   items (one 32-row tile each): {panel offset - src_off, ncol, rows | dense_root << 30, stride,
+//                                  xoff, wsplit, dst_a, dst_b, shared dst}.
+constexpr int kBundleMetaInts = 2560;   // shared-memory block of the sweep CTA (cuda/sweep.cu)
+constexpr int kBundleDefaultKB = 96;    // PDG_BUNDLE_KB
+struct Bundle {
+  std::int64_t src_off[2] = {0, 0};  // first panel double (F, H)
+  int bytes[2] = {0, 0};
+  int meta_off[2] = {0, 0}, meta_n[2] = {0, 0};
+  int nlev = 0, xneed = 0, n_task = 0;
+  int root_off = 0, n_root = 0;      // bundle_roots: the subtree roots (task ids)
+  int par_off = 0, n_par = 0;        // bundle_parents: their distinct parents (task ids)
 };
 
 struct Problem {
@@ -70,6 +97,8 @@ struct Problem {
   // Schwarz local solves
   std::vector<TaskDesc> tasks;
   std::vector<int> task_child, fwd_order, bwd_order;
+  std::vector<Bundle> bundles;
+  std::vector<int> bmeta, bundle_roots, bundle_parents;
   // Row-tiled dense panels: tile t covers output rows [32k, 32k+rows) of its
   // task; element (row r0+l, input col0+j) at mat[off + j*stride + l]. The
   // panels themselves are formed on the device (cuda/panels.cu) from the
