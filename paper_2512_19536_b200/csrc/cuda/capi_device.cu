@@ -298,6 +298,10 @@ int DeviceSim::trace_sweep(long long* out, int cap) {
     o[9] = h_units[u].nchunk;
     o[10] = P->tasks[h_units[u].task].height;
     o[11] = P->tasks[h_units[u].task].coarse;
+    if (h_units[u].nchunk == 0) {  // level chunk: first tile's round trip (ns) and tile count
+      o[10] = tr[8 * u + 6];
+      o[11] = tr[8 * u + 7];
+    }
   }
   return nu;
 }

@@ -33,12 +33,12 @@ struct DevTask {
 // chunk [c0, c1) of a single wide tile (nchunk > 1) whose partial sums land in
 // part slot part_base + chunk; the last chunk to finish (tile counter) reduces
 // them in chunk order.
-// A third kind, nchunk == 0: a subtree bundle (host/problem.hpp Bundle),
-// tile_begin = bundle id, src_off / bytes = its contiguous panels in this
-// direction, [in_e0, in_e0 + in_n) = its record in bmeta, part_base / tile_ctr
-// = first entry / count of its forward publish list, c0 / c1 = first entry /
-// count of its backward wait list, own_fwd / own_need = the forward counter
-// that proves the bundle's own forward pass is complete.
+// A third kind, nchunk == 0: a level chunk of bottom supernodes
+// (host/problem.hpp LevelChunk), tile_begin = chunk id, src_off / bytes = its
+// contiguous panels, [in_e0, in_e0 + in_n) = its record in bmeta, dep[0] /
+// need[0] = the level counter it waits for (n_dep), chunk = the level counter
+// it adds to, part_base / tile_ctr = first entry / count of its forward
+// publish list, c0 / c1 = first entry / count of its backward wait list.
 struct DevUnit {
   int task, tile_begin, tile_end, c0, c1, chunk, nchunk, part_base, tile_ctr, dir;
   int n_dep;          // flags to wait on (> 2: walk the task's children)

@@ -109,7 +109,7 @@ struct SweepArgs {
   double* yc;
   const double* r0part;   // non-null: the coarse forward sums r0 from the restriction chunks
   const int* node_chunk_ptr;
-  // subtree bundles (host/problem.hpp Bundle): records, forward publish list
+  // level chunks of the bottom supernodes (host/problem.hpp LevelChunk): records, forward publish list
   // {root task, its forward tiles}, backward wait list {counter, count}
   const int* bmeta;
   const int2* broots;

@@ -328,15 +328,13 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   // cost model of the simulated schedule (ns); calibrating it to the traced
   // unit times (7 us fixed, 10 GB/s per CTA) changed nothing measurable
   // (profiles/r02l sched_*)
-  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0, kLevel = 1500.0;
-  // schedule nodes: an unbundled task is its own node, a subtree bundle is
-  // one node whose parents are the distinct parents of its roots
-  const int nt = static_cast<int>(pr.tasks.size()), nb = static_cast<int>(pr.bundles.size());
-  const int nn = nt + nb, nu = static_cast<int>(units.size());
-  auto node_of_unit = [&](const DevUnit& u) { return u.nchunk == 0 ? nt + u.tile_begin : u.task; };
-  auto cost = [&](const DevUnit& u) {
-    return kFixed + kPerByte * u.bytes + (u.nchunk == 0 ? kLevel * pr.bundles[u.tile_begin].nlev : 0.0);
-  };
+  constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;
+  // only the individually scheduled supernodes take part: the bottom levels
+  // (TaskDesc::bundle >= 0) run before (forward) and after (backward) them
+  const int nt = static_cast<int>(pr.tasks.size());
+  const int nn = nt, nu = static_cast<int>(units.size());
+  auto node_of_unit = [&](const DevUnit& u) { return u.task; };
+  auto cost = [&](const DevUnit& u) { return kFixed + kPerByte * u.bytes; };
   std::vector<std::vector<int>> pars(nn), kids(nn);
   std::vector<char> dense_root(nn, 0);
   for (int s = 0; s < nt; ++s) {
@@ -346,14 +344,6 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
     if (t.parent >= 0) {
       pars[s].push_back(t.parent);
       kids[t.parent].push_back(s);
-    }
-  }
-  for (int b = 0; b < nb; ++b) {
-    const Bundle& B = pr.bundles[b];
-    for (int k = 0; k < B.n_par; ++k) {
-      const int p = pr.bundle_parents[B.par_off + k];
-      pars[nt + b].push_back(p);
-      kids[p].push_back(nt + b);
     }
   }
   std::vector<double> cmax_f(nn, 0.0), cmax_b(nn, 0.0);
@@ -370,11 +360,10 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
       units_b[n].push_back(i);
     }
   }
-  // longest remaining path (bottom level) per node and direction; bundles
-  // have no children, and children precede parents in task order
+  // longest remaining path (bottom level) per node and direction; children
+  // precede parents in task order
   std::vector<int> topo;
   topo.reserve(nn);
-  for (int b = 0; b < nb; ++b) topo.push_back(nt + b);
   for (int s = 0; s < nt; ++s)
     if (pr.tasks[s].bundle < 0) topo.push_back(s);
   std::vector<double> Lb(nn, 0.0), Lf(nn, 0.0);
@@ -567,7 +556,7 @@ void DeviceSim::upload_tasks() {
   auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units) {
     for (int tk : order) {
       const TaskDesc& s = pr.tasks[tk];
-      if (s.bundle >= 0) continue;  // solved inside its subtree bundle (below)
+      if (s.bundle >= 0) continue;  // a bottom-level supernode: solved in level chunks (below)
       const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
       auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };
@@ -649,44 +638,61 @@ void DeviceSim::upload_tasks() {
   std::vector<DevUnit> fu, bu;
   make_units(fo, true, fu);
   make_units(bo, false, bu);
-  // subtree bundles: one unit per direction (sweep.cu run_bundle). Forward
-  // publish list {root, its forward tiles}; backward wait list = the roots'
-  // distinct parents (their backward tiles, or a dense root's forward ones).
+  // bottom levels: one unit per level chunk (sweep.cu run_chunk). A level
+  // waits for the previous one through one counter per level and direction
+  // (after the task counters in d_flags); forward chunks also publish the
+  // counters of their supernodes that have an individually scheduled parent,
+  // backward chunks wait for the distinct such parents (their backward tiles,
+  // or a dense root's forward ones). The first backward level waits for the
+  // last forward one (a whole tree inside the bottom levels has no such parent).
   std::vector<int2> broots, bdeps;
-  for (std::size_t b = 0; b < pr.bundles.size(); ++b) {
-    const Bundle& B = pr.bundles[b];
-    const int root0 = pr.bundle_roots[B.root_off];
-    for (int dir = 0; dir < 2; ++dir) {
-      DevUnit u{};
-      u.task = root0;
-      u.tile_begin = static_cast<int>(b);
-      u.nchunk = 0;
-      u.dir = dir;
-      u.src_off = B.src_off[dir];
-      u.bytes = B.bytes[dir];
-      u.in_e0 = B.meta_off[dir];
-      u.in_n = B.meta_n[dir];
-      u.own_fwd = dir ? root0 : -1;
-      u.own_need = dir ? pr.tasks[root0].f_ntile : 0;
-      if (dir == 0) {
-        u.part_base = static_cast<int>(broots.size());
-        u.tile_ctr = B.n_root;
-        for (int k = 0; k < B.n_root; ++k) {
-          const int r = pr.bundle_roots[B.root_off + k];
-          broots.push_back(make_int2(r, pr.tasks[r].f_ntile));
-        }
-      } else {
-        u.c0 = static_cast<int>(bdeps.size());
-        u.c1 = B.n_par;
-        for (int k = 0; k < B.n_par; ++k) {
-          const int p = pr.bundle_parents[B.par_off + k];
-          const TaskDesc& ps = pr.tasks[p];
-          bdeps.push_back(ps.root_dense ? make_int2(p, ps.f_ntile) : make_int2(nt_flag + p, ps.h_ntile));
-        }
+  std::vector<DevUnit> cfu, cbu;
+  const int nlev = pr.n_bottom_levels;
+  const int lev_flag0 = 2 * nt_flag;
+  for (std::size_t ci = 0; ci < pr.chunks.size(); ++ci) {
+    const LevelChunk& C = pr.chunks[ci];
+    DevUnit u{};
+    u.task = C.first_task;
+    u.tile_begin = static_cast<int>(ci);
+    u.nchunk = 0;
+    u.dir = C.dir;
+    u.src_off = C.src_off;
+    u.bytes = C.bytes;
+    u.in_e0 = C.meta_off;
+    u.in_n = C.meta_n;
+    u.own_fwd = -1;
+    u.chunk = lev_flag0 + C.dir * nlev + C.level;  // the counter this chunk adds to
+    if (C.dir == 0) {
+      if (C.level > 0) {
+        u.n_dep = 1;
+        u.dep[0] = lev_flag0 + C.level - 1;
+        u.need[0] = pr.level_chunks[0][C.level - 1];
       }
-      max_in = std::max<long long>(max_in, B.xneed);
-      (dir ? bu : fu).push_back(u);
+      u.part_base = static_cast<int>(broots.size());
+      u.tile_ctr = C.n_root;
+      for (int k = 0; k < C.n_root; ++k) {
+        const int r = pr.chunk_roots[C.root_off + k];
+        broots.push_back(make_int2(r, pr.tasks[r].f_ntile));
+      }
+    } else {
+      u.n_dep = 1;
+      if (C.level < nlev - 1) {
+        u.dep[0] = lev_flag0 + nlev + C.level + 1;
+        u.need[0] = pr.level_chunks[1][C.level + 1];
+      } else {
+        u.dep[0] = lev_flag0 + nlev - 1;
+        u.need[0] = pr.level_chunks[0][nlev - 1];
+      }
+      u.c0 = static_cast<int>(bdeps.size());
+      u.c1 = C.n_par;
+      for (int k = 0; k < C.n_par; ++k) {
+        const int p = pr.chunk_parents[C.par_off + k];
+        const TaskDesc& ps = pr.tasks[p];
+        bdeps.push_back(ps.root_dense ? make_int2(p, ps.f_ntile) : make_int2(nt_flag + p, ps.h_ntile));
+      }
     }
+    max_in = std::max<long long>(max_in, C.xneed);
+    (C.dir ? cbu : cfu).push_back(u);
   }
   d_bmeta = dupload(pr.bmeta, st);
   d_broots = dupload(broots, st);
@@ -712,9 +718,15 @@ void DeviceSim::upload_tasks() {
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const std::vector<int> perm = list_schedule(pr, fu, sms * sweep_ctas_per_sm(smem_fwd, sweep_threads));
-    std::vector<DevUnit> o(fu.size());
-    for (std::size_t i = 0; i < perm.size(); ++i) o[i] = fu[perm[i]];
+    // tickets: forward bottom levels, the scheduled supernodes, backward bottom levels
+    std::vector<DevUnit> o;
+    o.reserve(fu.size() + cfu.size() + cbu.size());
+    o.insert(o.end(), cfu.begin(), cfu.end());
+    for (std::size_t i = 0; i < perm.size(); ++i) o.push_back(fu[perm[i]]);
+    o.insert(o.end(), cbu.begin(), cbu.end());
     fu.swap(o);
+    n_units_f += static_cast<int>(cfu.size());
+    n_units_b += static_cast<int>(cbu.size());
   }
   h_units = fu;
   d_fwd_units = dupload(fu, st);
@@ -741,8 +753,10 @@ void DeviceSim::upload_tasks() {
   d_in_idx = dupload(ii, st);
   d_ubuf = dalloc<double>(std::max<std::int64_t>(pr.ubuf_size, 1));
   d_yfwd = dalloc<double>(n + static_cast<std::size_t>(pr.two_level ? pr.n_agg * pr.bq : 0));
-  d_flags = dalloc<int>(2 * std::max(n_tasks, 1));
-  PDG_CUDA(cudaMemsetAsync(d_flags, 0, 2 * std::max(n_tasks, 1) * sizeof(int), st));
+  // tile counters per task and direction, then one counter per bottom level and direction
+  const std::size_t n_flags = 2 * static_cast<std::size_t>(std::max(n_tasks, 1)) + 2 * pr.n_bottom_levels;
+  d_flags = dalloc<int>(n_flags);
+  PDG_CUDA(cudaMemsetAsync(d_flags, 0, n_flags * sizeof(int), st));
   // [0] next ticket, [1] sweep number, [2] CTAs finished (sweep.cu)
   d_ticket = dalloc<unsigned int>(4);
   PDG_CUDA(cudaMemsetAsync(d_ticket, 0, 4 * sizeof(unsigned int), st));
@@ -841,6 +855,10 @@ SweepArgs DeviceSim::sweep_args(bool, const double* r, double* z, const PcgScala
   a.xcap = sweep_xcap;
   a.live = d_live;
   a.trace = d_trace;
+  // diagnostics for traced sweeps only (results become wrong): bit 4 = level
+  // chunks skip their scattered gather loads, bit 5 = skip their stores
+  if (d_trace)
+    if (const char* dbg = std::getenv("PDG_CHUNK_DEBUG")) a.prefetch |= std::atoi(dbg) << 4;
   return a;
 }
 

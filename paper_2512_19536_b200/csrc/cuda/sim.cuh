@@ -78,7 +78,7 @@ class DeviceSim {
   // sweep
   DevTask* d_tasks = nullptr;
   int *d_nunit = nullptr, *d_task_child = nullptr, *d_in_ptr = nullptr;
-  int* d_bmeta = nullptr;                       // subtree bundle records (host/problem.hpp Bundle)
+  int* d_bmeta = nullptr;                       // level chunk records (host/problem.hpp LevelChunk)
   int2 *d_broots = nullptr, *d_bdeps = nullptr;  // their forward publish / backward wait lists
   DevUnit *d_fwd_units = nullptr, *d_bwd_units = nullptr;
   int n_units_f = 0, n_units_b = 0, n_tile_ctrs = 0;

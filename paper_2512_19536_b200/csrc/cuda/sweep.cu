@@ -44,7 +44,8 @@
 #ifdef PDG_SWEEP_MINB
 #define PDG_SWEEP_BOUNDS __launch_bounds__(NT, PDG_SWEEP_MINB)
 #else
-#define PDG_SWEEP_BOUNDS __launch_bounds__(NT)
+// 1024 resident threads per SM (8 CTAs of 128 or 16 of 64): at most 64 registers
+#define PDG_SWEEP_BOUNDS __launch_bounds__(NT, 1024 / NT)
 #endif
 static_assert(PDG_DOT_DEPTH % 4 == 0, "tile_dot consumes loads four at a time");
 
@@ -64,6 +65,9 @@ __device__ __forceinline__ int ld_relaxed_s(const int* p) {
 }
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_add(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ int atom_acq_rel_add(int* p, int v) {
   int old;
@@ -128,10 +132,11 @@ struct UnitSmem {
       int iptr[kMetaCells];
       long long idx[kMetaIdx];
     };
-    alignas(16) int blob[kBundleMetaInts];  // a subtree bundle's record (host/problem.hpp Bundle)
+    alignas(16) int blob[kChunkMetaInts];  // a level chunk's record (host/problem.hpp LevelChunk)
   };
   Ahead q[kAhead];
   int qh;
+  int seen_level;  // level chunks: the last level counter this CTA waited for (this sweep)
 };
 
 // takes the next ticket into lookahead slot `q`: descriptor, task record, and
@@ -142,7 +147,7 @@ __device__ __forceinline__ void fetch_ahead(const SweepArgs& a, Ahead& q) {
   if (tk < a.n_units) {
     q.u = a.units[tk];
     q.t = a.tasks[q.u.task];
-    // a bundle's record is the first thing its CTA needs: bring it to L2 now
+    // a level chunk's record is the first thing its CTA needs: bring it to L2 now
     if (q.u.nchunk == 0)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.bmeta + q.u.in_e0), "r"(q.u.in_n * 4)
                    : "memory");
@@ -203,51 +208,84 @@ __device__ __forceinline__ double2 tile_dot(const double* m, const DevTile& tl, 
   return make_double2(vx, vy);
 }
 
-// one warp, narrow or short tiles of a subtree bundle: the lanes form G =
-// 32 / lg column groups of lg = 2..16 row pairs (lg = the power of two >= the
-// tile's row pairs), so a 10-row tile still keeps 20 lanes loading; group sums
-// are added in a fixed shuffle order. (row 2*l2, row 2*l2+1) sums in lanes < lg.
+// level chunks: one panel column entry per lane (row), read-only path with the
+// same evict-first policy as the tiled panel loads
 template <bool EF>
-__device__ __forceinline__ double2 tile_dot_g(const double* m, int rows, int stride, int ncol, const double* x,
-                                              int lg) {
-  unsigned long long pol = 0;
-  if (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+__device__ __forceinline__ double ld_col(const double* p, unsigned long long pol) {
+  if (!EF) return __ldg(p);
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// one warp, one tile of a level chunk (rows R <= 32, ncol a multiple of the
+// block size BS), one row per lane. Tall tiles (R > 16): one column per load
+// instruction, BS columns in flight, no predicates. Short tiles: the lanes form
+// G = 32 / R column groups, G columns per load instruction, sixteen in flight;
+// the group sums are added in group order. Row r's sum in lane r < R.
+template <int BS, bool EF>
+__device__ __forceinline__ double tile_rows(const double* m, int R, int stride, int ncol, const double* x,
+                                            unsigned long long pol) {
   const int lane = threadIdx.x & 31;
-  const int G = 32 / lg, l2 = lane & (lg - 1), grp = lane / lg;
-  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
-  if (2 * l2 < rows) {
-    const double2* mm = reinterpret_cast<const double2*>(m) + l2;
-    const long long cs = stride >> 1;
-    constexpr int D = PDG_DOT_DEPTH;
-    for (int j = grp; j < ncol; j += D * G) {
-      double2 v[D];
-      double xv[D];
+  double acc0 = 0.0, acc1 = 0.0;
+  if (R > 16) {
+    if (lane < R) {
+      const double* p = m + lane;
+      for (int j = 0; j < ncol; j += BS) {
+        double v[BS];
 #pragma unroll
-      for (int u = 0; u < D; ++u) {
-        const int jj = j + u * G;
-        const bool on = jj < ncol;
-        v[u] = on ? ld_panel<EF>(mm + jj * cs, pol) : make_double2(0.0, 0.0);
-        xv[u] = on ? x[jj] : 0.0;
-      }
+        for (int u = 0; u < BS; ++u) v[u] = ld_col<EF>(p + static_cast<long long>(j + u) * stride, pol);
 #pragma unroll
-      for (int u = 0; u < D; u += 4) {
-        acc0.x = fma(v[u].x, xv[u], acc0.x);
-        acc0.y = fma(v[u].y, xv[u], acc0.y);
-        acc1.x = fma(v[u + 1].x, xv[u + 1], acc1.x);
-        acc1.y = fma(v[u + 1].y, xv[u + 1], acc1.y);
-        acc2.x = fma(v[u + 2].x, xv[u + 2], acc2.x);
-        acc2.y = fma(v[u + 2].y, xv[u + 2], acc2.y);
-        acc3.x = fma(v[u + 3].x, xv[u + 3], acc3.x);
-        acc3.y = fma(v[u + 3].y, xv[u + 3], acc3.y);
+        for (int u = 0; u < BS; ++u) {
+          if (u & 1) acc1 = fma(v[u], x[j + u], acc1);
+          else acc0 = fma(v[u], x[j + u], acc0);
+        }
       }
     }
+    return acc0 + acc1;
   }
-  double vx = (acc0.x + acc1.x) + (acc2.x + acc3.x), vy = (acc0.y + acc1.y) + (acc2.y + acc3.y);
-  for (int off = 16; off >= lg; off >>= 1) {
-    vx += __shfl_down_sync(0xffffffffu, vx, off);
-    vy += __shfl_down_sync(0xffffffffu, vy, off);
+  const int G = 32 / R, g = lane / R, r = lane - g * R;
+  if (g < G) {
+    const double* p = m + r;
+    constexpr int D = 16;
+    for (int j = g; j < ncol; j += D * G) {
+      double v[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        v[u] = 0.0;
+        if (j + u * G < ncol) v[u] = ld_col<EF>(p + static_cast<long long>(j + u * G) * stride, pol);
+      }
+#pragma unroll
+      for (int u = 0; u < D; ++u)
+        if (j + u * G < ncol) {
+          if (u & 1) acc1 = fma(v[u], x[j + u * G], acc1);
+          else acc0 = fma(v[u], x[j + u * G], acc0);
+        }
+    }
   }
-  return make_double2(vx, vy);
+  const double acc = acc0 + acc1;
+  double sum = acc;
+  for (int k = 1; k < G; ++k) sum += __shfl_sync(0xffffffffu, acc, (lane + k * R) & 31);
+  return sum;
+}
+
+// the tiles of a level chunk over the CTA's warps
+template <int BS, bool FWD, bool EF, int NT>
+__device__ __forceinline__ void chunk_tiles(const SweepArgs& a, const int* items, int nitem, const double* pan,
+                                            const double* xin) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long pol = 0;
+  if (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  for (int it = warp; it < nitem; it += NT / 32) {
+    const int4 e0 = *reinterpret_cast<const int4*>(items + 8 * it);
+    const int4 e1 = *reinterpret_cast<const int4*>(items + 8 * it + 4);
+    const int rows = e0.z & 63;
+    const double val = tile_rows<BS, EF>(pan + e0.x, rows, e0.w, e0.y, xin + e1.x, pol);
+    if (lane < rows && !(a.prefetch & 32)) {
+      if (!FWD) a.z[e1.z + lane] = val;
+      else if (lane < e1.y) ((e0.z >> 30) ? a.z : a.yf)[e1.z + lane] = val;
+      else a.ubuf[e1.w + lane] = val;
+    }
+  }
 }
 
 template <bool FWD>
@@ -502,130 +540,103 @@ __device__ __forceinline__ void run_unit(const SweepArgs& a, UnitSmem& s, double
   if (tr && threadIdx.x == 0) tr[3] = gtimer();
 }
 
-// A subtree bundle (host/problem.hpp Bundle): every supernode of a few whole
-// bottom subtrees, solved by this CTA alone level by level. No counters inside
-// the bundle and no global round trips between its levels: the bundle's vectors
-// live in shared memory. Forward: t_S = r_S for every member is loaded up
-// front; per level the members' incoming updates (shared u_D slices) are
-// subtracted, one barrier, one warp per 32-row tile (y_S to global, u_S to
-// global and shared), one barrier. Backward: y_S and the rows owned by outside
-// ancestors are loaded up front; per level the rows owned by members are copied
-// from their shared x_S. The forward pass has no dependencies and publishes the
-// subtree roots' counters at the end; the backward pass waits for the roots'
-// parents and for the bundle's own forward pass.
+// A level chunk (host/problem.hpp LevelChunk): some bottom-level supernodes of
+// one tree height, all independent of each other. The CTA gathers the inputs
+// of all of them into shared memory (forward: r_S minus the descendants'
+// updates; backward: [y_S ; -x_R]), one barrier, then one warp per 32-row
+// tile (tile_rows). A forward chunk waits for the previous level's counter,
+// adds to its own level's, and publishes the task counters of its supernodes
+// whose parent is scheduled individually; a backward chunk waits for the level
+// above (the top level: for the last forward level) and for those parents.
 template <bool FWD, bool EF, int NT>
-__device__ __forceinline__ void run_bundle(const SweepArgs& a, UnitSmem& s, double* xin, int tk) {
+__device__ __forceinline__ void run_chunk(const SweepArgs& a, UnitSmem& s, double* xin, int tk) {
   long long* tr = a.trace ? a.trace + 8LL * tk : nullptr;
   const int ep = s.ep;
   const DevUnit& U = s.u;
-  if (threadIdx.x == 0) {
-    if (tr) tr[0] = gtimer();
-    if (!FWD) {
-      for (int d = 0; d < U.c1; ++d) {
+  if (threadIdx.x < 32) {
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
+    if (threadIdx.x == 1) {
+      const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
+      Ahead& q = s.q[target];
+      if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
+      else q.tk = a.n_units;
+    }
+    // the level counter this CTA already saw complete needs no second acquire
+    if (threadIdx.x == 0 && U.n_dep && s.seen_level != U.dep[0]) {
+      wait_count(a.flags + U.dep[0], (ep + 1) * U.need[0]);
+      s.seen_level = U.dep[0];
+    }
+    if (!FWD)
+      for (int d = threadIdx.x; d < U.c1; d += 32) {
         const int2 w = a.bdeps[U.c0 + d];
         wait_count(a.flags + w.x, (ep + 1) * w.y);
       }
-      wait_count(a.flags + U.own_fwd, (ep + 1) * U.own_need);
-    }
-    if (tr) tr[1] = gtimer();
-  } else if (threadIdx.x == 1) {
-    const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
-    Ahead& q = s.q[target];
-    if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
-    else q.tk = a.n_units;
-  } else if (threadIdx.x >= 32) {
+    __syncwarp();
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+  } else {
     const int t = threadIdx.x - 32;
     if (t == 0 && (a.prefetch & 1)) prefetch_panel(a, U);
     const int4* src = reinterpret_cast<const int4*>(a.bmeta + U.in_e0);
     int4* dst = reinterpret_cast<int4*>(s.blob);
     for (int i = t; i < (U.in_n >> 2); i += NT - 32) dst[i] = __ldg(src + i);
+    if (tr && t == 0) tr[4] = gtimer();
   }
   __syncthreads();
-  if (tr && threadIdx.x == 0) tr[4] = gtimer();
-  const int nlev = s.blob[0], ncell = s.blob[1], naux = s.blob[3];
-  const int* lev = s.blob + 4;
-  const int* cells = lev + 2 * nlev;
+  const int ncell = s.blob[0], nitem = s.blob[1], naux = s.blob[2];
+  const int* cells = s.blob + 4;
   const int* aux = cells + (FWD ? 4 : 2) * ncell;
-  const int* items = aux + (FWD ? naux : 2 * naux);
+  // items start 16-byte aligned (the header, cells and aux are padded by the host)
+  const int* items = aux + ((naux + 3) & ~3);
   const int bs = s.t.bs;
   const double* pan = (FWD ? a.fmat : a.hmat) + U.src_off;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // everything known at the start, in one round of independent loads
   if (FWD) {
     for (int q = threadIdx.x; q < ncell * bs; q += NT) {
-      const int c = q / bs, rr = q - c * bs;
-      xin[cells[4 * c + 1] + rr] = a.r[cells[4 * c] + rr];
+      const int cc = q / bs, rr = q - cc * bs;
+      const int* ce = cells + 4 * cc;
+      double x = a.r[ce[0] + rr];
+      const int ke = ce[3];
+      for (int k = ce[2]; k < ke && !(a.prefetch & 16); k += 4) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = k + u < ke ? __ldcg(a.ubuf + aux[k + u] + rr) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k + u < ke) x -= t[u];
+      }
+      xin[ce[1] + rr] = x;
     }
   } else {
-    for (int q = threadIdx.x; q < naux * bs; q += NT) {
-      const int c = q / bs, rr = q - c * bs;
-      const int src = aux[2 * c];
-      xin[aux[2 * c + 1] + rr] = src >= 0 ? __ldcg(a.yf + src + rr) : -__ldcg(a.z + (-1 - src) + rr);
+    for (int q = threadIdx.x; q < ncell * bs; q += NT) {
+      const int cc = q / bs, rr = q - cc * bs, src = cells[2 * cc];
+      xin[cells[2 * cc + 1] + rr] =
+          (a.prefetch & 16) ? 1.0 : src >= 0 ? __ldcg(a.yf + src + rr) : -__ldcg(a.z + (-1 - src) + rr);
     }
   }
-  int c0 = 0, i0 = 0;
-  for (int l = 0; l < nlev; ++l) {
-    const int c1 = lev[2 * l], i1 = lev[2 * l + 1];
-    if ((FWD && l == 0) || c1 > c0) {
-      if (FWD && l == 0) __syncthreads();  // leaves: inputs are r itself
-      else {
-        if (FWD) {
-          for (int q = c0 * bs + threadIdx.x; q < c1 * bs; q += NT) {
-            const int c = q / bs, rr = q - c * bs;
-            const int* ce = cells + 4 * c;
-            double v = xin[ce[1] + rr];
-            for (int k = ce[2]; k < ce[3]; ++k) v -= xin[aux[k] + rr];
-            xin[ce[1] + rr] = v;
-          }
-        } else {
-          for (int q = c0 * bs + threadIdx.x; q < c1 * bs; q += NT) {
-            const int c = q / bs, rr = q - c * bs;
-            xin[cells[2 * c + 1] + rr] = -xin[cells[2 * c] + rr];
-          }
-        }
-        __syncthreads();
-      }
-    } else {
-      __syncthreads();  // the up-front loads of the top level
-    }
-    for (int it = i0 + warp; it < i1; it += NT / 32) {
-      const int* e = items + 9 * it;
-      const int rows = e[2] & 63, dense = e[2] >> 30;
-      int lg = 2;
-      while (2 * lg < rows) lg <<= 1;
-      const double2 v = tile_dot_g<EF>(pan + e[0], rows, e[3], e[1], xin + e[4], lg);
-      const int l2 = lane & (lg - 1);
-      if (lane < lg && 2 * l2 < rows) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = 2 * l2 + h;
-          if (row >= rows) break;
-          const double val = h ? v.y : v.x;
-          if (!FWD) {
-            a.z[e[6] + row] = val;
-            xin[e[8] + row] = val;
-          } else if (row < e[5]) {
-            (dense ? a.z : a.yf)[e[6] + row] = val;
-          } else {
-            a.ubuf[e[7] + row] = val;
-            xin[e[8] + row] = val;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tr && l == 0 && threadIdx.x == 0) tr[5] = gtimer();
-    c0 = c1;
-    i0 = i1;
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[2] = gtimer();
+  switch (bs) {
+    case 3: chunk_tiles<3, FWD, EF, NT>(a, items, nitem, pan, xin); break;
+    case 6: chunk_tiles<6, FWD, EF, NT>(a, items, nitem, pan, xin); break;
+    case 10: chunk_tiles<10, FWD, EF, NT>(a, items, nitem, pan, xin); break;
+    case 15: chunk_tiles<15, FWD, EF, NT>(a, items, nitem, pan, xin); break;
+    default: chunk_tiles<1, FWD, EF, NT>(a, items, nitem, pan, xin); break;
   }
-  if (threadIdx.x == 0) {
-    if (tr) tr[2] = gtimer();
+  __syncthreads();
+  // publish: one release fence for warp 0 (the barrier ordered the CTA's
+  // stores before it), then relaxed additions spread over its lanes
+  if (threadIdx.x < 32) {
+    if (tr && threadIdx.x == 0) {
+      tr[5] = gtimer();
+      tr[7] = nitem;
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (FWD)
-      for (int k = 0; k < U.tile_ctr; ++k) {
+      for (int k = threadIdx.x; k < U.tile_ctr; k += 32) {
         const int2 r = a.broots[U.part_base + k];
-        red_release_add(a.flags + r.x, r.y);
+        red_relaxed_add(a.flags + r.x, r.y);
       }
-    if (tr) tr[3] = gtimer();
+    if (threadIdx.x == 0) red_relaxed_add(a.flags + U.chunk, 1);
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
   }
 }
 
@@ -648,6 +659,7 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
     }
     s.q[kAhead - 1].tk = a.n_units;
     s.qh = 0;
+    s.seen_level = -1;
   }
   __syncthreads();
   // slot layout: q[qh] running, q[qh+1] next, q[qh+2] fetched during the run
@@ -671,8 +683,8 @@ __global__ void PDG_SWEEP_BOUNDS sweep_kernel(SweepArgs a) {
     const int tk = s.tk;
     if (tk >= a.n_units) break;
     if (s.u.nchunk == 0) {
-      if (s.u.dir == 0) run_bundle<true, EF, NT>(a, s, xin, tk);
-      else run_bundle<false, EF, NT>(a, s, xin, tk);
+      if (s.u.dir == 0) run_chunk<true, EF, NT>(a, s, xin, tk);
+      else run_chunk<false, EF, NT>(a, s, xin, tk);
     } else if (s.u.dir == 0) {
       run_unit<true, EF, NT>(a, s, xin, part, tk);
     } else {

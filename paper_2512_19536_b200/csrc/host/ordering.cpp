@@ -186,6 +186,16 @@ NdTree etree_supernodes(int m, const std::vector<int>& adj_ptr, const std::vecto
   // ---- relaxed amalgamation (children merge into parents, bottom-up) ----
   auto stored = [](std::int64_t w, std::int64_t r) { return w * (w + 1) / 2 + w * r; };
   const double zr = relax_z();
+  // PDG_RELAX_MIN_SUBTREE = T: a child is only merged when its subtree holds
+  // at least T cells. The small bottom subtrees then keep their fundamental
+  // supernodes (no explicit zeros; the sweep solves them in level chunks,
+  // host/pack.cpp) while the supernodes above them are amalgamated as usual.
+  static const int min_subtree = std::getenv("PDG_RELAX_MIN_SUBTREE") ? std::atoi(std::getenv("PDG_RELAX_MIN_SUBTREE")) : 0;
+  std::vector<int> subtree_cells(ns, 0);
+  for (int s = 0; s < ns; ++s) {
+    subtree_cells[s] += static_cast<int>(sn[s].cols.size());
+    if (sn[s].parent >= 0) subtree_cells[sn[s].parent] += subtree_cells[s];
+  }
   for (int p = 0; p < ns; ++p) {
     Node& P = sn[p];
     if (P.kids.empty()) continue;
@@ -199,7 +209,7 @@ NdTree etree_supernodes(int m, const std::vector<int>& adj_ptr, const std::vecto
       const std::int64_t w = static_cast<std::int64_t>(P.cols.size() + Cn.cols.size());
       const std::int64_t st = stored(w, static_cast<std::int64_t>(P.rows.size()));
       const double z = 1.0 - static_cast<double>(P.nz + Cn.nz) / static_cast<double>(st);
-      const bool merge = (w <= relax && z < zr) || z < 0.02;
+      const bool merge = ((w <= relax && z < zr) || z < 0.02) && subtree_cells[c] >= min_subtree;
       if (!merge) {
         new_kids.push_back(c);
         continue;

@@ -20,38 +20,19 @@ namespace pdg {
 
 namespace {
 
-// Per-subtree totals used to decide what fits into one bundle.
-struct BundleAcc {
-  std::int64_t fb = 0, hb = 0;  // panel bytes (F, H)
-  int mf = 4, mb = 4;           // bmeta ints (forward, backward), header included
-  int nt = 0, hmax = 0;
-  int x = 0;                    // shared-memory doubles: sum of 2 w + nr (backward inputs + results)
-  void add(const BundleAcc& o) {
-    fb += o.fb;
-    hb += o.hb;
-    mf += o.mf - 4;
-    mb += o.mb - 4;
-    nt += o.nt;
-    x += o.x;
-    hmax = std::max(hmax, o.hmax);
-  }
-};
-
-struct BundleCaps {
-  std::int64_t bytes;
-  int meta, x, tasks;
-  bool fits(const BundleAcc& a) const {
-    if (a.fb > bytes || a.hb > bytes || a.nt > tasks || a.x > x) return false;
-    return a.mf + 2 * (a.hmax + 1) + 8 <= meta && a.mb + 2 * (a.hmax + 1) + 8 <= meta;
-  }
-};
-
 int env_int(const char* k, int d) {
   const char* e = std::getenv(k);
   return e ? std::atoi(e) : d;
 }
 
+constexpr int kTileAlign = 16;  // panel tiles start 128-byte aligned
+std::int64_t align_tile(std::int64_t off) { return (off + kTileAlign - 1) / kTileAlign * kTileAlign; }
+
 }  // namespace
+
+long long bottom_level_bytes(long long n_global_dofs, int b) {
+  return 1024LL * env_int("PDG_BOTTOM_KB", n_global_dofs >= 2000000 && b >= 10 ? kBottomDefaultKB : 0);
+}
 
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {
   constexpr int kTile = 32;
@@ -60,13 +41,10 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
   // only added bytes once the L2 re-reads were fixed (config4 sweep 6.40 ms
   // at 2 vs 6.51 ms at 8, profiles/r02e).
   static const int kRowAlign = std::getenv("PDG_ROW_ALIGN") ? std::max(2, std::atoi(std::getenv("PDG_ROW_ALIGN"))) : 2;
-  constexpr int kTileAlign = 16;    // 128 bytes
-  // Subtree bundles: bottom subtrees of the elimination tree whose panels
-  // total <= PDG_BUNDLE_KB per direction go to one CTA as one unit (0: off).
-  // Default: only where the sweep is bandwidth bound (>= 2M dofs); smaller
-  // problems have idle CTAs and want every supernode on its own one.
-  const BundleCaps caps{1024LL * env_int("PDG_BUNDLE_KB", 0), kBundleMetaInts,
-                               std::max(64, env_int("PDG_BUNDLE_X", 1536)), std::max(2, env_int("PDG_BUNDLE_TASKS", 64))};
+  // Bottom levels: the supernodes of every subtree whose panels total <=
+  // PDG_BOTTOM_KB per direction are not scheduled one by one; they are solved
+  // level by level in chunks (finish_bottom_levels below). 0: off.
+  const std::int64_t bottom_bytes = bottom_level_bytes(pr.n_global_dofs(), pr.b);
   const int bs = F.bs;
   const int base = static_cast<int>(pr.tasks.size());
   const int nsn = static_cast<int>(F.sn.size());
@@ -80,14 +58,33 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     if (F.sn[s].parent >= 0) depth[s] = depth[F.sn[s].parent] + 1;
 
   auto seg = [&](int rows) { return (rows + kRowAlign - 1) / kRowAlign * kRowAlign; };
-  auto align = [](std::int64_t off) { return (off + kTileAlign - 1) / kTileAlign * kTileAlign; };
-  auto tile_len = [&](const Problem::Tile& t) { return align(static_cast<std::int64_t>(t.ncol) * t.stride); };
+  auto align = [](std::int64_t off) { return align_tile(off); };
+
+  // ---- bottom levels: whole subtrees under the byte cap, at most
+  // PDG_BOTTOM_LEVELS high, supernodes at most 32 columns wide ----
+  std::vector<char> bottom(nsn, 0);
+  if (!coarse && bottom_bytes > 0 && pr.n_global_dofs() < (1LL << 30)) {  // chunk records hold int offsets
+    const int max_levels = std::max(1, env_int("PDG_BOTTOM_LEVELS", kBottomDefaultLevels));
+    std::vector<std::int64_t> fb(nsn, 0);
+    for (int s = 0; s < nsn; ++s) {
+      const Supernode& S = F.sn[s];
+      const int w = S.w(bs), h = w + static_cast<int>(S.rows.size()) * bs;
+      for (int r0 = 0; r0 < h; r0 += kTile) fb[s] += 8 * align(static_cast<std::int64_t>(w) * seg(std::min(kTile, h - r0)));
+      bool ok = w <= 32 && height[s] < max_levels;
+      for (int c : kids[s]) {
+        ok = ok && bottom[c];
+        fb[s] += fb[c];
+      }
+      bottom[s] = ok && fb[s] <= bottom_bytes;
+    }
+  }
 
   std::vector<int> slot(nsn);
   for (int s = 0; s < nsn; ++s) {
     const Supernode& S = F.sn[s];
     const int w = S.w(bs), nr = static_cast<int>(S.rows.size()) * bs, h = w + nr;
     TaskDesc t;
+    t.bundle = bottom[s] ? 0 : -1;
     t.coarse = coarse;
     t.bs = bs;
     t.w = w;
@@ -143,13 +140,10 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
   }
   // incoming lists: (S, cell) <- ubuf slices of descendants D, in D order
   std::vector<std::vector<std::int64_t>> inc(F.m);
-  std::vector<std::vector<int>> inc_d(F.m);  // the descendant behind each entry
   for (int d = 0; d < nsn; ++d) {
     const Supernode& D = F.sn[d];
-    for (std::size_t k = 0; k < D.rows.size(); ++k) {
+    for (std::size_t k = 0; k < D.rows.size(); ++k)
       inc[D.rows[k]].push_back(pr.tasks[base + d].ubuf_off + static_cast<std::int64_t>(k) * bs);
-      inc_d[D.rows[k]].push_back(d);
-    }
   }
   for (int s = 0; s < nsn; ++s) {
     const Supernode& S = F.sn[s];
@@ -161,245 +155,191 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     }
   }
 
-  // ---- subtree bundles ----
-  // Bottom-up: a supernode "fits" when its whole subtree stays under the caps;
-  // the maximal fitting subtrees, taken in postorder, are packed greedily into
-  // bundles (neighbours in postorder are neighbours in the tree). Offsets into
-  // dof / ubuf vectors are kept as ints in the bundle records.
-  std::vector<std::vector<int>> groups;
-  const bool int_ok = pr.ubuf_size < (1LL << 31) - (1 << 20) && dof_base + static_cast<std::int64_t>(F.m) * bs < (1LL << 31) - 1;
-  if (!coarse && caps.bytes > 0 && nsn >= 2 && int_ok) {
-    std::vector<BundleAcc> acc(nsn);
-    std::vector<char> fit(nsn, 1);
-    auto own = [&](int s) {
-      const TaskDesc& t = pr.tasks[base + s];
-      BundleAcc a;
-      for (int k = 0; k < t.f_ntile; ++k) a.fb += 8 * tile_len(pr.ftiles[t.f_tile0 + k]);
-      for (int k = 0; k < t.h_ntile; ++k) a.hb += 8 * tile_len(pr.htiles[t.h_tile0 + k]);
-      const Supernode& S = F.sn[s];
-      int nin = 0;
-      for (int cc = S.s0; cc < S.s1; ++cc) nin += static_cast<int>(inc[cc].size());
-      a.mf += 4 * (S.s1 - S.s0) + nin + 9 * t.f_ntile;
-      a.mb += t.h_ntile ? 2 * ((t.w + t.nr) / bs) + 9 * t.h_ntile : 0;
-      a.nt = 1;
-      a.hmax = height[s];
-      a.x = 2 * t.w + t.nr;
-      return a;
-    };
-    for (int s = 0; s < nsn; ++s) {
-      bool ok = true;
-      for (int c : kids[s]) ok = ok && fit[c];
-      if (ok) {
-        BundleAcc a = own(s);
-        for (int c : kids[s]) a.add(acc[c]);
-        ok = caps.fits(a);
-        if (ok) acc[s] = std::move(a);
-      }
-      fit[s] = ok;
-      // children's records are only needed while their parent is undecided
-      if (ok)
-        for (int c : kids[s]) acc[c] = BundleAcc{};
-    }
-    BundleAcc cur;
-    std::vector<int> cur_roots;
-    auto flush = [&]() {
-      if (cur.nt >= 2) groups.push_back(cur_roots);
-      cur = BundleAcc{};
-      cur_roots.clear();
-    };
-    for (int s = 0; s < nsn; ++s) {
-      const int p = F.sn[s].parent;
-      if (!fit[s] || (p >= 0 && fit[p])) continue;  // maximal fitting subtrees only
-      BundleAcc tryacc = cur;
-      tryacc.add(acc[s]);
-      if (!cur_roots.empty() && !caps.fits(tryacc)) {
-        flush();
-        tryacc = acc[s];
-      }
-      cur = std::move(tryacc);
-      cur_roots.push_back(s);
-    }
-    flush();
-  }
-  // members of each bundle (subtrees are contiguous in postorder), ordered
-  // by level for the forward pass
-  std::vector<std::vector<int>> members(groups.size());
-  {
-    std::vector<int> first_desc(nsn);
-    for (int s = 0; s < nsn; ++s) {
-      first_desc[s] = s;
-      for (int c : kids[s]) first_desc[s] = std::min(first_desc[s], first_desc[c]);
-    }
-    for (std::size_t g = 0; g < groups.size(); ++g) {
-      for (int r : groups[g])
-        for (int s = first_desc[r]; s <= r; ++s) {
-          members[g].push_back(s);
-          pr.tasks[base + s].bundle = static_cast<int>(pr.bundles.size() + g);
-        }
-      std::stable_sort(members[g].begin(), members[g].end(), [&](int a, int c) { return height[a] < height[c]; });
-    }
-  }
-  // ---- panel offsets: bundles first (each contiguous per direction), then
-  // the remaining supernodes in order ----
-  auto place_f = [&](int s) {
+  // ---- panel offsets of the individually scheduled supernodes (the bottom
+  // levels are laid out level by level in finish_bottom_levels) ----
+  for (int s = 0; s < nsn; ++s) {
     const TaskDesc& t = pr.tasks[base + s];
+    if (t.bundle >= 0) continue;
     for (int k = 0; k < t.f_ntile; ++k) {
       Problem::Tile& tl = pr.ftiles[t.f_tile0 + k];
       pr.fmat_len = align(pr.fmat_len);
       tl.off = pr.fmat_len;
       pr.fmat_len += static_cast<std::int64_t>(tl.ncol) * tl.stride;
     }
-  };
-  auto place_h = [&](int s) {
-    const TaskDesc& t = pr.tasks[base + s];
     for (int k = 0; k < t.h_ntile; ++k) {
       Problem::Tile& tl = pr.htiles[t.h_tile0 + k];
       pr.hmat_len = align(pr.hmat_len);
       tl.off = pr.hmat_len;
       pr.hmat_len += static_cast<std::int64_t>(tl.ncol) * tl.stride;
     }
-  };
-  for (std::size_t g = 0; g < groups.size(); ++g) {
-    const std::vector<int>& mem = members[g];
-    Bundle B;
-    B.n_task = static_cast<int>(mem.size());
-    pr.fmat_len = align(pr.fmat_len);
-    pr.hmat_len = align(pr.hmat_len);
-    B.src_off[0] = pr.fmat_len;
-    B.src_off[1] = pr.hmat_len;
-    for (int s : mem) place_f(s);
-    for (auto it = mem.rbegin(); it != mem.rend(); ++it) place_h(*it);  // top level first
-    B.bytes[0] = static_cast<int>(8 * (align(pr.fmat_len) - B.src_off[0]));
-    B.bytes[1] = static_cast<int>(8 * (align(pr.hmat_len) - B.src_off[1]));
-    B.root_off = static_cast<int>(pr.bundle_roots.size());
-    B.par_off = static_cast<int>(pr.bundle_parents.size());
-    for (int r : groups[g]) {
-      pr.bundle_roots.push_back(base + r);
-      const int p = F.sn[r].parent;
-      if (p >= 0 && std::find(pr.bundle_parents.begin() + B.par_off, pr.bundle_parents.end(), base + p) ==
-                        pr.bundle_parents.end())
-        pr.bundle_parents.push_back(base + p);
-    }
-    B.n_root = static_cast<int>(groups[g].size());
-    B.n_par = static_cast<int>(pr.bundle_parents.size()) - B.par_off;
-    B.nlev = height[mem.back()] + 1;
-    // shared-memory layout of the CTA's vector block (doubles). Forward:
-    // [t_S of every member][u_S of every member]; backward: [[y_S ; -x_R] of
-    // every member with backward tiles][x_S of every member].
-    std::vector<int> vx(nsn, -1), ul(nsn, -1), bin(nsn, -1), xs(nsn, -1);
-    int sw = 0, snr = 0, sh = 0;
-    for (int s : mem) {
-      const TaskDesc& t = pr.tasks[base + s];
-      vx[s] = sw;
-      xs[s] = sw;
-      sw += t.w;
-    }
-    for (int s : mem) {
-      const TaskDesc& t = pr.tasks[base + s];
-      ul[s] = sw + snr;
-      snr += t.nr;
-      if (t.h_ntile) {
-        bin[s] = sh;
-        sh += t.w + t.nr;
-      }
-    }
-    for (int s : mem) xs[s] += sh;
-    B.xneed = std::max(sw + snr, sh + sw);
-    for (int dir = 0; dir < 2; ++dir) {
-      std::vector<int> lev, cells, aux, items;
-      int ncell = 0, nitem = 0;
-      for (int l = 0; l < B.nlev; ++l) {
-        const int hgt = dir == 0 ? l : B.nlev - 1 - l;
-        for (int s : mem) {
-          if (height[s] != hgt) continue;
-          const TaskDesc& t = pr.tasks[base + s];
-          const Supernode& S = F.sn[s];
+  }
+  pr.factor_values = pr.fmat_len + pr.hmat_len;
+}
+
+// The bottom levels of all subdomains as level chunks (problem.hpp LevelChunk):
+// per direction and per height, the bottom supernodes in task order are cut
+// into chunks of <= PDG_CHUNK_KB of panel whose input vectors fit the sweep
+// CTA's shared block; each chunk's panels are contiguous and its record lists
+// where every input comes from and where every tile's rows go.
+void finish_bottom_levels(Problem& pr) {
+  constexpr int kTile = 32;
+  const std::int64_t chunk_bytes = 1024LL * std::max(4, env_int("PDG_CHUNK_KB", 64));
+  const int xcap = std::max(64, env_int("PDG_CHUNK_X", 1536));
+  const int nt = static_cast<int>(pr.tasks.size());
+  int lmax = -1;
+  for (const TaskDesc& t : pr.tasks)
+    if (t.bundle >= 0) lmax = std::max(lmax, t.height);
+  pr.n_bottom_levels = lmax + 1;
+  pr.level_chunks[0].assign(lmax + 1, 0);
+  pr.level_chunks[1].assign(lmax + 1, 0);
+  if (lmax < 0) return;
+  if (pr.ubuf_size >= (1LL << 31)) throw SolverError("pack: update buffer too large for the level chunk records");
+  std::vector<std::vector<int>> by_level(lmax + 1);
+  for (int i = 0; i < nt; ++i)
+    if (pr.tasks[i].bundle >= 0) by_level[pr.tasks[i].height].push_back(i);
+  auto is_regular = [&](int p) { return p >= 0 && pr.tasks[p].bundle < 0; };
+  for (int dir = 0; dir < 2; ++dir) {
+    auto& tiles = dir == 0 ? pr.ftiles : pr.htiles;
+    std::int64_t& mat_len = dir == 0 ? pr.fmat_len : pr.hmat_len;
+    for (int li = 0; li <= lmax; ++li) {
+      const int level = dir == 0 ? li : lmax - li;
+      const std::vector<int>& lt = by_level[level];
+      std::size_t at = 0;
+      while (at < lt.size()) {
+        // greedy: tasks [at, e) while the chunk stays under every cap
+        std::int64_t bytes = 0;
+        int x = 0, meta = 4;
+        std::size_t e = at;
+        while (e < lt.size()) {
+          const TaskDesc& t = pr.tasks[lt[e]];
+          const int t0 = dir == 0 ? t.f_tile0 : t.h_tile0, n = dir == 0 ? t.f_ntile : t.h_ntile;
+          std::int64_t tb = 0;
+          for (int k = 0; k < n; ++k) tb += 8 * align_tile(static_cast<std::int64_t>(tiles[t0 + k].ncol) * tiles[t0 + k].stride);
+          int tm = 8 * n, tx = 0;
           if (dir == 0) {
-            for (int cc = S.s0; cc < S.s1; ++cc) {
-              cells.push_back(static_cast<int>(dof_base + static_cast<std::int64_t>(cc) * bs));
-              cells.push_back(vx[s] + (cc - S.s0) * bs);
+            const int nc = t.w / t.bs;
+            tm += 4 * nc + pr.in_ptr[t.in_off + nc] - pr.in_ptr[t.in_off];
+            tx = t.w;
+          } else if (n) {
+            tm += 2 * ((t.w + t.nr) / t.bs);
+            tx = t.w + t.nr;
+          }
+          if (e > at && (bytes + tb > chunk_bytes || x + tx > xcap || meta + tm + 12 > kChunkMetaInts)) break;
+          if (tx > xcap || meta + tm + 12 > kChunkMetaInts)
+            throw SolverError("pack: a bottom-level supernode does not fit a level chunk");
+          bytes += tb;
+          x += tx;
+          meta += tm;
+          ++e;
+        }
+        LevelChunk C;
+        C.dir = dir;
+        C.level = level;
+        C.first_task = lt[at];
+        C.n_task = static_cast<int>(e - at);
+        mat_len = align_tile(mat_len);
+        C.src_off = mat_len;
+        C.root_off = static_cast<int>(pr.chunk_roots.size());
+        C.par_off = static_cast<int>(pr.chunk_parents.size());
+        std::vector<int> cells, aux, items;
+        int ncell = 0, nitem = 0, xo = 0;
+        for (std::size_t q = at; q < e; ++q) {
+          const int ti = lt[q];
+          const TaskDesc& t = pr.tasks[ti];
+          const int t0 = dir == 0 ? t.f_tile0 : t.h_tile0, n = dir == 0 ? t.f_ntile : t.h_ntile;
+          for (int k = 0; k < n; ++k) {  // panels: contiguous in chunk order
+            Problem::Tile& tl = tiles[t0 + k];
+            mat_len = align_tile(mat_len);
+            tl.off = mat_len;
+            mat_len += static_cast<std::int64_t>(tl.ncol) * tl.stride;
+            if (tl.ncol % t.bs) throw SolverError("pack: bottom-level tile width is not a whole number of blocks");
+          }
+          if (dir == 0) {
+            if (is_regular(t.parent)) pr.chunk_roots.push_back(ti);
+            const int nc = t.w / t.bs;
+            for (int c = 0; c < nc; ++c) {
+              cells.push_back(static_cast<int>(t.dof0) + c * t.bs);
+              cells.push_back(xo + c * t.bs);
               cells.push_back(static_cast<int>(aux.size()));
-              for (std::size_t e = 0; e < inc[cc].size(); ++e) {
-                const int d = inc_d[cc][e];  // a descendant, hence a member
-                aux.push_back(ul[d] + static_cast<int>(inc[cc][e] - pr.tasks[base + d].ubuf_off));
-              }
+              for (int k = pr.in_ptr[t.in_off + c]; k < pr.in_ptr[t.in_off + c + 1]; ++k)
+                aux.push_back(static_cast<int>(pr.in_idx[k]));
               cells.push_back(static_cast<int>(aux.size()));
               ++ncell;
             }
-            for (int k = 0; k < t.f_ntile; ++k) {
-              const Problem::Tile& tl = pr.ftiles[t.f_tile0 + k];
+            for (int k = 0; k < n; ++k) {
+              const Problem::Tile& tl = tiles[t0 + k];
               const int r0 = k * kTile;
-              items.push_back(static_cast<int>(tl.off - B.src_off[0]));
+              items.push_back(static_cast<int>(tl.off - C.src_off));
               items.push_back(tl.ncol);
               items.push_back(tl.rows | (t.root_dense << 30));
               items.push_back(tl.stride);
-              items.push_back(vx[s]);
+              items.push_back(xo);
               items.push_back(t.root_dense ? tl.rows : std::clamp(t.w - r0, 0, tl.rows));
               items.push_back(static_cast<int>(t.dof0) + r0);
               items.push_back(static_cast<int>(t.ubuf_off) + r0 - t.w);
-              items.push_back(ul[s] + r0 - t.w);
               ++nitem;
             }
-          } else if (t.h_ntile) {
-            // own y_S and the rows owned by supernodes outside the bundle (or
-            // by its dense root, whose x_S the forward pass left in z) are
-            // known when the unit starts; rows of members are copied level by
-            // level from the x_S block
-            for (int cc = S.s0; cc < S.s1; ++cc) {
-              aux.push_back(static_cast<int>(dof_base + static_cast<std::int64_t>(cc) * bs));
-              aux.push_back(bin[s] + (cc - S.s0) * bs);
+            xo += t.w;
+          } else if (n) {
+            if (is_regular(t.parent) &&
+                std::find(pr.chunk_parents.begin() + C.par_off, pr.chunk_parents.end(), t.parent) == pr.chunk_parents.end())
+              pr.chunk_parents.push_back(t.parent);
+            for (int c = 0; c < t.w / t.bs; ++c) {
+              cells.push_back(static_cast<int>(t.dof0) + c * t.bs);
+              cells.push_back(xo + c * t.bs);
+              ++ncell;
             }
-            for (std::size_t k = 0; k < S.rows.size(); ++k) {
-              const int q = S.rows[k], m = F.sn_of[q];
-              const int xo = bin[s] + t.w + static_cast<int>(k) * bs;
-              if (pr.tasks[base + m].bundle == pr.tasks[base + s].bundle && !pr.tasks[base + m].root_dense) {
-                cells.push_back(xs[m] + (q - F.sn[m].s0) * bs);
-                cells.push_back(xo);
-                ++ncell;
-              } else {
-                aux.push_back(-1 - static_cast<int>(dof_base + static_cast<std::int64_t>(q) * bs));
-                aux.push_back(xo);
-              }
+            for (int c = 0; c < t.nr / t.bs; ++c) {
+              cells.push_back(-1 - static_cast<int>(pr.row_dof[t.rows_off + c]));
+              cells.push_back(xo + t.w + c * t.bs);
+              ++ncell;
             }
-            for (int k = 0; k < t.h_ntile; ++k) {
-              const Problem::Tile& tl = pr.htiles[t.h_tile0 + k];
-              items.push_back(static_cast<int>(tl.off - B.src_off[1]));
+            for (int k = 0; k < n; ++k) {
+              const Problem::Tile& tl = tiles[t0 + k];
+              items.push_back(static_cast<int>(tl.off - C.src_off));
               items.push_back(tl.ncol);
               items.push_back(tl.rows);
               items.push_back(tl.stride);
-              items.push_back(bin[s] + tl.col0);
+              items.push_back(xo + tl.col0);
               items.push_back(tl.rows);
               items.push_back(static_cast<int>(t.dof0) + tl.col0);
               items.push_back(0);
-              items.push_back(xs[s] + tl.col0);
               ++nitem;
             }
+            xo += t.w + t.nr;
           }
         }
-        lev.push_back(ncell);
-        lev.push_back(nitem);
+        C.bytes = static_cast<int>(8 * (align_tile(mat_len) - C.src_off));
+        C.n_root = static_cast<int>(pr.chunk_roots.size()) - C.root_off;
+        C.n_par = static_cast<int>(pr.chunk_parents.size()) - C.par_off;
+        C.xneed = xo;
+        while (pr.bmeta.size() % 4) pr.bmeta.push_back(0);  // 16-byte aligned records
+        C.meta_off = static_cast<int>(pr.bmeta.size());
+        // the items are read as int4 pairs: an even number of backward cells
+        // (2 ints each) and the aux list padded to a multiple of 4 ints
+        if (dir == 1 && (ncell & 1)) {
+          cells.push_back(cells[cells.size() - 2]);  // repeat the last cell (same value, same slot)
+          cells.push_back(cells[cells.size() - 2]);
+          ++ncell;
+        }
+        pr.bmeta.push_back(ncell);
+        pr.bmeta.push_back(nitem);
+        pr.bmeta.push_back(static_cast<int>(aux.size()));
+        pr.bmeta.push_back(0);
+        while (aux.size() % 4) aux.push_back(0);
+        pr.bmeta.insert(pr.bmeta.end(), cells.begin(), cells.end());
+        pr.bmeta.insert(pr.bmeta.end(), aux.begin(), aux.end());
+        pr.bmeta.insert(pr.bmeta.end(), items.begin(), items.end());
+        while (pr.bmeta.size() % 4) pr.bmeta.push_back(0);
+        C.meta_n = static_cast<int>(pr.bmeta.size()) - C.meta_off;
+        if (C.meta_n > kChunkMetaInts) throw SolverError("pack: level chunk record exceeds its shared-memory block");
+        // a chunk with no tiles (backward, dense roots only) still counts for its level
+        pr.chunks.push_back(C);
+        ++pr.level_chunks[dir][level];
+        at = e;
       }
-      while (pr.bmeta.size() % 4) pr.bmeta.push_back(0);  // 16-byte aligned records (L2 bulk prefetch)
-      B.meta_off[dir] = static_cast<int>(pr.bmeta.size());
-      pr.bmeta.push_back(B.nlev);
-      pr.bmeta.push_back(ncell);
-      pr.bmeta.push_back(nitem);
-      pr.bmeta.push_back(static_cast<int>(dir == 0 ? aux.size() : aux.size() / 2));
-      pr.bmeta.insert(pr.bmeta.end(), lev.begin(), lev.end());
-      pr.bmeta.insert(pr.bmeta.end(), cells.begin(), cells.end());
-      pr.bmeta.insert(pr.bmeta.end(), aux.begin(), aux.end());
-      pr.bmeta.insert(pr.bmeta.end(), items.begin(), items.end());
-      while (pr.bmeta.size() % 4) pr.bmeta.push_back(0);
-      B.meta_n[dir] = static_cast<int>(pr.bmeta.size()) - B.meta_off[dir];
-      if (B.meta_n[dir] > kBundleMetaInts) throw SolverError("pack: bundle record exceeds its shared-memory block");
     }
-    pr.bundles.push_back(B);
   }
-  for (int s = 0; s < nsn; ++s)
-    if (pr.tasks[base + s].bundle < 0) {
-      place_f(s);
-      place_h(s);
-    }
   pr.factor_values = pr.fmat_len + pr.hmat_len;
 }
 

@@ -372,7 +372,13 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   const bool md_default = static_cast<std::int64_t>(N) * b >= 2000000;
   const char* ord_env = std::getenv("PDG_ORDER");
   const bool md_order = !pos || (ord_env ? std::string(ord_env) == "md" : md_default);
-  const int md_relax = std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : 8;
+  // With the bottom levels solved in level chunks (host/pack.cpp) the small
+  // supernodes cost no per-unit round trips, so no amalgamation: fundamental
+  // supernodes store no explicit zeros (config 4: 26.6 GB of panels instead
+  // of 35.0 GB; sweep 6.17 -> 5.86 ms, profiles/r02u).
+  const bool bottom_on = md_order && bottom_level_bytes(static_cast<std::int64_t>(N) * b, b) > 0;
+  const int md_relax =
+      std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : bottom_on ? 1 : 8;
   pl.nd.assign(n_units, NdTree{});
   auto& nd = pl.nd;
   pl.unit_cells.assign(n_units, {});
@@ -546,13 +552,12 @@ static void factor_units(Problem& pr, const Placement& pl) {
       pack_unit_tasks(pr, uf.F, 0, static_cast<std::int64_t>(&uf - factors.data()) * b);
   pr.n_fine_tasks = static_cast<int>(pr.tasks.size());
   factors.clear();
+  finish_bottom_levels(pr);
   if (std::getenv("PDG_SETUP_TIMES")) {
-    std::int64_t bt = 0, bb = 0, mx = 0, lev = 0;
-    for (const Bundle& B : pr.bundles) {
-      bt += B.n_task;
-      bb += B.bytes[0] + B.bytes[1];
-      mx = std::max<std::int64_t>(mx, B.xneed);
-      lev += B.nlev;
+    std::int64_t bt = 0, bb = 0;
+    for (const LevelChunk& c : pr.chunks) {
+      bb += c.bytes;
+      if (c.dir == 0) bt += c.n_task;
     }
     int small16 = 0, small48 = 0, reg = 0;
     for (const TaskDesc& t : pr.tasks) {
@@ -562,15 +567,12 @@ static void factor_units(Problem& pr, const Placement& pl) {
       small16 += fb < 16384;
       small48 += fb < 49152;
     }
-    std::fprintf(stderr, "[pdg] unbundled tasks %d, of which %d under 16 KB and %d under 48 KB\n", reg, small16, small48);
     std::fprintf(stderr,
-                 "[pdg] sweep tasks %zu, bundles %zu holding %lld tasks (%.2f GB of %.2f GB panels, "
-                 "%.1f levels each, x <= %lld)\n",
-                 pr.tasks.size(), pr.bundles.size(), static_cast<long long>(bt), bb / 1e9,
-                 8.0 * (pr.fmat_len + pr.hmat_len) / 1e9, pr.bundles.empty() ? 0.0 : double(lev) / pr.bundles.size(),
-                 static_cast<long long>(mx));
+                 "[pdg] sweep tasks %zu: %d scheduled one by one (%d under 16 KB, %d under 48 KB), %lld in %d bottom "
+                 "levels, %zu level chunks (%.2f GB of %.2f GB panels)\n",
+                 pr.tasks.size(), reg, small16, small48, static_cast<long long>(bt), pr.n_bottom_levels,
+                 pr.chunks.size(), bb / 1e9, 8.0 * (pr.fmat_len + pr.hmat_len) / 1e9);
   }
-
 }
 
 

@@ -47,33 +47,41 @@ struct TaskDesc {
   // forward and backward solves collapse into one level of the sweep
   int root_dense = 0;
   std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
-  int bundle = -1;     // >= 0: solved inside subtree bundle Problem::bundles[bundle] (host/pack.cpp)
+  int bundle = -1;     // >= 0: a bottom-level supernode, solved inside level chunks (LevelChunk)
 };
 
-// A descendant-closed set of small supernodes of one subdomain (whole subtrees
-// of the elimination tree) that ONE CTA solves as one sweep unit per
-// direction, level by level with CTA barriers only (cuda/sweep.cu run_bundle).
-// Its panels are contiguous (forward: leaves first; backward: top level
-// first). The CTA keeps the bundle's vectors in shared memory (xneed doubles;
-// forward [t_S of every member][u_S of every member], backward [[y_S ; -x_R]
-// of every member][x_S of every member]) and everything it needs to know is
-// one block of ints in bmeta (16-byte aligned):
-//   [nlev, ncell, nitem, naux] , nlev x {cell_end, item_end} ,
-//   cells, forward {dof, xoff, in0, in1}: t = r[dof..] minus aux[in0..in1) (shared u_D slices),
-//          backward {src, xoff}: x_R rows owned by members, copied from their x_S ,
-//   aux, forward: the incoming-update lists; backward {src, xoff} pairs known at
-//        the start: y_S (src >= 0) and -x_R rows from outside (z at -1-src) ,
+// Bottom levels of the sweep. The supernodes of every small bottom subtree
+// (TaskDesc::bundle >= 0; host/pack.cpp) are not scheduled one by one: per
+// direction and per tree height they are cut into LEVEL CHUNKS, each solved by
+// one CTA as one unit (cuda/sweep.cu run_chunk): gather the inputs of all its
+// supernodes into shared memory, one barrier, one warp per 32-row tile. All
+// chunks of a level are independent; a level waits for the previous one
+// through one counter per level, so no per-supernode dependency is tracked.
+// A chunk's panels are contiguous and its record is one block of ints in
+// bmeta (16-byte aligned):
+//   [ncell, nitem, naux, 0] ,
+//   cells, forward {dof, xoff, in0, in1}: t = r[dof..] minus ubuf[aux[in0..in1)] ,
+//          backward {src, xoff}: y_S (src >= 0) or -x_R (z at -1-src) ,
+//   aux (forward): ubuf offsets of the incoming updates ,
 //   items (one 32-row tile each): {panel offset - src_off, ncol, rows | dense_root << 30, stride,
-//                                  xoff, wsplit, dst_a, dst_b, shared dst}.
-constexpr int kBundleMetaInts = 2560;   // shared-memory block of the sweep CTA (cuda/sweep.cu)
-constexpr int kBundleDefaultKB = 96;    // PDG_BUNDLE_KB
-struct Bundle {
-  std::int64_t src_off[2] = {0, 0};  // first panel double (F, H)
-  int bytes[2] = {0, 0};
-  int meta_off[2] = {0, 0}, meta_n[2] = {0, 0};
-  int nlev = 0, xneed = 0, n_task = 0;
-  int root_off = 0, n_root = 0;      // bundle_roots: the subtree roots (task ids)
-  int par_off = 0, n_par = 0;        // bundle_parents: their distinct parents (task ids)
+//                                  xoff, wsplit, dst_a, dst_b}: rows < wsplit go to y_S (dense
+//                                  root: x_S) at dst_a, the rest to ubuf at dst_b; backward rows to z at dst_a.
+constexpr int kChunkMetaInts = 2560;  // shared-memory block of the sweep CTA (cuda/sweep.cu)
+constexpr int kBottomDefaultKB = 160;  // PDG_BOTTOM_KB
+constexpr int kBottomDefaultLevels = 8;  // PDG_BOTTOM_LEVELS
+// Bottom levels on? Default: where the sweep is bandwidth bound (>= 2M dofs,
+// the minimum-degree ordering) and the blocks are large enough for one tile
+// row per lane to pay (b >= 10; config 5 p=2, b = 6: 2.36 -> 3.29 ms, worse).
+// Smaller problems have idle CTAs and want every supernode on its own one.
+// PDG_BOTTOM_KB overrides (0: off). Returns the subtree byte cap.
+long long bottom_level_bytes(long long n_global_dofs, int b);
+struct LevelChunk {
+  int dir = 0, level = 0, first_task = 0, n_task = 0;
+  std::int64_t src_off = 0;  // first panel double (F or H)
+  int bytes = 0;
+  int meta_off = 0, meta_n = 0, xneed = 0;
+  int root_off = 0, n_root = 0;  // forward: chunk_roots, its supernodes with an individually scheduled parent
+  int par_off = 0, n_par = 0;    // backward: chunk_parents, the distinct such parents
 };
 
 struct Problem {
@@ -97,8 +105,10 @@ struct Problem {
   // Schwarz local solves
   std::vector<TaskDesc> tasks;
   std::vector<int> task_child, fwd_order, bwd_order;
-  std::vector<Bundle> bundles;
-  std::vector<int> bmeta, bundle_roots, bundle_parents;
+  std::vector<LevelChunk> chunks;  // forward chunks (levels bottom-up), then backward ones (top-down)
+  std::vector<int> bmeta, chunk_roots, chunk_parents;
+  int n_bottom_levels = 0;
+  std::vector<int> level_chunks[2];  // chunks per level (forward, backward)
   // Row-tiled dense panels: tile t covers output rows [32k, 32k+rows) of its
   // task; element (row r0+l, input col0+j) at mat[off + j*stride + l]. The
   // panels themselves are formed on the device (cuda/panels.cu) from the
@@ -186,6 +196,8 @@ struct Problem {
 // or the coarse problem, coarse=1) as device tasks: panels, tiles, row maps,
 // incoming update lists and the tree links (host/pack.cpp).
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base);
+// After the last fine pack_unit_tasks: level chunks of the bottom supernodes.
+void finish_bottom_levels(Problem& pr);
 
 // Multi-rank SpMV halo, identical on every rank:
 // send[peer] = this rank's local cells adjacent to peer's cells (ascending),

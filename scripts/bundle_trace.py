@@ -29,16 +29,18 @@ st, dep, stg, done, staged, comp = (t[:, i] - t0 for i in range(6))
 task, direc, nbytes, nchunk, height, coarse = (t[:, i] for i in range(6, 12))
 span = done.max()
 print(f"units {n}: span {span / 1e3:.1f} us, {nbytes.sum() / 1e9:.2f} GB -> {nbytes.sum() / span:.0f} GB/s")
-for lab, m in (("bundle fwd", (nchunk == 0) & (direc == 0)), ("bundle bwd", (nchunk == 0) & (direc == 1)),
+for lab, m in (("chunk fwd", (nchunk == 0) & (direc == 0)), ("chunk bwd", (nchunk == 0) & (direc == 1)),
                ("regular fwd", (nchunk > 0) & (direc == 0)), ("regular bwd", (nchunk > 0) & (direc == 1))):
     if not m.any():
         continue
     tot = (done - st)[m]
     print(f"{lab}: {int(m.sum())} units, {nbytes[m].sum() / 1e9:.2f} GB, mean {nbytes[m].mean() / 1024:.1f} KB; "
           f"CTA time {tot.sum() / 1e6:.1f} ms total -> {nbytes[m].sum() / tot.sum():.2f} GB/s per CTA")
-    bun = lab.startswith("bundle")
-    phases = ((("wait", (dep - st)[m]), ("record", (staged - dep)[m]), ("first level", (comp - staged)[m]),
-               ("other levels", (stg - comp)[m]), ("publish", (done - stg)[m]), ("total", tot)) if bun else
+    ck = lab.startswith("chunk")
+    # chunk stamps: [0] start, [1] waits done, [4] record in smem, [2] inputs gathered, [5] tiles done, [3] published
+    phases = ((("wait", (dep - st)[m]), ("record", (staged - st)[m]), ("gather", (stg - np.maximum(dep, staged))[m]),
+               ("tiles", (comp - stg)[m]), ("publish", (done - comp)[m]), ("total", tot),
+               ("first tile", height[m]), ("tiles/chunk", coarse[m] * 1e3)) if ck else
               (("wait", (dep - st)[m]), ("stage", (staged - dep)[m]), ("work", (comp - staged)[m]),
                ("publish", (done - comp)[m]), ("total", tot)))
     for ph, v in phases:

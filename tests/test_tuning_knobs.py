@@ -29,6 +29,15 @@ CASES = {
     "host_assembly": {"PDG_HOST_ASSEMBLY": "1"},
     "sweep_cta_64": {"PDG_SWEEP_THREADS": "64"},
     "one_cta_per_chunk": {"PDG_PERSIST": "0"},
+    # bottom levels of the elimination trees solved in level chunks (off by default at this size)
+    "bottom_levels": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96"},
+    "bottom_levels_nd": {"PDG_BOTTOM_KB": "64", "PDG_BOTTOM_LEVELS": "3"},
+    "bottom_levels_small_chunks": {"PDG_ORDER": "md", "PDG_MD_RELAX": "2", "PDG_BOTTOM_KB": "160",
+                                   "PDG_BOTTOM_LEVELS": "12", "PDG_CHUNK_KB": "8", "PDG_CHUNK_X": "256"},
+    "bottom_levels_cta_64": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96",
+                             "PDG_SWEEP_THREADS": "64"},
+    "bottom_levels_hybrid_relax": {"PDG_ORDER": "md", "PDG_RELAX_MIN_SUBTREE": "12", "PDG_BOTTOM_KB": "96"},
+    "bottom_levels_off": {"PDG_BOTTOM_KB": "0", "PDG_ORDER": "md"},
 }
 
 
