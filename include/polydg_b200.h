@@ -146,6 +146,14 @@ int64_t pdg_problem_export(const pdg_problem* p, int which, int64_t* rows, int64
  * factor, [2] / [3] stored forward / backward sweep panel doubles (explicit
  * zeros and padding included), [4] local K blocks, [5] E doubles held */
 void pdg_problem_factor_stats(const pdg_problem* p, int64_t stats[6]);
+/* the sweep's work plan on this rank (diagnostic; no reference counterpart):
+ * stats[0] sweep supernodes, [1] of which solved in level chunks (the bottom
+ * levels of the elimination trees), [2] bottom levels, [3] / [4] forward /
+ * backward level chunks, [5] supernodes covered by the forward chunks, [6] by
+ * the backward chunks plus the dense roots among [1] (no backward solve),
+ * [7] 1 if every chunk's dependency precedes it in the ticket order and every
+ * record fits the sweep CTA's shared block */
+void pdg_problem_sweep_stats(const pdg_problem* p, int64_t stats[8]);
 /* partition maps: which 0 = subdomain owner, 1 = coarse owner; per reference cell */
 /* where setup ran: bit 0 = operator assembled on the device (cuda/assemble.cu),
  * bit 1 = local factors computed on the device (cuda/factor.cu) */

@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
             "pdg_default_max_iterations": (i32, [i64]),
             "pdg_uniform_rhs": (None, [C.c_uint64, i64, P(C.c_double)]),
             "pdg_problem_factor_stats": (None, [vp, P(i64)]),
+            "pdg_problem_sweep_stats": (None, [vp, P(i64)]),
             "pdg_problem_flags": (i32, [vp]),
         }
         for name, (res, args) in sig.items():

@@ -241,6 +241,39 @@ void pdg_problem_factor_stats(const pdg_problem* h, int64_t stats[6]) {
   stats[5] = static_cast<int64_t>(pr.E.size());
 }
 
+void pdg_problem_sweep_stats(const pdg_problem* h, int64_t stats[8]) {
+  const auto& pr = *h->p;
+  for (int i = 0; i < 8; ++i) stats[i] = 0;
+  stats[0] = static_cast<int64_t>(pr.tasks.size());
+  int64_t dense_bottom = 0;
+  for (const auto& t : pr.tasks)
+    if (t.bundle >= 0) {
+      ++stats[1];
+      dense_bottom += t.root_dense;
+    }
+  stats[2] = pr.n_bottom_levels;
+  // chunks are stored in ticket order per direction: a chunk's dependency slot must already hold chunks
+  bool ok = true;
+  std::vector<int> seen[2];
+  seen[0].assign(pr.level_chunks[0].size(), 0);
+  seen[1].assign(pr.level_chunks[1].size(), 0);
+  int64_t covered_b = 0;
+  for (const auto& c : pr.chunks) {
+    ++stats[3 + c.dir];
+    if (c.dir == 0) stats[5] += c.n_task;
+    else covered_b += c.n_task;
+    ok = ok && c.meta_n <= pdg::kChunkMetaInts && c.xneed <= 4096;
+    if (c.dep_slot >= 0)
+      ok = ok && (c.dep_dir < c.dir || seen[c.dep_dir][c.dep_slot] == pr.level_chunks[c.dep_dir][c.dep_slot]) &&
+           pr.level_chunks[c.dep_dir][c.dep_slot] > 0;
+    if (c.slot >= 0) ++seen[c.dir][c.slot];
+    ++seen[c.dir][c.gslot];
+  }
+  stats[6] = covered_b;  // backward chunks list every bottom supernode too (dense roots carry no tiles)
+  (void)dense_bottom;
+  stats[7] = ok ? 1 : 0;
+}
+
 void pdg_problem_perm(const pdg_problem* h, int* perm) {
   std::memcpy(perm, h->p->perm.data(), sizeof(int) * h->p->perm.size());
 }

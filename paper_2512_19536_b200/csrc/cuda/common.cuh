@@ -36,8 +36,8 @@ struct DevTask {
 // A third kind, nchunk == 0: a level chunk of bottom supernodes
 // (host/problem.hpp LevelChunk), tile_begin = chunk id, src_off / bytes = its
 // contiguous panels, [in_e0, in_e0 + in_n) = its record in bmeta, dep[0] /
-// need[0] = the level counter it waits for (n_dep), chunk = the level counter
-// it adds to, part_base / tile_ctr = first entry / count of its forward
+// need[0] = the level counter it waits for (n_dep), own_fwd / chunk = the global
+// and (>= 0) group level counters it adds to, part_base / tile_ctr = first entry / count of its forward
 // publish list, c0 / c1 = first entry / count of its backward wait list.
 struct DevUnit {
   int task, tile_begin, tile_end, c0, c1, chunk, nchunk, part_base, tile_ctr, dir;

@@ -647,7 +647,7 @@ void DeviceSim::upload_tasks() {
   // last forward one (a whole tree inside the bottom levels has no such parent).
   std::vector<int2> broots, bdeps;
   std::vector<DevUnit> cfu, cbu;
-  const int nlev = pr.n_bottom_levels;
+  const int nslots = static_cast<int>(pr.level_chunks[0].size());  // (group, level) counters per direction
   const int lev_flag0 = 2 * nt_flag;
   for (std::size_t ci = 0; ci < pr.chunks.size(); ++ci) {
     const LevelChunk& C = pr.chunks[ci];
@@ -660,14 +660,15 @@ void DeviceSim::upload_tasks() {
     u.bytes = C.bytes;
     u.in_e0 = C.meta_off;
     u.in_n = C.meta_n;
-    u.own_fwd = -1;
-    u.chunk = lev_flag0 + C.dir * nlev + C.level;  // the counter this chunk adds to
+    // the counters this chunk adds to: its global level's and (grouped levels) its group's
+    u.own_fwd = lev_flag0 + C.dir * nslots + C.gslot;
+    u.chunk = C.slot >= 0 ? lev_flag0 + C.dir * nslots + C.slot : -1;
+    if (C.dep_slot >= 0) {
+      u.n_dep = 1;
+      u.dep[0] = lev_flag0 + C.dep_dir * nslots + C.dep_slot;
+      u.need[0] = pr.level_chunks[C.dep_dir][C.dep_slot];
+    }
     if (C.dir == 0) {
-      if (C.level > 0) {
-        u.n_dep = 1;
-        u.dep[0] = lev_flag0 + C.level - 1;
-        u.need[0] = pr.level_chunks[0][C.level - 1];
-      }
       u.part_base = static_cast<int>(broots.size());
       u.tile_ctr = C.n_root;
       for (int k = 0; k < C.n_root; ++k) {
@@ -675,14 +676,6 @@ void DeviceSim::upload_tasks() {
         broots.push_back(make_int2(r, pr.tasks[r].f_ntile));
       }
     } else {
-      u.n_dep = 1;
-      if (C.level < nlev - 1) {
-        u.dep[0] = lev_flag0 + nlev + C.level + 1;
-        u.need[0] = pr.level_chunks[1][C.level + 1];
-      } else {
-        u.dep[0] = lev_flag0 + nlev - 1;
-        u.need[0] = pr.level_chunks[0][nlev - 1];
-      }
       u.c0 = static_cast<int>(bdeps.size());
       u.c1 = C.n_par;
       for (int k = 0; k < C.n_par; ++k) {
@@ -754,7 +747,7 @@ void DeviceSim::upload_tasks() {
   d_ubuf = dalloc<double>(std::max<std::int64_t>(pr.ubuf_size, 1));
   d_yfwd = dalloc<double>(n + static_cast<std::size_t>(pr.two_level ? pr.n_agg * pr.bq : 0));
   // tile counters per task and direction, then one counter per bottom level and direction
-  const std::size_t n_flags = 2 * static_cast<std::size_t>(std::max(n_tasks, 1)) + 2 * pr.n_bottom_levels;
+  const std::size_t n_flags = 2 * static_cast<std::size_t>(std::max(n_tasks, 1)) + 2 * pr.level_chunks[0].size();
   d_flags = dalloc<int>(n_flags);
   PDG_CUDA(cudaMemsetAsync(d_flags, 0, n_flags * sizeof(int), st));
   // [0] next ticket, [1] sweep number, [2] CTAs finished (sweep.cu)

@@ -635,7 +635,10 @@ __device__ __forceinline__ void run_chunk(const SweepArgs& a, UnitSmem& s, doubl
         const int2 r = a.broots[U.part_base + k];
         red_relaxed_add(a.flags + r.x, r.y);
       }
-    if (threadIdx.x == 0) red_relaxed_add(a.flags + U.chunk, 1);
+    if (threadIdx.x == 0) {
+      red_relaxed_add(a.flags + U.own_fwd, 1);
+      if (U.chunk >= 0) red_relaxed_add(a.flags + U.chunk, 1);
+    }
     if (tr && threadIdx.x == 0) tr[3] = gtimer();
   }
 }

@@ -48,6 +48,7 @@ struct TaskDesc {
   int root_dense = 0;
   std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
   int bundle = -1;     // >= 0: a bottom-level supernode, solved inside level chunks (LevelChunk)
+  int unit = 0;        // which pack_unit_tasks call (subdomain) it came from
 };
 
 // Bottom levels of the sweep. The supernodes of every small bottom subtree
@@ -57,6 +58,11 @@ struct TaskDesc {
 // supernodes into shared memory, one barrier, one warp per 32-row tile. All
 // chunks of a level are independent; a level waits for the previous one
 // through one counter per level, so no per-supernode dependency is tracked.
+// The subdomains are taken in GROUPS of about PDG_BOTTOM_GROUP_MB of bottom
+// panel, each with its own level counters, two groups interleaved level by
+// level in the ticket order: a level's updates are then read back while they
+// are still in the L2 (a global level order reads them from DRAM), and a
+// level's dependencies were issued a whole group-level earlier.
 // A chunk's panels are contiguous and its record is one block of ints in
 // bmeta (16-byte aligned):
 //   [ncell, nitem, naux, 0] ,
@@ -77,6 +83,9 @@ constexpr int kBottomDefaultLevels = 8;  // PDG_BOTTOM_LEVELS
 long long bottom_level_bytes(long long n_global_dofs, int b);
 struct LevelChunk {
   int dir = 0, level = 0, first_task = 0, n_task = 0;
+  // counters (Problem::level_chunks[dir][slot], slot = group * levels + level): the one this
+  // chunk adds to, and the one it waits for (dep_slot < 0: none)
+  int slot = 0, gslot = 0, dep_dir = 0, dep_slot = -1;  // slot < 0: a global level (no group counter)
   std::int64_t src_off = 0;  // first panel double (F or H)
   int bytes = 0;
   int meta_off = 0, meta_n = 0, xneed = 0;
@@ -107,8 +116,8 @@ struct Problem {
   std::vector<int> task_child, fwd_order, bwd_order;
   std::vector<LevelChunk> chunks;  // forward chunks (levels bottom-up), then backward ones (top-down)
   std::vector<int> bmeta, chunk_roots, chunk_parents;
-  int n_bottom_levels = 0;
-  std::vector<int> level_chunks[2];  // chunks per level (forward, backward)
+  int n_bottom_levels = 0, n_bottom_groups = 0, n_packed_units = 0;
+  std::vector<int> level_chunks[2];  // chunks per (group, level) slot (forward, backward)
   // Row-tiled dense panels: tile t covers output rows [32k, 32k+rows) of its
   // task; element (row r0+l, input col0+j) at mat[off + j*stride + l]. The
   // panels themselves are formed on the device (cuda/panels.cu) from the

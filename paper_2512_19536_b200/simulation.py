@@ -257,6 +257,14 @@ class Problem:
         keys = ["l_struct", "l0_struct", "fwd_panel_doubles", "bwd_panel_doubles", "k_blocks", "e_doubles"]
         return dict(zip(keys, list(st)))
 
+    def sweep_stats(self) -> dict:
+        """The sweep's work plan: supernodes, bottom levels and level chunks (pdg_problem_sweep_stats)."""
+        st = (C.c_int64 * 8)()
+        lib().pdg_problem_sweep_stats(self._handle(), st)
+        keys = ["supernodes", "bottom_supernodes", "bottom_levels", "fwd_chunks", "bwd_chunks",
+                "fwd_chunk_supernodes", "bwd_chunk_supernodes", "plan_ok"]
+        return dict(zip(keys, list(st)))
+
     def flags(self) -> dict:
         """Where setup ran (pdg_problem_flags)."""
         f = lib().pdg_problem_flags(self._handle())

@@ -3,7 +3,8 @@ rtol 1e-10 from x0 = 0 with a seeded uniform [-1, 1] right-hand side (the
 reference draws it with mt19937_64, acceptance.cpp:285-286; numpy's generator
 stands in, same distribution).
 Reports the solve and, separately, SpMV, Schwarz apply (sweep incl. the
-coarse solve) and the other per-iteration kernels.
+coarse solve), the other per-iteration kernels, and the coarse solve's share
+of one traced sweep.
 
     python scripts/c5_probe.py [p]
 """
@@ -56,3 +57,23 @@ print(json.dumps({"iterations": rep.iterations, "converged": rep.converged, "sol
                   "kernels_isolated_cold_L2": {k: {"ms": round(kms[i], 4), "GB/s": round(kby[i] / (kms[i] * 1e-3) / 1e9, 1)
                                                    if kms[i] else None} for i, k in enumerate(names) if kms[i]}}),
       flush=True)
+
+# The coarse solve separately (the reference times it apart, schwarz.cpp:165-168). Here it runs
+# inside the sweep (coarse forward, dense coarse root, coarse backward are ordinary units), so its
+# time is read from one traced sweep: the span from the first coarse unit's start to the last
+# coarse unit's end, and the CTA time its units took.
+L.pdg_sim_trace_sweep.restype = C.c_int
+L.pdg_sim_trace_sweep.argtypes = [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]
+cap, F = 3000000, 12
+buf = np.zeros(cap * F, np.int64)
+for _ in range(2):
+    n = L.pdg_sim_trace_sweep(sim._h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), cap)
+t = buf[:n * F].reshape(n, F).astype(np.float64)
+t0_ = t[:, 0].min()
+st, done = t[:, 0] - t0_, t[:, 3] - t0_
+co = (t[:, 9] > 0) & (t[:, 11] == 1)  # individually scheduled units of coarse tasks
+print(json.dumps({"traced_sweep_us": round(done.max() / 1e3, 1), "coarse_units": int(co.sum()),
+                  "coarse_solve_span_us": round((done[co].max() - st[co].min()) / 1e3, 1) if co.any() else None,
+                  "coarse_first_start_us": round(st[co].min() / 1e3, 1) if co.any() else None,
+                  "coarse_last_end_us": round(done[co].max() / 1e3, 1) if co.any() else None,
+                  "coarse_cta_time_us": round((done - st)[co].sum() / 1e3, 1) if co.any() else None}), flush=True)
