@@ -555,12 +555,6 @@ __device__ __forceinline__ void run_chunk(const SweepArgs& a, UnitSmem& s, doubl
   const DevUnit& U = s.u;
   if (threadIdx.x < 32) {
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
-    if (threadIdx.x == 1) {
-      const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
-      Ahead& q = s.q[target];
-      if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
-      else q.tk = a.n_units;
-    }
     // the level counter this CTA already saw complete needs no second acquire
     if (threadIdx.x == 0 && U.n_dep && s.seen_level != U.dep[0]) {
       wait_count(a.flags + U.dep[0], (ep + 1) * U.need[0]);
@@ -589,8 +583,17 @@ __device__ __forceinline__ void run_chunk(const SweepArgs& a, UnitSmem& s, doubl
   const int* items = aux + ((naux + 3) & ~3);
   const int bs = s.t.bs;
   const double* pan = (FWD ? a.fmat : a.hmat) + U.src_off;
-  if (FWD) {
-    for (int q = threadIdx.x; q < ncell * bs; q += NT) {
+  // warp 0 takes the lookahead ticket (three dependent round trips) while the
+  // other warps gather
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 1) {
+      const int target = (s.qh + kAhead - 2) % kAhead, latest = (target + kAhead - 1) % kAhead;
+      Ahead& q = s.q[target];
+      if (s.q[latest].tk < a.n_units) fetch_ahead(a, q);
+      else q.tk = a.n_units;
+    }
+  } else if (FWD) {
+    for (int q = threadIdx.x - 32; q < ncell * bs; q += NT - 32) {
       const int cc = q / bs, rr = q - cc * bs;
       const int* ce = cells + 4 * cc;
       double x = a.r[ce[0] + rr];
@@ -606,10 +609,18 @@ __device__ __forceinline__ void run_chunk(const SweepArgs& a, UnitSmem& s, doubl
       xin[ce[1] + rr] = x;
     }
   } else {
-    for (int q = threadIdx.x; q < ncell * bs; q += NT) {
-      const int cc = q / bs, rr = q - cc * bs, src = cells[2 * cc];
-      xin[cells[2 * cc + 1] + rr] =
-          (a.prefetch & 16) ? 1.0 : src >= 0 ? __ldcg(a.yf + src + rr) : -__ldcg(a.z + (-1 - src) + rr);
+    // two independent loads per thread per pass
+    const int n = ncell * bs;
+    for (int q = threadIdx.x - 32; q < n; q += 2 * (NT - 32)) {
+      const int q1 = q + NT - 32;
+      const int c0 = q / bs, r0 = q - c0 * bs, s0 = cells[2 * c0];
+      const bool two = q1 < n;
+      const int c1 = two ? q1 / bs : c0, r1 = two ? q1 - c1 * bs : r0, s1 = cells[2 * c1];
+      const bool dbg = (a.prefetch & 16) != 0;
+      const double v0 = dbg ? 1.0 : s0 >= 0 ? __ldcg(a.yf + s0 + r0) : -__ldcg(a.z + (-1 - s0) + r0);
+      const double v1 = dbg ? 1.0 : s1 >= 0 ? __ldcg(a.yf + s1 + r1) : -__ldcg(a.z + (-1 - s1) + r1);
+      xin[cells[2 * c0 + 1] + r0] = v0;
+      if (two) xin[cells[2 * c1 + 1] + r1] = v1;
     }
   }
   __syncthreads();

@@ -31,7 +31,7 @@ std::int64_t align_tile(std::int64_t off) { return (off + kTileAlign - 1) / kTil
 }  // namespace
 
 long long bottom_level_bytes(long long n_global_dofs, int b) {
-  return 1024LL * env_int("PDG_BOTTOM_KB", n_global_dofs >= 2000000 && b >= 10 ? kBottomDefaultKB : 0);
+  return 1024LL * env_int("PDG_BOTTOM_KB", n_global_dofs >= 2000000 && b >= 6 ? kBottomDefaultKB : 0);
 }
 
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {

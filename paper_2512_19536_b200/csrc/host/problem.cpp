@@ -375,10 +375,11 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   // With the bottom levels solved in level chunks (host/pack.cpp) the small
   // supernodes cost no per-unit round trips, so no amalgamation: fundamental
   // supernodes store no explicit zeros (config 4: 26.6 GB of panels instead
-  // of 35.0 GB; sweep 6.17 -> 5.86 ms, profiles/r02u).
+  // of 35.0 GB; sweep 6.17 -> 5.86 ms, profiles/r02u). Small blocks (b < 10)
+  // merge up to 2 cells (config 5 p=2: 2.22 ms vs 2.48 ms fundamental).
   const bool bottom_on = md_order && bottom_level_bytes(static_cast<std::int64_t>(N) * b, b) > 0;
   const int md_relax =
-      std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : bottom_on ? 1 : 8;
+      std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : bottom_on ? (b >= 10 ? 1 : 2) : 8;
   pl.nd.assign(n_units, NdTree{});
   auto& nd = pl.nd;
   pl.unit_cells.assign(n_units, {});

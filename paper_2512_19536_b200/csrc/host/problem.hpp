@@ -76,8 +76,8 @@ constexpr int kChunkMetaInts = 2560;  // shared-memory block of the sweep CTA (c
 constexpr int kBottomDefaultKB = 160;  // PDG_BOTTOM_KB
 constexpr int kBottomDefaultLevels = 8;  // PDG_BOTTOM_LEVELS
 // Bottom levels on? Default: where the sweep is bandwidth bound (>= 2M dofs,
-// the minimum-degree ordering) and the blocks are large enough for one tile
-// row per lane to pay (b >= 10; config 5 p=2, b = 6: 2.36 -> 3.29 ms, worse).
+// the minimum-degree ordering) and b >= 6 (config 5 p=2, b = 6: 2.35 -> 2.22 ms
+// with 128-thread CTAs and supernodes of <= 2 cells; profiles/r02aa).
 // Smaller problems have idle CTAs and want every supernode on its own one.
 // PDG_BOTTOM_KB overrides (0: off). Returns the subtree byte cap.
 long long bottom_level_bytes(long long n_global_dofs, int b);
