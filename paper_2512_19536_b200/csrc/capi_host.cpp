@@ -247,7 +247,7 @@ void pdg_problem_sweep_stats(const pdg_problem* h, int64_t stats[8]) {
   stats[0] = static_cast<int64_t>(pr.tasks.size());
   int64_t dense_bottom = 0;
   for (const auto& t : pr.tasks)
-    if (t.bundle >= 0) {
+    if (t.bottom >= 0) {
       ++stats[1];
       dense_bottom += t.root_dense;
     }

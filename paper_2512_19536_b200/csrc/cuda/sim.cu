@@ -330,7 +330,7 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   // (profiles/r02l sched_*)
   constexpr double kFixed = 1500.0, kPerByte = 1.0 / 25.0, kPublish = 700.0;
   // only the individually scheduled supernodes take part: the bottom levels
-  // (TaskDesc::bundle >= 0) run before (forward) and after (backward) them
+  // (TaskDesc::bottom >= 0) run before (forward) and after (backward) them
   const int nt = static_cast<int>(pr.tasks.size());
   const int nn = nt, nu = static_cast<int>(units.size());
   auto node_of_unit = [&](const DevUnit& u) { return u.task; };
@@ -339,7 +339,7 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   std::vector<char> dense_root(nn, 0);
   for (int s = 0; s < nt; ++s) {
     const TaskDesc& t = pr.tasks[s];
-    if (t.bundle >= 0) continue;
+    if (t.bottom >= 0) continue;
     dense_root[s] = static_cast<char>(t.root_dense);
     if (t.parent >= 0) {
       pars[s].push_back(t.parent);
@@ -365,7 +365,7 @@ std::vector<int> list_schedule(const Problem& pr, const std::vector<DevUnit>& un
   std::vector<int> topo;
   topo.reserve(nn);
   for (int s = 0; s < nt; ++s)
-    if (pr.tasks[s].bundle < 0) topo.push_back(s);
+    if (pr.tasks[s].bottom < 0) topo.push_back(s);
   std::vector<double> Lb(nn, 0.0), Lf(nn, 0.0);
   for (int n : topo) {
     double kid = 0.0;
@@ -556,7 +556,7 @@ void DeviceSim::upload_tasks() {
   auto make_units = [&](const std::vector<int>& order, bool fwd, std::vector<DevUnit>& units) {
     for (int tk : order) {
       const TaskDesc& s = pr.tasks[tk];
-      if (s.bundle >= 0) continue;  // a bottom-level supernode: solved in level chunks (below)
+      if (s.bottom >= 0) continue;  // a bottom-level supernode: solved in level chunks (below)
       const int t0 = fwd ? s.f_tile0 : s.h_tile0, nt = fwd ? s.f_ntile : s.h_ntile;
       const auto& tiles = fwd ? pr.ftiles : pr.htiles;
       auto tbytes = [&](int r) { return 8LL * tiles[t0 + r].ncol * tiles[t0 + r].stride; };

@@ -84,7 +84,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     const Supernode& S = F.sn[s];
     const int w = S.w(bs), nr = static_cast<int>(S.rows.size()) * bs, h = w + nr;
     TaskDesc t;
-    t.bundle = bottom[s] ? 0 : -1;
+    t.bottom = bottom[s] ? 0 : -1;
     t.unit = pr.n_packed_units;
     t.coarse = coarse;
     t.bs = bs;
@@ -108,7 +108,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
     // a root with no below rows takes one dense symmetric panel
     t.root_dense = S.parent < 0 && nr == 0 ? 1 : 0;
     // forward tiles: output rows of F. Each lane streams double2 pairs of
-    // rows; the offsets (128-byte aligned) are assigned below, bundles first.
+    // rows; the offsets (128-byte aligned) are assigned below (the bottom levels in finish_bottom_levels).
     t.f_tile0 = static_cast<int>(pr.ftiles.size());
     for (int r0 = 0; r0 < h; r0 += kTile) {
       const int rows = std::min(kTile, h - r0), rs = seg(rows);
@@ -161,7 +161,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
   // levels are laid out level by level in finish_bottom_levels) ----
   for (int s = 0; s < nsn; ++s) {
     const TaskDesc& t = pr.tasks[base + s];
-    if (t.bundle >= 0) continue;
+    if (t.bottom >= 0) continue;
     for (int k = 0; k < t.f_ntile; ++k) {
       Problem::Tile& tl = pr.ftiles[t.f_tile0 + k];
       pr.fmat_len = align(pr.fmat_len);
@@ -190,7 +190,7 @@ void finish_bottom_levels(Problem& pr) {
   const int nt = static_cast<int>(pr.tasks.size());
   int lmax = -1;
   for (const TaskDesc& t : pr.tasks)
-    if (t.bundle >= 0) lmax = std::max(lmax, t.height);
+    if (t.bottom >= 0) lmax = std::max(lmax, t.height);
   pr.n_bottom_levels = lmax + 1;
   pr.n_bottom_groups = 0;
   pr.level_chunks[0].clear();
@@ -204,7 +204,7 @@ void finish_bottom_levels(Problem& pr) {
   {
     std::vector<std::int64_t> ub(group_of_unit.size(), 0);
     for (const TaskDesc& t : pr.tasks)
-      if (t.bundle >= 0) ub[t.unit] += 8LL * t.w * (t.w + t.nr);
+      if (t.bottom >= 0) ub[t.unit] += 8LL * t.w * (t.w + t.nr);
     std::int64_t acc = 0;
     int g = 0;
     for (std::size_t u = 0; u < ub.size(); ++u) {
@@ -234,12 +234,12 @@ void finish_bottom_levels(Problem& pr) {
   std::vector<std::vector<int>> by_slot(nslots);
   std::vector<int> gmax(ngroups, -1);  // highest bottom level of each group
   for (int i = 0; i < nt; ++i)
-    if (pr.tasks[i].bundle >= 0) {
+    if (pr.tasks[i].bottom >= 0) {
       const int g = group_of_unit[pr.tasks[i].unit], l = pr.tasks[i].height;
       by_slot[l < glev ? g * nlev + l : gslot(l)].push_back(i);
       gmax[g] = std::max(gmax[g], l);
     }
-  auto is_regular = [&](int p) { return p >= 0 && pr.tasks[p].bundle < 0; };
+  auto is_regular = [&](int p) { return p >= 0 && pr.tasks[p].bottom < 0; };
   for (int dir = 0; dir < 2; ++dir) {
     auto& tiles = dir == 0 ? pr.ftiles : pr.htiles;
     std::int64_t& mat_len = dir == 0 ? pr.fmat_len : pr.hmat_len;

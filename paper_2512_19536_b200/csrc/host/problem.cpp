@@ -562,7 +562,7 @@ static void factor_units(Problem& pr, const Placement& pl) {
     }
     int small16 = 0, small48 = 0, reg = 0;
     for (const TaskDesc& t : pr.tasks) {
-      if (t.bundle >= 0) continue;
+      if (t.bottom >= 0) continue;
       ++reg;
       const std::int64_t fb = 8LL * t.w * (t.w + t.nr);
       small16 += fb < 16384;

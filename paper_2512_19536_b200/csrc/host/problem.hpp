@@ -47,12 +47,12 @@ struct TaskDesc {
   // forward and backward solves collapse into one level of the sweep
   int root_dense = 0;
   std::int64_t linv_off = 0, b_off = 0;  // inv(L_SS) and L_RS of this supernode in Problem::lval
-  int bundle = -1;     // >= 0: a bottom-level supernode, solved inside level chunks (LevelChunk)
+  int bottom = -1;     // >= 0: a bottom-level supernode, solved inside level chunks (LevelChunk)
   int unit = 0;        // which pack_unit_tasks call (subdomain) it came from
 };
 
 // Bottom levels of the sweep. The supernodes of every small bottom subtree
-// (TaskDesc::bundle >= 0; host/pack.cpp) are not scheduled one by one: per
+// (TaskDesc::bottom >= 0; host/pack.cpp) are not scheduled one by one: per
 // direction and per tree height they are cut into LEVEL CHUNKS, each solved by
 // one CTA as one unit (cuda/sweep.cu run_chunk): gather the inputs of all its
 // supernodes into shared memory, one barrier, one warp per 32-row tile. All

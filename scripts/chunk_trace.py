@@ -1,6 +1,6 @@
-"""Traces one Schwarz sweep and summarises subtree-bundle units against regular units.
+"""Traces one Schwarz sweep and summarises level-chunk units against the individually scheduled ones.
 
-    PDG_MD_RELAX=1 python scripts/bundle_trace.py config4
+    python scripts/chunk_trace.py config4
 """
 import ctypes as C
 import pathlib
@@ -46,7 +46,7 @@ for lab, m in (("chunk fwd", (nchunk == 0) & (direc == 0)), ("chunk bwd", (nchun
     for ph, v in phases:
         print(f"   {ph:13s} mean {v.mean() / 1e3:6.2f} us  p50 {np.median(v) / 1e3:6.2f}  p90 {np.percentile(v, 90) / 1e3:6.2f}")
 edges = np.linspace(0, span, 21)
-print("time(us) active bundle-active:")
+print("time(us) active chunk-active:")
 for e in edges:
     a_ = (st <= e) & (done > e)
     print(f"  {e / 1e3:7.1f} {int(a_.sum()):6d} {int((a_ & (nchunk == 0)).sum()):6d}")

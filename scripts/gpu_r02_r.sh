@@ -11,5 +11,5 @@ run c4_b96_r1_c32 config4 PDG_MD_RELAX=1 PDG_CHUNK_KB=32
 run c4_b96_r1_c128 config4 PDG_MD_RELAX=1 PDG_CHUNK_KB=128
 run c4_b256_r1 config4 PDG_MD_RELAX=1 PDG_BOTTOM_KB=256
 run c4_b32_r1 config4 PDG_MD_RELAX=1 PDG_BOTTOM_KB=32
-PDG_MD_RELAX=1 timeout 500 python scripts/bundle_trace.py config4 > $O/trace_b96_r1.txt 2>&1
+PDG_MD_RELAX=1 timeout 500 python scripts/chunk_trace.py config4 > $O/trace_b96_r1.txt 2>&1
 run c2_b96 config2 PDG_BOTTOM_KB=96

@@ -11,5 +11,5 @@ run c4_r1_l4 config4 PDG_MD_RELAX=1 PDG_BOTTOM_LEVELS=4
 run c4_r1_l10 config4 PDG_MD_RELAX=1 PDG_BOTTOM_LEVELS=10
 run c4_r1_c128 config4 PDG_MD_RELAX=1 PDG_CHUNK_KB=128
 run c4_r1_b256 config4 PDG_MD_RELAX=1 PDG_BOTTOM_KB=256
-PDG_MD_RELAX=1 timeout 500 python scripts/bundle_trace.py config4 > $O/trace_r1.txt 2>&1
+PDG_MD_RELAX=1 timeout 500 python scripts/chunk_trace.py config4 > $O/trace_r1.txt 2>&1
 run c2_b96 config2 PDG_BOTTOM_KB=96

@@ -12,7 +12,7 @@ run c4_r8_m32 config4 PDG_RELAX_MIN_SUBTREE=32
 run c4_r8_m20_b160 config4 PDG_RELAX_MIN_SUBTREE=20 PDG_BOTTOM_KB=160
 run c4_r1_b48 config4 PDG_MD_RELAX=1 PDG_BOTTOM_KB=48
 run c4_r1_b160_l8 config4 PDG_MD_RELAX=1 PDG_BOTTOM_KB=160 PDG_BOTTOM_LEVELS=8
-PDG_MD_RELAX=1 timeout 500 python scripts/bundle_trace.py config4 > $O/trace_r1.txt 2>&1
+PDG_MD_RELAX=1 timeout 500 python scripts/chunk_trace.py config4 > $O/trace_r1.txt 2>&1
 run c5p2_off config5:2 PDG_BOTTOM_KB=0
 run c5p2_r1 config5:2 PDG_MD_RELAX=1
 run c5p4_off config5:4 PDG_BOTTOM_KB=0

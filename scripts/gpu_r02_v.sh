@@ -9,4 +9,4 @@ run c5p4 config5:4
 run c5p4_off config5:4 PDG_BOTTOM_KB=0
 run c5p2 config5:2
 run c2 config2
-timeout 500 python scripts/bundle_trace.py config4 > $O/trace_c4.txt 2>&1
+timeout 500 python scripts/chunk_trace.py config4 > $O/trace_c4.txt 2>&1

@@ -11,4 +11,4 @@ run c4_gl2_i8 config4 PDG_BOTTOM_GROUP_LEVELS=2 PDG_BOTTOM_INTERLEAVE=8
 run c4_gl3_i8 config4 PDG_BOTTOM_INTERLEAVE=8
 run c4_gl2_g64_i4 config4 PDG_BOTTOM_GROUP_LEVELS=2 PDG_BOTTOM_GROUP_MB=64
 run c4_gl2_g16_i8 config4 PDG_BOTTOM_GROUP_LEVELS=2 PDG_BOTTOM_GROUP_MB=16 PDG_BOTTOM_INTERLEAVE=8
-timeout 500 python scripts/bundle_trace.py config4 > $O/trace_c4.txt 2>&1
+timeout 500 python scripts/chunk_trace.py config4 > $O/trace_c4.txt 2>&1
