@@ -25,6 +25,9 @@ int env_int(const char* k, int d) {
   return e ? std::atoi(e) : d;
 }
 
+// doubles of a level chunk's input vectors in the sweep CTA's shared block
+int chunk_x_cap() { return std::max(64, env_int("PDG_CHUNK_X", 1536)); }
+
 constexpr int kTileAlign = 16;  // panel tiles start 128-byte aligned
 std::int64_t align_tile(std::int64_t off) { return (off + kTileAlign - 1) / kTileAlign * kTileAlign; }
 
@@ -65,12 +68,23 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
   std::vector<char> bottom(nsn, 0);
   if (!coarse && bottom_bytes > 0 && pr.n_global_dofs() < (1LL << 30)) {  // chunk records hold int offsets
     const int max_levels = std::max(1, env_int("PDG_BOTTOM_LEVELS", kBottomDefaultLevels));
+    const int chunk_x = chunk_x_cap();
+    // incoming updates per cell (one per descendant row block): part of a chunk record's size
+    std::vector<int> incount(F.m, 0);
+    for (const Supernode& D : F.sn)
+      for (int q : D.rows) ++incount[q];
     std::vector<std::int64_t> fb(nsn, 0);
     for (int s = 0; s < nsn; ++s) {
       const Supernode& S = F.sn[s];
       const int w = S.w(bs), h = w + static_cast<int>(S.rows.size()) * bs;
-      for (int r0 = 0; r0 < h; r0 += kTile) fb[s] += 8 * align(static_cast<std::int64_t>(w) * seg(std::min(kTile, h - r0)));
-      bool ok = w <= 32 && height[s] < max_levels;
+      int ntile = 0, nin = 0;
+      for (int r0 = 0; r0 < h; r0 += kTile, ++ntile)
+        fb[s] += 8 * align(static_cast<std::int64_t>(w) * seg(std::min(kTile, h - r0)));
+      for (int cc = S.s0; cc < S.s1; ++cc) nin += incount[cc];
+      // a supernode must fit a level chunk on its own: its input vector in the
+      // CTA's shared block and its share of the record in half the record block
+      const int rec = 4 * (S.s1 - S.s0) + nin + 2 * (h / bs) + 8 * (ntile + 1);
+      bool ok = w <= 32 && height[s] < max_levels && h <= chunk_x && rec <= kChunkMetaInts / 2;
       for (int c : kids[s]) {
         ok = ok && bottom[c];
         fb[s] += fb[c];
@@ -186,7 +200,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
 void finish_bottom_levels(Problem& pr) {
   constexpr int kTile = 32;
   const std::int64_t chunk_bytes = 1024LL * std::max(4, env_int("PDG_CHUNK_KB", 64));
-  const int xcap = std::max(64, env_int("PDG_CHUNK_X", 1536));
+  const int xcap = chunk_x_cap();
   const int nt = static_cast<int>(pr.tasks.size());
   int lmax = -1;
   for (const TaskDesc& t : pr.tasks)

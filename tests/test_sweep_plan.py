@@ -16,6 +16,8 @@ CASES = {
     "nested_dissection": {"PDG_ORDER": "nd", "PDG_BOTTOM_KB": "64"},
     "small_chunks": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_CHUNK_KB": "8",
                      "PDG_CHUNK_X": "256"},
+    # supernodes taller than the chunk's input block stay individually scheduled (no setup error)
+    "tiny_input_block": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_CHUNK_X": "64"},
     "grouped": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "1",
                 "PDG_BOTTOM_GROUP_LEVELS": "2", "PDG_BOTTOM_INTERLEAVE": "2"},
     "grouped_all_levels": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "2",
