@@ -703,7 +703,7 @@ void DeviceSim::upload_tasks() {
   // (config4 6.35 vs 7.16 ms, config2 0.098 vs 0.129 ms; profiles/r02l)
   // With bottom levels (level chunks: one warp per tile) 128 again: config5
   // p=2 2.22 ms vs 3.29 ms at 64 (profiles/r02aa).
-  sweep_threads = (pr.b <= 6 && pr.n_global_dofs() >= 2000000 && pr.chunks.empty()) ? 64 : 128;
+  sweep_threads = (pr.b <= 6 && pr.n_global_dofs() / std::max(1, pr.cfg.world) >= 2000000 && pr.chunks.empty()) ? 64 : 128;
   if (const char* e = std::getenv("PDG_SWEEP_THREADS")) sweep_threads = std::atoi(e) == 64 ? 64 : 128;
   smem_fwd = smem_bwd = sweep_smem_bytes(sweep_xcap, sweep_threads);
   if (smem_fwd > 220 * 1024) throw SolverError("schwarz: sweep unit does not fit in shared memory");

@@ -33,8 +33,8 @@ std::int64_t align_tile(std::int64_t off) { return (off + kTileAlign - 1) / kTil
 
 }  // namespace
 
-long long bottom_level_bytes(long long n_global_dofs, int b) {
-  return 1024LL * env_int("PDG_BOTTOM_KB", n_global_dofs >= 2000000 && b >= 6 ? kBottomDefaultKB : 0);
+long long bottom_level_bytes(long long dofs_per_rank, int b) {
+  return 1024LL * env_int("PDG_BOTTOM_KB", dofs_per_rank >= 2000000 && b >= 6 ? kBottomDefaultKB : 0);
 }
 
 void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::int64_t dof_base) {
@@ -47,7 +47,7 @@ void pack_unit_tasks(Problem& pr, const SupernodalFactor& F, int coarse, std::in
   // Bottom levels: the supernodes of every subtree whose panels total <=
   // PDG_BOTTOM_KB per direction are not scheduled one by one; they are solved
   // level by level in chunks (finish_bottom_levels below). 0: off.
-  const std::int64_t bottom_bytes = bottom_level_bytes(pr.n_global_dofs(), pr.b);
+  const std::int64_t bottom_bytes = bottom_level_bytes(pr.n_global_dofs() / std::max(1, pr.cfg.world), pr.b);
   const int bs = F.bs;
   const int base = static_cast<int>(pr.tasks.size());
   const int nsn = static_cast<int>(F.sn.size());

@@ -369,7 +369,11 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   // 0.22 ms, config3 p=3 0.43 vs 0.56 ms). Without cell positions (an
   // operator handed over by the caller) the order is graph-only MD.
   // PDG_ORDER=nd|md and PDG_MD_RELAX override.
-  const bool md_default = static_cast<std::int64_t>(N) * b >= 2000000;
+  // The size that matters is what one rank holds (config 4 strong-scaled over 8
+  // GPUs is a 1.3M-dof problem per rank); every rank orders every subdomain,
+  // so the choice depends on (N, b, world) only.
+  const std::int64_t dofs_per_rank = static_cast<std::int64_t>(N) * b / std::max(1, cfg.world);
+  const bool md_default = dofs_per_rank >= 2000000;
   const char* ord_env = std::getenv("PDG_ORDER");
   const bool md_order = !pos || (ord_env ? std::string(ord_env) == "md" : md_default);
   // With the bottom levels solved in level chunks (host/pack.cpp) the small
@@ -377,7 +381,7 @@ static void place_units(Problem& pr, Placement& pl, const std::vector<std::vecto
   // supernodes store no explicit zeros (config 4: 26.6 GB of panels instead
   // of 35.0 GB; sweep 6.17 -> 5.86 ms, profiles/r02u). Small blocks (b < 10)
   // merge up to 2 cells (config 5 p=2: 2.22 ms vs 2.48 ms fundamental).
-  const bool bottom_on = md_order && bottom_level_bytes(static_cast<std::int64_t>(N) * b, b) > 0;
+  const bool bottom_on = md_order && bottom_level_bytes(dofs_per_rank, b) > 0;
   const int md_relax =
       std::getenv("PDG_MD_RELAX") ? std::max(1, std::atoi(std::getenv("PDG_MD_RELAX"))) : bottom_on ? (b >= 10 ? 1 : 2) : 8;
   pl.nd.assign(n_units, NdTree{});

@@ -75,12 +75,12 @@ struct TaskDesc {
 constexpr int kChunkMetaInts = 2560;  // shared-memory block of the sweep CTA (cuda/sweep.cu)
 constexpr int kBottomDefaultKB = 160;  // PDG_BOTTOM_KB
 constexpr int kBottomDefaultLevels = 8;  // PDG_BOTTOM_LEVELS
-// Bottom levels on? Default: where the sweep is bandwidth bound (>= 2M dofs,
-// the minimum-degree ordering) and b >= 6 (config 5 p=2, b = 6: 2.35 -> 2.22 ms
+// Bottom levels on? Default: where the sweep is bandwidth bound (>= 2M dofs
+// per rank, the minimum-degree ordering) and b >= 6 (config 5 p=2, b = 6: 2.35 -> 2.22 ms
 // with 128-thread CTAs and supernodes of <= 2 cells; profiles/r02aa).
 // Smaller problems have idle CTAs and want every supernode on its own one.
 // PDG_BOTTOM_KB overrides (0: off). Returns the subtree byte cap.
-long long bottom_level_bytes(long long n_global_dofs, int b);
+long long bottom_level_bytes(long long dofs_per_rank, int b);
 struct LevelChunk {
   int dir = 0, level = 0, first_task = 0, n_task = 0;
   // counters (Problem::level_chunks[dir][slot], slot = group * levels + level): the one this
