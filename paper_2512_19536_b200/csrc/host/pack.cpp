@@ -213,7 +213,7 @@ void finish_bottom_levels(Problem& pr) {
   if (pr.ubuf_size >= (1LL << 31)) throw SolverError("pack: update buffer too large for the level chunk records");
   const int nlev = lmax + 1;
   // groups of consecutive subdomains holding about group_bytes of bottom forward panel
-  const std::int64_t group_bytes = (1LL << 20) * std::max(1, env_int("PDG_BOTTOM_GROUP_MB", 32));
+  const std::int64_t group_bytes = (1LL << 20) * std::max(1, env_int("PDG_BOTTOM_GROUP_MB", 192));
   std::vector<int> group_of_unit(std::max(pr.n_packed_units, 1), 0);
   {
     std::vector<std::int64_t> ub(group_of_unit.size(), 0);
@@ -235,12 +235,13 @@ void finish_bottom_levels(Problem& pr) {
   // the few supernodes above them level by level over all groups (global
   // counters, slots ngroups * nlev + level): near the top a group has too few
   // chunks to keep a level's dependencies a safe distance behind it.
-  // Default 0 (every level global): on B200 the grouped order's shorter reuse
-  // distance did speed the chunks up (config 4: 12 -> 8 us of work each) but
-  // its dependencies sit too close behind them in the ticket order and the
-  // CTAs wait (sweep 5.87 -> 7.0 ms with two grouped levels, profiles/r02y).
-  const int glev = std::clamp(env_int("PDG_BOTTOM_GROUP_LEVELS", 0), 0, nlev);
-  const int inter = std::max(1, env_int("PDG_BOTTOM_INTERLEAVE", 4));
+  // Default: every level grouped, in the skewed order below with groups of
+  // ~192 MB (config 4 sweep 5.55 -> 5.45 ms, config 5 p=2 2.21 -> 2.10 ms,
+  // profiles/r02af, r02ag). Smaller groups or the block-interleaved order
+  // (PDG_BOTTOM_INTERLEAVE > 0) put a level's dependencies too close behind it
+  // in the ticket order and the CTAs wait (>= 7 ms, profiles/r02y).
+  const int glev = std::clamp(env_int("PDG_BOTTOM_GROUP_LEVELS", 99), 0, nlev);
+  const int inter = std::max(0, env_int("PDG_BOTTOM_INTERLEAVE", 0));
   const int ngroups = pr.n_bottom_groups, nslots = ngroups * nlev + nlev;
   auto gslot = [&](int level) { return ngroups * nlev + level; };
   pr.level_chunks[0].assign(nslots, 0);
@@ -262,10 +263,21 @@ void finish_bottom_levels(Problem& pr) {
     std::vector<int> slot_order;
     if (dir == 1)
       for (int l = nlev - 1; l >= glev; --l) slot_order.push_back(gslot(l));
-    for (int g0 = 0; g0 < ngroups; g0 += inter)
-      for (int li = 0; li < glev; ++li)
-        for (int g = g0; g < std::min(ngroups, g0 + inter); ++g)
-          slot_order.push_back(g * nlev + (dir == 0 ? li : glev - 1 - li));
+    if (inter > 0) {  // `inter` groups at a time, level by level
+      for (int g0 = 0; g0 < ngroups; g0 += inter)
+        for (int li = 0; li < glev; ++li)
+          for (int g = g0; g < std::min(ngroups, g0 + inter); ++g)
+            slot_order.push_back(g * nlev + (dir == 0 ? li : glev - 1 - li));
+    } else {
+      // skewed: step t runs level li of group t - li for every li, so a
+      // group's consecutive levels are always one whole step (about one
+      // group's worth of chunks from glev different groups) apart
+      for (int t = 0; t < ngroups + glev - 1; ++t)
+        for (int li = 0; li < glev; ++li) {
+          const int g = t - li;
+          if (g >= 0 && g < ngroups) slot_order.push_back(g * nlev + (dir == 0 ? li : glev - 1 - li));
+        }
+    }
     if (dir == 0)
       for (int l = glev; l < nlev; ++l) slot_order.push_back(gslot(l));
     for (int slot : slot_order) {

@@ -59,10 +59,10 @@ struct TaskDesc {
 // chunks of a level are independent; a level waits for the previous one
 // through one counter per level, so no per-supernode dependency is tracked.
 // The subdomains are taken in GROUPS of about PDG_BOTTOM_GROUP_MB of bottom
-// panel, each with its own level counters, two groups interleaved level by
-// level in the ticket order: a level's updates are then read back while they
-// are still in the L2 (a global level order reads them from DRAM), and a
-// level's dependencies were issued a whole group-level earlier.
+// panel, each with its own level counters, in a skewed ticket order (step t
+// runs level l of group t - l): part of a level's updates is then read back
+// from the L2 instead of DRAM, and a level's dependencies were issued one
+// whole step (about a group's worth of chunks) earlier.
 // A chunk's panels are contiguous and its record is one block of ints in
 // bmeta (16-byte aligned):
 //   [ncell, nitem, naux, 0] ,

@@ -20,6 +20,9 @@ CASES = {
     "tiny_input_block": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_CHUNK_X": "64"},
     "grouped": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "1",
                 "PDG_BOTTOM_GROUP_LEVELS": "2", "PDG_BOTTOM_INTERLEAVE": "2"},
+    "grouped_skewed": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "1",
+                       "PDG_BOTTOM_GROUP_LEVELS": "99", "PDG_BOTTOM_INTERLEAVE": "0"},
+    "global_levels": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_LEVELS": "0"},
     "grouped_all_levels": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "2",
                            "PDG_BOTTOM_GROUP_LEVELS": "99", "PDG_BOTTOM_INTERLEAVE": "1"},
 }

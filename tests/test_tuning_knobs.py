@@ -39,6 +39,9 @@ CASES = {
     "bottom_levels_hybrid_relax": {"PDG_ORDER": "md", "PDG_RELAX_MIN_SUBTREE": "12", "PDG_BOTTOM_KB": "96"},
     "bottom_levels_grouped": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_MB": "1",
                               "PDG_BOTTOM_GROUP_LEVELS": "2", "PDG_BOTTOM_INTERLEAVE": "3"},
+    "bottom_levels_global": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96", "PDG_BOTTOM_GROUP_LEVELS": "0"},
+    "bottom_levels_skewed_groups": {"PDG_ORDER": "md", "PDG_MD_RELAX": "1", "PDG_BOTTOM_KB": "96",
+                                    "PDG_BOTTOM_GROUP_MB": "1", "PDG_BOTTOM_GROUP_LEVELS": "3"},
     "bottom_levels_off": {"PDG_BOTTOM_KB": "0", "PDG_ORDER": "md"},
 }
 
